@@ -1,0 +1,209 @@
+/*
+ * qzcuda.h — C ABI of the B200-native compressed-chunk state-vector engine.
+ *
+ * This is the drop-in boundary for the MEMQSim hot path (reference:
+ * /root/reference/proj, C++ library `qzsim`).  The reference has no FFI of its
+ * own; its accelerator extension point is the abstract `qzsim::Device`
+ * (include/qzsim/device.hpp:76-95) driven by `qzsim::run`
+ * (src/pipeline.cpp:128-314), plus the chunk codec
+ * (include/qzsim/codec.hpp:61-70).  Every entry point below replaces one of
+ * those interfaces and cites it.  Plain C types only: pointers, sizes,
+ * doubles, status ints.  The C++ host library (include/qzsim/*.hpp in this
+ * repo) and the Python package both bind exactly these symbols.
+ *
+ * Conventions
+ *   - Every function returns QZC_OK (0) or a negative QZC_E* status; the
+ *     message of the last failure on the calling thread is qzc_last_error().
+ *     The C++ layer maps status classes onto the reference's exception
+ *     hierarchy (CodecError/StoreError/PlanError/DeviceError, util.hpp:34-37).
+ *   - Amplitudes are interleaved complex<double> (re, im), 16 bytes each,
+ *     exactly std::complex<double> / qzsim::Amplitude (util.hpp:32).
+ *   - Payload bytes, CRC-32 and FNV-1a digests are bit-identical to the
+ *     reference (codec.cpp:95-266, util.cpp:20-31, store.cpp:129-136).
+ *   - "host" pointers may be pageable or pinned; "dev" pointers are CUDA
+ *     device pointers on the context's device.
+ */
+#ifndef QZCUDA_H
+#define QZCUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------ */
+#define QZC_OK 0
+#define QZC_EINVAL (-1)   /* bad argument (reference: Error / PlanError)     */
+#define QZC_ECODEC (-2)   /* malformed or corrupt payload (CodecError)        */
+#define QZC_ESTORE (-3)   /* store geometry / index error (StoreError)        */
+#define QZC_EPLAN (-4)    /* planner precondition (PlanError)                 */
+#define QZC_EDEVICE (-5)  /* device bound / bad buffer bit (DeviceError)      */
+#define QZC_ECUDA (-6)    /* CUDA runtime failure                             */
+#define QZC_ENOMEM (-7)   /* HBM / arena capacity exhausted                   */
+
+const char *qzc_last_error(void);
+const char *qzc_version(void);
+
+/* ---- gates -------------------------------------------------------------- */
+/* Gate kinds in the reference's enum order (include/qzsim/gates.hpp:27-45). */
+enum qzc_gate_kind {
+    QZC_H = 0, QZC_X, QZC_Y, QZC_Z, QZC_S, QZC_SDG, QZC_T, QZC_TDG,
+    QZC_RX, QZC_RY, QZC_RZ, QZC_U1, QZC_U2, QZC_U3,
+    QZC_CX, QZC_CZ, QZC_SWAP
+};
+
+/* One gate (reference qzsim::Gate, gates.hpp:49-55).  For two-qubit kinds
+ * qubits[0] is the control / higher-order matrix bit. */
+typedef struct qzc_gate {
+    uint32_t kind;
+    uint32_t nqubits;
+    uint32_t qubits[2];
+    double params[3];
+} qzc_gate;
+
+/* Unitary of a gate, row-major, interleaved complex; dim 2 or 4.
+ * Bit-identical to qzsim::gate_matrix (gates.cpp:114-182). */
+int qzc_gate_matrix(const qzc_gate *gate, double *mat_out /* 32 doubles */,
+                    uint32_t *dim_out);
+
+/* ---- context ------------------------------------------------------------ */
+typedef struct qzc_context qzc_context;
+
+/* One context per GPU.  hbm_budget_bytes = 0 means "all free HBM minus a
+ * safety margin".  Replaces make_reference_device's memory bound
+ * (device.hpp:36-40, device.cpp:273-299). */
+int qzc_context_create(int device, uint64_t hbm_budget_bytes,
+                       qzc_context **out);
+void qzc_context_destroy(qzc_context *ctx);
+int qzc_synchronize(qzc_context *ctx);
+/* Number of engine kernels launched on this context so far. */
+uint64_t qzc_kernel_launches(const qzc_context *ctx);
+
+/* ---- chunk codec (replaces codec.hpp:61-70) ----------------------------- */
+/* Worst-case payload bytes for one chunk of `elements` amplitudes. */
+uint64_t qzc_payload_bound(uint64_t elements, double error_bound);
+
+/* Compress `count` chunks of `elements` amplitudes each (host arrays).
+ * Chunk k's amplitudes are amps[k*elements .. (k+1)*elements).  Payloads are
+ * written back to back into payload_out (capacity payload_cap) with
+ * offsets[k], sizes[k] and crcs[k] (CRC-32 of the payload).  forced_raw lists
+ * flat component indices (real plane [0,N), imaginary [N,2N)) forced onto the
+ * raw path for EVERY chunk of the call (codec.hpp:55-64).
+ * Reference: qzsim::compress, codec.cpp:95-185. */
+int qzc_compress_host(qzc_context *ctx, const double *amps, uint64_t count,
+                      uint64_t elements, double error_bound,
+                      const uint64_t *forced_raw, uint64_t n_forced,
+                      uint8_t *payload_out, uint64_t payload_cap,
+                      uint64_t *offsets, uint32_t *sizes, uint32_t *crcs);
+
+/* Decompress `count` payloads (host arrays) into amps_out.  Verifies each
+ * CRC first; on failure returns QZC_ECODEC and names the chunk index
+ * (chunk_index_base + k) in qzc_last_error(), like codec.cpp:187-190.
+ * Reference: qzsim::decompress, codec.cpp:187-266. */
+int qzc_decompress_host(qzc_context *ctx, const uint8_t *payloads,
+                        const uint64_t *offsets, const uint32_t *sizes,
+                        const uint32_t *crcs, uint64_t count,
+                        uint64_t elements, uint64_t chunk_index_base,
+                        double *amps_out);
+
+/* CRC-32 (zlib polynomial) and FNV-1a-64 of a host byte span
+ * (util.cpp:20-31).  Host helpers for the report path. */
+uint32_t qzc_crc32(const uint8_t *bytes, uint64_t len);
+uint64_t qzc_fnv1a64(const uint8_t *bytes, uint64_t len, uint64_t state);
+
+/* ---- gate kernels (replaces kernels.hpp:24-38 / Device::apply_gates) ---- */
+/* Apply gates (already remapped to buffer bits) in order to a host buffer of
+ * 2^nbits amplitudes.  Bit-exact with qzsim::apply_gates. */
+int qzc_apply_gates_host(qzc_context *ctx, double *amps, uint32_t nbits,
+                         const qzc_gate *gates, uint64_t ngates);
+/* Same on a device buffer (stream-ordered on the context stream). */
+int qzc_apply_gates_dev(qzc_context *ctx, double *amps_dev, uint32_t nbits,
+                        const qzc_gate *gates, uint64_t ngates);
+
+/* ---- simulator (replaces qzsim::run, pipeline.cpp:128-314) -------------- */
+typedef struct qzc_sim qzc_sim;
+
+typedef struct qzc_sim_config {
+    uint32_t num_qubits;     /* n                                             */
+    uint32_t chunk_qubits;   /* c  (PipelineConfig::chunk_qubits)             */
+    uint32_t batch_qubits;   /* m  (PipelineConfig::batch_qubits)             */
+    uint32_t reserved0;
+    double error_bound;      /* 0 selects the lossless codec                  */
+    uint64_t window_amps;    /* dense amplitudes per device window; 0 = auto  */
+    uint32_t residency;      /* 0 = compressed store in HBM, 1 = pinned host  */
+    uint32_t renormalize;    /* PipelineConfig::renormalize                   */
+    uint32_t fuse_gates;     /* 1 = fused smem gate passes (default)          */
+    uint32_t reserved1;
+} qzc_sim_config;
+
+/* Per-run statistics (SimulationReport subset, pipeline.hpp:53-67, plus
+ * device-event phase times). */
+typedef struct qzc_sim_stats {
+    double wall_seconds;         /* stage loop, host clock                   */
+    double decode_seconds;       /* CUDA-event phase sums                    */
+    double gate_seconds;
+    double encode_seconds;
+    double h2d_seconds;
+    double d2h_seconds;
+    uint64_t stages;
+    uint64_t batches;
+    uint64_t gate_passes;
+    uint64_t chunk_decompress_count;
+    uint64_t chunk_recompress_count;
+    uint64_t h2d_bytes;
+    uint64_t d2h_bytes;
+    uint64_t kernel_launches;
+    uint64_t current_bytes;      /* Footprint (store.hpp:31-36)              */
+    uint64_t peak_bytes;
+    uint64_t dense_bytes;
+    uint64_t windows;
+} qzc_sim_stats;
+
+int qzc_sim_create(qzc_context *ctx, const qzc_sim_config *cfg,
+                   qzc_sim **out);
+void qzc_sim_destroy(qzc_sim *sim);
+/* |0...0> through the reference's init (store.cpp:26-81). */
+int qzc_sim_init_basis(qzc_sim *sim);
+/* Execute a circuit through the staged, batched, compressed pipeline. */
+int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates);
+int qzc_sim_stats_get(const qzc_sim *sim, qzc_sim_stats *out);
+/* Number of stages the planner produces (plan(), planner.cpp:46-96). */
+int qzc_sim_plan_stages(const qzc_sim *sim, const qzc_gate *gates,
+                        uint64_t ngates, uint64_t *stages_out);
+/* FNV-1a over payloads in chunk order (store.cpp:129-136). */
+int qzc_sim_digest(qzc_sim *sim, uint64_t *digest_out);
+/* Σ|a|^2, compensated (pipeline.cpp:119-126). */
+int qzc_sim_norm(qzc_sim *sim, double *norm_out);
+/* Total payload bytes and per-chunk sizes (chunk order). */
+int qzc_sim_chunk_count(const qzc_sim *sim, uint64_t *count_out);
+int qzc_sim_payload_bytes(qzc_sim *sim, uint64_t *total_out);
+/* Copy all payloads to host in chunk order (the reference's ChunkStore
+ * contents): payload_out gets the concatenation, sizes/crcs per chunk. */
+int qzc_sim_export(qzc_sim *sim, uint8_t *payload_out, uint64_t cap,
+                   uint32_t *sizes, uint32_t *crcs);
+/* Replace the store with host payloads (QZST load / store_chunk path). */
+int qzc_sim_import(qzc_sim *sim, const uint8_t *payloads,
+                   const uint32_t *sizes, const uint32_t *crcs);
+/* Decompress chunk range [first, first+count) to host amplitudes. */
+int qzc_sim_read_chunks(qzc_sim *sim, uint64_t first, uint64_t count,
+                        double *amps_out);
+/* Compress host amplitudes into chunk `index` (ChunkStore::store_chunk). */
+int qzc_sim_write_chunk(qzc_sim *sim, uint64_t index, const double *amps);
+/* Normalised |<dense|store>|^2 against a dense device state of 2^n
+ * amplitudes (oracle.cpp:95-113). */
+int qzc_sim_fidelity_dev(qzc_sim *sim, const double *dense_dev,
+                         double *fidelity_out);
+
+/* ---- dense fp64 reference run on the GPU (fidelity baseline) ------------ */
+/* Uncompressed double-precision state on the device, same gate kernels.
+ * Used for fidelity at n beyond the CPU oracle (oracle.hpp:21). */
+int qzc_dense_run(qzc_context *ctx, uint32_t num_qubits, const qzc_gate *gates,
+                  uint64_t ngates, double **dense_dev_out);
+void qzc_dense_free(qzc_context *ctx, double *dense_dev);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QZCUDA_H */
