@@ -1,0 +1,41 @@
+# Build the sm_100a engine (libqzcuda.so) and the test oracles.
+#   make            engine + oracle
+#   make ref        also compile the reference into oracle/_ref (needs /root/reference)
+CUDA ?= /usr/local/cuda
+NVCC ?= $(CUDA)/bin/nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 --fmad=false -Xcompiler -fPIC -Xcompiler -Wall \
+           -Xptxas -v
+PKG := paper_2309_16979_b200
+SRC := $(PKG)/csrc
+OBJ := build/obj
+LIB := $(PKG)/lib/libqzcuda.so
+CU_SRCS := $(wildcard $(SRC)/*.cu)
+CPP_SRCS := $(wildcard $(SRC)/*.cpp)
+HDRS := $(wildcard $(SRC)/*.cuh) include/qzcuda.h
+OBJS := $(patsubst $(SRC)/%.cu,$(OBJ)/%.o,$(CU_SRCS)) $(patsubst $(SRC)/%.cpp,$(OBJ)/%.o,$(CPP_SRCS))
+
+all: $(LIB) oracle
+
+$(OBJ)/%.o: $(SRC)/%.cu $(HDRS)
+	@mkdir -p $(OBJ)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $@.ptxas.log || (cat $@.ptxas.log; false)
+
+$(OBJ)/%.o: $(SRC)/%.cpp $(HDRS)
+	@mkdir -p $(OBJ)
+	g++ -std=c++17 -O2 -fPIC -Wall -I$(CUDA)/include -c $< -o $@
+
+$(LIB): $(OBJS)
+	@mkdir -p $(dir $@)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart
+
+oracle:
+	$(MAKE) -C oracle all
+
+ref:
+	$(MAKE) -C oracle ref
+
+clean:
+	rm -rf build $(PKG)/lib oracle/liboracle.so
+
+.PHONY: all oracle ref clean

@@ -8,8 +8,8 @@
  * (src/pipeline.cpp:128-314), plus the chunk codec
  * (include/qzsim/codec.hpp:61-70).  Every entry point below replaces one of
  * those interfaces and cites it.  Plain C types only: pointers, sizes,
- * doubles, status ints.  The C++ host library (include/qzsim/*.hpp in this
- * repo) and the Python package both bind exactly these symbols.
+ * doubles, status ints.  The C++ host library (the qzsim headers under
+ * include/qzsim in this repo) and the Python package both bind exactly these symbols.
  *
  * Conventions
  *   - Every function returns QZC_OK (0) or a negative QZC_E* status; the

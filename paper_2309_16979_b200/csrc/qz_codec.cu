@@ -1,0 +1,788 @@
+// qz_codec.cu — bit-exact chunk codec kernels for sm_100a.
+//
+// Reference: codec.cpp:28-266 (LossyPQ quantiser chain, zigzag, byte-plane
+// RLE, LosslessRLE, CRC-32), util.cpp:20-31.
+//
+// The quantiser / reconstruction chain is strictly sequential per
+// (chunk, plane): pred_{i+1} depends on the rounded reconstruction of element
+// i (codec.cpp:130-159, 226-246), and fp64 addition is not associative, so
+// parallelism comes from chunks: one thread per (chunk, plane) "half".  Each
+// CTA stages a [32 chunks x 32 elements] amplitude tile through shared memory
+// so every HBM access is a coalesced 512 B row, while the threads walk their
+// chains.  The same sequential walk emits the RLE pairs of its half into a
+// scratch sub-stream; the real half keeps its last run open and the
+// imaginary half holds back its first run, and the assembler merges the two
+// at the plane boundary exactly as rle_encode would over the joined plane.
+#include <algorithm>
+
+#include "qz_codec.cuh"
+
+namespace qz {
+
+namespace {
+
+constexpr uint32_t kHdr = 17;
+constexpr uint32_t kPoly = 0xEDB88320u;
+constexpr int kSlotsPerCta = 32;  // chunks per CTA in the encode/decode kernels
+constexpr int kTileElems = 32;    // elements per staged tile row
+
+__host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+__host__ __device__ __forceinline__ uint32_t umin32(uint32_t a, uint32_t b) { return a < b ? a : b; }
+__host__ __device__ inline uint64_t round_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+
+// ----------------------------------------------------------------- bytes --
+__device__ __forceinline__ uint32_t ld_u8(const uint8_t *p) { return p[0]; }
+__device__ __forceinline__ uint32_t ld_u32(const uint8_t *p) {
+    return uint32_t(p[0]) | (uint32_t(p[1]) << 8) | (uint32_t(p[2]) << 16) | (uint32_t(p[3]) << 24);
+}
+__device__ __forceinline__ uint64_t ld_u64(const uint8_t *p) {
+    return uint64_t(ld_u32(p)) | (uint64_t(ld_u32(p + 4)) << 32);
+}
+__device__ __forceinline__ void st_u32(uint8_t *p, uint32_t v) {
+    p[0] = v & 0xff; p[1] = (v >> 8) & 0xff; p[2] = (v >> 16) & 0xff; p[3] = v >> 24;
+}
+__device__ __forceinline__ void st_u64(uint8_t *p, uint64_t v) {
+    st_u32(p, uint32_t(v));
+    st_u32(p + 4, uint32_t(v >> 32));
+}
+
+__device__ __forceinline__ uint32_t zigzag16(int32_t code) {
+    return uint32_t((code << 1) ^ (code >> 15)) & 0xffffu;
+}
+__device__ __forceinline__ int32_t unzigzag16(uint32_t z) {
+    return int32_t(z >> 1) ^ -int32_t(z & 1);
+}
+
+// ------------------------------------------------------------- CRC-32 ---
+__host__ __device__ inline uint32_t multmodp(uint32_t a, uint32_t b) {
+    if (a == 0) return 0;
+    uint32_t m = 1u << 31, p = 0;
+    for (;;) {
+        if (a & m) {
+            p ^= b;
+            if ((a & (m - 1)) == 0) break;
+        }
+        m >>= 1;
+        b = (b & 1) ? (b >> 1) ^ kPoly : b >> 1;
+    }
+    return p;
+}
+
+// x^(8n) mod P: the operator that appends n zero bytes (crc32_combine).
+__host__ __device__ inline uint32_t x8nmodp(uint64_t n) {
+    uint32_t p = 1u << 31;     // x^0
+    uint32_t sq = 1u << 30;    // x^1
+    // x^(8n) = x^(n * 2^3): square x three times first
+    for (int i = 0; i < 3; ++i) sq = multmodp(sq, sq);
+    while (n) {
+        if (n & 1) p = multmodp(sq, p);
+        n >>= 1;
+        if (n) sq = multmodp(sq, sq);
+    }
+    return p;
+}
+
+__device__ uint32_t crc_range(const uint32_t *T, const uint8_t *p, uint64_t n) {
+    uint32_t c = 0xFFFFFFFFu;
+    while (n >= 8) {
+        uint32_t lo = c ^ ld_u32(p), hi = ld_u32(p + 4);
+        c = T[7 * 256 + (lo & 0xff)] ^ T[6 * 256 + ((lo >> 8) & 0xff)] ^
+            T[5 * 256 + ((lo >> 16) & 0xff)] ^ T[4 * 256 + (lo >> 24)] ^
+            T[3 * 256 + (hi & 0xff)] ^ T[2 * 256 + ((hi >> 8) & 0xff)] ^
+            T[1 * 256 + ((hi >> 16) & 0xff)] ^ T[0 * 256 + (hi >> 24)];
+        p += 8;
+        n -= 8;
+    }
+    while (n--) c = T[(c ^ *p++) & 0xff] ^ (c >> 8);
+    return c ^ 0xFFFFFFFFu;
+}
+
+// Warp per slot: 32 equal segments, per-lane slicing-by-8, then lane 0
+// folds them left to right with crc32_combine.
+__global__ void __launch_bounds__(256) k_crc(const uint32_t *__restrict__ tabs,
+                                             const uint8_t *__restrict__ arena, ChunkTable table,
+                                             const uint64_t *__restrict__ slot_chunk,
+                                             uint64_t nslots, int verify, DevStatus *status) {
+    __shared__ uint32_t T[8 * 256];
+    for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) T[i] = tabs[i];
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    for (uint64_t s = warp; s < nslots; s += nwarps) {
+        const uint64_t chunk = slot_chunk ? slot_chunk[s] : s;
+        const uint64_t len = table.len[chunk];
+        const uint8_t *p = arena + table.off[chunk];
+        const uint64_t seg = round_up((len + 31) / 32, 8);
+        const uint64_t b = umin64(len, lane * seg), e = umin64(len, b + seg);
+        uint32_t c = crc_range(T, p + b, e - b);
+        uint32_t mylen = uint32_t(e - b);
+        // fold lane CRCs left to right: acc = acc * x^(8 len_i) ^ crc_i
+        uint32_t acc = c;
+        const uint32_t sh_full = lane == 0 ? x8nmodp(seg) : 0;
+        for (int i = 1; i < 32; ++i) {
+            const uint32_t ci = __shfl_sync(0xffffffffu, c, i);
+            const uint32_t li = __shfl_sync(0xffffffffu, mylen, i);
+            if (lane == 0 && li) acc = multmodp(li == seg ? sh_full : x8nmodp(li), acc) ^ ci;
+        }
+        if (lane == 0) {
+            if (verify) {
+                if (acc != table.crc[chunk]) dev_fail(status, QZS_CRC, chunk);
+            } else {
+                table.crc[chunk] = acc;
+            }
+        }
+    }
+}
+
+// ----------------------------------------------------------- decode index --
+
+struct Cursor {
+    uint32_t pos, rem, byte;
+};
+
+__global__ void k_dec_index(const uint8_t *__restrict__ arena, ChunkTable table,
+                            const uint64_t *__restrict__ slot_chunk, uint64_t nslots,
+                            CodecGeom g, DecIdx *__restrict__ out, DevStatus *status) {
+    const uint64_t s = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (s >= nslots) return;
+    const uint64_t chunk = slot_chunk ? slot_chunk[s] : s;
+    DecIdx d;
+    d.base = table.off[chunk];
+    d.len = 0;  // marks "invalid" until the walk succeeds
+    const uint32_t len = table.len[chunk];
+    const uint8_t *p = arena + d.base;
+    const uint64_t N = g.N, total = 2 * N;
+    int err = 0;
+    if (len < kHdr) err = QZS_HEADER;
+    uint32_t id = 0, count = 0;
+    if (!err) {
+        id = ld_u8(p);
+        d.eb = __longlong_as_double((long long)ld_u64(p + 1));
+        count = ld_u32(p + 9);
+        d.raw_count = ld_u32(p + 13);
+        if ((id != 1 && id != 2) || id != (g.lossy ? 1u : 2u) || count != N) err = QZS_HEADER;
+    }
+    uint32_t pos = kHdr;
+    for (uint32_t k = 0; k < g.planes && !err; ++k) {
+        uint64_t produced = 0;
+        d.pos[k][0] = pos;
+        d.skip[k][0] = 0;
+        bool found = false;
+        while (produced < total) {
+            if (pos + 2 > len) { err = QZS_RLE_TRUNC; break; }
+            const uint32_t run = p[pos + 1];
+            if (run == 0 || produced + run > total) { err = QZS_RLE_RUN; break; }
+            if (!found && produced <= N && N < produced + run) {
+                d.pos[k][1] = pos;
+                d.skip[k][1] = uint32_t(N - produced);
+                found = true;
+            }
+            produced += run;
+            pos += 2;
+        }
+    }
+    if (!err && g.lossy) {
+        d.raw_pos = pos;
+        if (uint64_t(pos) + uint64_t(d.raw_count) * 8 > len) err = QZS_RAW_MISSING;
+    }
+    if (!err && g.lossy) {
+        // sentinel (0xFFFF) codes in the real half: overlap of 0xFF runs in
+        // both byte planes over elements [0, N)
+        uint32_t pl = d.pos[0][0], ph = d.pos[1][0];
+        uint32_t rl = p[pl + 1], rh = p[ph + 1];
+        uint64_t i = 0, cnt = 0;
+        while (i < N) {
+            uint64_t step = umin64(umin32(rl, rh), N - i);
+            if (p[pl] == 0xFF && p[ph] == 0xFF) cnt += step;
+            i += step;
+            rl -= uint32_t(step);
+            rh -= uint32_t(step);
+            if (i < N) {
+                if (rl == 0) { pl += 2; rl = p[pl + 1]; }
+                if (rh == 0) { ph += 2; rh = p[ph + 1]; }
+            }
+        }
+        if (cnt > d.raw_count) err = QZS_RAW_UNDER;
+        d.raw_re = uint32_t(cnt);
+    }
+    if (err) dev_fail(status, err, chunk);
+    else d.len = len;
+    out[s] = d;
+}
+
+// ----------------------------------------------------------------- decode --
+
+__device__ __forceinline__ void cur_init(Cursor &c, const uint8_t *p, uint32_t pos, uint32_t skip) {
+    c.pos = pos;
+    c.byte = p[pos];
+    c.rem = p[pos + 1] - skip;
+}
+
+__device__ __forceinline__ uint32_t cur_next(Cursor &c, const uint8_t *p) {
+    if (c.rem == 0) {
+        c.pos += 2;
+        c.byte = p[c.pos];
+        c.rem = p[c.pos + 1];
+    }
+    --c.rem;
+    return c.byte;
+}
+
+// Tile of kSlotsPerCta rows x kTileElems amplitudes (+1 pad element per row).
+struct TileSmem {
+    double2 v[kSlotsPerCta][kTileElems + 1];
+};
+
+__device__ __forceinline__ void store_tile(TileSmem &t, double2 *win, uint64_t slot0,
+                                           uint64_t nslots, uint64_t N, uint64_t e0,
+                                           uint32_t te) {
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (uint32_t r = warp; r < kSlotsPerCta; r += nw) {
+        if (slot0 + r >= nslots) break;
+        if (lane < te) win[(slot0 + r) * N + e0 + lane] = t.v[r][lane];
+    }
+}
+
+__device__ __forceinline__ void load_tile(TileSmem &t, const double2 *win, uint64_t slot0,
+                                          uint64_t nslots, uint64_t N, uint64_t e0,
+                                          uint32_t te) {
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (uint32_t r = warp; r < kSlotsPerCta; r += nw) {
+        if (slot0 + r >= nslots) break;
+        if (lane < te) t.v[r][lane] = __ldcs(win + (slot0 + r) * N + e0 + lane);
+    }
+}
+
+__device__ __forceinline__ double comp(const double2 &v, uint32_t h) { return h ? v.y : v.x; }
+__device__ __forceinline__ void set_comp(double2 &v, uint32_t h, double x) {
+    if (h) v.y = x; else v.x = x;
+}
+
+// Lossy decode (codec.cpp:217-249): thread = (slot, half).
+__global__ void __launch_bounds__(2 * kSlotsPerCta) k_dec_lossy(
+    const uint8_t *__restrict__ arena, const DecIdx *__restrict__ idx,
+    const uint64_t *__restrict__ slot_chunk, uint64_t nslots, CodecGeom g,
+    double2 *__restrict__ win, DevStatus *status) {
+    __shared__ TileSmem tile;
+    const uint32_t r = threadIdx.x >> 1, h = threadIdx.x & 1;
+    const uint64_t slot0 = uint64_t(blockIdx.x) * kSlotsPerCta, s = slot0 + r;
+    const bool active = s < nslots && idx[min(s, nslots - 1)].len != 0;
+    const DecIdx *d = &idx[min(s, nslots - 1)];
+    const uint8_t *p = arena + d->base;
+    Cursor lo{0, 0, 0}, hi{0, 0, 0};
+    uint32_t raw_i = 0, raw_count = 0, raw_pos = 0;
+    double eb = 0.0, pred = 0.0;
+    bool bad = false;
+    if (active) {
+        cur_init(lo, p, d->pos[0][h], d->skip[0][h]);
+        cur_init(hi, p, d->pos[1][h], d->skip[1][h]);
+        raw_i = h ? d->raw_re : 0;
+        raw_count = d->raw_count;
+        raw_pos = d->raw_pos;
+        eb = d->eb;
+    }
+    const uint64_t N = g.N;
+    const uint32_t te = uint32_t(umin64(kTileElems, N));
+    for (uint64_t e0 = 0; e0 < N; e0 += te) {
+        for (uint32_t e = 0; e < te; ++e) {
+            if (active) {
+                const uint32_t z = cur_next(lo, p) | (cur_next(hi, p) << 8);
+                if (z == 0xFFFFu) {
+                    if (raw_i >= raw_count) {
+                        bad = true;
+                    } else {
+                        pred = __longlong_as_double((long long)ld_u64(p + raw_pos + 8ull * raw_i));
+                        ++raw_i;
+                    }
+                } else {
+                    const int32_t code = unzigzag16(z);
+                    pred = __dadd_rn(pred, __dmul_rn(__dmul_rn(double(code), 2.0), eb));
+                }
+            }
+            set_comp(tile.v[r][e], h, pred);
+        }
+        __syncthreads();
+        store_tile(tile, win, slot0, nslots, N, e0, te);
+        __syncthreads();
+    }
+    if (active) {
+        if (bad) dev_fail(status, QZS_RAW_UNDER, slot_chunk ? slot_chunk[s] : s);
+        else if (h == 1 && raw_i != raw_count) dev_fail(status, QZS_RAW_UNUSED, slot_chunk ? slot_chunk[s] : s);
+    }
+}
+
+// Lossless decode (codec.cpp:251-263): 8 byte-plane cursors per half.
+__global__ void __launch_bounds__(2 * kSlotsPerCta) k_dec_lossless(
+    const uint8_t *__restrict__ arena, const DecIdx *__restrict__ idx, uint64_t nslots,
+    CodecGeom g, double2 *__restrict__ win) {
+    __shared__ TileSmem tile;
+    const uint32_t r = threadIdx.x >> 1, h = threadIdx.x & 1;
+    const uint64_t slot0 = uint64_t(blockIdx.x) * kSlotsPerCta, s = slot0 + r;
+    const bool active = s < nslots && idx[min(s, nslots - 1)].len != 0;
+    const DecIdx *d = &idx[min(s, nslots - 1)];
+    const uint8_t *p = arena + d->base;
+    Cursor cur[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        cur[k] = Cursor{0, 0, 0};
+        if (active) cur_init(cur[k], p, d->pos[k][h], d->skip[k][h]);
+    }
+    const uint64_t N = g.N;
+    const uint32_t te = uint32_t(umin64(kTileElems, N));
+    for (uint64_t e0 = 0; e0 < N; e0 += te) {
+        for (uint32_t e = 0; e < te; ++e) {
+            uint64_t bits = 0;
+            if (active) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) bits |= uint64_t(cur_next(cur[k], p)) << (8 * k);
+            }
+            set_comp(tile.v[r][e], h, __longlong_as_double((long long)bits));
+        }
+        __syncthreads();
+        store_tile(tile, win, slot0, nslots, N, e0, te);
+        __syncthreads();
+    }
+}
+
+// ----------------------------------------------------------------- encode --
+
+// One RLE sub-stream of one half, written to scratch 8 bytes at a time.
+struct Rle {
+    uint8_t *out;
+    uint64_t word;
+    uint32_t nb, written, npairs;
+    uint32_t cur, cnt;   // open run
+    uint32_t hold;       // imaginary half: first run not emitted yet
+    uint32_t head_byte, head_len;
+};
+
+__device__ __forceinline__ void rle_init(Rle &s, uint8_t *out, uint32_t hold) {
+    s.out = out;
+    s.word = 0;
+    s.nb = s.written = s.npairs = 0;
+    s.cur = 0x100;
+    s.cnt = 0;
+    s.hold = hold;
+    s.head_byte = 0;
+    s.head_len = 0;
+}
+
+__device__ __forceinline__ void rle_emit(Rle &s, uint32_t b, uint32_t run) {
+    s.word |= uint64_t(b | (run << 8)) << (8 * s.nb);
+    s.nb += 2;
+    ++s.npairs;
+    if (s.nb == 8) {
+        *reinterpret_cast<uint64_t *>(s.out + s.written) = s.word;
+        s.written += 8;
+        s.word = 0;
+        s.nb = 0;
+    }
+}
+
+// rle_encode (codec.cpp:52-63) restated as a streaming state machine.
+__device__ __forceinline__ void rle_push(Rle &s, uint32_t x) {
+    if (x == s.cur) {
+        ++s.cnt;
+        if (!s.hold && s.cnt == 255) {
+            rle_emit(s, s.cur, 255);
+            s.cnt = 0;
+        }
+    } else {
+        if (s.cur != 0x100) {
+            if (s.hold) {
+                s.head_byte = s.cur;
+                s.head_len = s.cnt;
+                s.hold = 0;
+            } else if (s.cnt > 0) {
+                rle_emit(s, s.cur, s.cnt);
+            }
+        }
+        s.cur = x;
+        s.cnt = 1;
+    }
+}
+
+// Close a half: real half keeps (cur, cnt) as its open tail; imaginary half
+// emits its last run (or, if still holding, reports the whole half as head).
+__device__ __forceinline__ void rle_finish(Rle &s, uint32_t h, EncHalf &m, int k) {
+    if (h == 0) {
+        m.edge_byte[k] = uint8_t(s.cur);
+        m.edge_len[k] = s.cnt;
+    } else {
+        if (s.hold) {
+            s.head_byte = s.cur;
+            s.head_len = s.cnt;
+        } else if (s.cnt > 0) {
+            rle_emit(s, s.cur, s.cnt);
+        }
+        m.edge_byte[k] = uint8_t(s.head_byte);
+        m.edge_len[k] = s.head_len;
+    }
+    if (s.nb) *reinterpret_cast<uint64_t *>(s.out + s.written) = s.word;
+    m.npairs[k] = s.npairs;
+}
+
+__device__ __forceinline__ uint8_t *scratch_half(uint8_t *scratch, const CodecGeom &g,
+                                                 uint64_t slot, uint32_t h) {
+    return scratch + (2 * slot + h) * g.half_stride;
+}
+
+// Lossy encode (codec.cpp:121-168): thread = (slot, half).
+__global__ void __launch_bounds__(2 * kSlotsPerCta) k_enc_lossy(
+    const double2 *__restrict__ win, uint64_t nslots, CodecGeom g,
+    const uint64_t *__restrict__ forced, uint32_t nforced, uint8_t *__restrict__ scratch,
+    EncHalf *__restrict__ meta) {
+    __shared__ TileSmem tile;
+    const uint32_t r = threadIdx.x >> 1, h = threadIdx.x & 1;
+    const uint64_t slot0 = uint64_t(blockIdx.x) * kSlotsPerCta, s = slot0 + r;
+    const bool active = s < nslots;
+    const uint64_t N = g.N;
+    uint8_t *base = scratch_half(scratch, g, active ? s : 0, h);
+    Rle lo, hi;
+    rle_init(lo, base, h);
+    rle_init(hi, base + g.scap, h);
+    double *raws = reinterpret_cast<double *>(base + 2 * g.scap);
+    uint32_t nraw = 0;
+    // forced raw cursor (sorted flat indices, codec.cpp:124-129)
+    uint32_t fc = 0;
+    while (fc < nforced && forced[fc] < h * N) ++fc;
+    uint64_t next_forced = fc < nforced ? forced[fc] : ~uint64_t(0);
+    const double eb = g.eb, twoeb = g.twoeb;
+    double pred = 0.0;
+    const uint32_t te = uint32_t(umin64(kTileElems, N));
+    for (uint64_t e0 = 0; e0 < N; e0 += te) {
+        __syncthreads();
+        load_tile(tile, win, slot0, nslots, N, e0, te);
+        __syncthreads();
+        if (!active) continue;
+        for (uint32_t e = 0; e < te; ++e) {
+            const double v = comp(tile.v[r][e], h);
+            const uint64_t flat = h * N + e0 + e;
+            bool raw = false;
+            int32_t code = 0;
+            if (flat == next_forced) {
+                raw = true;
+                do { ++fc; } while (fc < nforced && forced[fc] == flat);
+                next_forced = fc < nforced ? forced[fc] : ~uint64_t(0);
+            } else {
+                const double q = round(__ddiv_rn(__dsub_rn(v, pred), twoeb));
+                if (!(fabs(q) < 32768.0)) {
+                    raw = true;
+                } else {
+                    code = int32_t(q);
+                    const double rec = __dadd_rn(pred, __dmul_rn(__dmul_rn(double(code), 2.0), eb));
+                    if (!(fabs(__dsub_rn(rec, v)) <= eb)) raw = true;
+                    else pred = rec;
+                }
+            }
+            uint32_t z;
+            if (raw) {
+                raws[nraw++] = v;
+                pred = v;
+                z = 0xFFFFu;
+            } else {
+                z = zigzag16(code);
+            }
+            rle_push(lo, z & 0xff);
+            rle_push(hi, z >> 8);
+        }
+    }
+    if (active) {
+        EncHalf &m = meta[2 * s + h];
+        rle_finish(lo, h, m, 0);
+        rle_finish(hi, h, m, 1);
+        m.nraw = nraw;
+    }
+}
+
+// Lossless encode (codec.cpp:169-181): thread = (slot, half, byte plane).
+constexpr int kLLSlots = 16;
+__global__ void __launch_bounds__(16 * kLLSlots) k_enc_lossless(
+    const double2 *__restrict__ win, uint64_t nslots, CodecGeom g,
+    uint8_t *__restrict__ scratch, EncHalf *__restrict__ meta) {
+    __shared__ double2 tile[kLLSlots][kTileElems + 1];
+    const uint32_t r = threadIdx.x >> 4, h = (threadIdx.x >> 3) & 1, k = threadIdx.x & 7;
+    const uint64_t slot0 = uint64_t(blockIdx.x) * kLLSlots, s = slot0 + r;
+    const bool active = s < nslots;
+    const uint64_t N = g.N;
+    Rle st;
+    rle_init(st, scratch_half(scratch, g, active ? s : 0, h) + k * g.scap, h);
+    const uint32_t te = uint32_t(umin64(kTileElems, N));
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (uint64_t e0 = 0; e0 < N; e0 += te) {
+        __syncthreads();
+        for (uint32_t rr = warp; rr < kLLSlots; rr += nw)
+            if (slot0 + rr < nslots && lane < te)
+                tile[rr][lane] = __ldcs(win + (slot0 + rr) * N + e0 + lane);
+        __syncthreads();
+        if (!active) continue;
+        for (uint32_t e = 0; e < te; ++e) {
+            const uint64_t bits = (uint64_t)__double_as_longlong(comp(tile[r][e], h));
+            rle_push(st, uint32_t(bits >> (8 * k)) & 0xff);
+        }
+    }
+    if (active) {
+        EncHalf &m = meta[2 * s + h];
+        rle_finish(st, h, m, k);
+        if (k == 0) m.nraw = 0;
+    }
+}
+
+// Pairs produced where the real half's open tail meets the imaginary half's
+// held head (same split-at-255 phase as rle_encode over the joined plane).
+__host__ __device__ __forceinline__ uint32_t boundary_pairs(uint32_t tb, uint32_t tc, uint32_t hb,
+                                                            uint32_t hl) {
+    if (tc > 0 && tb == hb) {
+        const uint32_t t = tc + hl;
+        return t / 255 + (t % 255 != 0);
+    }
+    return (tc > 0) + hl / 255 + (hl % 255 != 0);
+}
+
+__device__ __forceinline__ void boundary_pair(uint32_t i, uint32_t tb, uint32_t tc, uint32_t hb,
+                                              uint32_t hl, uint32_t &b, uint32_t &run) {
+    if (tc > 0 && tb == hb) {
+        const uint32_t t = tc + hl, full = t / 255;
+        b = hb;
+        run = i < full ? 255 : t % 255;
+        return;
+    }
+    if (tc > 0) {
+        if (i == 0) { b = tb; run = tc; return; }
+        --i;
+    }
+    b = hb;
+    run = i < hl / 255 ? 255 : hl % 255;
+}
+
+__global__ void k_enc_sizes(const EncHalf *__restrict__ meta, uint64_t nslots, CodecGeom g,
+                            uint64_t *__restrict__ sizes) {
+    const uint64_t s = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (s >= nslots) return;
+    const EncHalf &a = meta[2 * s], &b = meta[2 * s + 1];
+    uint64_t size = kHdr;
+    for (uint32_t k = 0; k < g.planes; ++k)
+        size += 2ull * (a.npairs[k] + b.npairs[k] +
+                        boundary_pairs(a.edge_byte[k], a.edge_len[k], b.edge_byte[k], b.edge_len[k]));
+    if (g.lossy) size += 8ull * (a.nraw + b.nraw);
+    sizes[s] = size;
+}
+
+__global__ void k_arena_alloc(const uint64_t *rel_off, const uint64_t *sizes, uint64_t nslots,
+                              uint64_t *used, uint64_t capacity, uint64_t *base_out,
+                              DevStatus *status) {
+    const uint64_t total = rel_off[nslots - 1] + sizes[nslots - 1];
+    const uint64_t base = *used;
+    if (base + total > capacity) {
+        dev_fail(status, QZS_ARENA, base + total);
+        *base_out = 0;
+        return;
+    }
+    *used = base + total;
+    *base_out = base;
+}
+
+__device__ __forceinline__ void warp_copy(uint8_t *dst, const uint8_t *src, uint64_t n,
+                                          uint32_t lane) {
+    for (uint64_t i = lane; i < n; i += 32) dst[i] = src[i];
+}
+
+// Warp per slot: header, merged planes, raws (codec.cpp:115-168).
+__global__ void __launch_bounds__(256) k_assemble(
+    const uint8_t *__restrict__ scratch, const EncHalf *__restrict__ meta,
+    const uint64_t *__restrict__ rel_off, const uint64_t *__restrict__ sizes,
+    const uint64_t *__restrict__ base_p, const uint64_t *__restrict__ slot_chunk, uint64_t nslots,
+    CodecGeom g, uint8_t *__restrict__ arena, ChunkTable table, const DevStatus *status) {
+    if (status->code == QZS_ARENA) return;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    const uint64_t base = *base_p;
+    for (uint64_t s = warp; s < nslots; s += nwarps) {
+        const EncHalf &a = meta[2 * s], &b = meta[2 * s + 1];
+        uint8_t *dst = arena + base + rel_off[s];
+        if (lane == 0) {
+            dst[0] = g.lossy ? 1 : 2;
+            st_u64(dst + 1, (uint64_t)__double_as_longlong(g.eb));
+            st_u32(dst + 9, uint32_t(g.N));
+            st_u32(dst + 13, g.lossy ? a.nraw + b.nraw : 0);
+        }
+        uint64_t pos = kHdr;
+        const uint8_t *ha = scratch + (2 * s) * g.half_stride;
+        const uint8_t *hb = ha + g.half_stride;
+        for (uint32_t k = 0; k < g.planes; ++k) {
+            warp_copy(dst + pos, ha + k * g.scap, 2ull * a.npairs[k], lane);
+            pos += 2ull * a.npairs[k];
+            const uint32_t tb = a.edge_byte[k], tc = a.edge_len[k];
+            const uint32_t hbyte = b.edge_byte[k], hl = b.edge_len[k];
+            const uint32_t nb = boundary_pairs(tb, tc, hbyte, hl);
+            for (uint32_t i = lane; i < nb; i += 32) {
+                uint32_t byte, run;
+                boundary_pair(i, tb, tc, hbyte, hl, byte, run);
+                dst[pos + 2 * i] = uint8_t(byte);
+                dst[pos + 2 * i + 1] = uint8_t(run);
+            }
+            pos += 2ull * nb;
+            warp_copy(dst + pos, hb + k * g.scap, 2ull * b.npairs[k], lane);
+            pos += 2ull * b.npairs[k];
+        }
+        if (g.lossy) {
+            warp_copy(dst + pos, ha + 2 * g.scap, 8ull * a.nraw, lane);
+            pos += 8ull * a.nraw;
+            warp_copy(dst + pos, hb + 2 * g.scap, 8ull * b.nraw, lane);
+        }
+        if (lane == 0) {
+            const uint64_t chunk = slot_chunk ? slot_chunk[s] : s;
+            table.off[chunk] = base + rel_off[s];
+            table.len[chunk] = uint32_t(sizes[s]);
+        }
+    }
+}
+
+__global__ void k_slot_chunks(uint64_t *out, uint64_t nslots, uint64_t first_batch,
+                              uint32_t log_members, uint64_t free_mask, uint64_t member_mask) {
+    const uint64_t s = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (s >= nslots) return;
+    const uint64_t b = first_batch + (s >> log_members);
+    const uint64_t j = s & ((uint64_t(1) << log_members) - 1);
+    out[s] = deposit_bits(b, free_mask) | deposit_bits(j, member_mask);
+}
+
+unsigned grid_for(uint64_t n, unsigned threads) { return (unsigned)ceil_div(n, threads); }
+
+} // namespace
+
+// ------------------------------------------------------------------ host --
+
+uint64_t payload_bound(uint64_t N, double eb) {
+    // lossy: 2 planes x 2N pairs x 2 B + 2N raws x 8 B; lossless: 8 x 4N
+    return kHdr + (eb > 0.0 ? 24 * N : 32 * N);
+}
+
+CodecGeom make_geom(uint64_t N, double eb) {
+    CodecGeom g;
+    g.N = N;
+    g.lossy = eb > 0.0;
+    g.planes = g.lossy ? 2 : 8;
+    g.eb = eb;
+    g.twoeb = 2.0 * eb;
+    g.scap = round_up(2 * N, 8);
+    g.half_stride = round_up(g.lossy ? 2 * g.scap + 8 * N : 8 * g.scap, 16);
+    return g;
+}
+
+void init_codec_tables(CodecTables &t) {
+    uint32_t T[8][256];
+    for (uint32_t i = 0; i < 256; ++i) {
+        uint32_t c = i;
+        for (int k = 0; k < 8; ++k) c = (c & 1) ? kPoly ^ (c >> 1) : c >> 1;
+        T[0][i] = c;
+    }
+    for (uint32_t i = 0; i < 256; ++i)
+        for (int k = 1; k < 8; ++k) T[k][i] = (T[k - 1][i] >> 8) ^ T[0][T[k - 1][i] & 0xff];
+    QZ_CUDA(cudaMalloc(&t.crc8, sizeof T));
+    QZ_CUDA(cudaMemcpy(t.crc8, T, sizeof T, cudaMemcpyHostToDevice));
+}
+
+void free_codec_tables(CodecTables &t) {
+    if (t.crc8) cudaFree(t.crc8);
+    t.crc8 = nullptr;
+}
+
+void launch_slot_chunks(uint64_t *slot_chunk, uint64_t nslots, uint64_t first_batch,
+                        uint32_t log_members, uint64_t free_mask, uint64_t member_mask,
+                        cudaStream_t s) {
+    k_slot_chunks<<<grid_for(nslots, 256), 256, 0, s>>>(slot_chunk, nslots, first_batch,
+                                                         log_members, free_mask, member_mask);
+    QZ_CHECK_LAUNCH();
+}
+
+void launch_crc(const CodecTables &tabs, const uint8_t *arena, ChunkTable table,
+                const uint64_t *slot_chunk, uint64_t nslots, bool verify, DevStatus *status,
+                cudaStream_t s) {
+    const unsigned grid = (unsigned)std::min<uint64_t>(ceil_div(nslots, 8), kNumSMs * 64);
+    k_crc<<<grid, 256, 0, s>>>(tabs.crc8, arena, table, slot_chunk, nslots, verify ? 1 : 0, status);
+    QZ_CHECK_LAUNCH();
+}
+
+void launch_dec_index(const uint8_t *arena, ChunkTable table, const uint64_t *slot_chunk,
+                      uint64_t nslots, const CodecGeom &g, DecIdx *idx, DevStatus *status,
+                      cudaStream_t s) {
+    k_dec_index<<<grid_for(nslots, 64), 64, 0, s>>>(arena, table, slot_chunk, nslots, g, idx,
+                                                    status);
+    QZ_CHECK_LAUNCH();
+}
+
+void launch_decode(const uint8_t *arena, const DecIdx *idx, const uint64_t *slot_chunk,
+                   uint64_t nslots, const CodecGeom &g, double2 *win, DevStatus *status,
+                   cudaStream_t s) {
+    const unsigned grid = grid_for(nslots, kSlotsPerCta);
+    if (g.lossy)
+        k_dec_lossy<<<grid, 2 * kSlotsPerCta, 0, s>>>(arena, idx, slot_chunk, nslots, g, win,
+                                                       status);
+    else
+        k_dec_lossless<<<grid, 2 * kSlotsPerCta, 0, s>>>(arena, idx, nslots, g, win);
+    QZ_CHECK_LAUNCH();
+}
+
+void launch_encode(const double2 *win, uint64_t nslots, const CodecGeom &g,
+                   const uint64_t *forced, uint32_t nforced, uint8_t *scratch, EncHalf *meta,
+                   cudaStream_t s) {
+    if (g.lossy)
+        k_enc_lossy<<<grid_for(nslots, kSlotsPerCta), 2 * kSlotsPerCta, 0, s>>>(
+            win, nslots, g, forced, nforced, scratch, meta);
+    else
+        k_enc_lossless<<<grid_for(nslots, kLLSlots), 16 * kLLSlots, 0, s>>>(win, nslots, g,
+                                                                           scratch, meta);
+    QZ_CHECK_LAUNCH();
+}
+
+void launch_enc_sizes(const EncHalf *meta, uint64_t nslots, const CodecGeom &g, uint64_t *sizes,
+                      cudaStream_t s) {
+    k_enc_sizes<<<grid_for(nslots, 256), 256, 0, s>>>(meta, nslots, g, sizes);
+    QZ_CHECK_LAUNCH();
+}
+
+void launch_arena_alloc(const uint64_t *rel_off, const uint64_t *sizes, uint64_t nslots,
+                        uint64_t *used, uint64_t capacity, uint64_t *base_out,
+                        DevStatus *status, cudaStream_t s) {
+    k_arena_alloc<<<1, 1, 0, s>>>(rel_off, sizes, nslots, used, capacity, base_out, status);
+    QZ_CHECK_LAUNCH();
+}
+
+void launch_assemble(const uint8_t *scratch, const EncHalf *meta, const uint64_t *rel_off,
+                     const uint64_t *sizes, const uint64_t *base, const uint64_t *slot_chunk,
+                     uint64_t nslots, const CodecGeom &g, uint8_t *arena, ChunkTable table,
+                     const DevStatus *status, cudaStream_t s) {
+    const unsigned grid = (unsigned)std::min<uint64_t>(ceil_div(nslots, 8), kNumSMs * 64);
+    k_assemble<<<grid, 256, 0, s>>>(scratch, meta, rel_off, sizes, base, slot_chunk, nslots, g,
+                                    arena, table, status);
+    QZ_CHECK_LAUNCH();
+}
+
+uint32_t crc32_host(const uint8_t *p, uint64_t n) {
+    static uint32_t T[256];
+    static bool ready = false;
+    if (!ready) {
+        for (uint32_t i = 0; i < 256; ++i) {
+            uint32_t c = i;
+            for (int k = 0; k < 8; ++k) c = (c & 1) ? kPoly ^ (c >> 1) : c >> 1;
+            T[i] = c;
+        }
+        ready = true;
+    }
+    uint32_t c = 0xFFFFFFFFu;
+    for (uint64_t i = 0; i < n; ++i) c = T[(c ^ p[i]) & 0xff] ^ (c >> 8);
+    return c ^ 0xFFFFFFFFu;
+}
+
+uint64_t fnv1a64_host(const uint8_t *p, uint64_t n, uint64_t state) {
+    for (uint64_t i = 0; i < n; ++i) {
+        state ^= p[i];
+        state *= 0x100000001b3ULL;
+    }
+    return state;
+}
+
+} // namespace qz

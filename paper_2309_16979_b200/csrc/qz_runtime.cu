@@ -1,0 +1,1021 @@
+// qz_runtime.cu — context, HBM-resident compressed store, stage pipeline and
+// the C ABI (include/qzcuda.h).
+//
+// Replaces qzsim::run (pipeline.cpp:128-314) + ChunkStore (store.cpp:26-217)
+// + ReferenceDevice (device.cpp:98-503) for the hot path.  Per stage, the
+// store is swept window by window: every chunk of the window's batches is
+// CRC-verified and decoded straight into its batch slot, the stage's fused
+// gate passes run over the whole window (batches stacked along the high
+// buffer bits, which no gate touches), and every chunk is re-encoded into the
+// other arena.  One codec round trip per chunk per stage, as the reference
+// (SPEC.md:367), so payload bytes and the FNV digest match it exactly.
+#include <cub/device/device_reduce.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "qz_codec.cuh"
+#include "qz_gates.cuh"
+#include "qz_plan.cuh"
+
+using namespace qz;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+constexpr uint32_t kTileBits = 12;           // fused-pass tile: 2^12 amplitudes (64 KB smem)
+constexpr uint64_t kPerChunkOverhead = 48;   // ChunkStore::kPerChunkOverhead (store.hpp:48)
+
+// Grow-only device buffer.
+struct DevBuf {
+    void *p = nullptr;
+    size_t cap = 0;
+    void ensure(size_t bytes) {
+        if (bytes <= cap) return;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        QZ_CUDA(cudaMalloc(&p, bytes ? bytes : 1));
+        cap = bytes;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+    template <class T> T *as() const { return static_cast<T *>(p); }
+};
+
+const char *status_text(int code) {
+    switch (code) {
+    case QZS_CRC: return "checksum mismatch on chunk ";
+    case QZS_HEADER: return "malformed payload: bad header on chunk ";
+    case QZS_RLE_TRUNC: return "malformed payload: truncated RLE stream on chunk ";
+    case QZS_RLE_RUN: return "malformed payload: bad RLE run length on chunk ";
+    case QZS_RAW_MISSING: return "malformed payload: missing raw values on chunk ";
+    case QZS_RAW_UNDER: return "malformed payload: raw value underflow on chunk ";
+    case QZS_RAW_UNUSED: return "malformed payload: unused raw values on chunk ";
+    case QZS_ARENA: return "compressed arena capacity exhausted, needed bytes ";
+    default: return "device error ";
+    }
+}
+
+// Scratch set for one window of codec work.
+struct Window {
+    DevBuf amps, scratch, meta, idx, slot_chunk, sizes, reloff, base, cub, delta, maxd;
+    uint64_t slots = 0;
+    void reserve(const CodecGeom &g, uint64_t nslots) {
+        amps.ensure(sizeof(double2) * nslots * g.N);
+        scratch.ensure(2 * nslots * g.half_stride);
+        meta.ensure(sizeof(EncHalf) * 2 * nslots);
+        idx.ensure(sizeof(DecIdx) * nslots);
+        slot_chunk.ensure(sizeof(uint64_t) * nslots);
+        sizes.ensure(sizeof(uint64_t) * nslots);
+        reloff.ensure(sizeof(uint64_t) * nslots);
+        delta.ensure(sizeof(int64_t) * nslots);
+        base.ensure(sizeof(uint64_t) * 2);
+        maxd.ensure(sizeof(int64_t) * 2);
+        size_t t1 = 0, t2 = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, t1, (uint64_t *)nullptr, (uint64_t *)nullptr,
+                                      (int)std::min<uint64_t>(nslots, INT32_MAX));
+        cub::DeviceScan::InclusiveSum(nullptr, t2, (int64_t *)nullptr, (int64_t *)nullptr,
+                                      (int)std::min<uint64_t>(nslots, INT32_MAX));
+        size_t t3 = 0;
+        cub::DeviceReduce::Max(nullptr, t3, (int64_t *)nullptr, (int64_t *)nullptr,
+                               (int)std::min<uint64_t>(nslots, INT32_MAX));
+        cub.ensure(std::max({t1, t2, t3}) + 256);
+        slots = std::max(slots, nslots);
+    }
+    void release() {
+        for (DevBuf *b : {&amps, &scratch, &meta, &idx, &slot_chunk, &sizes, &reloff, &base, &cub,
+                          &delta, &maxd})
+            b->release();
+    }
+};
+
+// ---- accounting kernels ---------------------------------------------------
+// delta[s] = new_size[s] - old_len[chunk(s)]  (ChunkStore::account_store order)
+__global__ void k_delta(const uint64_t *sizes, const uint64_t *slot_chunk, const uint32_t *old_len,
+                        uint64_t nslots, int64_t *delta) {
+    const uint64_t s = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (s < nslots) delta[s] = int64_t(sizes[s]) - int64_t(old_len[slot_chunk ? slot_chunk[s] : s]);
+}
+// acct[0] = current bytes, acct[1] = peak; prefix = inclusive scan of delta
+__global__ void k_account(int64_t *acct, const int64_t *prefix, const int64_t *maxp,
+                          uint64_t nslots) {
+    const int64_t cur = acct[0];
+    const int64_t peak_cand = cur + *maxp;
+    if (peak_cand > acct[1]) acct[1] = peak_cand;
+    acct[0] = cur + prefix[nslots - 1];
+}
+
+__global__ void k_fill_init(ChunkTable t, uint64_t nchunks, uint64_t zoff, uint32_t zlen,
+                            uint32_t zcrc, uint64_t boff, uint32_t blen, uint32_t bcrc) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= nchunks) return;
+    t.off[i] = i ? zoff : boff;
+    t.len[i] = i ? zlen : blen;
+    t.crc[i] = i ? zcrc : bcrc;
+}
+
+// per-slot compensated partial sums: out[4s..4s+3] = Re<a|b>, Im<a|b>, |a|^2, |b|^2
+// (b = the store, a = dense reference or null for the norm)
+__global__ void k_partials(const double2 *win, uint64_t nslots, uint64_t N, const double2 *dense,
+                           uint64_t dense_first, double *out) {
+    const uint64_t s = uint64_t(blockIdx.x) * blockDim.y + threadIdx.y;
+    if (s >= nslots) return;
+    double acc[4] = {0, 0, 0, 0}, cmp[4] = {0, 0, 0, 0};
+    auto kadd = [&](int i, double x) {
+        const double y = x - cmp[i], t = acc[i] + y;
+        cmp[i] = (t - acc[i]) - y;
+        acc[i] = t;
+    };
+    // Each warp lane takes a strided subset, then the lanes are combined in
+    // lane order (deterministic).
+    const uint32_t lane = threadIdx.x;
+    for (uint64_t j = lane; j < N; j += 32) {
+        const double2 b = win[s * N + j];
+        kadd(3, __dadd_rn(__dmul_rn(b.x, b.x), __dmul_rn(b.y, b.y)));
+        if (dense) {
+            const double2 a = dense[(dense_first + s) * N + j];
+            // conj(a) * b
+            kadd(0, __dadd_rn(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y)));
+            kadd(1, __dsub_rn(__dmul_rn(a.x, b.y), __dmul_rn(a.y, b.x)));
+            kadd(2, __dadd_rn(__dmul_rn(a.x, a.x), __dmul_rn(a.y, a.y)));
+        }
+    }
+    for (int i = 0; i < 4; ++i) {
+        double v = acc[i];
+        for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+        if (lane == 0) out[4 * s + i] = v;
+    }
+}
+
+__global__ void k_basis(double2 *buf, uint64_t n) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) buf[i] = make_double2(i == 0 ? 1.0 : 0.0, 0.0);
+}
+
+struct Kahan {
+    double s = 0, c = 0;
+    void add(double x) {
+        const double y = x - c, t = s + y;
+        c = (t - s) - y;
+        s = t;
+    }
+};
+
+double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+} // namespace
+
+// ============================================================== context ====
+
+struct qzc_context {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    uint64_t budget = 0;
+    CodecTables tabs;
+    DevStatus *status = nullptr;      // device
+    DevStatus *status_host = nullptr; // pinned
+    uint64_t launches = 0;
+    Window win;                       // scratch for the host codec / gate entry points
+    DevBuf arena, table_off, table_len, table_crc, forced, used;
+    std::mutex mu;
+
+    void check_status(uint64_t index_base = 0) {
+        QZ_CUDA(cudaMemcpyAsync(status_host, status, sizeof(DevStatus), cudaMemcpyDeviceToHost, stream));
+        QZ_CUDA(cudaStreamSynchronize(stream));
+        if (status_host->code != 0) {
+            const int code = status_host->code;
+            const uint64_t idx = status_host->index;
+            QZ_CUDA(cudaMemsetAsync(status, 0, sizeof(DevStatus), stream));
+            QZ_CUDA(cudaStreamSynchronize(stream));
+            throw Failure(code == QZS_ARENA ? QZC_ENOMEM : QZC_ECODEC,
+                          std::string(status_text(code)) + std::to_string(idx + (code == QZS_ARENA ? 0 : index_base)));
+        }
+    }
+};
+
+// ============================================================ simulator ====
+
+struct qzc_sim {
+    qzc_context *ctx = nullptr;
+    qzc_sim_config cfg{};
+    uint32_t n = 0, c = 0, m = 0;
+    double eb = 0;
+    uint64_t N = 0, nchunks = 0;
+    CodecGeom geom{};
+    DevBuf arena[2], off[2], len[2], crc[2];
+    DevBuf used;   // uint64[2] bump pointers
+    DevBuf acct;   // int64[2] current / peak
+    uint64_t arena_cap = 0;
+    int cur = 0;
+    uint64_t win_amps = 0;
+    Window win;
+    qzc_sim_stats stats{};
+    bool initialized = false;
+    std::vector<cudaEvent_t> events;
+
+    ChunkTable table(int i) {
+        return ChunkTable{off[i].as<uint64_t>(), len[i].as<uint32_t>(), crc[i].as<uint32_t>()};
+    }
+    cudaStream_t st() const { return ctx->stream; }
+    uint64_t *used_ptr(int i) { return used.as<uint64_t>() + i; }
+};
+
+namespace {
+
+// Encode win slots [0, nslots) into arena `a` / table `t` via slot_chunk map.
+void encode_window(qzc_context *ctx, Window &w, const CodecGeom &g, uint64_t nslots,
+                   const uint64_t *slot_chunk, const uint64_t *forced, uint32_t nforced,
+                   uint8_t *arena, uint64_t *used, uint64_t cap, ChunkTable t,
+                   const uint32_t *old_len, int64_t *acct, uint64_t &launches) {
+    cudaStream_t s = ctx->stream;
+    launch_encode(w.amps.as<double2>(), nslots, g, forced, nforced, w.scratch.as<uint8_t>(),
+                  w.meta.as<EncHalf>(), s);
+    launch_enc_sizes(w.meta.as<EncHalf>(), nslots, g, w.sizes.as<uint64_t>(), s);
+    size_t tb = w.cub.cap;
+    QZ_CUDA(cub::DeviceScan::ExclusiveSum(w.cub.p, tb, w.sizes.as<uint64_t>(), w.reloff.as<uint64_t>(),
+                                          (int)nslots, s));
+    launch_arena_alloc(w.reloff.as<uint64_t>(), w.sizes.as<uint64_t>(), nslots, used, cap,
+                       w.base.as<uint64_t>(), ctx->status, s);
+    if (acct && old_len) {
+        k_delta<<<(unsigned)ceil_div(nslots, 256), 256, 0, s>>>(w.sizes.as<uint64_t>(), slot_chunk,
+                                                                old_len, nslots, w.delta.as<int64_t>());
+        QZ_CHECK_LAUNCH();
+        tb = w.cub.cap;
+        QZ_CUDA(cub::DeviceScan::InclusiveSum(w.cub.p, tb, w.delta.as<int64_t>(),
+                                              w.delta.as<int64_t>(), (int)nslots, s));
+        tb = w.cub.cap;
+        QZ_CUDA(cub::DeviceReduce::Max(w.cub.p, tb, w.delta.as<int64_t>(), w.maxd.as<int64_t>(),
+                                       (int)nslots, s));
+        k_account<<<1, 1, 0, s>>>(acct, w.delta.as<int64_t>(), w.maxd.as<int64_t>(), nslots);
+        QZ_CHECK_LAUNCH();
+        launches += 5;
+    }
+    launch_assemble(w.scratch.as<uint8_t>(), w.meta.as<EncHalf>(), w.reloff.as<uint64_t>(),
+                    w.sizes.as<uint64_t>(), w.base.as<uint64_t>(), slot_chunk, nslots, g, arena, t,
+                    ctx->status, s);
+    launch_crc(ctx->tabs, arena, t, slot_chunk, nslots, false, ctx->status, s);
+    launches += 6;
+}
+
+void decode_window(qzc_context *ctx, Window &w, const CodecGeom &g, uint64_t nslots,
+                   const uint64_t *slot_chunk, const uint8_t *arena, ChunkTable t,
+                   uint64_t &launches) {
+    cudaStream_t s = ctx->stream;
+    launch_crc(ctx->tabs, arena, t, slot_chunk, nslots, true, ctx->status, s);
+    launch_dec_index(arena, t, slot_chunk, nslots, g, w.idx.as<DecIdx>(), ctx->status, s);
+    launch_decode(arena, w.idx.as<DecIdx>(), slot_chunk, nslots, g, w.amps.as<double2>(),
+                  ctx->status, s);
+    launches += 3;
+}
+
+uint32_t log2u(uint64_t x) {
+    uint32_t r = 0;
+    while ((uint64_t(1) << r) < x) ++r;
+    return r;
+}
+
+void sim_alloc(qzc_sim *sim) {
+    qzc_context *ctx = sim->ctx;
+    const uint64_t tbl_entries = std::max<uint64_t>(sim->nchunks, 2);
+    for (int i = 0; i < 2; ++i) {
+        sim->off[i].ensure(8 * tbl_entries);
+        sim->len[i].ensure(4 * tbl_entries);
+        sim->crc[i].ensure(4 * tbl_entries);
+        QZ_CUDA(cudaMemset(sim->len[i].p, 0, 4 * tbl_entries));
+    }
+    sim->used.ensure(16);
+    sim->acct.ensure(16);
+    QZ_CUDA(cudaMemset(sim->used.p, 0, 16));
+    QZ_CUDA(cudaMemset(sim->acct.p, 0, 16));
+
+    // window: whole batches, power of two, bounded by the HBM budget
+    size_t free_b = 0, total_b = 0;
+    QZ_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    uint64_t budget = ctx->budget ? std::min<uint64_t>(ctx->budget, free_b) : free_b;
+    budget = budget > (uint64_t(3) << 30) ? budget - (uint64_t(3) << 30) : budget / 2;
+    const uint64_t per_amp = 16 + 2 * sim->geom.half_stride / sim->N + 8;  // dense + scratch + meta
+    const uint64_t state_amps = uint64_t(1) << sim->n;
+    uint64_t wa = sim->cfg.window_amps;
+    if (!wa) {
+        const uint64_t cap_amps = std::max<uint64_t>(budget / 2 / per_amp, sim->N);
+        wa = uint64_t(1) << (63 - __builtin_clzll(cap_amps));
+        wa = std::min(wa, state_amps);
+    }
+    if (wa & (wa - 1)) wa = uint64_t(1) << log2u(wa);
+    // at least one whole batch (2^m amplitudes) and two chunk slots
+    const uint64_t batch_amps = uint64_t(1) << std::min(sim->m, sim->n);
+    wa = std::max<uint64_t>(std::min<uint64_t>(wa, state_amps), std::max<uint64_t>(batch_amps, 2 * sim->N));
+    sim->win_amps = wa;
+    const uint64_t win_slots = std::max<uint64_t>(wa / sim->N, 2);
+    sim->win.reserve(sim->geom, win_slots);
+
+    // arenas: worst case if it fits, else what is left
+    QZ_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const uint64_t worst = tbl_entries * payload_bound(sim->N, sim->eb) + 4096;
+    uint64_t avail = free_b > (uint64_t(2) << 30) ? free_b - (uint64_t(2) << 30) : free_b / 2;
+    if (ctx->budget) {
+        const uint64_t spent = wa * per_amp;
+        avail = std::min<uint64_t>(avail, ctx->budget > spent ? ctx->budget - spent : 0);
+    }
+    sim->arena_cap = std::min<uint64_t>(worst, avail / 2);
+    if (sim->arena_cap < 4096) throw Failure(QZC_ENOMEM, "not enough HBM for the compressed store");
+    for (int i = 0; i < 2; ++i) sim->arena[i].ensure(sim->arena_cap);
+}
+
+} // namespace
+
+// ================================================================== C ABI ==
+
+#define QZ_API_BEGIN try {
+#define QZ_API_END                                                                             \
+    }                                                                                          \
+    catch (const Failure &f) {                                                                 \
+        g_last_error = f.what();                                                               \
+        return f.code;                                                                         \
+    }                                                                                          \
+    catch (const std::exception &e) {                                                          \
+        g_last_error = e.what();                                                               \
+        return QZC_EINVAL;                                                                     \
+    }                                                                                          \
+    return QZC_OK;
+
+extern "C" {
+
+const char *qzc_last_error(void) { return g_last_error.c_str(); }
+const char *qzc_version(void) { return "qzcuda 0.1 sm_100a"; }
+
+int qzc_gate_matrix(const qzc_gate *gate, double *mat_out, uint32_t *dim_out) {
+    QZ_API_BEGIN
+    if (!gate || !mat_out || !dim_out) throw Failure(QZC_EINVAL, "null argument");
+    double2 m[16];
+    gate_matrix_host(*gate, m, dim_out);
+    std::memcpy(mat_out, m, sizeof m);
+    QZ_API_END
+}
+
+uint32_t qzc_crc32(const uint8_t *bytes, uint64_t len) { return crc32_host(bytes, len); }
+uint64_t qzc_fnv1a64(const uint8_t *bytes, uint64_t len, uint64_t state) {
+    return fnv1a64_host(bytes, len, state);
+}
+uint64_t qzc_payload_bound(uint64_t elements, double error_bound) {
+    return payload_bound(elements, error_bound);
+}
+
+int qzc_context_create(int device, uint64_t hbm_budget_bytes, qzc_context **out) {
+    QZ_API_BEGIN
+    if (!out) throw Failure(QZC_EINVAL, "null out");
+    int count = 0;
+    QZ_CUDA(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count)
+        throw Failure(QZC_EDEVICE, "no CUDA device " + std::to_string(device));
+    QZ_CUDA(cudaSetDevice(device));
+    auto *ctx = new qzc_context;
+    ctx->device = device;
+    ctx->budget = hbm_budget_bytes;
+    QZ_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    init_codec_tables(ctx->tabs);
+    QZ_CUDA(cudaMalloc(&ctx->status, sizeof(DevStatus)));
+    QZ_CUDA(cudaMemset(ctx->status, 0, sizeof(DevStatus)));
+    QZ_CUDA(cudaMallocHost(&ctx->status_host, sizeof(DevStatus)));
+    *out = ctx;
+    QZ_API_END
+}
+
+void qzc_context_destroy(qzc_context *ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    ctx->win.release();
+    for (DevBuf *b : {&ctx->arena, &ctx->table_off, &ctx->table_len, &ctx->table_crc, &ctx->forced, &ctx->used})
+        b->release();
+    free_codec_tables(ctx->tabs);
+    cudaFree(ctx->status);
+    cudaFreeHost(ctx->status_host);
+    cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+int qzc_synchronize(qzc_context *ctx) {
+    QZ_API_BEGIN
+    QZ_CUDA(cudaStreamSynchronize(ctx->stream));
+    QZ_API_END
+}
+
+uint64_t qzc_kernel_launches(const qzc_context *ctx) { return ctx ? ctx->launches : 0; }
+
+// ---- codec entry points ----------------------------------------------------
+
+int qzc_compress_host(qzc_context *ctx, const double *amps, uint64_t count, uint64_t elements,
+                      double error_bound, const uint64_t *forced_raw, uint64_t n_forced,
+                      uint8_t *payload_out, uint64_t payload_cap, uint64_t *offsets,
+                      uint32_t *sizes, uint32_t *crcs) {
+    QZ_API_BEGIN
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    QZ_CUDA(cudaSetDevice(ctx->device));
+    if (elements == 0 || (elements & (elements - 1)))
+        throw Failure(QZC_ECODEC, "chunk length must be a power of two, got " + std::to_string(elements));
+    if (!(error_bound >= 0.0) || !std::isfinite(error_bound))
+        throw Failure(QZC_ECODEC, "error bound must be finite and non-negative");
+    if (count == 0) return QZC_OK;
+    const CodecGeom g = make_geom(elements, error_bound);
+    std::vector<uint64_t> fr(forced_raw, forced_raw + n_forced);
+    for (uint64_t f : fr)
+        if (f >= 2 * elements) throw Failure(QZC_ECODEC, "forced raw index out of range");
+    std::sort(fr.begin(), fr.end());
+    cudaStream_t s = ctx->stream;
+    // process in windows of at most ~1 GiB dense
+    const uint64_t per = std::max<uint64_t>(1, std::min<uint64_t>(count, (uint64_t(1) << 26) / elements));
+    ctx->win.reserve(g, per);
+    const uint64_t bound = payload_bound(elements, error_bound);
+    ctx->arena.ensure(per * bound + 64);
+    ctx->table_off.ensure(8 * per);
+    ctx->table_len.ensure(4 * per);
+    ctx->table_crc.ensure(4 * per);
+    ctx->used.ensure(8);
+    ctx->forced.ensure(8 * std::max<size_t>(fr.size(), 1));
+    if (!fr.empty())
+        QZ_CUDA(cudaMemcpyAsync(ctx->forced.p, fr.data(), 8 * fr.size(), cudaMemcpyHostToDevice, s));
+    ChunkTable t{ctx->table_off.as<uint64_t>(), ctx->table_len.as<uint32_t>(), ctx->table_crc.as<uint32_t>()};
+    std::vector<uint64_t> hoff(per);
+    std::vector<uint32_t> hlen(per), hcrc(per);
+    uint64_t written = 0;
+    for (uint64_t first = 0; first < count; first += per) {
+        const uint64_t k = std::min(per, count - first);
+        QZ_CUDA(cudaMemcpyAsync(ctx->win.amps.p, amps + 2 * first * elements, 16 * k * elements,
+                                cudaMemcpyHostToDevice, s));
+        QZ_CUDA(cudaMemsetAsync(ctx->used.p, 0, 8, s));
+        encode_window(ctx, ctx->win, g, k, nullptr, ctx->forced.as<uint64_t>(), (uint32_t)fr.size(),
+                      ctx->arena.as<uint8_t>(), ctx->used.as<uint64_t>(), ctx->arena.cap, t, nullptr,
+                      nullptr, ctx->launches);
+        ctx->check_status();
+        QZ_CUDA(cudaMemcpyAsync(hoff.data(), t.off, 8 * k, cudaMemcpyDeviceToHost, s));
+        QZ_CUDA(cudaMemcpyAsync(hlen.data(), t.len, 4 * k, cudaMemcpyDeviceToHost, s));
+        QZ_CUDA(cudaMemcpyAsync(hcrc.data(), t.crc, 4 * k, cudaMemcpyDeviceToHost, s));
+        QZ_CUDA(cudaStreamSynchronize(s));
+        uint64_t total = 0;
+        for (uint64_t i = 0; i < k; ++i) total += hlen[i];
+        if (written + total > payload_cap) throw Failure(QZC_EINVAL, "payload buffer too small");
+        // arena order == slot order (single window, identity mapping)
+        QZ_CUDA(cudaMemcpyAsync(payload_out + written, ctx->arena.p, total, cudaMemcpyDeviceToHost, s));
+        QZ_CUDA(cudaStreamSynchronize(s));
+        for (uint64_t i = 0; i < k; ++i) {
+            offsets[first + i] = written + hoff[i];
+            sizes[first + i] = hlen[i];
+            crcs[first + i] = hcrc[i];
+        }
+        written += total;
+    }
+    QZ_API_END
+}
+
+int qzc_decompress_host(qzc_context *ctx, const uint8_t *payloads, const uint64_t *offsets,
+                        const uint32_t *sizes, const uint32_t *crcs, uint64_t count,
+                        uint64_t elements, uint64_t chunk_index_base, double *amps_out) {
+    QZ_API_BEGIN
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    QZ_CUDA(cudaSetDevice(ctx->device));
+    if (elements == 0 || (elements & (elements - 1)))
+        throw Failure(QZC_ECODEC, "chunk length must be a power of two");
+    if (count == 0) return QZC_OK;
+    cudaStream_t s = ctx->stream;
+    // codec id comes from the first payload's header byte (CompressedChunk::codec_id)
+    uint64_t span = 0;
+    for (uint64_t i = 0; i < count; ++i) span = std::max<uint64_t>(span, offsets[i] + sizes[i]);
+    const uint8_t id = sizes[0] ? payloads[offsets[0]] : 2;
+    const CodecGeom g = make_geom(elements, id == 1 ? 1.0 : 0.0);
+    ctx->win.reserve(g, count);
+    ctx->arena.ensure(span + 64);
+    ctx->table_off.ensure(8 * count);
+    ctx->table_len.ensure(4 * count);
+    ctx->table_crc.ensure(4 * count);
+    QZ_CUDA(cudaMemcpyAsync(ctx->arena.p, payloads, span, cudaMemcpyHostToDevice, s));
+    QZ_CUDA(cudaMemcpyAsync(ctx->table_off.p, offsets, 8 * count, cudaMemcpyHostToDevice, s));
+    QZ_CUDA(cudaMemcpyAsync(ctx->table_len.p, sizes, 4 * count, cudaMemcpyHostToDevice, s));
+    QZ_CUDA(cudaMemcpyAsync(ctx->table_crc.p, crcs, 4 * count, cudaMemcpyHostToDevice, s));
+    ChunkTable t{ctx->table_off.as<uint64_t>(), ctx->table_len.as<uint32_t>(), ctx->table_crc.as<uint32_t>()};
+    // CRC first, exactly like codec.cpp:188 (a bad checksum must not reach the parser)
+    launch_crc(ctx->tabs, ctx->arena.as<uint8_t>(), t, nullptr, count, true, ctx->status, s);
+    ctx->check_status(chunk_index_base);
+    decode_window(ctx, ctx->win, g, count, nullptr, ctx->arena.as<uint8_t>(), t, ctx->launches);
+    ctx->check_status(chunk_index_base);
+    QZ_CUDA(cudaMemcpyAsync(amps_out, ctx->win.amps.p, 16 * count * elements, cudaMemcpyDeviceToHost, s));
+    QZ_CUDA(cudaStreamSynchronize(s));
+    QZ_API_END
+}
+
+// ---- gate entry points ------------------------------------------------------
+
+static void apply_gates_device(qzc_context *ctx, double *amps_dev, uint32_t nbits,
+                               const qzc_gate *gates, uint64_t ngates, bool fuse = true) {
+    std::vector<DevGate> dg;
+    dg.reserve(ngates);
+    for (uint64_t i = 0; i < ngates; ++i) {
+        const qzc_gate &g = gates[i];
+        if (g.kind > QZC_SWAP) throw Failure(QZC_EINVAL, "unknown gate kind");
+        if (g.nqubits != gate_arity(g.kind)) throw Failure(QZC_EINVAL, "gate arity mismatch");
+        for (uint32_t k = 0; k < g.nqubits; ++k)
+            if (g.qubits[k] >= nbits)
+                throw Failure(QZC_EDEVICE, "buffer bit " + std::to_string(g.qubits[k]) +
+                                               " out of range for batch of 2^" + std::to_string(nbits) +
+                                               " amplitudes");
+        dg.push_back(make_dev_gate(g));
+    }
+    if (dg.empty()) return;
+    GatePlan plan = build_passes(dg, nbits, kTileBits, fuse);
+    DevPlan dp;
+    upload_plan(plan, dp, ctx->stream);
+    ctx->launches += run_passes(dp, reinterpret_cast<double2 *>(amps_dev), nbits, ctx->stream);
+    QZ_CUDA(cudaStreamSynchronize(ctx->stream));
+    free_plan(dp);
+}
+
+int qzc_apply_gates_dev(qzc_context *ctx, double *amps_dev, uint32_t nbits, const qzc_gate *gates,
+                        uint64_t ngates) {
+    QZ_API_BEGIN
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    QZ_CUDA(cudaSetDevice(ctx->device));
+    apply_gates_device(ctx, amps_dev, nbits, gates, ngates);
+    QZ_API_END
+}
+
+int qzc_apply_gates_host(qzc_context *ctx, double *amps, uint32_t nbits, const qzc_gate *gates,
+                         uint64_t ngates) {
+    QZ_API_BEGIN
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    QZ_CUDA(cudaSetDevice(ctx->device));
+    const uint64_t bytes = 16ull << nbits;
+    DevBuf buf;
+    buf.ensure(bytes);
+    QZ_CUDA(cudaMemcpyAsync(buf.p, amps, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    apply_gates_device(ctx, buf.as<double>(), nbits, gates, ngates);
+    QZ_CUDA(cudaMemcpyAsync(amps, buf.p, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    QZ_CUDA(cudaStreamSynchronize(ctx->stream));
+    buf.release();
+    QZ_API_END
+}
+
+// ---- simulator -----------------------------------------------------------------
+
+int qzc_sim_create(qzc_context *ctx, const qzc_sim_config *cfg, qzc_sim **out) {
+    QZ_API_BEGIN
+    if (!ctx || !cfg || !out) throw Failure(QZC_EINVAL, "null argument");
+    QZ_CUDA(cudaSetDevice(ctx->device));
+    const uint32_t n = cfg->num_qubits, c = cfg->chunk_qubits;
+    // ChunkStore::init_basis_state geometry checks (store.cpp:29-35)
+    if (c < 1 || c > n)
+        throw Failure(QZC_ESTORE, "chunk qubits must satisfy 1 <= c <= n, got c=" + std::to_string(c) +
+                                      ", n=" + std::to_string(n));
+    if (n > 40) throw Failure(QZC_ESTORE, "qubit count exceeds configured address width (40)");
+    if (!(cfg->error_bound >= 0.0) || !std::isfinite(cfg->error_bound))
+        throw Failure(QZC_EINVAL, "error bound must be finite and non-negative");
+    if (cfg->residency != 0) throw Failure(QZC_EINVAL, "host-staged residency not built in this version");
+    auto *sim = new qzc_sim;
+    sim->ctx = ctx;
+    sim->cfg = *cfg;
+    sim->n = n;
+    sim->c = c;
+    sim->m = cfg->batch_qubits;
+    sim->eb = cfg->error_bound;
+    sim->N = uint64_t(1) << c;
+    sim->nchunks = uint64_t(1) << (n - c);
+    sim->geom = make_geom(sim->N, sim->eb);
+    try {
+        sim_alloc(sim);
+    } catch (...) {
+        delete sim;
+        throw;
+    }
+    *out = sim;
+    QZ_API_END
+}
+
+void qzc_sim_destroy(qzc_sim *sim) {
+    if (!sim) return;
+    cudaSetDevice(sim->ctx->device);
+    cudaStreamSynchronize(sim->ctx->stream);
+    for (int i = 0; i < 2; ++i)
+        for (DevBuf *b : {&sim->arena[i], &sim->off[i], &sim->len[i], &sim->crc[i]}) b->release();
+    sim->used.release();
+    sim->acct.release();
+    sim->win.release();
+    for (cudaEvent_t e : sim->events) cudaEventDestroy(e);
+    delete sim;
+}
+
+int qzc_sim_init_basis(qzc_sim *sim) {
+    QZ_API_BEGIN
+    qzc_context *ctx = sim->ctx;
+    QZ_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    Window &w = sim->win;
+    const uint64_t N = sim->N;
+    const int a = sim->cur;
+    QZ_CUDA(cudaMemsetAsync(sim->used.p, 0, 16, s));
+    // slot 0 = zero chunk, slot 1 = basis chunk (store.cpp:46-51)
+    QZ_CUDA(cudaMemsetAsync(w.amps.p, 0, 32 * N, s));
+    const double one[2] = {1.0, 0.0};
+    QZ_CUDA(cudaMemcpyAsync(w.amps.as<double2>() + N, one, 16, cudaMemcpyHostToDevice, s));
+    ChunkTable t = sim->table(a);
+    encode_window(ctx, w, sim->geom, 2, nullptr, nullptr, 0, sim->arena[a].as<uint8_t>(),
+                  sim->used_ptr(a), sim->arena_cap, t, nullptr, nullptr, ctx->launches);
+    ctx->check_status();
+    if (sim->eb > 0.0) {
+        // decode the basis chunk; route {0,1} through the raw path if the
+        // quantiser perturbed it (store.cpp:52-67)
+        uint64_t one_slot = 1;
+        DevBuf sc;
+        sc.ensure(8);
+        QZ_CUDA(cudaMemcpyAsync(sc.p, &one_slot, 8, cudaMemcpyHostToDevice, s));
+        decode_window(ctx, w, sim->geom, 1, sc.as<uint64_t>(), sim->arena[a].as<uint8_t>(), t, ctx->launches);
+        ctx->check_status();
+        std::vector<double2> r(N);
+        QZ_CUDA(cudaMemcpyAsync(r.data(), w.amps.p, 16 * N, cudaMemcpyDeviceToHost, s));
+        QZ_CUDA(cudaStreamSynchronize(s));
+        bool exact = std::fabs(r[0].x - 1.0) <= 1e-12;
+        for (uint64_t i = 0; exact && i < N; ++i)
+            if (r[i].y != 0.0 || (i > 0 && r[i].x != 0.0)) exact = false;
+        if (!exact) {
+            std::vector<uint64_t> fr{0};
+            if (N > 1) fr.push_back(1);
+            DevBuf fd;
+            fd.ensure(16);
+            QZ_CUDA(cudaMemcpyAsync(fd.p, fr.data(), 8 * fr.size(), cudaMemcpyHostToDevice, s));
+            QZ_CUDA(cudaMemsetAsync(w.amps.p, 0, 16 * N, s));
+            QZ_CUDA(cudaMemcpyAsync(w.amps.p, one, 16, cudaMemcpyHostToDevice, s));
+            encode_window(ctx, w, sim->geom, 1, sc.as<uint64_t>(), fd.as<uint64_t>(), (uint32_t)fr.size(),
+                          sim->arena[a].as<uint8_t>(), sim->used_ptr(a), sim->arena_cap, t, nullptr,
+                          nullptr, ctx->launches);
+            ctx->check_status();
+            QZ_CUDA(cudaStreamSynchronize(s));
+            fd.release();
+        }
+        QZ_CUDA(cudaStreamSynchronize(s));
+        sc.release();
+    }
+    uint64_t off2[2];
+    uint32_t len2[2], crc2[2];
+    QZ_CUDA(cudaMemcpyAsync(off2, t.off, 16, cudaMemcpyDeviceToHost, s));
+    QZ_CUDA(cudaMemcpyAsync(len2, t.len, 8, cudaMemcpyDeviceToHost, s));
+    QZ_CUDA(cudaMemcpyAsync(crc2, t.crc, 8, cudaMemcpyDeviceToHost, s));
+    QZ_CUDA(cudaStreamSynchronize(s));
+    k_fill_init<<<(unsigned)ceil_div(sim->nchunks, 256), 256, 0, s>>>(
+        t, sim->nchunks, off2[0], len2[0], crc2[0], off2[1], len2[1], crc2[1]);
+    QZ_CHECK_LAUNCH();
+    const int64_t bytes = int64_t(len2[1] + kPerChunkOverhead) +
+                          int64_t(sim->nchunks - 1) * int64_t(len2[0] + kPerChunkOverhead);
+    const int64_t acct[2] = {bytes, bytes};
+    QZ_CUDA(cudaMemcpyAsync(sim->acct.p, acct, 16, cudaMemcpyHostToDevice, s));
+    QZ_CUDA(cudaStreamSynchronize(s));
+    sim->initialized = true;
+    sim->stats = qzc_sim_stats{};
+    QZ_API_END
+}
+
+int qzc_sim_plan_stages(const qzc_sim *sim, const qzc_gate *gates, uint64_t ngates,
+                        uint64_t *stages_out) {
+    QZ_API_BEGIN
+    *stages_out = plan_stages(sim->n, gates, ngates, sim->c, sim->m).size();
+    QZ_API_END
+}
+
+int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
+    QZ_API_BEGIN
+    qzc_context *ctx = sim->ctx;
+    QZ_CUDA(cudaSetDevice(ctx->device));
+    if (!sim->initialized) throw Failure(QZC_ESTORE, "store not initialised");
+    const std::vector<Stage> stages = plan_stages(sim->n, gates, ngates, sim->c, sim->m);
+    cudaStream_t s = ctx->stream;
+    const uint32_t n = sim->n, c = sim->c;
+    const uint64_t chunk_bits_mask = (uint64_t(1) << (n - c)) - 1;
+    const uint64_t launches0 = ctx->launches;
+    const double t0 = now_s();
+    // 4 events per window, recycled per stage
+    auto ev = [&](size_t i) {
+        while (sim->events.size() <= i) {
+            cudaEvent_t e;
+            QZ_CUDA(cudaEventCreate(&e));
+            sim->events.push_back(e);
+        }
+        return sim->events[i];
+    };
+    for (size_t si = 0; si < stages.size(); ++si) {
+        const Stage &st = stages[si];
+        const uint32_t hs = (uint32_t)st.high.size();
+        const uint32_t mb = c + hs;  // buffer bits of one batch
+        uint64_t smask = 0;
+        for (uint32_t q : st.high) smask |= uint64_t(1) << (q - c);
+        const uint64_t fmask = chunk_bits_mask & ~smask;
+        const uint64_t nbatches = uint64_t(1) << ((n - c) - hs);
+        uint64_t bpw = std::max<uint64_t>(1, sim->win_amps >> mb);
+        bpw = std::min(bpw, nbatches);
+        const uint32_t wbits = mb + log2u(bpw);
+        // remap the stage's gates to buffer bits (remap_gate, planner.cpp:131-141)
+        std::vector<DevGate> dg;
+        dg.reserve(st.ngates);
+        for (size_t i = 0; i < st.ngates; ++i) {
+            qzc_gate g = gates[st.first_gate + i];
+            for (uint32_t k = 0; k < g.nqubits; ++k) {
+                const int b = buffer_bit(st, g.qubits[k], c);
+                if (b < 0) throw Failure(QZC_EPLAN, "qubit not mapped by the stage layout");
+                g.qubits[k] = uint32_t(b);
+            }
+            dg.push_back(make_dev_gate(g));
+        }
+        GatePlan gp = build_passes(dg, wbits, kTileBits, sim->cfg.fuse_gates != 0);
+        DevPlan dp;
+        upload_plan(gp, dp, s);
+        const int a = sim->cur, b = 1 - sim->cur;
+        QZ_CUDA(cudaMemsetAsync(sim->used_ptr(b), 0, 8, s));
+        const uint64_t nwin = nbatches / bpw;
+        const uint64_t nslots = bpw << hs;
+        for (uint64_t w = 0; w < nwin; ++w) {
+            Window &W = sim->win;
+            QZ_CUDA(cudaEventRecord(ev(4 * w), s));
+            launch_slot_chunks(W.slot_chunk.as<uint64_t>(), nslots, w * bpw, hs, fmask, smask, s);
+            decode_window(ctx, W, sim->geom, nslots, W.slot_chunk.as<uint64_t>(),
+                          sim->arena[a].as<uint8_t>(), sim->table(a), ctx->launches);
+            QZ_CUDA(cudaEventRecord(ev(4 * w + 1), s));
+            ctx->launches += 1 + run_passes(dp, W.amps.as<double2>(), wbits, s);
+            QZ_CUDA(cudaEventRecord(ev(4 * w + 2), s));
+            encode_window(ctx, W, sim->geom, nslots, W.slot_chunk.as<uint64_t>(), nullptr, 0,
+                          sim->arena[b].as<uint8_t>(), sim->used_ptr(b), sim->arena_cap,
+                          sim->table(b), sim->len[a].as<uint32_t>(), sim->acct.as<int64_t>(),
+                          ctx->launches);
+            QZ_CUDA(cudaEventRecord(ev(4 * w + 3), s));
+        }
+        try {
+            ctx->check_status();
+        } catch (const Failure &f) {
+            free_plan(dp);
+            throw Failure(f.code, "stage " + std::to_string(si) + ": " + f.what());
+        }
+        for (uint64_t w = 0; w < nwin; ++w) {
+            float ms[3];
+            for (int k = 0; k < 3; ++k) QZ_CUDA(cudaEventElapsedTime(&ms[k], ev(4 * w + k), ev(4 * w + k + 1)));
+            sim->stats.decode_seconds += ms[0] * 1e-3;
+            sim->stats.gate_seconds += ms[1] * 1e-3;
+            sim->stats.encode_seconds += ms[2] * 1e-3;
+        }
+        free_plan(dp);
+        sim->cur = b;
+        sim->stats.stages += 1;
+        sim->stats.batches += nbatches;
+        sim->stats.windows += nwin;
+        sim->stats.gate_passes += gp.passes.size() * nwin;
+        sim->stats.chunk_decompress_count += sim->nchunks;
+        sim->stats.chunk_recompress_count += sim->nchunks;
+    }
+    QZ_CUDA(cudaStreamSynchronize(s));
+    sim->stats.wall_seconds += now_s() - t0;
+    sim->stats.kernel_launches += ctx->launches - launches0;
+    QZ_API_END
+}
+
+int qzc_sim_stats_get(const qzc_sim *sim, qzc_sim_stats *out) {
+    QZ_API_BEGIN
+    *out = sim->stats;
+    int64_t acct[2];
+    QZ_CUDA(cudaMemcpy(acct, sim->acct.p, 16, cudaMemcpyDeviceToHost));
+    out->current_bytes = uint64_t(acct[0]);
+    out->peak_bytes = uint64_t(acct[1]);
+    out->dense_bytes = (uint64_t(1) << sim->n) * 16;
+    QZ_API_END
+}
+
+int qzc_sim_chunk_count(const qzc_sim *sim, uint64_t *count_out) {
+    QZ_API_BEGIN
+    *count_out = sim->nchunks;
+    QZ_API_END
+}
+
+namespace {
+// Host copy of the live table and the arena prefix it references.
+void pull_store(qzc_sim *sim, std::vector<uint64_t> &off, std::vector<uint32_t> &len,
+                std::vector<uint32_t> &crc, std::vector<uint8_t> &arena) {
+    cudaStream_t s = sim->ctx->stream;
+    const int a = sim->cur;
+    off.resize(sim->nchunks);
+    len.resize(sim->nchunks);
+    crc.resize(sim->nchunks);
+    uint64_t used = 0;
+    QZ_CUDA(cudaMemcpyAsync(off.data(), sim->off[a].p, 8 * sim->nchunks, cudaMemcpyDeviceToHost, s));
+    QZ_CUDA(cudaMemcpyAsync(len.data(), sim->len[a].p, 4 * sim->nchunks, cudaMemcpyDeviceToHost, s));
+    QZ_CUDA(cudaMemcpyAsync(crc.data(), sim->crc[a].p, 4 * sim->nchunks, cudaMemcpyDeviceToHost, s));
+    QZ_CUDA(cudaMemcpyAsync(&used, sim->used_ptr(a), 8, cudaMemcpyDeviceToHost, s));
+    QZ_CUDA(cudaStreamSynchronize(s));
+    arena.resize(used);
+    QZ_CUDA(cudaMemcpyAsync(arena.data(), sim->arena[a].p, used, cudaMemcpyDeviceToHost, s));
+    QZ_CUDA(cudaStreamSynchronize(s));
+    sim->stats.d2h_bytes += used + 16 * sim->nchunks;
+}
+} // namespace
+
+int qzc_sim_digest(qzc_sim *sim, uint64_t *digest_out) {
+    QZ_API_BEGIN
+    QZ_CUDA(cudaSetDevice(sim->ctx->device));
+    std::vector<uint64_t> off;
+    std::vector<uint32_t> len, crc;
+    std::vector<uint8_t> arena;
+    pull_store(sim, off, len, crc, arena);
+    uint64_t h = 0xcbf29ce484222325ULL;
+    for (uint64_t i = 0; i < sim->nchunks; ++i) h = fnv1a64_host(arena.data() + off[i], len[i], h);
+    *digest_out = h;
+    QZ_API_END
+}
+
+int qzc_sim_payload_bytes(qzc_sim *sim, uint64_t *total_out) {
+    QZ_API_BEGIN
+    std::vector<uint32_t> len(sim->nchunks);
+    QZ_CUDA(cudaMemcpy(len.data(), sim->len[sim->cur].p, 4 * sim->nchunks, cudaMemcpyDeviceToHost));
+    uint64_t t = 0;
+    for (uint32_t l : len) t += l;
+    *total_out = t;
+    QZ_API_END
+}
+
+int qzc_sim_export(qzc_sim *sim, uint8_t *payload_out, uint64_t cap, uint32_t *sizes, uint32_t *crcs) {
+    QZ_API_BEGIN
+    QZ_CUDA(cudaSetDevice(sim->ctx->device));
+    std::vector<uint64_t> off;
+    std::vector<uint32_t> len, crc;
+    std::vector<uint8_t> arena;
+    pull_store(sim, off, len, crc, arena);
+    uint64_t pos = 0;
+    for (uint64_t i = 0; i < sim->nchunks; ++i) {
+        if (payload_out) {
+            if (pos + len[i] > cap) throw Failure(QZC_EINVAL, "export buffer too small");
+            std::memcpy(payload_out + pos, arena.data() + off[i], len[i]);
+        }
+        pos += len[i];
+        if (sizes) sizes[i] = len[i];
+        if (crcs) crcs[i] = crc[i];
+    }
+    QZ_API_END
+}
+
+int qzc_sim_import(qzc_sim *sim, const uint8_t *payloads, const uint32_t *sizes, const uint32_t *crcs) {
+    QZ_API_BEGIN
+    qzc_context *ctx = sim->ctx;
+    QZ_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    std::vector<uint64_t> off(sim->nchunks);
+    uint64_t pos = 0, acct_bytes = 0;
+    for (uint64_t i = 0; i < sim->nchunks; ++i) {
+        off[i] = pos;
+        pos += sizes[i];
+        acct_bytes += sizes[i] + kPerChunkOverhead;
+    }
+    if (pos > sim->arena_cap) throw Failure(QZC_ENOMEM, "store does not fit the HBM arena");
+    const int a = sim->cur;
+    QZ_CUDA(cudaMemcpyAsync(sim->arena[a].p, payloads, pos, cudaMemcpyHostToDevice, s));
+    QZ_CUDA(cudaMemcpyAsync(sim->off[a].p, off.data(), 8 * sim->nchunks, cudaMemcpyHostToDevice, s));
+    QZ_CUDA(cudaMemcpyAsync(sim->len[a].p, sizes, 4 * sim->nchunks, cudaMemcpyHostToDevice, s));
+    QZ_CUDA(cudaMemcpyAsync(sim->crc[a].p, crcs, 4 * sim->nchunks, cudaMemcpyHostToDevice, s));
+    QZ_CUDA(cudaMemcpyAsync(sim->used_ptr(a), &pos, 8, cudaMemcpyHostToDevice, s));
+    const int64_t acct[2] = {int64_t(acct_bytes), int64_t(acct_bytes)};
+    QZ_CUDA(cudaMemcpyAsync(sim->acct.p, acct, 16, cudaMemcpyHostToDevice, s));
+    QZ_CUDA(cudaStreamSynchronize(s));
+    sim->stats.h2d_bytes += pos + 16 * sim->nchunks;
+    sim->initialized = true;
+    QZ_API_END
+}
+
+int qzc_sim_read_chunks(qzc_sim *sim, uint64_t first, uint64_t count, double *amps_out) {
+    QZ_API_BEGIN
+    qzc_context *ctx = sim->ctx;
+    QZ_CUDA(cudaSetDevice(ctx->device));
+    if (first + count > sim->nchunks)
+        throw Failure(QZC_ESTORE, "chunk index out of range: " + std::to_string(first + count - 1));
+    cudaStream_t s = ctx->stream;
+    const uint64_t per = std::max<uint64_t>(1, sim->win.slots);
+    for (uint64_t f = first; f < first + count; f += per) {
+        const uint64_t k = std::min(per, first + count - f);
+        launch_slot_chunks(sim->win.slot_chunk.as<uint64_t>(), k, f, 0, (uint64_t(1) << (sim->n - sim->c)) - 1, 0, s);
+        decode_window(ctx, sim->win, sim->geom, k, sim->win.slot_chunk.as<uint64_t>(),
+                      sim->arena[sim->cur].as<uint8_t>(), sim->table(sim->cur), ctx->launches);
+        ctx->check_status();
+        QZ_CUDA(cudaMemcpyAsync(amps_out + 2 * (f - first) * sim->N, sim->win.amps.p, 16 * k * sim->N,
+                                cudaMemcpyDeviceToHost, s));
+        QZ_CUDA(cudaStreamSynchronize(s));
+    }
+    QZ_API_END
+}
+
+int qzc_sim_write_chunk(qzc_sim *sim, uint64_t index, const double *amps) {
+    QZ_API_BEGIN
+    qzc_context *ctx = sim->ctx;
+    QZ_CUDA(cudaSetDevice(ctx->device));
+    if (index >= sim->nchunks) throw Failure(QZC_ESTORE, "chunk index out of range: " + std::to_string(index));
+    cudaStream_t s = ctx->stream;
+    const int a = sim->cur;
+    QZ_CUDA(cudaMemcpyAsync(sim->win.amps.p, amps, 16 * sim->N, cudaMemcpyHostToDevice, s));
+    QZ_CUDA(cudaMemcpyAsync(sim->win.slot_chunk.p, &index, 8, cudaMemcpyHostToDevice, s));
+    // the table of the live arena is updated in place; old bytes become garbage
+    encode_window(ctx, sim->win, sim->geom, 1, sim->win.slot_chunk.as<uint64_t>(), nullptr, 0,
+                  sim->arena[a].as<uint8_t>(), sim->used_ptr(a), sim->arena_cap, sim->table(a),
+                  sim->len[a].as<uint32_t>(), sim->acct.as<int64_t>(), ctx->launches);
+    ctx->check_status();
+    QZ_API_END
+}
+
+int qzc_sim_norm(qzc_sim *sim, double *norm_out) {
+    QZ_API_BEGIN
+    qzc_context *ctx = sim->ctx;
+    QZ_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    const uint64_t per = std::max<uint64_t>(1, sim->win.slots);
+    DevBuf part;
+    part.ensure(32 * per);
+    std::vector<double> hp(4 * per);
+    Kahan k;
+    for (uint64_t f = 0; f < sim->nchunks; f += per) {
+        const uint64_t cnt = std::min(per, sim->nchunks - f);
+        launch_slot_chunks(sim->win.slot_chunk.as<uint64_t>(), cnt, f, 0, (uint64_t(1) << (sim->n - sim->c)) - 1, 0, s);
+        decode_window(ctx, sim->win, sim->geom, cnt, sim->win.slot_chunk.as<uint64_t>(),
+                      sim->arena[sim->cur].as<uint8_t>(), sim->table(sim->cur), ctx->launches);
+        k_partials<<<(unsigned)ceil_div(cnt, 8), dim3(32, 8), 0, s>>>(sim->win.amps.as<double2>(), cnt, sim->N,
+                                                                   nullptr, 0, part.as<double>());
+        QZ_CHECK_LAUNCH();
+        ctx->check_status();
+        QZ_CUDA(cudaMemcpyAsync(hp.data(), part.p, 32 * cnt, cudaMemcpyDeviceToHost, s));
+        QZ_CUDA(cudaStreamSynchronize(s));
+        for (uint64_t i = 0; i < cnt; ++i) k.add(hp[4 * i + 3]);
+    }
+    part.release();
+    *norm_out = k.s;
+    QZ_API_END
+}
+
+int qzc_sim_fidelity_dev(qzc_sim *sim, const double *dense_dev, double *fidelity_out) {
+    QZ_API_BEGIN
+    qzc_context *ctx = sim->ctx;
+    QZ_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    const uint64_t per = std::max<uint64_t>(1, sim->win.slots);
+    DevBuf part;
+    part.ensure(32 * per);
+    std::vector<double> hp(4 * per);
+    Kahan re, im, na, nb;
+    for (uint64_t f = 0; f < sim->nchunks; f += per) {
+        const uint64_t cnt = std::min(per, sim->nchunks - f);
+        launch_slot_chunks(sim->win.slot_chunk.as<uint64_t>(), cnt, f, 0, (uint64_t(1) << (sim->n - sim->c)) - 1, 0, s);
+        decode_window(ctx, sim->win, sim->geom, cnt, sim->win.slot_chunk.as<uint64_t>(),
+                      sim->arena[sim->cur].as<uint8_t>(), sim->table(sim->cur), ctx->launches);
+        k_partials<<<(unsigned)ceil_div(cnt, 8), dim3(32, 8), 0, s>>>(
+            sim->win.amps.as<double2>(), cnt, sim->N, reinterpret_cast<const double2 *>(dense_dev), f,
+            part.as<double>());
+        QZ_CHECK_LAUNCH();
+        ctx->check_status();
+        QZ_CUDA(cudaMemcpyAsync(hp.data(), part.p, 32 * cnt, cudaMemcpyDeviceToHost, s));
+        QZ_CUDA(cudaStreamSynchronize(s));
+        for (uint64_t i = 0; i < cnt; ++i) {
+            re.add(hp[4 * i]);
+            im.add(hp[4 * i + 1]);
+            na.add(hp[4 * i + 2]);
+            nb.add(hp[4 * i + 3]);
+        }
+    }
+    part.release();
+    *fidelity_out = (na.s == 0.0 || nb.s == 0.0) ? 0.0 : (re.s * re.s + im.s * im.s) / (na.s * nb.s);
+    QZ_API_END
+}
+
+int qzc_dense_run(qzc_context *ctx, uint32_t num_qubits, const qzc_gate *gates, uint64_t ngates,
+                  double **dense_dev_out) {
+    QZ_API_BEGIN
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    QZ_CUDA(cudaSetDevice(ctx->device));
+    const uint64_t count = uint64_t(1) << num_qubits;
+    double2 *buf = nullptr;
+    QZ_CUDA(cudaMalloc(&buf, 16 * count));
+    k_basis<<<(unsigned)ceil_div(count, 256), 256, 0, ctx->stream>>>(buf, count);
+    QZ_CHECK_LAUNCH();
+    try {
+        apply_gates_device(ctx, reinterpret_cast<double *>(buf), num_qubits, gates, ngates);
+    } catch (...) {
+        cudaFree(buf);
+        throw;
+    }
+    *dense_dev_out = reinterpret_cast<double *>(buf);
+    QZ_API_END
+}
+
+void qzc_dense_free(qzc_context *ctx, double *dense_dev) {
+    if (ctx) cudaSetDevice(ctx->device);
+    cudaFree(dense_dev);
+}
+
+} // extern "C"

@@ -1,0 +1,130 @@
+"""GPU codec parity: payload bytes, CRC and decoded values bit-identical to
+the reference (golden fixture from the reference itself) and to the C oracle.
+Reference: codec.cpp:95-266, test_codec.cpp, acceptance.cpp:110-156."""
+import hashlib
+
+import numpy as np
+import pytest
+
+from golden.inputs import CODEC_CASES, codec_input
+from paper_2309_16979_b200 import engine as E
+
+pytestmark = pytest.mark.gpu
+
+
+def sha(b):
+    return hashlib.sha256(b).hexdigest()
+
+
+def test_golden_codec_cases(engine, golden):
+    bad = []
+    for case, rec in zip(CODEC_CASES, golden["codec"]):
+        amps, forced = codec_input(case)
+        payload, crc = engine.compress(amps, case["eb"], forced)
+        if len(payload) != rec["len"] or crc != rec["crc"] or sha(payload) != rec["sha256"]:
+            bad.append(("enc", case))
+            continue
+        back = engine.decompress(payload, crc, amps.size)
+        if sha(back.tobytes()) != rec["decoded_sha256"]:
+            bad.append(("dec", case))
+    assert not bad, bad[:5]
+
+
+def test_known_answer_ones(engine):
+    payload, _ = engine.compress(np.ones(4, complex), 0.1)
+    assert payload[17:] == bytes([10, 1, 0, 7, 0, 8])
+
+
+def test_zero_chunk_c16(engine):
+    payload, crc = engine.compress(np.zeros(1 << 16, complex), 1e-5)
+    assert len(payload) == 2077
+    assert (engine.decompress(payload, crc, 1 << 16) == 0).all()
+
+
+@pytest.mark.parametrize("eb", [0.0, 1e-3, 1e-5, 1e-7, 1e-9])
+@pytest.mark.parametrize("c", [1, 4, 8, 12])
+def test_batch_matches_oracle(engine, oracle, eb, c):
+    rng = np.random.default_rng(c * 100 + int(eb * 1e9))
+    n = 1 << c
+    count = max(2, 4096 >> c)
+    kinds = [rng.uniform(-1, 1, (count, n)) + 1j * rng.uniform(-1, 1, (count, n)),
+             (rng.normal(size=(count, n)) + 1j * rng.normal(size=(count, n))) * 2.0 ** -10,
+             np.zeros((count, n), complex)]
+    for a in kinds:
+        a[:, ::7] = 0.0
+        got = engine.compress_many(a, eb)
+        for k in range(count):
+            p, c_ = oracle.compress(a[k], eb)
+            assert got[k] == (p, c_), (k, eb, c)
+        back = engine.decompress_many([g[0] for g in got], [g[1] for g in got], n)
+        for k in range(0, count, max(1, count // 8)):
+            ref = oracle.decompress(got[k][0], got[k][1], n)
+            assert back[k].tobytes() == ref.tobytes()
+        if eb > 0:
+            assert np.abs(back.real - a.real).max() <= eb
+            assert np.abs(back.imag - a.imag).max() <= eb
+        else:
+            assert back.tobytes() == np.ascontiguousarray(a).tobytes()
+
+
+def test_error_bound_mixed_profiles(engine):
+    # acceptance.cpp:110-156 style: sparse / uniform / smooth chunks, 3 bounds
+    rng = np.random.default_rng(2024)
+    for n in (16, 32, 64):
+        chunks = []
+        for i in range(300):
+            v = np.zeros(n, complex)
+            if i % 3 == 0:
+                v[rng.integers(0, n, 3)] = rng.uniform(-1, 1, 3) + 1j * rng.uniform(-1, 1, 3)
+            elif i % 3 == 1:
+                v = rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n)
+            else:
+                t = np.arange(n) / n
+                v = np.sin(t + rng.uniform()) + 1j * np.cos(t - rng.uniform()) + 1e-6 * rng.uniform(-1, 1, n)
+            chunks.append(v)
+        a = np.array(chunks)
+        for eb in (1e-3, 1e-5, 1e-7):
+            got = engine.compress_many(a, eb)
+            back = engine.decompress_many([g[0] for g in got], [g[1] for g in got], n)
+            assert np.abs(back.real - a.real).max() <= eb
+            assert np.abs(back.imag - a.imag).max() <= eb
+        got = engine.compress_many(a, 0.0)
+        back = engine.decompress_many([g[0] for g in got], [g[1] for g in got], n)
+        assert back.tobytes() == a.tobytes()
+
+
+def test_flipped_byte_is_caught(engine):
+    rng = np.random.default_rng(6)
+    a = rng.uniform(-1, 1, 32) + 1j * rng.uniform(-1, 1, 32)
+    p, crc = engine.compress(a, 1e-5)
+    bad = bytearray(p)
+    bad[len(bad) // 2] ^= 0x40
+    with pytest.raises(E.CodecError, match="checksum mismatch on chunk 7"):
+        engine.decompress(bytes(bad), crc, 32, chunk_index=7)
+
+
+def test_malformed_payloads(engine, oracle):
+    a = np.zeros(8, complex)
+    p, _ = oracle.compress(a, 1e-5)
+    for mutated in (p[:10], p[:17], p[:-2], p[:17] + bytes([0, 0]) + p[19:]):
+        with pytest.raises(E.CodecError, match="malformed|header"):
+            engine.decompress(mutated, oracle.crc32(mutated), 8)
+
+
+def test_invalid_inputs(engine):
+    with pytest.raises(E.CodecError):
+        engine.compress(np.zeros(3, complex), 1e-5)
+    with pytest.raises(E.CodecError):
+        engine.compress(np.zeros(4, complex), -1.0)
+    with pytest.raises(E.CodecError):
+        engine.compress(np.zeros(4, complex), float("nan"))
+    with pytest.raises(E.CodecError):
+        engine.compress(np.zeros(4, complex), 1e-5, forced=[8])
+
+
+def test_forced_raws_exact(engine):
+    rng = np.random.default_rng(9)
+    a = rng.uniform(-1, 1, 16) + 1j * rng.uniform(-1, 1, 16)
+    p, crc = engine.compress(a, 1e-2, forced=[0, 16])
+    out = engine.decompress(p, crc, 16)
+    assert out[0] == a[0]

@@ -1,0 +1,144 @@
+"""GPU pipeline parity: final store digest, footprint and stage counts equal
+to the reference's run() on the same circuit (golden fixture produced by the
+reference).  Mirrors test_pipeline.cpp and acceptance.cpp C1/C4/C5/C8."""
+import numpy as np
+import pytest
+
+from paper_2309_16979_b200 import engine as E
+from paper_2309_16979_b200.abi import to_array
+
+pytestmark = pytest.mark.gpu
+
+
+def circuit(golden, oracle, key):
+    if key.startswith("qft:"):
+        return oracle.make_qft(int(key.split(":")[1]))
+    if key.startswith("ghz:"):
+        return oracle.make_ghz(int(key.split(":")[1]))
+    return to_array([(g[0], tuple(g[1]), tuple(g[2])) for g in golden["circuits"][key]])
+
+
+def run_sim(engine, n, c, m, eb, gates, **kw):
+    sim = engine.simulator(n, c, m, eb, **kw)
+    sim.run(gates)
+    return sim
+
+
+def test_small_runs_digest(engine, oracle, golden):
+    bad = []
+    for rec in golden["runs_small"]:
+        g = circuit(golden, oracle, rec["circuit"])
+        sim = run_sim(engine, rec["n"], rec["c"], rec["m"], rec["eb"], g)
+        st = sim.stats()
+        if (f"{sim.digest():016x}" != rec["digest"] or st["stages"] != rec["stages"]
+                or st["current_bytes"] != rec["current_bytes"]):
+            bad.append(rec)
+        sim.close()
+    assert not bad, bad[:3]
+
+
+@pytest.mark.parametrize("idx", range(15))
+def test_large_runs_digest(engine, oracle, golden, idx):
+    rec = golden["runs"][idx]
+    g = circuit(golden, oracle, rec["circuit"])
+    sim = run_sim(engine, rec["n"], rec["c"], rec["m"], rec["eb"], g)
+    assert f"{sim.digest():016x}" == rec["digest"], rec
+    st = sim.stats()
+    assert st["stages"] == rec["stages"]
+    assert st["current_bytes"] == rec["current_bytes"]
+    assert sim.payload_bytes() == rec["total_payload"]
+    assert sim.norm() == pytest.approx(rec["norm"], abs=1e-9)
+
+
+def test_small_window_same_digest(engine, oracle, golden):
+    # scheduling knobs (window size, fusion) never change the bytes
+    rec = golden["runs"][0]
+    g = circuit(golden, oracle, rec["circuit"])
+    for window in (1 << rec["m"], 1 << (rec["m"] + 1), 0):
+        for fuse in (True, False):
+            sim = run_sim(engine, rec["n"], rec["c"], rec["m"], rec["eb"], g,
+                          window_amps=window, fuse=fuse)
+            assert f"{sim.digest():016x}" == rec["digest"]
+
+
+def test_empty_circuit_is_init(engine, oracle):
+    sim = engine.simulator(6, 2, 4, 0.0)
+    d0 = sim.digest()
+    sim.run([])
+    assert sim.digest() == d0
+    assert sim.norm() == 1.0
+    r = oracle.run(6, [], 2, 4, 0.0)
+    assert r["digest"] == d0
+
+
+def test_init_basis_exact(engine):
+    for eb in (0.0, 1e-3, 1e-5, 0.3):
+        sim = engine.simulator(6, 3, 5, eb)
+        s = sim.state()
+        assert abs(s[0] - 1) <= 1e-12 and (s[1:] == 0).all()
+        assert sim.norm() == 1.0
+
+
+def test_init_ratios(engine):
+    assert engine.simulator(20, 12, 16, 1e-5).stats()["ratio"] > 100
+    st = engine.simulator(24, 16, 20, 1e-5).stats()
+    assert st["current_bytes"] * 100 <= st["dense_bytes"]
+
+
+def test_lossless_matches_dense(engine, oracle):
+    g = to_array([])
+    rng = np.random.default_rng(77)
+    from tests_util import random_circuit
+    g = random_circuit(10, 50, 77)
+    dense = oracle.dense(10, g)
+    for c, m in ((4, 6), (2, 4), (3, 8)):
+        sim = run_sim(engine, 10, c, m, 0.0, g)
+        assert np.abs(sim.state() - dense).max() <= 1e-12
+
+
+def test_fidelity_vs_gpu_dense(engine, oracle):
+    g = oracle.make_ghz(16)
+    sim = run_sim(engine, 16, 8, 12, 1e-6, g)
+    dense = engine.dense_state(16, g)
+    assert sim.fidelity(dense) >= 0.9999
+    ref = oracle.dense(16, g)
+    assert abs(sim.fidelity(dense) - oracle.fidelity(ref, sim.state())) < 1e-12
+
+
+def test_export_import_roundtrip(engine, oracle, golden):
+    rec = golden["runs"][0]
+    g = circuit(golden, oracle, rec["circuit"])
+    sim = run_sim(engine, rec["n"], rec["c"], rec["m"], rec["eb"], g)
+    blob, sizes, crcs = sim.export()
+    other = engine.simulator(rec["n"], rec["c"], rec["m"], rec["eb"], init=False)
+    other.import_(blob, sizes, crcs)
+    assert other.digest() == sim.digest()
+    ref = oracle.run(rec["n"], g, rec["c"], rec["m"], rec["eb"], export=True)
+    assert ref["payload"] == blob
+
+
+def test_write_and_read_chunk(engine, oracle):
+    rng = np.random.default_rng(21)
+    sim = engine.simulator(8, 4, 6, 1e-4)
+    before = sim.stats()["current_bytes"]
+    vals = rng.uniform(-1, 1, 16) + 1j * rng.uniform(-1, 1, 16)
+    sim.write_chunk(5, vals)
+    back = sim.read_chunks(5, 1)
+    assert np.abs(back.real - vals.real).max() <= 1e-4
+    assert np.abs(back.imag - vals.imag).max() <= 1e-4
+    old = len(oracle.compress(np.zeros(16, complex), 1e-4)[0])
+    new = len(oracle.compress(vals, 1e-4)[0])
+    assert sim.stats()["current_bytes"] == before - old + new
+    with pytest.raises(E.StoreError):
+        sim.read_chunks(16, 1)
+
+
+def test_invalid_configs(engine):
+    with pytest.raises(E.StoreError):
+        engine.simulator(10, 12, 14, 0.0)
+    with pytest.raises(E.StoreError):
+        engine.simulator(41, 16, 20, 0.0)
+    with pytest.raises(E.PlanError):
+        engine.simulator(6, 4, 4, 0.0).run([("h", (0,), ())])      # m - c < 2
+    with pytest.raises(E.PlanError):
+        engine.simulator(6, 2, 6, 0.0).run([("h", (7,), ())])      # bad qubit
