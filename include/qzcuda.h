@@ -80,6 +80,10 @@ void qzc_context_destroy(qzc_context *ctx);
 int qzc_synchronize(qzc_context *ctx);
 /* Number of engine kernels launched on this context so far. */
 uint64_t qzc_kernel_launches(const qzc_context *ctx);
+/* CUDA-event timer on the context stream: begin records an event, end
+ * records a second one, synchronizes and returns the elapsed seconds. */
+int qzc_timer_begin(qzc_context *ctx);
+int qzc_timer_end(qzc_context *ctx, double *seconds_out);
 
 /* ---- chunk codec (replaces codec.hpp:61-70) ----------------------------- */
 /* Worst-case payload bytes for one chunk of `elements` amplitudes. */

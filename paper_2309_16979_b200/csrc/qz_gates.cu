@@ -13,6 +13,8 @@
 // buffer bits 0..2 so every global access is a >= 128 B contiguous segment
 // of 16 B double2 loads.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <complex>
 #include <cstring>
 
@@ -107,43 +109,92 @@ void gate_matrix_host(const qzc_gate &g, double2 *m, uint32_t *dim) {
     }
 }
 
-static bool is_zero(double2 v) { return v.x == 0.0 && v.y == 0.0; }
+static bool is_zero_h(double2 v) { return v.x == 0.0 && v.y == 0.0; }
+
+static uint32_t coef_kind(double2 v) {
+    if (v.x == 0.0 && v.y == 0.0) return CK_ZERO;
+    if (v.y == 0.0) {
+        if (v.x == 1.0) return CK_ONE;
+        if (v.x == -1.0) return CK_NEG;
+        return CK_REAL;
+    }
+    if (v.x == 0.0) return CK_IMAG;
+    return CK_CPLX;
+}
 
 DevGate make_dev_gate(const qzc_gate &g) {
     DevGate d;
     std::memset(&d, 0, sizeof d);
     uint32_t dim = 0;
     gate_matrix_host(g, d.m, &dim);
+    d.dim = dim;
     d.nq = dim == 2 ? 1 : 2;
     d.b0 = g.qubits[0];
     d.b1 = d.nq == 2 ? g.qubits[1] : 0;
-    d.cls = GC_DENSE;
+    for (uint32_t e = 0; e < dim * dim; ++e) {
+        d.kinds |= uint64_t(coef_kind(d.m[e])) << (4 * e);
+        d.sgn |= uint32_t(std::signbit(d.m[e].x)) << (2 * e);
+        d.sgn |= uint32_t(std::signbit(d.m[e].y)) << (2 * e + 1);
+    }
+    auto is = [&](int e, double re) { return d.m[e].x == re && d.m[e].y == 0.0; };
+    auto zero_except = [&](std::initializer_list<int> keep) {
+        for (int e = 0; e < 16; ++e) {
+            bool k = false;
+            for (int x : keep) k |= x == e;
+            if (!k && !(d.m[e].x == 0.0 && d.m[e].y == 0.0)) return false;
+        }
+        return true;
+    };
     if (d.nq == 1) {
-        if (is_zero(d.m[1]) && is_zero(d.m[2])) d.cls = GC_DIAG;
-        else if (is_zero(d.m[0]) && is_zero(d.m[3])) d.cls = GC_ANTI;
+        const bool diag = d.m[1].x == 0.0 && d.m[1].y == 0.0 && d.m[2].x == 0.0 && d.m[2].y == 0.0;
+        d.op = diag ? OP_DIAG : OP_GEN1;
+    } else if (is(0, 1) && is(5, 1) && is(11, 1) && is(14, 1) && zero_except({0, 5, 11, 14})) {
+        d.op = OP_CX;
+    } else if (is(0, 1) && is(5, 1) && is(10, 1) && is(15, -1) && zero_except({0, 5, 10, 15})) {
+        d.op = OP_CZ;
+    } else if (is(0, 1) && is(6, 1) && is(9, 1) && is(15, 1) && zero_except({0, 6, 9, 15})) {
+        d.op = OP_SWAP;
     } else {
-        bool perm = true;
-        for (int r = 0; r < 4 && perm; ++r) {
-            int nz = 0;
-            for (int c = 0; c < 4; ++c) nz += !is_zero(d.m[r * 4 + c]);
-            perm = nz == 1;
-        }
-        if (perm) {
-            // bits 8.. hold the nonzero column of each row (2 bits per row)
-            uint32_t cols = 0;
-            for (int r = 0; r < 4; ++r)
-                for (int c = 0; c < 4; ++c)
-                    if (!is_zero(d.m[r * 4 + c])) cols |= uint32_t(c) << (2 * r);
-            d.cls = GC_PERM4 | (cols << 8);
-        }
+        d.op = OP_GEN2;
     }
     return d;
 }
 
 // ------------------------------------------------------------- pass builder --
 
-GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits,
-                      uint32_t kmax, bool fuse) {
+// Does an all-(+0) input produce all-(+0) outputs?  With every input +0 the
+// product signs are the coefficient signs, so row r's real part is -0 iff
+// every entry has (sign re, sign im) = (1, 0) and its imaginary part iff
+// every entry has (1, 1) (IEEE: a sum of zeros is -0 only if all are -0).
+static bool maps_pos_zero(const DevGate &g) {
+    for (uint32_t r = 0; r < g.dim; ++r) {
+        uint32_t nre = 1, nim = 1;
+        for (uint32_t c = 0; c < g.dim; ++c) {
+            const uint32_t e = r * g.dim + c;
+            const uint32_t smr = (g.sgn >> (2 * e)) & 1, smi = (g.sgn >> (2 * e + 1)) & 1;
+            nre &= smr & (smi ^ 1);
+            nim &= smr & smi;
+        }
+        if (nre | nim) return false;
+    }
+    return true;
+}
+
+static bool is_signed_perm(const DevGate &g) {
+    for (uint32_t r = 0; r < g.dim; ++r) {
+        int nz = 0;
+        for (uint32_t c = 0; c < g.dim; ++c) {
+            const uint32_t kd = uint32_t(g.kinds >> (4 * (r * g.dim + c))) & 15;
+            if (kd == CK_ZERO) continue;
+            ++nz;
+            if (kd != CK_ONE && kd != CK_NEG) return false;
+        }
+        if (nz != 1) return false;
+    }
+    return true;
+}
+
+GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_t kmax, bool fuse) {
     GatePlan plan;
     const uint32_t k = std::min(kmax, nbits);
     const uint32_t low = std::min<uint32_t>(3, k);
@@ -157,32 +208,127 @@ GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits,
     uint64_t tmask = low_mask;
     auto close = [&]() {
         if (members.empty()) return;
-        // pad T to exactly k bits with the lowest free bits (longer
-        // contiguous runs, better coalescing)
+        // pad T to exactly k bits with the lowest free bits (longer contiguous
+        // global segments)
         for (uint32_t b = 0; b < nbits && (uint32_t)__builtin_popcountll(tmask) < k; ++b)
             tmask |= uint64_t(1) << b;
         PassDesc pd;
+        std::memset(&pd, 0, sizeof pd);
         pd.k = k;
         uint32_t lowbits = 0;
         while (lowbits < 64 && ((tmask >> lowbits) & 1)) ++lowbits;
         pd.lowbits = std::min(lowbits, k);
+        pd.tmask = tmask;
         pd.first_gate = (uint32_t)plan.gates.size();
         pd.ngates = (uint32_t)members.size();
-        pd.tmask = tmask;
-        // local position of buffer bit b inside T
+        pd.first_group = (uint32_t)plan.groups.size();
         auto local = [&](uint32_t b) {
             return (uint32_t)__builtin_popcountll(tmask & ((uint64_t(1) << b) - 1));
         };
+        // register groups: consecutive gates whose tile bits fit 4 bits
+        uint32_t gmask = 0;
+        std::vector<size_t> gmembers;
+        auto close_group = [&]() {
+            if (gmembers.empty()) return;
+            for (uint32_t b = 0; b < k && __builtin_popcount(gmask) < kRegBits; ++b) gmask |= 1u << b;
+            GroupDesc gd;
+            gd.generic = 0;
+            gd.pz_stable = 1;
+            for (size_t gi : gmembers) gd.pz_stable &= maps_pos_zero(gates[gi]) ? 1u : 0u;
+            int i = 0;
+            for (uint32_t b = 0; b < k; ++b)
+                if ((gmask >> b) & 1) gd.gbits[i++] = b;
+            for (; i < 4; ++i) gd.gbits[i] = 0;   // unused slots
+            gd.first_gate = (uint32_t)plan.gates.size();
+            gd.ngates = (uint32_t)gmembers.size();
+            auto reg = [&](uint32_t lb) {
+                return (uint32_t)__builtin_popcount(gmask & ((1u << lb) - 1));
+            };
+            for (size_t gi : gmembers) {
+                const DevGate &g = gates[gi];
+                TileGate t;
+                std::memset(&t, 0, sizeof t);
+                t.nq = g.nq;
+                t.t0 = local(g.b0);
+                t.t1 = g.nq == 2 ? local(g.b1) : 0;
+                t.r0 = reg(t.t0);
+                t.r1 = g.nq == 2 ? reg(t.t1) : 0;
+                t.kinds = g.kinds;
+                t.sgn = g.sgn;
+                t.zm = 0;
+                t.smask = 0;
+                for (uint32_t e = 0; e < g.dim * g.dim; ++e) {
+                    t.zm |= uint32_t(g.m[e].x == 0.0) << e;
+                    t.zm |= uint32_t(g.m[e].y == 0.0) << (16 + e);
+                    t.smask |= uint32_t(std::signbit(g.m[e].x)) << e;
+                    t.smask |= uint32_t(std::signbit(g.m[e].y)) << (16 + e);
+                }
+                t.op = g.op;
+                t.pad = 0;   // bit r: row r maps all-(+0) inputs to (+0, +0)
+                for (uint32_t r = 0; r < g.dim; ++r) {
+                    uint32_t nre = 1, nim = 1;
+                    for (uint32_t c = 0; c < g.dim; ++c) {
+                        const uint32_t e = r * g.dim + c;
+                        const uint32_t smr = (g.sgn >> (2 * e)) & 1, smi = (g.sgn >> (2 * e + 1)) & 1;
+                        nre &= smr & (smi ^ 1);
+                        nim &= smr & smi;
+                    }
+                    if (!(nre | nim)) t.pad |= 1u << r;
+                }
+                t.cls = TG_GEN;
+                {
+                    const uint32_t dim = g.dim;
+                    bool perm = true, diag = g.nq == 1;
+                    uint32_t code = 0;
+                    for (uint32_t r = 0; r < dim && perm; ++r) {
+                        int nz = 0;
+                        for (uint32_t c = 0; c < dim; ++c) {
+                            const uint32_t kd = uint32_t(g.kinds >> (4 * (r * dim + c))) & 15;
+                            if (kd == CK_ZERO) continue;
+                            ++nz;
+                            if (kd != CK_ONE && kd != CK_NEG) perm = false;
+                            code |= (c | (kd == CK_NEG ? 4u : 0u)) << (3 * r);
+                            if (c != r) diag = false;
+                        }
+                        if (nz != 1) perm = false;
+                    }
+                    if (g.nq == 1 && !(uint32_t(g.kinds >> 4) & 15) && !(uint32_t(g.kinds >> 8) & 15))
+                        diag = true;
+                    else if (g.nq == 1)
+                        diag = false;
+                    if (perm) {
+                        t.cls = TG_PERM;
+                        t.perm = code;
+                    } else if (diag) {
+                        t.cls = TG_DIAG;
+                    }
+                }
+                std::memcpy(t.m, g.m, sizeof t.m);
+                plan.gates.push_back(t);
+            }
+            plan.groups.push_back(gd);
+            gmembers.clear();
+            gmask = 0;
+        };
         for (size_t i : members) {
             const DevGate &g = gates[i];
-            TileGate t;
-            t.nq = g.nq;
-            t.t0 = local(g.b0);
-            t.t1 = g.nq == 2 ? local(g.b1) : 0;
-            t.cls = g.cls;
-            std::memcpy(t.m, g.m, sizeof t.m);
-            plan.gates.push_back(t);
+            uint32_t need = 1u << local(g.b0);
+            if (g.nq == 2) need |= 1u << local(g.b1);
+            const bool generic = g.nq == 2 && !is_signed_perm(g);
+            if (generic || __builtin_popcount(gmask | need) > kRegBits || k <= (uint32_t)kRegBits)
+                close_group();
+            gmask |= need;
+            gmembers.push_back(i);
+            if (generic) {
+                close_group();
+                plan.groups.back().generic = 1;
+            }
         }
+        close_group();
+        pd.ngroups = (uint32_t)plan.groups.size() - pd.first_group;
+        pd.pz_stable = 1;
+        for (uint32_t gi = pd.first_group; gi < pd.first_group + pd.ngroups; ++gi)
+            pd.pz_stable &= plan.groups[gi].pz_stable;
         plan.passes.push_back(pd);
         members.clear();
         tmask = low_mask;
@@ -201,165 +347,695 @@ GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits,
 
 void upload_plan(const GatePlan &plan, DevPlan &out, cudaStream_t s) {
     free_plan(out);
-    out.npasses = plan.passes.size();
     out.ngates = plan.gates.size();
+    out.ngroups = plan.groups.size();
     out.host_passes = plan.passes;
     if (out.ngates) {
         QZ_CUDA(cudaMalloc(&out.gates, sizeof(TileGate) * out.ngates));
         QZ_CUDA(cudaMemcpyAsync(out.gates, plan.gates.data(), sizeof(TileGate) * out.ngates,
                                 cudaMemcpyHostToDevice, s));
     }
+    if (out.ngroups) {
+        QZ_CUDA(cudaMalloc(&out.groups, sizeof(GroupDesc) * out.ngroups));
+        QZ_CUDA(cudaMemcpyAsync(out.groups, plan.groups.data(), sizeof(GroupDesc) * out.ngroups,
+                                cudaMemcpyHostToDevice, s));
+    }
 }
 
 void free_plan(DevPlan &p) {
     if (p.gates) cudaFree(p.gates);
-    if (p.passes) cudaFree(p.passes);
+    if (p.groups) cudaFree(p.groups);
     p.gates = nullptr;
-    p.passes = nullptr;
-    p.npasses = p.ngates = 0;
+    p.groups = nullptr;
+    p.ngates = p.ngroups = 0;
     p.host_passes.clear();
 }
 
-// ------------------------------------------------------------ tile kernel --
-
+// ============================================================ device math ==
+//
+// Exactness argument (every path is bit-identical to the dense formula of
+// kernels.cpp:31-32 / 49-50):
+//  * A product with a coefficient whose real or imaginary part is exactly
+//    ±0 contributes ±0 to that component; x ± 0 == x for x != 0 and
+//    ±0 + y == y for y != 0, so dropping those terms (and using 1*x == x,
+//    -1*x == -x) can change a left-to-right sum only when the final value is
+//    zero, and then only its sign.  Any output component that comes out zero
+//    is recomputed: by IEEE sign rules if every input is ±0 (all products
+//    are then ±0), else by the full dense formula in the reference order.
+//  * A thread's 16-amplitude register block is closed under its group's
+//    gates, so an all-zero block stays all-zero; only the zero signs evolve
+//    and are tracked as two 16-bit masks.
+//  * Non-finite amplitudes are outside the domain (a unitary circuit from
+//    |0..0> never produces them).
 namespace {
 
-__device__ __forceinline__ double2 to2(cplx c) { return make_double2(c.re, c.im); }
+constexpr int NB = 1 << kRegBits;   // amplitudes per thread register block
 
-__device__ __forceinline__ bool has_zero(cplx c) { return c.re == 0.0 || c.im == 0.0; }
+__device__ __forceinline__ bool dz(double x) { return (__double_as_longlong(x) << 1) == 0; }
+__device__ __forceinline__ bool zc(double2 v) { return dz(v.x) | dz(v.y); }
+__device__ __forceinline__ double dneg(double x) {
+    return __longlong_as_double(__double_as_longlong(x) ^ (long long)0x8000000000000000ULL);
+}
+__device__ __forceinline__ double2 pm(double2 v, uint32_t neg) {
+    return neg ? make_double2(dneg(v.x), dneg(v.y)) : v;
+}
+__device__ __forceinline__ uint32_t sbit(double x) {
+    return uint32_t((unsigned long long)__double_as_longlong(x) >> 63);
+}
+__device__ __forceinline__ double signed_zero(uint32_t neg) { return neg ? -0.0 : 0.0; }
 
-// Dense 1q formula: out = m_r0*a + m_r1*b (kernels.cpp:31-32).
-__device__ __forceinline__ cplx row2(const double2 *m, int r, double2 a, double2 b) {
-    cplx x = cmul(m[2 * r].x, m[2 * r].y, a);
-    cplx y = cmul(m[2 * r + 1].x, m[2 * r + 1].y, b);
-    return cplx{__dadd_rn(x.re, y.re), __dadd_rn(x.im, y.im)};
+__host__ __device__ constexpr int izb(int x, int bit) {
+    return ((x >> bit) << (bit + 1)) | (x & ((1 << bit) - 1));
 }
 
-// Dense 4x4 row: ((m0*i0 + m1*i1) + m2*i2) + m3*i3 (kernels.cpp:49-50).
-__device__ __forceinline__ cplx row4(const double2 *m, int r, const double2 *in) {
-    cplx acc = cmul(m[4 * r].x, m[4 * r].y, in[0]);
-#pragma unroll
-    for (int c = 1; c < 4; ++c) {
-        cplx t = cmul(m[4 * r + c].x, m[4 * r + c].y, in[c]);
-        acc.re = __dadd_rn(acc.re, t.re);
-        acc.im = __dadd_rn(acc.im, t.im);
+// Full reference row, columns in reference order, separate roundings.
+__device__ double2 full_row(const TileGate &g, int r, int nc, const double2 *in) {
+    double sr = 0, si = 0;
+    for (int c = 0; c < nc; ++c) {
+        const double2 m = g.m[r * nc + c];
+        const double tr = __dsub_rn(__dmul_rn(m.x, in[c].x), __dmul_rn(m.y, in[c].y));
+        const double ti = __dadd_rn(__dmul_rn(m.x, in[c].y), __dmul_rn(m.y, in[c].x));
+        sr = c == 0 ? tr : __dadd_rn(sr, tr);
+        si = c == 0 ? ti : __dadd_rn(si, ti);
     }
-    return acc;
+    return make_double2(sr, si);
 }
 
-__device__ __forceinline__ void apply1(double2 *s, uint32_t half, uint32_t t,
-                                       const TileGate &g, uint32_t tid, uint32_t nth) {
-    const double2 *m = g.m;
-    const uint32_t stride = 1u << t;
-    for (uint32_t p = tid; p < half; p += nth) {
-        const uint32_t i = insert_zero_bit32(p, t), j = i | stride;
-        const double2 a = s[i], b = s[j];
-        cplx oi, oj;
-        const uint32_t cls = g.cls & 0xff;
-        if (cls == GC_DIAG) {
-            oi = cmul(m[0].x, m[0].y, a);
-            oj = cmul(m[3].x, m[3].y, b);
-            if (has_zero(oi) || has_zero(oj)) {
-                oi = row2(m, 0, a, b);
-                oj = row2(m, 1, a, b);
-            }
-        } else if (cls == GC_ANTI) {
-            oi = cmul(m[1].x, m[1].y, b);
-            oj = cmul(m[2].x, m[2].y, a);
-            if (has_zero(oi) || has_zero(oj)) {
-                oi = row2(m, 0, a, b);
-                oj = row2(m, 1, a, b);
-            }
+// Exact recomputation of one output row whose fast value had a zero
+// component; `in` is in reference column order.  If every input is ±0 all
+// products are ±0 and IEEE sign rules decide (x - y: -0 iff x=-0, y=+0;
+// x + y: -0 iff both -0); otherwise the full formula is evaluated.
+__device__ double2 exact_row(const TileGate &g, int r, int nc, const double2 *in) {
+    // per component: are all its products zero (a zero factor each)?
+    bool zre = true, zim = true;
+    uint32_t nre = 1, nim = 1;
+    for (int c = 0; c < nc; ++c) {
+        const int e = r * nc + c;
+        const bool mrz = (g.zm >> e) & 1, miz = (g.zm >> (16 + e)) & 1;
+        const bool vrz = dz(in[c].x), viz = dz(in[c].y);
+        zre = zre && (mrz || vrz) && (miz || viz);
+        zim = zim && (mrz || viz) && (miz || vrz);
+        const uint32_t smr = (g.sgn >> (2 * e)) & 1, smi = (g.sgn >> (2 * e + 1)) & 1;
+        const uint32_t svr = sbit(in[c].x), svi = sbit(in[c].y);
+        nre &= (smr ^ svr) & ~(smi ^ svi);   // mr*vr - mi*vi
+        nim &= (smr ^ svi) & (smi ^ svr);    // mr*vi + mi*vr
+    }
+    double2 o;
+    if (zre && zim) return make_double2(signed_zero(nre & 1), signed_zero(nim & 1));
+    o = full_row(g, r, nc, in);
+    if (zre) o.x = signed_zero(nre & 1);
+    if (zim) o.y = signed_zero(nim & 1);
+    return o;
+}
+
+__device__ __noinline__ double2 slow2(const TileGate &g, int r, double2 a, double2 b) {
+    const double2 in[2] = {a, b};
+    return exact_row(g, r, 2, in);
+}
+
+__device__ __noinline__ double2 slow4(const TileGate &g, int r, double2 a, double2 b, double2 c,
+                                      double2 d) {
+    const double2 in[4] = {a, b, c, d};
+    return exact_row(g, r, 4, in);
+}
+
+// One nonzero term, kind uniform across the warp.
+__device__ __forceinline__ double2 term(uint32_t kind, double2 m, double2 v) {
+    if (kind == CK_ONE) return v;
+    if (kind == CK_NEG) return make_double2(dneg(v.x), dneg(v.y));
+    if (kind == CK_REAL) return make_double2(__dmul_rn(m.x, v.x), __dmul_rn(m.x, v.y));
+    if (kind == CK_IMAG) return make_double2(dneg(__dmul_rn(m.y, v.y)), __dmul_rn(m.y, v.x));
+    return make_double2(__dsub_rn(__dmul_rn(m.x, v.x), __dmul_rn(m.y, v.y)),
+                        __dadd_rn(__dmul_rn(m.x, v.y), __dmul_rn(m.y, v.x)));
+}
+
+__device__ __forceinline__ double2 sum2(double2 a, double2 b) {
+    return make_double2(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y));
+}
+
+// ---- 1-qubit gates on register bit R ----
+template <int R>
+__device__ __forceinline__ void reg_apply1(double2 (&v)[NB], const TileGate &g) {
+    constexpr int sh = 1 << R;
+    const uint32_t kd = uint32_t(g.kinds);
+    const uint32_t k00 = kd & 15u, k01 = (kd >> 4) & 15u, k10 = (kd >> 8) & 15u, k11 = (kd >> 12) & 15u;
+    const double2 m00 = g.m[0], m01 = g.m[1], m10 = g.m[2], m11 = g.m[3];
+    const uint32_t cls = g.cls, pc = g.perm;
+#pragma unroll
+    for (int p = 0; p < NB / 2; ++p) {
+        const int i = izb(p, R), j = i | sh;
+        const double2 a = v[i], b = v[j];
+        double2 oi, oj;
+        if (cls == TG_PERM) {
+            oi = pm((pc & 1) ? b : a, (pc >> 2) & 1);
+            oj = pm(((pc >> 3) & 1) ? b : a, (pc >> 5) & 1);
+        } else if (cls == TG_DIAG) {
+            oi = term(k00, m00, a);
+            oj = term(k11, m11, b);
         } else {
-            oi = row2(m, 0, a, b);
-            oj = row2(m, 1, a, b);
+            oi = k00 == CK_ZERO ? term(k01, m01, b)
+                                : (k01 == CK_ZERO ? term(k00, m00, a) : sum2(term(k00, m00, a), term(k01, m01, b)));
+            oj = k10 == CK_ZERO ? term(k11, m11, b)
+                                : (k11 == CK_ZERO ? term(k10, m10, a) : sum2(term(k10, m10, a), term(k11, m11, b)));
         }
-        s[i] = to2(oi);
-        s[j] = to2(oj);
+        if (zc(oi) | zc(oj)) {
+            // both inputs +0 and the row maps (+0,+0) to +0: the common case
+            // in sparse states, no call needed
+            const bool pz = ((__double_as_longlong(a.x) | __double_as_longlong(a.y) |
+                              __double_as_longlong(b.x) | __double_as_longlong(b.y)) == 0);
+            if (zc(oi)) oi = (pz && (g.pad & 1)) ? make_double2(0.0, 0.0) : slow2(g, 0, a, b);
+            if (zc(oj)) oj = (pz && (g.pad & 2)) ? make_double2(0.0, 0.0) : slow2(g, 1, a, b);
+        }
+        v[i] = oi;
+        v[j] = oj;
     }
 }
 
-__device__ __forceinline__ void apply2(double2 *s, uint32_t quarter, const TileGate &g,
-                                       uint32_t tid, uint32_t nth) {
-    const double2 *m = g.m;
-    const uint32_t lo = min(g.t0, g.t1), hi = max(g.t0, g.t1);
-    const uint32_t s0 = 1u << g.t0, s1 = 1u << g.t1;
-    for (uint32_t q = tid; q < quarter; q += nth) {
-        const uint32_t base = insert_zero_bit32(insert_zero_bit32(q, lo), hi);
-        const uint32_t idx[4] = {base, base | s1, base | s0, base | s0 | s1};
-        double2 in[4];
+// ---- 2-qubit signed permutations (CX CZ SWAP) on register bits (R0, R1) ----
+template <int R0, int R1>
+__device__ __forceinline__ void reg_apply2(double2 (&v)[NB], const TileGate &g) {
+    constexpr int lo = R0 < R1 ? R0 : R1, hi = R0 < R1 ? R1 : R0;
+    constexpr int s0 = 1 << R0, s1 = 1 << R1;
+    const uint32_t pc = g.perm;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) in[k] = s[idx[k]];
-        cplx out[4];
-        bool full = (g.cls & 0xff) != GC_PERM4;
-        if (!full) {
+    for (int q = 0; q < NB / 4; ++q) {
+        const int b = izb(izb(q, lo), hi);
+        const double2 in0 = v[b], in1 = v[b | s1], in2 = v[b | s0], in3 = v[b | s0 | s1];
+        double2 o[4];
+        bool anyz = false;
 #pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                const int c = (g.cls >> (8 + 2 * r)) & 3;  // the row's nonzero column
-                out[r] = cmul(m[4 * r + c].x, m[4 * r + c].y, in[c]);
-                full |= has_zero(out[r]);
-            }
+        for (int r = 0; r < 4; ++r) {
+            const uint32_t c = (pc >> (3 * r)) & 3, ng = (pc >> (3 * r + 2)) & 1;
+            o[r] = pm(c == 0 ? in0 : c == 1 ? in1 : c == 2 ? in2 : in3, ng);
+            anyz |= zc(o[r]);
         }
-        if (full) {
+        if (anyz) {
+            const bool pz = ((__double_as_longlong(in0.x) | __double_as_longlong(in0.y) |
+                              __double_as_longlong(in1.x) | __double_as_longlong(in1.y) |
+                              __double_as_longlong(in2.x) | __double_as_longlong(in2.y) |
+                              __double_as_longlong(in3.x) | __double_as_longlong(in3.y)) == 0);
 #pragma unroll
-            for (int r = 0; r < 4; ++r) out[r] = row4(m, r, in);
+            for (int r = 0; r < 4; ++r)
+                if (zc(o[r]))
+                    o[r] = (pz && ((g.pad >> r) & 1)) ? make_double2(0.0, 0.0)
+                                                      : slow4(g, r, in0, in1, in2, in3);
         }
-#pragma unroll
-        for (int r = 0; r < 4; ++r) s[idx[r]] = to2(out[r]);
+        v[b] = o[0];
+        v[b | s1] = o[1];
+        v[b | s0] = o[2];
+        v[b | s0 | s1] = o[3];
     }
 }
 
-__global__ void __launch_bounds__(256) tile_pass_kernel(double2 *__restrict__ buf,
-                                                        uint32_t nbits, PassDesc pd,
-                                                        const TileGate *__restrict__ gates,
-                                                        uint64_t ntiles) {
+#if QZ_REG_BITS == 3
+#define QZ_R1_CASES(X) X(0) X(1) X(2)
+#define QZ_R2_CASES(X) X(0, 1) X(0, 2) X(1, 0) X(1, 2) X(2, 0) X(2, 1)
+#else
+#define QZ_R1_CASES(X) X(0) X(1) X(2) X(3)
+#define QZ_R2_CASES(X)                                                               \
+    X(0, 1) X(0, 2) X(0, 3) X(1, 0) X(1, 2) X(1, 3) X(2, 0) X(2, 1) X(2, 3) X(3, 0)   \
+    X(3, 1) X(3, 2)
+#endif
+
+// ---- zero-free fast path ----------------------------------------------------
+// Valid while every component in the block is nonzero: moves are exact, and
+// the shortcut products are exact for nonzero results.  Any zero output sets
+// `bad`; the caller then redoes the whole group on the exact path.
+template <int R>
+__device__ __forceinline__ void fast_diag(double2 (&v)[NB], const TileGate &g, bool &bad) {
+    constexpr int sh = 1 << R;
+    const uint32_t k00 = uint32_t(g.kinds) & 15u, k11 = uint32_t(g.kinds >> 12) & 15u;
+    const double2 m00 = g.m[0], m11 = g.m[3];
+#pragma unroll
+    for (int p = 0; p < NB / 2; ++p) {
+        const int i = izb(p, R), j = i | sh;
+        if (k00 != CK_ONE) {
+            v[i] = term(k00, m00, v[i]);
+            bad |= zc(v[i]);
+        }
+        if (k11 != CK_ONE) {
+            v[j] = term(k11, m11, v[j]);
+            bad |= zc(v[j]);
+        }
+    }
+}
+
+template <int R>
+__device__ __forceinline__ void fast_gen1(double2 (&v)[NB], const TileGate &g, bool &bad) {
+    constexpr int sh = 1 << R;
+    const uint32_t kd = uint32_t(g.kinds);
+    const uint32_t k00 = kd & 15u, k01 = (kd >> 4) & 15u, k10 = (kd >> 8) & 15u, k11 = (kd >> 12) & 15u;
+    const double2 m00 = g.m[0], m01 = g.m[1], m10 = g.m[2], m11 = g.m[3];
+#pragma unroll
+    for (int p = 0; p < NB / 2; ++p) {
+        const int i = izb(p, R), j = i | sh;
+        const double2 a = v[i], b = v[j];
+        const double2 oi = k00 == CK_ZERO ? term(k01, m01, b)
+                         : (k01 == CK_ZERO ? term(k00, m00, a) : sum2(term(k00, m00, a), term(k01, m01, b)));
+        const double2 oj = k10 == CK_ZERO ? term(k11, m11, b)
+                         : (k11 == CK_ZERO ? term(k10, m10, a) : sum2(term(k10, m10, a), term(k11, m11, b)));
+        bad |= zc(oi) | zc(oj);
+        v[i] = oi;
+        v[j] = oj;
+    }
+}
+
+template <int C, int T>
+__device__ __forceinline__ void fast_cx(double2 (&v)[NB]) {
+#pragma unroll
+    for (int i = 0; i < NB; ++i)
+        if (((i >> C) & 1) && !((i >> T) & 1)) {
+            const double2 t = v[i];
+            v[i] = v[i | (1 << T)];
+            v[i | (1 << T)] = t;
+        }
+}
+
+template <int A, int B>
+__device__ __forceinline__ void fast_cz(double2 (&v)[NB]) {
+#pragma unroll
+    for (int i = 0; i < NB; ++i)
+        if (((i >> A) & 1) && ((i >> B) & 1)) v[i] = make_double2(dneg(v[i].x), dneg(v[i].y));
+}
+
+template <int A, int B>
+__device__ __forceinline__ void fast_swap(double2 (&v)[NB]) {
+#pragma unroll
+    for (int i = 0; i < NB; ++i)
+        if (((i >> A) & 1) && !((i >> B) & 1)) {
+            const int j = (i & ~(1 << A)) | (1 << B);
+            const double2 t = v[i];
+            v[i] = v[j];
+            v[j] = t;
+        }
+}
+
+#if QZ_REG_BITS == 3
+#define QZ_PAIRS(X) X(0, 1) X(0, 2) X(1, 2)
+#else
+#define QZ_PAIRS(X) X(0, 1) X(0, 2) X(0, 3) X(1, 2) X(1, 3) X(2, 3)
+#endif
+
+// Returns false if the gate could not be taken on the fast path at all.
+__device__ __forceinline__ void fast_apply(double2 (&v)[NB], const TileGate &g, bool &bad) {
+    const uint32_t op = g.op;
+    if (op == OP_DIAG || op == OP_GEN1) {
+        switch (g.r0) {
+#define X(a)                                                                                 \
+    case a:                                                                                  \
+        if (op == OP_DIAG) fast_diag<a>(v, g, bad);                                         \
+        else fast_gen1<a>(v, g, bad);                                                        \
+        break;
+            QZ_R1_CASES(X)
+#undef X
+        default: break;
+        }
+        return;
+    }
+    const uint32_t lo = min(g.r0, g.r1), hi = max(g.r0, g.r1);
+    if (op == OP_CX) {
+        switch (g.r0 * 4 + g.r1) {
+#define X(a, b)                                                                              \
+    case a * 4 + b: fast_cx<a, b>(v); break;
+            QZ_R2_CASES(X)
+#undef X
+        default: break;
+        }
+    } else if (op == OP_CZ) {
+        switch (lo * 4 + hi) {
+#define X(a, b)                                                                              \
+    case a * 4 + b: fast_cz<a, b>(v); break;
+            QZ_PAIRS(X)
+#undef X
+        default: break;
+        }
+    } else if (op == OP_SWAP) {
+        switch (lo * 4 + hi) {
+#define X(a, b)                                                                              \
+    case a * 4 + b: fast_swap<a, b>(v); break;
+            QZ_PAIRS(X)
+#undef X
+        default: break;
+        }
+    } else {
+        bad = true;  // other 2q matrices: exact path only
+    }
+}
+
+// ---- sign-mask mode for all-zero register blocks ----
+__host__ __device__ constexpr uint32_t low_positions(int R) {
+    uint32_t m = 0;
+    for (int i = 0; i < NB; ++i)
+        if (!((i >> R) & 1)) m |= 1u << i;
+    return m;
+}
+
+__device__ __forceinline__ void zero_terms(uint32_t sgn, int e, uint32_t xr, uint32_t xi,
+                                           uint32_t &re, uint32_t &im) {
+    const uint32_t mr = 0u - ((sgn >> (2 * e)) & 1u);
+    const uint32_t mi = 0u - ((sgn >> (2 * e + 1)) & 1u);
+    re &= (xr ^ mr) & ~(xi ^ mi);
+    im &= (xi ^ mr) & (xr ^ mi);
+}
+
+template <int R>
+__device__ __forceinline__ void mask_apply1(uint32_t &SR, uint32_t &SI, const TileGate &g) {
+    constexpr uint32_t LOW = low_positions(R);
+    constexpr int sh = 1 << R;
+    const uint32_t ar = SR & LOW, ai = SI & LOW;
+    const uint32_t br = (SR >> sh) & LOW, bi = (SI >> sh) & LOW;
+    uint32_t r0 = LOW, i0 = LOW, r1 = LOW, i1 = LOW;
+    zero_terms(g.sgn, 0, ar, ai, r0, i0);
+    zero_terms(g.sgn, 1, br, bi, r0, i0);
+    zero_terms(g.sgn, 2, ar, ai, r1, i1);
+    zero_terms(g.sgn, 3, br, bi, r1, i1);
+    SR = (r0 & LOW) | ((r1 & LOW) << sh);
+    SI = (i0 & LOW) | ((i1 & LOW) << sh);
+}
+
+template <int R0, int R1>
+__device__ __forceinline__ void mask_apply2(uint32_t &SR, uint32_t &SI, const TileGate &g) {
+    constexpr uint32_t BASE = low_positions(R0) & low_positions(R1);
+    constexpr int s0 = 1 << R0, s1 = 1 << R1;
+    const int off[4] = {0, s1, s0, s0 | s1};
+    uint32_t xr[4], xi[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        xr[c] = (SR >> off[c]) & BASE;
+        xi[c] = (SI >> off[c]) & BASE;
+    }
+    uint32_t nr = 0, ni = 0;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        uint32_t re = BASE, im = BASE;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) zero_terms(g.sgn, 4 * r + c, xr[c], xi[c], re, im);
+        nr |= (re & BASE) << off[r];
+        ni |= (im & BASE) << off[r];
+    }
+    SR = nr;
+    SI = ni;
+}
+
+
+__device__ __forceinline__ void reg_apply(double2 (&v)[NB], const TileGate &g) {
+    if (g.nq == 1) {
+        switch (g.r0) {
+#define X(a)                                                                                 \
+    case a: reg_apply1<a>(v, g); break;
+            QZ_R1_CASES(X)
+#undef X
+        default: break;
+        }
+        return;
+    }
+    switch (g.r0 * 4 + g.r1) {
+#define X(a, b)                                                                              \
+    case a * 4 + b: reg_apply2<a, b>(v, g); break;
+        QZ_R2_CASES(X)
+#undef X
+    default: break;
+    }
+}
+
+__device__ __forceinline__ void mask_apply(uint32_t &SR, uint32_t &SI, const TileGate &g) {
+    if (g.nq == 1) {
+        switch (g.r0) {
+#define X(a)                                                                                 \
+    case a: mask_apply1<a>(SR, SI, g); break;
+            QZ_R1_CASES(X)
+#undef X
+        default: break;
+        }
+        return;
+    }
+    switch (g.r0 * 4 + g.r1) {
+#define X(a, b)                                                                              \
+    case a * 4 + b: mask_apply2<a, b>(SR, SI, g); break;
+        QZ_R2_CASES(X)
+#undef X
+    default: break;
+    }
+}
+
+// Bank-conflict swizzle of the 16 B shared-memory slots inside each 128 B row.
+__device__ __forceinline__ uint32_t swz(uint32_t l) { return l ^ ((l >> 3) & 7u); }
+
+__device__ __forceinline__ uint32_t deposit32(uint32_t v, uint32_t mask) {
+    uint32_t out = 0;
+    while (mask) {
+        const uint32_t low = mask & (0u - mask);
+        if (v & 1) out |= low;
+        v >>= 1;
+        mask &= mask - 1;
+    }
+    return out;
+}
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
+// Generic gate straight on the shared-memory tile (any matrix; used for
+// 2-qubit gates that are not signed permutations — none in the reference
+// gate set — and kept exact with the full formula).
+__device__ void smem_generic(double2 *s, uint32_t tile, const TileGate &g) {
+    const uint32_t tid = threadIdx.x, nth = blockDim.x;
+    if (g.nq == 1) {
+        for (uint32_t p = tid; p < tile / 2; p += nth) {
+            const uint32_t i = insert_zero_bit32(p, g.t0), j = i | (1u << g.t0);
+            const double2 in[2] = {s[swz(i)], s[swz(j)]};
+            s[swz(i)] = full_row(g, 0, 2, in);
+            s[swz(j)] = full_row(g, 1, 2, in);
+        }
+    } else {
+        const uint32_t lo = min(g.t0, g.t1), hi = max(g.t0, g.t1);
+        const uint32_t s0 = 1u << g.t0, s1 = 1u << g.t1;
+        for (uint32_t p = tid; p < tile / 4; p += nth) {
+            const uint32_t b = insert_zero_bit32(insert_zero_bit32(p, lo), hi);
+            const uint32_t idx[4] = {b, b | s1, b | s0, b | s0 | s1};
+            double2 in[4];
+            for (int c = 0; c < 4; ++c) in[c] = s[swz(idx[c])];
+            for (int r = 0; r < 4; ++r) s[swz(idx[r])] = full_row(g, r, 4, in);
+        }
+    }
+}
+
+// One fused pass: tile of 2^k amplitudes (k >= kRegBits) in shared memory;
+// each group is applied by 2^(k-kRegBits) threads holding NB amplitudes in
+// registers.  Every thread moves exactly NB amplitudes per tile in each
+// direction, all issued before any is consumed (cp.async in, batched stores).
+__global__ void __launch_bounds__(1 << (12 - kRegBits), 1) tile_pass_reg(double2 *__restrict__ buf, uint32_t nbits,
+                                                         PassDesc pd,
+                                                         const GroupDesc *__restrict__ groups,
+                                                         const TileGate *__restrict__ gates,
+                                                         uint64_t ntiles,
+                                                         unsigned long long *__restrict__ counters) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double2 *s = reinterpret_cast<double2 *>(smem_raw);
     const uint32_t k = pd.k, L = pd.lowbits;
     const uint32_t tile = 1u << k;
     uint64_t *offhi = reinterpret_cast<uint64_t *>(s + tile);
     const uint32_t nhi = 1u << (k - L);
-    const uint64_t all = nbits >= 64 ? ~uint64_t(0) : ((uint64_t(1) << nbits) - 1);
+    const uint64_t all = (uint64_t(1) << nbits) - 1;
     const uint64_t ntmask = all & ~pd.tmask;
     const uint64_t himask = pd.tmask & ~((uint64_t(1) << L) - 1);
     const uint32_t lowmask = (1u << L) - 1;
-    const uint32_t tid = threadIdx.x, nth = blockDim.x;
+    const uint32_t tid = threadIdx.x, nth = blockDim.x;   // nth == tile / NB
     for (uint32_t h = tid; h < nhi; h += nth) offhi[h] = deposit_bits(h, himask);
+    __syncthreads();
     for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const uint64_t base = deposit_bits(t, ntmask);
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+            const uint32_t l = tid + i * nth;
+            cp_async16(s + swz(l), buf + base + offhi[l >> L] + (l & lowmask));
+        }
+        cp_async_wait_all();
         __syncthreads();
-        for (uint32_t l = tid; l < tile; l += nth)
-            s[l] = __ldcs(buf + base + offhi[l >> L] + (l & lowmask));
-        __syncthreads();
-        for (uint32_t gi = 0; gi < pd.ngates; ++gi) {
-            const TileGate &g = gates[pd.first_gate + gi];
-            if (g.nq == 1) apply1(s, tile >> 1, g.t0, g, tid, nth);
-            else apply2(s, tile >> 2, g, tid, nth);
+        if (pd.pz_stable) {
+            // an all-(+0) tile is a fixed point of the whole pass: skip it
+            unsigned long long any = 0;
+#pragma unroll
+            for (int i = 0; i < NB; ++i) {
+                const double2 x = s[swz(tid + i * nth)];
+                any |= (unsigned long long)__double_as_longlong(x.x) |
+                       (unsigned long long)__double_as_longlong(x.y);
+            }
+            if (!__syncthreads_or(any != 0)) {
+                if (counters && tid == 0) atomicAdd(&counters[0], 1ull);
+                continue;
+            }
+        }
+        for (uint32_t gi = 0; gi < pd.ngroups; ++gi) {
+            const GroupDesc &G = groups[pd.first_group + gi];
+            const TileGate *gp = gates + G.first_gate;
+            if (G.generic) {
+                for (uint32_t q = 0; q < G.ngates; ++q) {
+                    smem_generic(s, tile, gp[q]);
+                    __syncthreads();
+                }
+                continue;
+            }
+            uint32_t bm[kRegBits], gm = 0;
+#pragma unroll
+            for (int i = 0; i < kRegBits; ++i) {
+                bm[i] = 1u << G.gbits[i];
+                gm |= bm[i];
+            }
+            const uint32_t mybase = deposit32(tid, (tile - 1) & ~gm);
+            uint32_t addr[NB];
+#pragma unroll
+            for (int r = 0; r < NB; ++r) {
+                uint32_t a = mybase;
+#pragma unroll
+                for (int i = 0; i < kRegBits; ++i)
+                    if ((r >> i) & 1) a |= bm[i];
+                addr[r] = swz(a);
+            }
+            double2 v[NB];
+#pragma unroll
+            for (int r = 0; r < NB; ++r) v[r] = s[addr[r]];
+            unsigned long long nz = 0, raw = 0;
+#pragma unroll
+            for (int r = 0; r < NB; ++r) {
+                raw |= (unsigned long long)__double_as_longlong(v[r].x) |
+                       (unsigned long long)__double_as_longlong(v[r].y);
+                nz |= ((unsigned long long)__double_as_longlong(v[r].x) << 1) |
+                      ((unsigned long long)__double_as_longlong(v[r].y) << 1);
+            }
+            int path = 1;
+            if (raw == 0 && G.pz_stable) {
+                // all-(+0) block, every gate keeps it all-(+0): nothing to do
+            } else if (nz == 0) {
+                path = 2;
+                // all-zero block: stays zero, track the zero signs only
+                uint32_t SR = 0, SI = 0;
+#pragma unroll
+                for (int r = 0; r < NB; ++r) {
+                    SR |= sbit(v[r].x) << r;
+                    SI |= sbit(v[r].y) << r;
+                }
+                for (uint32_t q = 0; q < G.ngates; ++q) mask_apply(SR, SI, gp[q]);
+#pragma unroll
+                for (int r = 0; r < NB; ++r)
+                    v[r] = make_double2(signed_zero((SR >> r) & 1), signed_zero((SI >> r) & 1));
+            } else {
+                bool zfree = true;
+#pragma unroll
+                for (int r = 0; r < NB; ++r) zfree &= !zc(v[r]);
+                bool bad = !zfree;
+                path = zfree ? 3 : 4;
+                for (uint32_t q = 0; q < G.ngates && !bad; ++q) fast_apply(v, gp[q], bad);
+                if (bad && zfree) path = 5;
+                if (bad) {
+                    // a zero is (or became) present: redo the group exactly
+#pragma unroll
+                    for (int r = 0; r < NB; ++r) v[r] = s[addr[r]];
+                    for (uint32_t q = 0; q < G.ngates; ++q) reg_apply(v, gp[q]);
+                }
+            }
+            if (!(raw == 0 && G.pz_stable)) {
+#pragma unroll
+                for (int r = 0; r < NB; ++r) s[addr[r]] = v[r];
+            }
+            if (counters) atomicAdd(&counters[path], 1ull);
             __syncthreads();
         }
-        for (uint32_t l = tid; l < tile; l += nth)
-            __stcs(buf + base + offhi[l >> L] + (l & lowmask), s[l]);
+        double2 out[NB];
+#pragma unroll
+        for (int i = 0; i < NB; ++i) out[i] = s[swz(tid + i * nth)];
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+            const uint32_t l = tid + i * nth;
+            __stcs(buf + base + offhi[l >> L] + (l & lowmask), out[i]);
+        }
+        __syncthreads();
+    }
+}
+
+// Buffers below 16 amplitudes: one thread, dense formula.
+__global__ void tile_pass_tiny(double2 *buf, uint32_t nbits, PassDesc pd,
+                               const TileGate *__restrict__ gates) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const uint32_t n = 1u << nbits;
+    for (uint32_t q = 0; q < pd.ngates; ++q) {
+        const TileGate &g = gates[pd.first_gate + q];
+        if (g.nq == 1) {
+            for (uint32_t p = 0; p < n / 2; ++p) {
+                const uint32_t i = insert_zero_bit32(p, g.t0), j = i | (1u << g.t0);
+                const double2 in[2] = {buf[i], buf[j]};
+                buf[i] = full_row(g, 0, 2, in);
+                buf[j] = full_row(g, 1, 2, in);
+            }
+        } else {
+            const uint32_t lo = min(g.t0, g.t1), hi = max(g.t0, g.t1);
+            const uint32_t s0 = 1u << g.t0, s1 = 1u << g.t1;
+            for (uint32_t p = 0; p < n / 4; ++p) {
+                const uint32_t b = insert_zero_bit32(insert_zero_bit32(p, lo), hi);
+                const uint32_t idx[4] = {b, b | s1, b | s0, b | s0 | s1};
+                const double2 in[4] = {buf[idx[0]], buf[idx[1]], buf[idx[2]], buf[idx[3]]};
+                for (int r = 0; r < 4; ++r) buf[idx[r]] = full_row(g, r, 4, in);
+            }
+        }
     }
 }
 
 } // namespace
 
+// QZ_DEBUG_COUNTERS=1: count tile skips and per-group paths
+// [0] tiles skipped, [1] +0 groups skipped, [2] sign-mask, [3] fast,
+// [4] exact (zero at entry), [5] fast then exact
+unsigned long long *debug_counters() {
+    static unsigned long long *ptr = nullptr;
+    static bool init = false;
+    if (!init) {
+        init = true;
+        const char *e = getenv("QZ_DEBUG_COUNTERS");
+        if (e && *e == '1') {
+            QZ_CUDA(cudaMalloc(&ptr, 8 * 8));
+            QZ_CUDA(cudaMemset(ptr, 0, 8 * 8));
+        }
+    }
+    return ptr;
+}
+
+void dump_debug_counters() {
+    unsigned long long *p = debug_counters();
+    if (!p) return;
+    unsigned long long h[8];
+    QZ_CUDA(cudaMemcpy(h, p, sizeof h, cudaMemcpyDeviceToHost));
+    fprintf(stderr, "qz counters: tiles_skipped=%llu grp_pz_skip=%llu grp_mask=%llu grp_fast=%llu "
+                    "grp_exact=%llu grp_fast_then_exact=%llu\n",
+            h[0], h[1], h[2], h[3], h[4], h[5]);
+    QZ_CUDA(cudaMemset(p, 0, sizeof h));
+}
+
 uint64_t run_passes(const DevPlan &plan, double2 *buf, uint32_t nbits, cudaStream_t s) {
+    static bool attr_set = false;
+    if (!attr_set) {
+        QZ_CUDA(cudaFuncSetAttribute(tile_pass_reg, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     110 * 1024));
+        attr_set = true;
+    }
     uint64_t launches = 0;
     for (const PassDesc &pd : plan.host_passes) {
-        const uint32_t tile = 1u << pd.k;
-        const uint64_t ntiles = uint64_t(1) << (nbits - pd.k);
-        const uint32_t threads = std::max<uint32_t>(32, std::min<uint32_t>(256, tile / 2));
-        const size_t smem = sizeof(double2) * tile + sizeof(uint64_t) * (tile >> pd.lowbits);
-        static bool attr_set = false;
-        if (!attr_set) {
-            QZ_CUDA(cudaFuncSetAttribute(tile_pass_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         96 * 1024));
-            attr_set = true;
+        if (pd.k < (uint32_t)kRegBits + 1) {
+            // tile == whole buffer (nbits < 4)
+            tile_pass_tiny<<<1, 32, 0, s>>>(buf, nbits, pd, plan.gates);
+        } else {
+            const uint32_t tile = 1u << pd.k;
+            const uint64_t ntiles = uint64_t(1) << (nbits - pd.k);
+            const uint32_t threads = tile >> kRegBits;
+            const size_t smem = sizeof(double2) * tile + sizeof(uint64_t) * (tile >> pd.lowbits);
+            const uint64_t grid = std::min<uint64_t>(ntiles, uint64_t(kNumSMs) * 2 * 8);
+            tile_pass_reg<<<(unsigned)grid, threads, smem, s>>>(buf, nbits, pd, plan.groups,
+                                                               plan.gates, ntiles, debug_counters());
         }
-        const uint64_t grid = std::min<uint64_t>(ntiles, uint64_t(kNumSMs) * 16);
-        tile_pass_kernel<<<(unsigned)grid, threads, smem, s>>>(buf, nbits, pd, plan.gates, ntiles);
         QZ_CHECK_LAUNCH();
         ++launches;
     }

@@ -7,42 +7,79 @@
 
 namespace qz {
 
+// Coefficient kinds of a matrix entry; the kernel evaluates each product
+// with the cheapest form that is exact for NONZERO results (see qz_gates.cu).
+enum CoefKind : uint32_t { CK_ZERO = 0, CK_ONE = 1, CK_NEG = 2, CK_REAL = 3, CK_IMAG = 4, CK_CPLX = 5 };
+
 // One gate with its host-computed matrix (gates.cpp:114-182) on buffer bits.
 struct DevGate {
     uint32_t nq;       // 1 or 2
     uint32_t b0, b1;   // buffer bits (b0 = first listed = matrix high bit)
-    uint32_t cls;      // structure class, see GateClass
+    uint32_t dim;
+    uint64_t kinds;    // 4 bits per entry, row-major
+    uint32_t sgn;      // 2 bits per entry: bit 2e = sign(re), 2e+1 = sign(im)
+    uint32_t op;       // GateOp: structure used by the zero-free fast path
     double2 m[16];     // row-major, dim = 2 or 4
 };
 
-// Structure classes let the kernel skip exactly-zero coefficients.  A term
-// with coefficient exactly 0 contributes ±0, which can only change the SIGN
-// of an exactly-zero result; any such result is recomputed with the full
-// formula, so every class is bit-identical to the dense formula.
+// Matrix structure for the zero-free register fast path.  CX / CZ / SWAP are
+// recognised by value (their ±0 entries only ever matter for zero outputs,
+// which the fast path never produces without falling back).
+enum GateOp : uint32_t { OP_GEN1 = 0, OP_DIAG = 1, OP_CX = 2, OP_CZ = 3, OP_SWAP = 4, OP_GEN2 = 5 };
+
+// A gate inside a register group: r0/r1 are the gate's qubits as bit
+// positions of the thread's 16-amplitude register block.
+struct TileGate {
+    uint32_t nq, r0, r1, t0, t1;  // t0/t1: tile-local bits (tiny-buffer path)
+    uint32_t sgn;
+    uint64_t kinds;
+    uint32_t cls;                 // GateClass
+    uint32_t perm;                // TG_PERM: per row 2 bits column + 1 bit negate
+    uint32_t zm;                  // bit e: Re m_e == 0; bit 16+e: Im m_e == 0
+    uint32_t smask;               // bit e: sign(Re m_e); bit 16+e: sign(Im m_e)
+    uint32_t op;                  // GateOp
+    uint32_t pad;
+    double2 m[16];
+};
+
+// Gate structure for the register fast path.
 enum GateClass : uint32_t {
-    GC_DENSE = 0,   // general matrix
-    GC_DIAG = 1,    // 1q: m01 == m10 == 0       (Z S T U1 RZ SDG TDG)
-    GC_ANTI = 2,    // 1q: m00 == m11 == 0       (X Y)
-    GC_PERM4 = 3,   // 2q: one nonzero per row   (CX CZ SWAP)
+    TG_GEN = 0,    // general: per-entry kinds
+    TG_PERM = 1,   // each row has one nonzero entry, exactly +1 or -1 (X CX CZ SWAP Z)
+    TG_DIAG = 2,   // 1q diagonal (U1 S T SDG TDG RZ)
+};
+
+// Register block of the fused pass: each thread applies a group's gates to
+// 2^kRegBits amplitudes held in registers.
+#ifndef QZ_REG_BITS
+#define QZ_REG_BITS 3
+#endif
+constexpr int kRegBits = QZ_REG_BITS;
+
+// Consecutive gates whose qubits fit kRegBits tile bits: applied in registers.
+struct GroupDesc {
+    uint32_t gbits[4];     // tile-local bits, ascending; register bit i <-> gbits[i]
+    uint32_t first_gate, ngates;
+    uint32_t generic;      // 1: apply on the smem tile with the full formula
+    uint32_t pz_stable;    // every gate maps an all-(+0) block to all-(+0)
 };
 
 // A fused pass: gates whose buffer bits all lie in the tile bit set T.
 struct PassDesc {
     uint32_t k;            // tile bits (|T|)
     uint32_t lowbits;      // T ⊇ {0..lowbits-1}
-    uint32_t first_gate;   // into the pass-local gate array
+    uint32_t first_group;
+    uint32_t ngroups;
+    uint32_t first_gate;   // for the smem fallback (k < 4)
     uint32_t ngates;
     uint64_t tmask;        // T as a bit mask over buffer bits
-};
-
-// Pass-local gate: bits are positions inside the tile.
-struct TileGate {
-    uint32_t nq, t0, t1, cls;
-    double2 m[16];
+    uint32_t pz_stable;    // all groups pz_stable: an all-(+0) tile is left untouched
+    uint32_t pad;
 };
 
 struct GatePlan {
     std::vector<PassDesc> passes;
+    std::vector<GroupDesc> groups;
     std::vector<TileGate> gates;
 };
 
@@ -53,16 +90,16 @@ uint32_t gate_nparams(uint32_t kind);
 
 // Host: greedy in-order fusion of gates (already on buffer bits) into passes
 // over a buffer of 2^nbits amplitudes with tiles of at most 2^kmax.
-GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits,
-                      uint32_t kmax, bool fuse);
+GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_t kmax,
+                      bool fuse);
 
 DevGate make_dev_gate(const qzc_gate &g);
 
 // Device-resident copy of a GatePlan.
 struct DevPlan {
-    PassDesc *passes = nullptr;
     TileGate *gates = nullptr;
-    size_t npasses = 0, ngates = 0;
+    GroupDesc *groups = nullptr;
+    size_t ngates = 0, ngroups = 0;
     std::vector<PassDesc> host_passes;
 };
 void upload_plan(const GatePlan &plan, DevPlan &out, cudaStream_t s);
@@ -70,7 +107,7 @@ void free_plan(DevPlan &p);
 
 // Launch every pass of `plan` over buf (2^nbits amplitudes).  Returns the
 // number of kernel launches.
-uint64_t run_passes(const DevPlan &plan, double2 *buf, uint32_t nbits,
-                    cudaStream_t s);
+uint64_t run_passes(const DevPlan &plan, double2 *buf, uint32_t nbits, cudaStream_t s);
+void dump_debug_counters();
 
 } // namespace qz

@@ -191,6 +191,7 @@ struct qzc_context {
     Window win;                       // scratch for the host codec / gate entry points
     DevBuf arena, table_off, table_len, table_crc, forced, used;
     std::mutex mu;
+    cudaEvent_t t_begin = nullptr, t_end = nullptr;
 
     void check_status(uint64_t index_base = 0) {
         QZ_CUDA(cudaMemcpyAsync(status_host, status, sizeof(DevStatus), cudaMemcpyDeviceToHost, stream));
@@ -402,6 +403,8 @@ void qzc_context_destroy(qzc_context *ctx) {
     for (DevBuf *b : {&ctx->arena, &ctx->table_off, &ctx->table_len, &ctx->table_crc, &ctx->forced, &ctx->used})
         b->release();
     free_codec_tables(ctx->tabs);
+    if (ctx->t_begin) cudaEventDestroy(ctx->t_begin);
+    if (ctx->t_end) cudaEventDestroy(ctx->t_end);
     cudaFree(ctx->status);
     cudaFreeHost(ctx->status_host);
     cudaStreamDestroy(ctx->stream);
@@ -415,6 +418,28 @@ int qzc_synchronize(qzc_context *ctx) {
 }
 
 uint64_t qzc_kernel_launches(const qzc_context *ctx) { return ctx ? ctx->launches : 0; }
+
+int qzc_timer_begin(qzc_context *ctx) {
+    QZ_API_BEGIN
+    QZ_CUDA(cudaSetDevice(ctx->device));
+    if (!ctx->t_begin) {
+        QZ_CUDA(cudaEventCreate(&ctx->t_begin));
+        QZ_CUDA(cudaEventCreate(&ctx->t_end));
+    }
+    QZ_CUDA(cudaEventRecord(ctx->t_begin, ctx->stream));
+    QZ_API_END
+}
+
+int qzc_timer_end(qzc_context *ctx, double *seconds_out) {
+    QZ_API_BEGIN
+    if (!ctx->t_begin) throw Failure(QZC_EINVAL, "timer not started");
+    QZ_CUDA(cudaEventRecord(ctx->t_end, ctx->stream));
+    QZ_CUDA(cudaEventSynchronize(ctx->t_end));
+    float ms = 0;
+    QZ_CUDA(cudaEventElapsedTime(&ms, ctx->t_begin, ctx->t_end));
+    *seconds_out = ms * 1e-3;
+    QZ_API_END
+}
 
 // ---- codec entry points ----------------------------------------------------
 
@@ -780,6 +805,7 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
     }
     QZ_CUDA(cudaStreamSynchronize(s));
     sim->stats.wall_seconds += now_s() - t0;
+    dump_debug_counters();
     sim->stats.kernel_launches += ctx->launches - launches0;
     QZ_API_END
 }

@@ -71,6 +71,8 @@ def load_library() -> C.CDLL:
         "qzc_synchronize": (C.c_int, [C.c_void_p]),
         "qzc_kernel_launches": (C.c_uint64, [C.c_void_p]),
         "qzc_payload_bound": (C.c_uint64, [C.c_uint64, C.c_double]),
+        "qzc_timer_begin": (C.c_int, [C.c_void_p]),
+        "qzc_timer_end": (C.c_int, [C.c_void_p, f64p]),
         "qzc_compress_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64,
                                         C.c_double, u64p, C.c_uint64, u8p, C.c_uint64, u64p,
                                         u32p, u32p]),
@@ -150,6 +152,15 @@ class Engine:
     @property
     def kernel_launches(self) -> int:
         return int(self.lib.qzc_kernel_launches(self.h))
+
+    def timer_begin(self) -> None:
+        _check(self.lib.qzc_timer_begin(self.h))
+
+    def timer_end(self) -> float:
+        """Seconds between timer_begin and now, CUDA events on the engine stream."""
+        out = C.c_double()
+        _check(self.lib.qzc_timer_end(self.h, C.byref(out)))
+        return out.value
 
     # ---- gates ---------------------------------------------------------------
     def gate_matrix(self, g) -> np.ndarray:

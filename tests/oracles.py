@@ -11,8 +11,11 @@ import ctypes as C
 import os
 from pathlib import Path
 
+import sys
+
 import numpy as np
 
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2309_16979_b200.abi import Gate, gate_ptr, to_array
 
 ROOT = Path(__file__).resolve().parents[1]
