@@ -180,6 +180,29 @@ static bool maps_pos_zero(const DevGate &g) {
     return true;
 }
 
+// Row r is "+0-safe" if it has a structural entry whose product can only be
+// a +0 zero when its input has no -0 component: kind ONE, REAL or CPLX with
+// a real part of sign 0 (then m_r*(+0) = +0 and x - (±0), x + (±0) keep +0).
+// The row's exact value is then either nonzero (and equal to the shortcut
+// sum) or +0, which the shortcut also yields.  Gates with a nonzero
+// coefficient part below 2^-100 get no safe rows (products must not
+// underflow for the argument to hold).
+static uint32_t safe_rows(const DevGate &g) {
+    for (uint32_t e = 0; e < g.dim * g.dim; ++e) {
+        const double re = std::fabs(g.m[e].x), im = std::fabs(g.m[e].y);
+        if ((re != 0.0 && re < 0x1p-100) || (im != 0.0 && im < 0x1p-100)) return 0;
+    }
+    uint32_t out = 0;
+    for (uint32_t r = 0; r < g.dim; ++r)
+        for (uint32_t c = 0; c < g.dim; ++c) {
+            const uint32_t e = r * g.dim + c;
+            const uint32_t kd = uint32_t(g.kinds >> (4 * e)) & 15;
+            if ((kd == CK_ONE || kd == CK_REAL || kd == CK_CPLX) && !std::signbit(g.m[e].x))
+                out |= 1u << r;
+        }
+    return out;
+}
+
 static bool is_signed_perm(const DevGate &g) {
     for (uint32_t r = 0; r < g.dim; ++r) {
         int nz = 0;
@@ -264,6 +287,8 @@ GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_
                     t.smask |= uint32_t(std::signbit(g.m[e].y)) << (16 + e);
                 }
                 t.op = g.op;
+                t.srow = safe_rows(g);
+                t.pad2 = 0;
                 t.pad = 0;   // bit r: row r maps all-(+0) inputs to (+0, +0)
                 for (uint32_t r = 0; r < g.dim; ++r) {
                     uint32_t nre = 1, nim = 1;
@@ -566,16 +591,17 @@ __device__ __forceinline__ void fast_diag(double2 (&v)[NB], const TileGate &g, b
     constexpr int sh = 1 << R;
     const uint32_t k00 = uint32_t(g.kinds) & 15u, k11 = uint32_t(g.kinds >> 12) & 15u;
     const double2 m00 = g.m[0], m11 = g.m[3];
+    const bool u0 = !(g.srow & 1), u1 = !(g.srow & 2);   // unsafe rows: check zeros
 #pragma unroll
     for (int p = 0; p < NB / 2; ++p) {
         const int i = izb(p, R), j = i | sh;
         if (k00 != CK_ONE) {
             v[i] = term(k00, m00, v[i]);
-            bad |= zc(v[i]);
+            if (u0) bad |= zc(v[i]);
         }
         if (k11 != CK_ONE) {
             v[j] = term(k11, m11, v[j]);
-            bad |= zc(v[j]);
+            if (u1) bad |= zc(v[j]);
         }
     }
 }
@@ -594,7 +620,8 @@ __device__ __forceinline__ void fast_gen1(double2 (&v)[NB], const TileGate &g, b
                          : (k01 == CK_ZERO ? term(k00, m00, a) : sum2(term(k00, m00, a), term(k01, m01, b)));
         const double2 oj = k10 == CK_ZERO ? term(k11, m11, b)
                          : (k11 == CK_ZERO ? term(k10, m10, a) : sum2(term(k10, m10, a), term(k11, m11, b)));
-        bad |= zc(oi) | zc(oj);
+        if (!(g.srow & 1)) bad |= zc(oi);
+        if (!(g.srow & 2)) bad |= zc(oj);
         v[i] = oi;
         v[j] = oj;
     }
@@ -612,10 +639,13 @@ __device__ __forceinline__ void fast_cx(double2 (&v)[NB]) {
 }
 
 template <int A, int B>
-__device__ __forceinline__ void fast_cz(double2 (&v)[NB]) {
+__device__ __forceinline__ void fast_cz(double2 (&v)[NB], bool &bad) {
 #pragma unroll
     for (int i = 0; i < NB; ++i)
-        if (((i >> A) & 1) && ((i >> B) & 1)) v[i] = make_double2(dneg(v[i].x), dneg(v[i].y));
+        if (((i >> A) & 1) && ((i >> B) & 1)) {
+            v[i] = make_double2(dneg(v[i].x), dneg(v[i].y));
+            bad |= zc(v[i]);   // the -1 row is not +0-safe
+        }
 }
 
 template <int A, int B>
@@ -664,7 +694,7 @@ __device__ __forceinline__ void fast_apply(double2 (&v)[NB], const TileGate &g, 
     } else if (op == OP_CZ) {
         switch (lo * 4 + hi) {
 #define X(a, b)                                                                              \
-    case a * 4 + b: fast_cz<a, b>(v); break;
+    case a * 4 + b: fast_cz<a, b>(v, bad); break;
             QZ_PAIRS(X)
 #undef X
         default: break;
@@ -925,13 +955,20 @@ __global__ void __launch_bounds__(1 << (12 - kRegBits), 1) tile_pass_reg(double2
                 for (int r = 0; r < NB; ++r)
                     v[r] = make_double2(signed_zero((SR >> r) & 1), signed_zero((SI >> r) & 1));
             } else {
-                bool zfree = true;
+                // fast path precondition: no -0 component and every nonzero
+                // component in [2^-900, 2^1023] (no underflow, no inf/nan)
+                bool okblk = true;
 #pragma unroll
-                for (int r = 0; r < NB; ++r) zfree &= !zc(v[r]);
-                bool bad = !zfree;
-                path = zfree ? 3 : 4;
+                for (int r = 0; r < NB; ++r) {
+                    const uint64_t xr = (uint64_t)__double_as_longlong(v[r].x);
+                    const uint64_t xi = (uint64_t)__double_as_longlong(v[r].y);
+                    const uint32_t er = uint32_t(xr >> 52) & 0x7ff, ei = uint32_t(xi >> 52) & 0x7ff;
+                    okblk &= (xr == 0 || (er >= 123 && er < 2047)) && (xi == 0 || (ei >= 123 && ei < 2047));
+                }
+                bool bad = !okblk;
+                path = okblk ? 3 : 4;
                 for (uint32_t q = 0; q < G.ngates && !bad; ++q) fast_apply(v, gp[q], bad);
-                if (bad && zfree) path = 5;
+                if (bad && okblk) path = 5;
                 if (bad) {
                     // a zero is (or became) present: redo the group exactly
 #pragma unroll

@@ -38,7 +38,9 @@ struct TileGate {
     uint32_t zm;                  // bit e: Re m_e == 0; bit 16+e: Im m_e == 0
     uint32_t smask;               // bit e: sign(Re m_e); bit 16+e: sign(Im m_e)
     uint32_t op;                  // GateOp
-    uint32_t pad;
+    uint32_t pad;                 // bit r: row r maps all-(+0) inputs to (+0,+0)
+    uint32_t srow;                // bit r: row r is "+0-safe" (see qz_gates.cu)
+    uint32_t pad2;
     double2 m[16];
 };
 
