@@ -15,7 +15,21 @@ CPP_SRCS := $(wildcard $(SRC)/*.cpp)
 HDRS := $(wildcard $(SRC)/*.cuh) include/qzcuda.h
 OBJS := $(patsubst $(SRC)/%.cu,$(OBJ)/%.o,$(CU_SRCS)) $(patsubst $(SRC)/%.cpp,$(OBJ)/%.o,$(CPP_SRCS))
 
-all: $(LIB) oracle
+HOSTLIB := $(PKG)/lib/libqzsim_b200.so
+HOST_SRCS := $(wildcard $(PKG)/host/*.cpp)
+HOST_OBJS := $(patsubst $(PKG)/host/%.cpp,$(OBJ)/host_%.o,$(HOST_SRCS))
+QZSIM_HDRS := $(wildcard include/qzsim/*.hpp) $(wildcard $(PKG)/host/*.hpp)
+
+all: $(LIB) $(HOSTLIB) oracle
+
+$(OBJ)/host_%.o: $(PKG)/host/%.cpp $(QZSIM_HDRS) include/qzcuda.h
+	@mkdir -p $(OBJ)
+	g++ -std=gnu++20 -O2 -fPIC -Wall -Iinclude -c $< -o $@
+
+# The C++ drop-in layer (include/qzsim/*.hpp) over the C ABI.
+$(HOSTLIB): $(HOST_OBJS) $(LIB)
+	g++ -shared -o $@ $(HOST_OBJS) -L$(PKG)/lib -lqzcuda -Wl,-rpath,'$$ORIGIN'
+
 
 $(OBJ)/%.o: $(SRC)/%.cu $(HDRS)
 	@mkdir -p $(OBJ)

@@ -126,6 +126,45 @@ int qzc_apply_gates_host(qzc_context *ctx, double *amps, uint32_t nbits,
 int qzc_apply_gates_dev(qzc_context *ctx, double *amps_dev, uint32_t nbits,
                         const qzc_gate *gates, uint64_t ngates);
 
+/* A gate given by an explicit matrix (qzsim::GateMatrix, gates.hpp:64-71):
+ * dim 2 or 4, row-major interleaved complex, qubits[0] = high matrix bit. */
+typedef struct qzc_matrix_gate {
+    uint32_t dim;
+    uint32_t qubits[2];
+    uint32_t reserved;
+    double m[32];
+} qzc_matrix_gate;
+/* apply_single_qubit / apply_two_qubit with caller matrices (kernels.cpp:20-54). */
+int qzc_apply_matrices_host(qzc_context *ctx, double *amps, uint32_t nbits,
+                            const qzc_matrix_gate *gates, uint64_t ngates);
+int qzc_apply_matrices_dev(qzc_context *ctx, double *amps_dev, uint32_t nbits,
+                           const qzc_matrix_gate *gates, uint64_t ngates);
+
+/* ---- device buffers (replaces ReferenceDevice's buffer / staging,
+ *      device.cpp:120-255, 404-449) --------------------------------------- */
+/* All operations are stream-ordered on the context stream (the in-order
+ * command queue of device.hpp:59-60); qzc_synchronize() waits for them. */
+int qzc_buffer_alloc(qzc_context *ctx, uint64_t amps, double **dev_out);
+void qzc_buffer_free(qzc_context *ctx, double *dev);
+/* Copy `amps` amplitudes host -> device at dev[dev_offset ...]. */
+int qzc_copy_h2d(qzc_context *ctx, double *dev, uint64_t dev_offset, const double *host,
+                 uint64_t amps);
+/* Copy `amps` amplitudes device -> host from dev[dev_offset ...]. */
+int qzc_copy_d2h(qzc_context *ctx, double *host, const double *dev, uint64_t dev_offset,
+                 uint64_t amps);
+/* Device-side mapping pass dst[i] = src[i] (the Buffered strategy's
+ * permutation, an identity over the gather layout, device.cpp:436-449). */
+int qzc_permute(qzc_context *ctx, double *dst, const double *src, uint64_t amps);
+/* Page-locked host memory for staging (cudaMallocHost). */
+int qzc_host_alloc(qzc_context *ctx, uint64_t bytes, void **host_out);
+void qzc_host_free(qzc_context *ctx, void *host);
+/* Event-timed region on the context stream, for TransferStats. */
+int qzc_event_record(qzc_context *ctx, void **event_out);
+int qzc_event_elapsed(qzc_context *ctx, void *start, void *end, double *seconds_out);
+void qzc_event_destroy(qzc_context *ctx, void *event);
+/* 1 if the event has completed, 0 if work before it is still pending. */
+int qzc_event_done(qzc_context *ctx, void *event);
+
 /* ---- simulator (replaces qzsim::run, pipeline.cpp:128-314) -------------- */
 typedef struct qzc_sim qzc_sim;
 

@@ -123,14 +123,22 @@ static uint32_t coef_kind(double2 v) {
 }
 
 DevGate make_dev_gate(const qzc_gate &g) {
+    double2 m[16];
+    uint32_t dim = 0;
+    gate_matrix_host(g, m, &dim);
+    return make_dev_gate_matrix(m, dim, g.qubits[0], dim == 4 ? g.qubits[1] : 0);
+}
+
+DevGate make_dev_gate_matrix(const double2 *mat, uint32_t dim, uint32_t b0, uint32_t b1) {
+    if (dim != 2 && dim != 4) throw Failure(QZC_EINVAL, "gate matrix dim must be 2 or 4");
     DevGate d;
     std::memset(&d, 0, sizeof d);
-    uint32_t dim = 0;
-    gate_matrix_host(g, d.m, &dim);
+    for (uint32_t e = 0; e < dim * dim; ++e) d.m[e] = mat[e];
     d.dim = dim;
     d.nq = dim == 2 ? 1 : 2;
-    d.b0 = g.qubits[0];
-    d.b1 = d.nq == 2 ? g.qubits[1] : 0;
+    d.b0 = b0;
+    d.b1 = d.nq == 2 ? b1 : 0;
+    if (d.nq == 2 && b0 == b1) throw Failure(QZC_EINVAL, "duplicate qubit in two-qubit gate");
     for (uint32_t e = 0; e < dim * dim; ++e) {
         d.kinds |= uint64_t(coef_kind(d.m[e])) << (4 * e);
         d.sgn |= uint32_t(std::signbit(d.m[e].x)) << (2 * e);

@@ -96,6 +96,7 @@ GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_
                       bool fuse);
 
 DevGate make_dev_gate(const qzc_gate &g);
+DevGate make_dev_gate_matrix(const double2 *m, uint32_t dim, uint32_t b0, uint32_t b1);
 
 // Device-resident copy of a GatePlan.
 struct DevPlan {

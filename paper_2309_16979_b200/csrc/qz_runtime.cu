@@ -543,6 +543,17 @@ int qzc_decompress_host(qzc_context *ctx, const uint8_t *payloads, const uint64_
 
 // ---- gate entry points ------------------------------------------------------
 
+static void check_bits(uint32_t nq, const uint32_t *q, uint32_t nbits) {
+    for (uint32_t k = 0; k < nq; ++k)
+        if (q[k] >= nbits)
+            throw Failure(QZC_EDEVICE, "buffer bit " + std::to_string(q[k]) +
+                                           " out of range for batch of 2^" + std::to_string(nbits) +
+                                           " amplitudes");
+}
+
+static void run_dev_gates(qzc_context *ctx, double *amps_dev, uint32_t nbits,
+                          const std::vector<DevGate> &dg, bool fuse = true);
+
 static void apply_gates_device(qzc_context *ctx, double *amps_dev, uint32_t nbits,
                                const qzc_gate *gates, uint64_t ngates, bool fuse = true) {
     std::vector<DevGate> dg;
@@ -551,13 +562,14 @@ static void apply_gates_device(qzc_context *ctx, double *amps_dev, uint32_t nbit
         const qzc_gate &g = gates[i];
         if (g.kind > QZC_SWAP) throw Failure(QZC_EINVAL, "unknown gate kind");
         if (g.nqubits != gate_arity(g.kind)) throw Failure(QZC_EINVAL, "gate arity mismatch");
-        for (uint32_t k = 0; k < g.nqubits; ++k)
-            if (g.qubits[k] >= nbits)
-                throw Failure(QZC_EDEVICE, "buffer bit " + std::to_string(g.qubits[k]) +
-                                               " out of range for batch of 2^" + std::to_string(nbits) +
-                                               " amplitudes");
+        check_bits(g.nqubits, g.qubits, nbits);
         dg.push_back(make_dev_gate(g));
     }
+    run_dev_gates(ctx, amps_dev, nbits, dg, fuse);
+}
+
+static void run_dev_gates(qzc_context *ctx, double *amps_dev, uint32_t nbits,
+                          const std::vector<DevGate> &dg, bool fuse) {
     if (dg.empty()) return;
     GatePlan plan = build_passes(dg, nbits, kTileBits, fuse);
     DevPlan dp;
@@ -565,6 +577,44 @@ static void apply_gates_device(qzc_context *ctx, double *amps_dev, uint32_t nbit
     ctx->launches += run_passes(dp, reinterpret_cast<double2 *>(amps_dev), nbits, ctx->stream);
     QZ_CUDA(cudaStreamSynchronize(ctx->stream));
     free_plan(dp);
+}
+
+static std::vector<DevGate> matrix_gates(const qzc_matrix_gate *gates, uint64_t ngates,
+                                         uint32_t nbits) {
+    std::vector<DevGate> dg;
+    for (uint64_t i = 0; i < ngates; ++i) {
+        const qzc_matrix_gate &g = gates[i];
+        check_bits(g.dim == 4 ? 2 : 1, g.qubits, nbits);
+        dg.push_back(make_dev_gate_matrix(reinterpret_cast<const double2 *>(g.m), g.dim, g.qubits[0],
+                                          g.qubits[1]));
+    }
+    return dg;
+}
+
+int qzc_apply_matrices_dev(qzc_context *ctx, double *amps_dev, uint32_t nbits,
+                           const qzc_matrix_gate *gates, uint64_t ngates) {
+    QZ_API_BEGIN
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    QZ_CUDA(cudaSetDevice(ctx->device));
+    run_dev_gates(ctx, amps_dev, nbits, matrix_gates(gates, ngates, nbits));
+    QZ_API_END
+}
+
+int qzc_apply_matrices_host(qzc_context *ctx, double *amps, uint32_t nbits,
+                            const qzc_matrix_gate *gates, uint64_t ngates) {
+    QZ_API_BEGIN
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    QZ_CUDA(cudaSetDevice(ctx->device));
+    const std::vector<DevGate> dg = matrix_gates(gates, ngates, nbits);
+    const uint64_t bytes = 16ull << nbits;
+    DevBuf buf;
+    buf.ensure(bytes);
+    QZ_CUDA(cudaMemcpyAsync(buf.p, amps, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    run_dev_gates(ctx, buf.as<double>(), nbits, dg);
+    QZ_CUDA(cudaMemcpyAsync(amps, buf.p, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    QZ_CUDA(cudaStreamSynchronize(ctx->stream));
+    buf.release();
+    QZ_API_END
 }
 
 int qzc_apply_gates_dev(qzc_context *ctx, double *amps_dev, uint32_t nbits, const qzc_gate *gates,
@@ -590,6 +640,97 @@ int qzc_apply_gates_host(qzc_context *ctx, double *amps, uint32_t nbits, const q
     QZ_CUDA(cudaStreamSynchronize(ctx->stream));
     buf.release();
     QZ_API_END
+}
+
+// ---- device buffers ---------------------------------------------------------------
+
+namespace {
+__global__ void k_copy(double2 *dst, const double2 *src, uint64_t n) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        dst[i] = src[i];
+}
+} // namespace
+
+int qzc_buffer_alloc(qzc_context *ctx, uint64_t amps, double **dev_out) {
+    QZ_API_BEGIN
+    QZ_CUDA(cudaSetDevice(ctx->device));
+    void *p = nullptr;
+    QZ_CUDA(cudaMalloc(&p, 16 * std::max<uint64_t>(amps, 1)));
+    *dev_out = static_cast<double *>(p);
+    QZ_API_END
+}
+
+void qzc_buffer_free(qzc_context *ctx, double *dev) {
+    if (ctx) cudaSetDevice(ctx->device);
+    cudaFree(dev);
+}
+
+int qzc_copy_h2d(qzc_context *ctx, double *dev, uint64_t dev_offset, const double *host,
+                 uint64_t amps) {
+    QZ_API_BEGIN
+    QZ_CUDA(cudaMemcpyAsync(dev + 2 * dev_offset, host, 16 * amps, cudaMemcpyHostToDevice,
+                            ctx->stream));
+    QZ_API_END
+}
+
+int qzc_copy_d2h(qzc_context *ctx, double *host, const double *dev, uint64_t dev_offset,
+                 uint64_t amps) {
+    QZ_API_BEGIN
+    QZ_CUDA(cudaMemcpyAsync(host, dev + 2 * dev_offset, 16 * amps, cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    QZ_API_END
+}
+
+int qzc_permute(qzc_context *ctx, double *dst, const double *src, uint64_t amps) {
+    QZ_API_BEGIN
+    const unsigned grid = (unsigned)std::min<uint64_t>(ceil_div(amps, 256), kNumSMs * 32);
+    k_copy<<<std::max(grid, 1u), 256, 0, ctx->stream>>>(reinterpret_cast<double2 *>(dst),
+                                                     reinterpret_cast<const double2 *>(src), amps);
+    QZ_CHECK_LAUNCH();
+    ++ctx->launches;
+    QZ_API_END
+}
+
+int qzc_host_alloc(qzc_context *ctx, uint64_t bytes, void **host_out) {
+    QZ_API_BEGIN
+    QZ_CUDA(cudaSetDevice(ctx->device));
+    QZ_CUDA(cudaMallocHost(host_out, std::max<uint64_t>(bytes, 1)));
+    QZ_API_END
+}
+
+void qzc_host_free(qzc_context *ctx, void *host) {
+    (void)ctx;
+    cudaFreeHost(host);
+}
+
+int qzc_event_record(qzc_context *ctx, void **event_out) {
+    QZ_API_BEGIN
+    cudaEvent_t e;
+    QZ_CUDA(cudaEventCreate(&e));
+    QZ_CUDA(cudaEventRecord(e, ctx->stream));
+    *event_out = e;
+    QZ_API_END
+}
+
+int qzc_event_elapsed(qzc_context *ctx, void *start, void *end, double *seconds_out) {
+    QZ_API_BEGIN
+    (void)ctx;
+    QZ_CUDA(cudaEventSynchronize(static_cast<cudaEvent_t>(end)));
+    float ms = 0;
+    QZ_CUDA(cudaEventElapsedTime(&ms, static_cast<cudaEvent_t>(start), static_cast<cudaEvent_t>(end)));
+    *seconds_out = ms * 1e-3;
+    QZ_API_END
+}
+
+int qzc_event_done(qzc_context *ctx, void *event) {
+    (void)ctx;
+    return cudaEventQuery(static_cast<cudaEvent_t>(event)) == cudaSuccess ? 1 : 0;
+}
+
+void qzc_event_destroy(qzc_context *ctx, void *event) {
+    (void)ctx;
+    if (event) cudaEventDestroy(static_cast<cudaEvent_t>(event));
 }
 
 // ---- simulator -----------------------------------------------------------------
