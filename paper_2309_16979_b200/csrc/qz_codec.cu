@@ -572,14 +572,14 @@ __global__ void k_enc_sizes(const EncHalf *__restrict__ meta, uint64_t nslots, C
 __global__ void k_arena_alloc(const uint64_t *rel_off, const uint64_t *sizes, uint64_t nslots,
                               uint64_t *used, uint64_t capacity, uint64_t *base_out,
                               DevStatus *status) {
+    // atomic bump: windows on concurrent streams share one output arena
     const uint64_t total = rel_off[nslots - 1] + sizes[nslots - 1];
-    const uint64_t base = *used;
+    const uint64_t base = atomicAdd((unsigned long long *)used, (unsigned long long)total);
     if (base + total > capacity) {
         dev_fail(status, QZS_ARENA, base + total);
         *base_out = 0;
         return;
     }
-    *used = base + total;
     *base_out = base;
 }
 

@@ -221,8 +221,12 @@ struct qzc_sim {
     DevBuf acct;   // int64[2] current / peak
     uint64_t arena_cap = 0;
     int cur = 0;
-    uint64_t win_amps = 0;
-    Window win;
+    uint64_t win_amps = 0;   // amplitudes per pipeline window
+    Window win;              // window set 0 (also used by the host entry points)
+    Window win2;             // window set 1: second stream of the stage pipeline
+    bool two_windows = false;
+    cudaStream_t streams[2] = {nullptr, nullptr};
+    cudaEvent_t acct_ev[2] = {nullptr, nullptr};
     qzc_sim_stats stats{};
     bool initialized = false;
     std::vector<cudaEvent_t> events;
@@ -240,8 +244,10 @@ namespace {
 void encode_window(qzc_context *ctx, Window &w, const CodecGeom &g, uint64_t nslots,
                    const uint64_t *slot_chunk, const uint64_t *forced, uint32_t nforced,
                    uint8_t *arena, uint64_t *used, uint64_t cap, ChunkTable t,
-                   const uint32_t *old_len, int64_t *acct, uint64_t &launches) {
-    cudaStream_t s = ctx->stream;
+                   const uint32_t *old_len, int64_t *acct, uint64_t &launches,
+                   cudaStream_t s = nullptr, cudaEvent_t acct_prev = nullptr,
+                   cudaEvent_t acct_done = nullptr) {
+    if (!s) s = ctx->stream;
     launch_encode(w.amps.as<double2>(), nslots, g, forced, nforced, w.scratch.as<uint8_t>(),
                   w.meta.as<EncHalf>(), s);
     launch_enc_sizes(w.meta.as<EncHalf>(), nslots, g, w.sizes.as<uint64_t>(), s);
@@ -260,8 +266,12 @@ void encode_window(qzc_context *ctx, Window &w, const CodecGeom &g, uint64_t nsl
         tb = w.cub.cap;
         QZ_CUDA(cub::DeviceReduce::Max(w.cub.p, tb, w.delta.as<int64_t>(), w.maxd.as<int64_t>(),
                                        (int)nslots, s));
+        // footprint accounting is a running sum in batch order: chain the
+        // windows of concurrent streams through events
+        if (acct_prev) QZ_CUDA(cudaStreamWaitEvent(s, acct_prev, 0));
         k_account<<<1, 1, 0, s>>>(acct, w.delta.as<int64_t>(), w.maxd.as<int64_t>(), nslots);
         QZ_CHECK_LAUNCH();
+        if (acct_done) QZ_CUDA(cudaEventRecord(acct_done, s));
         launches += 5;
     }
     launch_assemble(w.scratch.as<uint8_t>(), w.meta.as<EncHalf>(), w.reloff.as<uint64_t>(),
@@ -273,8 +283,8 @@ void encode_window(qzc_context *ctx, Window &w, const CodecGeom &g, uint64_t nsl
 
 void decode_window(qzc_context *ctx, Window &w, const CodecGeom &g, uint64_t nslots,
                    const uint64_t *slot_chunk, const uint8_t *arena, ChunkTable t,
-                   uint64_t &launches) {
-    cudaStream_t s = ctx->stream;
+                   uint64_t &launches, cudaStream_t s = nullptr) {
+    if (!s) s = ctx->stream;
     launch_crc(ctx->tabs, arena, t, slot_chunk, nslots, true, ctx->status, s);
     launch_dec_index(arena, t, slot_chunk, nslots, g, w.idx.as<DecIdx>(), ctx->status, s);
     launch_decode(arena, w.idx.as<DecIdx>(), slot_chunk, nslots, g, w.amps.as<double2>(),
@@ -319,9 +329,18 @@ void sim_alloc(qzc_sim *sim) {
     // at least one whole batch (2^m amplitudes) and two chunk slots
     const uint64_t batch_amps = uint64_t(1) << std::min(sim->m, sim->n);
     wa = std::max<uint64_t>(std::min<uint64_t>(wa, state_amps), std::max<uint64_t>(batch_amps, 2 * sim->N));
+    // two half-size windows on two streams when the window holds >= 2
+    // batches: decode / gate passes / encode of neighbouring windows overlap
+    sim->two_windows = wa >= 2 * batch_amps && wa >= 4 * sim->N;
+    if (sim->two_windows) wa /= 2;
     sim->win_amps = wa;
     const uint64_t win_slots = std::max<uint64_t>(wa / sim->N, 2);
     sim->win.reserve(sim->geom, win_slots);
+    if (sim->two_windows) sim->win2.reserve(sim->geom, win_slots);
+    for (int i = 0; i < 2; ++i) {
+        QZ_CUDA(cudaStreamCreateWithFlags(&sim->streams[i], cudaStreamNonBlocking));
+        QZ_CUDA(cudaEventCreateWithFlags(&sim->acct_ev[i], cudaEventDisableTiming));
+    }
 
     // arenas: worst case if it fits, else what is left
     QZ_CUDA(cudaMemGetInfo(&free_b, &total_b));
@@ -777,6 +796,14 @@ void qzc_sim_destroy(qzc_sim *sim) {
     sim->used.release();
     sim->acct.release();
     sim->win.release();
+    sim->win2.release();
+    for (int i = 0; i < 2; ++i) {
+        if (sim->streams[i]) {
+            cudaStreamSynchronize(sim->streams[i]);
+            cudaStreamDestroy(sim->streams[i]);
+        }
+        if (sim->acct_ev[i]) cudaEventDestroy(sim->acct_ev[i]);
+    }
     for (cudaEvent_t e : sim->events) cudaEventDestroy(e);
     delete sim;
 }
@@ -905,23 +932,32 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
         upload_plan(gp, dp, s);
         const int a = sim->cur, b = 1 - sim->cur;
         QZ_CUDA(cudaMemsetAsync(sim->used_ptr(b), 0, 8, s));
+        // the stage's plan upload and arena reset happen on the context
+        // stream; both window streams start after them
         const uint64_t nwin = nbatches / bpw;
+        cudaEvent_t ready = ev(4 * nwin);
+        QZ_CUDA(cudaEventRecord(ready, s));
         const uint64_t nslots = bpw << hs;
         for (uint64_t w = 0; w < nwin; ++w) {
-            Window &W = sim->win;
-            QZ_CUDA(cudaEventRecord(ev(4 * w), s));
-            launch_slot_chunks(W.slot_chunk.as<uint64_t>(), nslots, w * bpw, hs, fmask, smask, s);
+            const int ws = sim->two_windows ? int(w & 1) : 0;
+            Window &W = ws ? sim->win2 : sim->win;
+            cudaStream_t S = sim->streams[ws];
+            if (w < 2) QZ_CUDA(cudaStreamWaitEvent(S, ready, 0));
+            QZ_CUDA(cudaEventRecord(ev(4 * w), S));
+            launch_slot_chunks(W.slot_chunk.as<uint64_t>(), nslots, w * bpw, hs, fmask, smask, S);
             decode_window(ctx, W, sim->geom, nslots, W.slot_chunk.as<uint64_t>(),
-                          sim->arena[a].as<uint8_t>(), sim->table(a), ctx->launches);
-            QZ_CUDA(cudaEventRecord(ev(4 * w + 1), s));
-            ctx->launches += 1 + run_passes(dp, W.amps.as<double2>(), wbits, s);
-            QZ_CUDA(cudaEventRecord(ev(4 * w + 2), s));
+                          sim->arena[a].as<uint8_t>(), sim->table(a), ctx->launches, S);
+            QZ_CUDA(cudaEventRecord(ev(4 * w + 1), S));
+            ctx->launches += 1 + run_passes(dp, W.amps.as<double2>(), wbits, S);
+            QZ_CUDA(cudaEventRecord(ev(4 * w + 2), S));
             encode_window(ctx, W, sim->geom, nslots, W.slot_chunk.as<uint64_t>(), nullptr, 0,
                           sim->arena[b].as<uint8_t>(), sim->used_ptr(b), sim->arena_cap,
                           sim->table(b), sim->len[a].as<uint32_t>(), sim->acct.as<int64_t>(),
-                          ctx->launches);
-            QZ_CUDA(cudaEventRecord(ev(4 * w + 3), s));
+                          ctx->launches, S, w ? sim->acct_ev[(w - 1) & 1] : nullptr,
+                          sim->acct_ev[w & 1]);
+            QZ_CUDA(cudaEventRecord(ev(4 * w + 3), S));
         }
+        for (int i = 0; i < 2; ++i) QZ_CUDA(cudaStreamSynchronize(sim->streams[i]));
         try {
             ctx->check_status();
         } catch (const Failure &f) {

@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cstring>
 #include <deque>
+#include <thread>
 
 #include "engine_ctx.hpp"
 #include "qzsim/device.hpp"
@@ -51,7 +52,26 @@ CommandStatus CommandHandle::status() const {
 
 namespace {
 enum class Op { H2D, D2H, Kernel };
+
+// Copy chunk-sized pieces between pageable chunk memory and the pinned
+// staging area on several host threads (the host half of the Buffered
+// strategy; one thread for small batches).
+template <class Fn> void parallel_chunks(size_t count, uint64_t bytes_each, Fn fn) {
+    const uint64_t total = count * bytes_each;
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const unsigned nt = total < (uint64_t(4) << 20) ? 1u : std::min<unsigned>(hw, 8u);
+    if (nt == 1 || count < 2) {
+        for (size_t j = 0; j < count; ++j) fn(j);
+        return;
+    }
+    std::vector<std::thread> ts;
+    for (unsigned t = 0; t < nt; ++t)
+        ts.emplace_back([&, t] {
+            for (size_t j = t; j < count; j += nt) fn(j);
+        });
+    for (std::thread &t : ts) t.join();
 }
+} // namespace
 
 class CudaDevice final : public Device {
   public:
@@ -74,8 +94,9 @@ class CudaDevice final : public Device {
         qzc_context *c = b200::ctx();
         if (cfg_.strategy == Strategy::Buffered) {
             void *t0 = mark();
-            for (size_t j = 0; j < chunks.size(); ++j)
+            parallel_chunks(chunks.size(), chunk_len * sizeof(Amplitude), [&](size_t j) {
                 std::memcpy(pinned_ + j * chunk_len, chunks[j], chunk_len * sizeof(Amplitude));
+            });
             b200::check(qzc_copy_h2d(c, staging_, 0, reinterpret_cast<const double *>(pinned_), total));
             ++stats_.h2d_op_count;
             stats_.bytes_moved += total * sizeof(Amplitude);
@@ -133,8 +154,9 @@ class CudaDevice final : public Device {
             timers_.push_back({Op::Kernel, t0, t1});
             b200::check(qzc_copy_d2h(c, reinterpret_cast<double *>(pinned_), staging_, 0, total));
             b200::check(qzc_synchronize(c));
-            for (size_t j = 0; j < chunks.size(); ++j)
+            parallel_chunks(chunks.size(), chunk_len * sizeof(Amplitude), [&](size_t j) {
                 std::memcpy(chunks[j], pinned_ + j * chunk_len, chunk_len * sizeof(Amplitude));
+            });
             ++stats_.d2h_op_count;
             stats_.bytes_moved += total * sizeof(Amplitude);
             timers_.push_back({Op::D2H, t1, mark()});

@@ -33,7 +33,7 @@ def test_reference_unit_suite(name):
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
 
 
-@pytest.mark.parametrize("criterion", ["1", "2", "4", "5", "7", "8"])
+@pytest.mark.parametrize("criterion", ["1", "2", "3", "4", "5", "6", "7", "8"])
 def test_reference_acceptance(criterion):
     p = _run("acceptance", [criterion], timeout=1200)
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
