@@ -14,6 +14,7 @@
 // imaginary half holds back its first run, and the assembler merges the two
 // at the plane boundary exactly as rle_encode would over the joined plane.
 #include <algorithm>
+#include <cmath>
 
 #include "qz_codec.cuh"
 
@@ -272,7 +273,7 @@ __global__ void __launch_bounds__(2 * kSlotsPerCta) k_dec_lossy(
     const uint8_t *p = arena + d->base;
     Cursor lo{0, 0, 0}, hi{0, 0, 0};
     uint32_t raw_i = 0, raw_count = 0, raw_pos = 0;
-    double eb = 0.0, pred = 0.0;
+    double twoeb = 0.0, pred = 0.0;
     bool bad = false;
     if (active) {
         cur_init(lo, p, d->pos[0][h], d->skip[0][h]);
@@ -280,7 +281,7 @@ __global__ void __launch_bounds__(2 * kSlotsPerCta) k_dec_lossy(
         raw_i = h ? d->raw_re : 0;
         raw_count = d->raw_count;
         raw_pos = d->raw_pos;
-        eb = d->eb;
+        twoeb = 2.0 * d->eb;
     }
     const uint64_t N = g.N;
     const uint32_t te = uint32_t(umin64(kTileElems, N));
@@ -297,7 +298,8 @@ __global__ void __launch_bounds__(2 * kSlotsPerCta) k_dec_lossy(
                     }
                 } else {
                     const int32_t code = unzigzag16(z);
-                    pred = __dadd_rn(pred, __dmul_rn(__dmul_rn(double(code), 2.0), eb));
+                    // ((double)code * 2.0) * eb == (double)code * (2 eb) exactly
+                    pred = __dadd_rn(pred, __dmul_rn(double(code), twoeb));
                 }
             }
             set_comp(tile.v[r][e], h, pred);
@@ -428,12 +430,43 @@ __device__ __forceinline__ uint8_t *scratch_half(uint8_t *scratch, const CodecGe
     return scratch + (2 * slot + h) * g.half_stride;
 }
 
-// Lossy encode (codec.cpp:121-168): thread = (slot, half).
+// Double-buffered tile of kSlotsPerCta rows x kTileElems amplitudes.
+struct EncTiles {
+    double2 v[2][kSlotsPerCta][kTileElems + 1];
+};
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N> __device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// Quantiser step (codec.cpp:138): q = round((v - pred) / (2 eb)) with the
+// division replaced by a multiplication by the rounded reciprocal.  |t' - t|
+// <= |t'| 2^-52 (two roundings), so whenever t' is farther than |t'| 2^-49
+// from every half-integer, round(t') == round(t) exactly; otherwise (and for
+// non-finite values) the correctly rounded division decides.  With a
+// power-of-two 2eb the reciprocal is exact and no check is needed.
+__device__ __forceinline__ double quantise(double d, const CodecGeom &g) {
+    const double t = __dmul_rn(d, g.inv2eb);
+    double q = round(t);
+    if (!g.exact_inv) {
+        const double dist = fabs(__dsub_rn(fabs(__dsub_rn(t, trunc(t))), 0.5));
+        if (!(dist > __dmul_rn(fabs(t), 0x1p-49))) q = round(__ddiv_rn(d, g.twoeb));
+    }
+    return q;
+}
+
+// Lossy encode (codec.cpp:121-168): thread = (slot, half).  The next tile is
+// prefetched with cp.async while the current one is walked.
 __global__ void __launch_bounds__(2 * kSlotsPerCta) k_enc_lossy(
     const double2 *__restrict__ win, uint64_t nslots, CodecGeom g,
     const uint64_t *__restrict__ forced, uint32_t nforced, uint8_t *__restrict__ scratch,
     EncHalf *__restrict__ meta) {
-    __shared__ TileSmem tile;
+    __shared__ __align__(16) EncTiles tiles;
     const uint32_t r = threadIdx.x >> 1, h = threadIdx.x & 1;
     const uint64_t slot0 = uint64_t(blockIdx.x) * kSlotsPerCta, s = slot0 + r;
     const bool active = s < nslots;
@@ -451,42 +484,59 @@ __global__ void __launch_bounds__(2 * kSlotsPerCta) k_enc_lossy(
     const double eb = g.eb, twoeb = g.twoeb;
     double pred = 0.0;
     const uint32_t te = uint32_t(umin64(kTileElems, N));
-    for (uint64_t e0 = 0; e0 < N; e0 += te) {
-        __syncthreads();
-        load_tile(tile, win, slot0, nslots, N, e0, te);
-        __syncthreads();
-        if (!active) continue;
-        for (uint32_t e = 0; e < te; ++e) {
-            const double v = comp(tile.v[r][e], h);
-            const uint64_t flat = h * N + e0 + e;
-            bool raw = false;
-            int32_t code = 0;
-            if (flat == next_forced) {
-                raw = true;
-                do { ++fc; } while (fc < nforced && forced[fc] == flat);
-                next_forced = fc < nforced ? forced[fc] : ~uint64_t(0);
-            } else {
-                const double q = round(__ddiv_rn(__dsub_rn(v, pred), twoeb));
-                if (!(fabs(q) < 32768.0)) {
-                    raw = true;
-                } else {
-                    code = int32_t(q);
-                    const double rec = __dadd_rn(pred, __dmul_rn(__dmul_rn(double(code), 2.0), eb));
-                    if (!(fabs(__dsub_rn(rec, v)) <= eb)) raw = true;
-                    else pred = rec;
-                }
-            }
-            uint32_t z;
-            if (raw) {
-                raws[nraw++] = v;
-                pred = v;
-                z = 0xFFFFu;
-            } else {
-                z = zigzag16(code);
-            }
-            rle_push(lo, z & 0xff);
-            rle_push(hi, z >> 8);
+    const uint32_t rows = uint32_t(umin64(kSlotsPerCta, nslots - slot0));
+    auto issue = [&](int buf, uint64_t e0) {
+        for (uint32_t i = threadIdx.x; i < rows * te; i += blockDim.x) {
+            const uint32_t rr = i / te, e = i - rr * te;
+            cp_async16(&tiles.v[buf][rr][e], win + (slot0 + rr) * N + e0 + e);
         }
+        cp_async_commit();
+    };
+    issue(0, 0);
+    int buf = 0;
+    for (uint64_t e0 = 0; e0 < N; e0 += te, buf ^= 1) {
+        if (e0 + te < N) {
+            issue(buf ^ 1, e0 + te);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        if (active) {
+            for (uint32_t e = 0; e < te; ++e) {
+                const double v = comp(tiles.v[buf][r][e], h);
+                const uint64_t flat = h * N + e0 + e;
+                bool raw = false;
+                int32_t code = 0;
+                if (flat == next_forced) {
+                    raw = true;
+                    do { ++fc; } while (fc < nforced && forced[fc] == flat);
+                    next_forced = fc < nforced ? forced[fc] : ~uint64_t(0);
+                } else {
+                    const double q = quantise(__dsub_rn(v, pred), g);
+                    if (!(fabs(q) < 32768.0)) {
+                        raw = true;
+                    } else {
+                        code = int32_t(q);
+                        // (double)code * 2.0 * eb == q' * (2 eb) exactly (q' = q with -0 -> +0)
+                        const double rec = __dadd_rn(pred, __dmul_rn(__dadd_rn(q, 0.0), twoeb));
+                        if (!(fabs(__dsub_rn(rec, v)) <= eb)) raw = true;
+                        else pred = rec;
+                    }
+                }
+                uint32_t z;
+                if (raw) {
+                    raws[nraw++] = v;
+                    pred = v;
+                    z = 0xFFFFu;
+                } else {
+                    z = zigzag16(code);
+                }
+                rle_push(lo, z & 0xff);
+                rle_push(hi, z >> 8);
+            }
+        }
+        __syncthreads();  // the buffer is refilled two tiles later
     }
     if (active) {
         EncHalf &m = meta[2 * s + h];
@@ -667,6 +717,13 @@ CodecGeom make_geom(uint64_t N, double eb) {
     g.planes = g.lossy ? 2 : 8;
     g.eb = eb;
     g.twoeb = 2.0 * eb;
+    g.inv2eb = eb > 0.0 ? 1.0 / g.twoeb : 0.0;
+    {
+        int ex = 0;
+        const double mant = std::frexp(g.twoeb, &ex);
+        // exact reciprocal: power of two whose inverse is a normal double
+        g.exact_inv = eb > 0.0 && mant == 0.5 && ex > -1020 && ex < 1020 ? 1u : 0u;
+    }
     g.scap = round_up(2 * N, 8);
     g.half_stride = round_up(g.lossy ? 2 * g.scap + 8 * N : 8 * g.scap, 16);
     return g;

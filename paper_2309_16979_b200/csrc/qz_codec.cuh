@@ -47,6 +47,9 @@ struct CodecGeom {
     uint32_t lossy;         // error_bound > 0
     uint32_t planes;        // 2 or 8
     double eb, twoeb;       // store error bound, 2*eb
+    double inv2eb;          // fl(1 / (2 eb)) for the division-free quantiser
+    uint32_t exact_inv;     // 2 eb is a power of two: the reciprocal is exact
+    uint32_t pad;
     uint64_t scap;          // bytes per scratch stream (>= 2N, multiple of 8)
     uint64_t half_stride;   // scratch bytes per (slot, half)
 };

@@ -128,3 +128,31 @@ def test_forced_raws_exact(engine):
     p, crc = engine.compress(a, 1e-2, forced=[0, 16])
     out = engine.decompress(p, crc, 16)
     assert out[0] == a[0]
+
+
+@pytest.mark.parametrize("eb", [1e-5, 3e-7, 2.0 ** -17, 0.1])
+def test_quantiser_half_integer_boundaries(engine, oracle, eb):
+    """Values placed on and around the .5 rounding boundaries of the
+    quantiser (the division-free fast path must hand these to the exact
+    division).  A far value forces a raw reset of the predictor first."""
+    rng = np.random.default_rng(int(eb * 1e12) % 2**32)
+    far = 40000.0 * 2 * eb
+    vals = []
+    for k in rng.integers(-32800, 32800, size=1500):
+        base = far * (1 if k % 2 else -1)
+        step = (float(k) + 0.5) * 2 * eb
+        for nudge in (0.0, 1.0, -1.0, 3.0, -3.0):
+            v = base + step
+            v = np.nextafter(v, np.inf) if nudge > 0 else (np.nextafter(v, -np.inf) if nudge < 0 else v)
+            if abs(nudge) == 3.0:
+                v = v * (1 + np.sign(nudge) * 2.0 ** -51)
+            vals += [0.0, base, float(v)]
+    n = 1 << int(np.ceil(np.log2(len(vals))))
+    re = np.zeros(n)
+    re[: len(vals)] = vals
+    amps = re + 1j * np.roll(re, 7)
+    got = engine.compress(amps, eb)
+    want = oracle.compress(amps, eb)
+    assert got == want
+    back = engine.decompress(got[0], got[1], n)
+    assert back.tobytes() == oracle.decompress(want[0], want[1], n).tobytes()
