@@ -49,6 +49,8 @@ def parse_args():
     ap.add_argument("--cpu-budget", type=float, default=20.0,
                     help="seconds of reference CPU work per sample")
     ap.add_argument("--no-fuse", action="store_true")
+    ap.add_argument("--residency", default="hbm", choices=["hbm", "host"],
+                    help="compressed store in HBM (config 2) or pinned host memory (config 3)")
     return ap.parse_args()
 
 
@@ -188,7 +190,8 @@ def run_reference_arm(args, gates):
 
 
 def workload_config(args) -> dict:
-    return {"workload": f"{args.circuit}-{args.n} compressed-chunk pipeline, HBM-resident store",
+    where = "HBM-resident store" if args.residency == "hbm" else "host-staged store (pinned host RAM)"
+    return {"workload": f"{args.circuit}-{args.n} compressed-chunk pipeline, {where}",
             "circuit": args.circuit, "num_qubits": args.n, "chunk_qubits": args.c,
             "batch_qubits": args.m, "error_bound": args.eb,
             "l2": "inputs larger than L2 (2^n x 16 B dense state per stage sweep)"}
@@ -226,7 +229,8 @@ def main() -> int:
         return float(t.item())
 
     eng = Engine(device=local)
-    sim = eng.simulator(args.n, args.c, args.m, args.eb, init=False, fuse=not args.no_fuse)
+    sim = eng.simulator(args.n, args.c, args.m, args.eb, init=False, fuse=not args.no_fuse,
+                        residency=args.residency)
     ngates = len(gates)
 
     for _ in range(args.warmup):
@@ -303,6 +307,17 @@ def main() -> int:
             cpu = {"value": None, "unit": "gates/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {e}"}
 
+    host_link = None
+    if args.residency == "host":
+        link = eng.host_link_gbps()
+        io = st["h2d_bytes"] + st["d2h_bytes"]
+        ach = io / (t_max / args.steps) / 1e9
+        host_link = {"bound": "host-link", "achieved": ach, "unit": "GB/s",
+                     "h2d_peak": link["h2d"], "d2h_peak": link["d2h"],
+                     "frac": ach / max(link["h2d"], link["d2h"]),
+                     "bytes_per_step": io,
+                     "note": "compressed payload bytes moved host<->HBM per circuit / circuit "
+                             "time, vs measured pinned cudaMemcpy bandwidth"}
     line = {
         "metric": METRIC, "value": value, "unit": "gates/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps,
@@ -316,6 +331,7 @@ def main() -> int:
         "phases_s": phases, "stages": st["stages"], "gate_passes": st["gate_passes"],
         "gpu_launches": launches,
         "roofline": roofline,
+        "host_link": host_link,
         "cpu_baseline": cpu,
         "e2e": {"value": world * ngates / e2e_t, "unit": "gates/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h)},

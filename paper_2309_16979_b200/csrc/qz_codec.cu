@@ -699,6 +699,78 @@ __global__ void k_slot_chunks(uint64_t *out, uint64_t nslots, uint64_t first_bat
     out[s] = deposit_bits(b, free_mask) | deposit_bits(j, member_mask);
 }
 
+// ---- host-staged residency: move window payloads between a mapped
+// page-locked host arena and HBM with coalesced 16-byte zero-copy accesses ----
+
+// Staging size per slot: payload + room to keep (dst - src) % 16 == 0.
+__global__ void k_stage_sizes(ChunkTable table, const uint64_t *__restrict__ slot_chunk,
+                              uint64_t nslots, uint64_t *__restrict__ padded) {
+    const uint64_t s = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (s >= nslots) return;
+    padded[s] = round_up(uint64_t(table.len[slot_chunk[s]]) + 31, 16);
+}
+
+// Warp per slot: copy the 16-byte words covering the payload from the host
+// arena into the HBM staging area; fill the slot-indexed local table.
+__global__ void __launch_bounds__(256) k_gather(const uint8_t *__restrict__ host_arena, ChunkTable table,
+                                                const uint64_t *__restrict__ slot_chunk,
+                                                const uint64_t *__restrict__ soff, uint64_t nslots,
+                                                uint8_t *__restrict__ stage, ChunkTable local) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    for (uint64_t s = warp; s < nslots; s += nwarps) {
+        const uint64_t chunk = slot_chunk[s];
+        const uint64_t src = table.off[chunk];
+        const uint32_t len = table.len[chunk];
+        const uint64_t words = (uint64_t((src & 15) + len) + 15) / 16;
+        const uint4 *in = reinterpret_cast<const uint4 *>(host_arena + (src & ~uint64_t(15)));
+        uint4 *out = reinterpret_cast<uint4 *>(stage + soff[s]);
+        for (uint64_t w = lane; w < words; w += 32) out[w] = in[w];
+        if (lane == 0) {
+            local.off[s] = soff[s] + (src & 15);
+            local.len[s] = len;
+            local.crc[s] = table.crc[chunk];
+        }
+    }
+}
+
+// Reserve a 16-byte aligned block of the host arena for a window's output.
+__global__ void k_host_alloc(const uint64_t *__restrict__ used_local, uint64_t *host_used, uint64_t cap,
+                             uint64_t *base_out, DevStatus *status) {
+    const uint64_t total = round_up(*used_local, 16);
+    const uint64_t base = atomicAdd((unsigned long long *)host_used, (unsigned long long)total);
+    if (base + total > cap) {
+        dev_fail(status, QZS_ARENA, base + total);
+        *base_out = ~uint64_t(0);
+        return;
+    }
+    *base_out = base;
+}
+
+// Copy the window's contiguous output bytes HBM -> host arena (16 B words).
+__global__ void k_copy_out(const uint8_t *__restrict__ stage, const uint64_t *__restrict__ used_local,
+                           const uint64_t *__restrict__ base, uint8_t *__restrict__ host_arena) {
+    if (*base == ~uint64_t(0)) return;
+    const uint64_t words = round_up(*used_local, 16) / 16;
+    const uint4 *in = reinterpret_cast<const uint4 *>(stage);
+    uint4 *out = reinterpret_cast<uint4 *>(host_arena + *base);
+    for (uint64_t w = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; w < words;
+         w += uint64_t(gridDim.x) * blockDim.x)
+        out[w] = in[w];
+}
+
+// Publish the window's entries in the global (chunk-indexed) table.
+__global__ void k_table_out(ChunkTable local, const uint64_t *__restrict__ slot_chunk,
+                            const uint64_t *__restrict__ base, uint64_t nslots, ChunkTable table) {
+    const uint64_t s = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (s >= nslots || *base == ~uint64_t(0)) return;
+    const uint64_t chunk = slot_chunk[s];
+    table.off[chunk] = *base + local.off[s];
+    table.len[chunk] = local.len[s];
+    table.crc[chunk] = local.crc[s];
+}
+
 unsigned grid_for(uint64_t n, unsigned threads) { return (unsigned)ceil_div(n, threads); }
 
 } // namespace
@@ -815,6 +887,32 @@ void launch_assemble(const uint8_t *scratch, const EncHalf *meta, const uint64_t
     const unsigned grid = (unsigned)std::min<uint64_t>(ceil_div(nslots, 8), kNumSMs * 64);
     k_assemble<<<grid, 256, 0, s>>>(scratch, meta, rel_off, sizes, base, slot_chunk, nslots, g,
                                     arena, table, status);
+    QZ_CHECK_LAUNCH();
+}
+
+void launch_stage_sizes(ChunkTable table, const uint64_t *slot_chunk, uint64_t nslots,
+                        uint64_t *padded, cudaStream_t s) {
+    k_stage_sizes<<<grid_for(nslots, 256), 256, 0, s>>>(table, slot_chunk, nslots, padded);
+    QZ_CHECK_LAUNCH();
+}
+
+void launch_gather(const uint8_t *host_arena, ChunkTable table, const uint64_t *slot_chunk,
+                   const uint64_t *soff, uint64_t nslots, uint8_t *stage, ChunkTable local,
+                   cudaStream_t s) {
+    const unsigned grid = (unsigned)std::min<uint64_t>(ceil_div(nslots, 8), kNumSMs * 32);
+    k_gather<<<grid, 256, 0, s>>>(host_arena, table, slot_chunk, soff, nslots, stage, local);
+    QZ_CHECK_LAUNCH();
+}
+
+void launch_copy_out(const uint8_t *stage, const uint64_t *used_local, uint64_t *host_used,
+                     uint64_t cap, uint64_t *base, uint8_t *host_arena, ChunkTable local,
+                     const uint64_t *slot_chunk, uint64_t nslots, ChunkTable table,
+                     DevStatus *status, cudaStream_t s) {
+    k_host_alloc<<<1, 1, 0, s>>>(used_local, host_used, cap, base, status);
+    QZ_CHECK_LAUNCH();
+    k_copy_out<<<kNumSMs * 8, 256, 0, s>>>(stage, used_local, base, host_arena);
+    QZ_CHECK_LAUNCH();
+    k_table_out<<<grid_for(nslots, 256), 256, 0, s>>>(local, slot_chunk, base, nslots, table);
     QZ_CHECK_LAUNCH();
 }
 

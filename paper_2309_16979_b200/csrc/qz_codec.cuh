@@ -109,6 +109,21 @@ void launch_assemble(const uint8_t *scratch, const EncHalf *meta, const uint64_t
                      uint64_t nslots, const CodecGeom &g, uint8_t *arena, ChunkTable table,
                      const DevStatus *status, cudaStream_t s);
 
+// Host-staged residency (mapped page-locked host arena):
+//   padded[s] = staging bytes of slot s; soff = exclusive scan of padded;
+//   gather copies payloads into `stage` and fills the slot-indexed `local`
+//   table; copy_out moves a window's encoded bytes (stage[0, *used_local))
+//   to the host arena and publishes the chunk-indexed table entries.
+void launch_stage_sizes(ChunkTable table, const uint64_t *slot_chunk, uint64_t nslots,
+                        uint64_t *padded, cudaStream_t s);
+void launch_gather(const uint8_t *host_arena, ChunkTable table, const uint64_t *slot_chunk,
+                   const uint64_t *soff, uint64_t nslots, uint8_t *stage, ChunkTable local,
+                   cudaStream_t s);
+void launch_copy_out(const uint8_t *stage, const uint64_t *used_local, uint64_t *host_used,
+                     uint64_t cap, uint64_t *base, uint8_t *host_arena, ChunkTable local,
+                     const uint64_t *slot_chunk, uint64_t nslots, ChunkTable table,
+                     DevStatus *status, cudaStream_t s);
+
 // Host-side CRC-32 / FNV-1a (util.cpp:20-31).
 uint32_t crc32_host(const uint8_t *p, uint64_t n);
 uint64_t fnv1a64_host(const uint8_t *p, uint64_t n, uint64_t state);

@@ -12,6 +12,8 @@
 #include <cub/device/device_reduce.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include <unistd.h>
+
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -70,7 +72,26 @@ const char *status_text(int code) {
 // Scratch set for one window of codec work.
 struct Window {
     DevBuf amps, scratch, meta, idx, slot_chunk, sizes, reloff, base, cub, delta, maxd;
-    uint64_t slots = 0;
+    // host-staged residency: HBM staging of the window's payloads
+    DevBuf stage_in, stage_out, lt_off, lt_len, lt_crc, padded, soff, lused, hbase;
+    uint64_t slots = 0, stage_in_cap = 0, stage_out_cap = 0;
+    ChunkTable local() {
+        return ChunkTable{lt_off.as<uint64_t>(), lt_len.as<uint32_t>(), lt_crc.as<uint32_t>()};
+    }
+    void reserve_staging(const CodecGeom &g, uint64_t nslots) {
+        const uint64_t bound = payload_bound(g.N, g.lossy ? 1.0 : 0.0);
+        stage_in_cap = nslots * (bound + 48) + 64;
+        stage_out_cap = nslots * bound + 64;
+        stage_in.ensure(stage_in_cap);
+        stage_out.ensure(stage_out_cap);
+        lt_off.ensure(8 * nslots);
+        lt_len.ensure(4 * nslots);
+        lt_crc.ensure(4 * nslots);
+        padded.ensure(8 * nslots);
+        soff.ensure(8 * nslots);
+        lused.ensure(16);
+        hbase.ensure(16);
+    }
     void reserve(const CodecGeom &g, uint64_t nslots) {
         amps.ensure(sizeof(double2) * nslots * g.N);
         scratch.ensure(2 * nslots * g.half_stride);
@@ -95,7 +116,8 @@ struct Window {
     }
     void release() {
         for (DevBuf *b : {&amps, &scratch, &meta, &idx, &slot_chunk, &sizes, &reloff, &base, &cub,
-                          &delta, &maxd})
+                          &delta, &maxd, &stage_in, &stage_out, &lt_off, &lt_len, &lt_crc, &padded,
+                          &soff, &lused, &hbase})
             b->release();
     }
 };
@@ -114,6 +136,14 @@ __global__ void k_account(int64_t *acct, const int64_t *prefix, const int64_t *m
     const int64_t peak_cand = cur + *maxp;
     if (peak_cand > acct[1]) acct[1] = peak_cand;
     acct[0] = cur + prefix[nslots - 1];
+}
+
+__global__ void k_io_count(const uint64_t *soff, const uint64_t *padded, uint64_t nslots,
+                           uint64_t *io) {
+    atomicAdd((unsigned long long *)&io[0], (unsigned long long)(soff[nslots - 1] + padded[nslots - 1]));
+}
+__global__ void k_io_count_out(const uint64_t *used_local, uint64_t *io) {
+    atomicAdd((unsigned long long *)&io[1], (unsigned long long)((*used_local + 15) / 16 * 16));
 }
 
 __global__ void k_fill_init(ChunkTable t, uint64_t nchunks, uint64_t zoff, uint32_t zlen,
@@ -217,6 +247,11 @@ struct qzc_sim {
     uint64_t N = 0, nchunks = 0;
     CodecGeom geom{};
     DevBuf arena[2], off[2], len[2], crc[2];
+    // host-staged residency: the arenas live in mapped page-locked host memory
+    bool host_res = false;
+    uint8_t *harena[2] = {nullptr, nullptr};      // host view
+    uint8_t *harena_dev[2] = {nullptr, nullptr};  // device view of the same bytes
+    DevBuf io_bytes;  // uint64[2]: host->HBM and HBM->host payload bytes
     DevBuf used;   // uint64[2] bump pointers
     DevBuf acct;   // int64[2] current / peak
     uint64_t arena_cap = 0;
@@ -235,6 +270,7 @@ struct qzc_sim {
         return ChunkTable{off[i].as<uint64_t>(), len[i].as<uint32_t>(), crc[i].as<uint32_t>()};
     }
     cudaStream_t st() const { return ctx->stream; }
+    uint8_t *arena_ptr(int i) { return host_res ? harena_dev[i] : arena[i].as<uint8_t>(); }
     uint64_t *used_ptr(int i) { return used.as<uint64_t>() + i; }
 };
 
@@ -246,8 +282,9 @@ void encode_window(qzc_context *ctx, Window &w, const CodecGeom &g, uint64_t nsl
                    uint8_t *arena, uint64_t *used, uint64_t cap, ChunkTable t,
                    const uint32_t *old_len, int64_t *acct, uint64_t &launches,
                    cudaStream_t s = nullptr, cudaEvent_t acct_prev = nullptr,
-                   cudaEvent_t acct_done = nullptr) {
+                   cudaEvent_t acct_done = nullptr, const uint64_t *acct_map = nullptr) {
     if (!s) s = ctx->stream;
+    if (!acct_map) acct_map = slot_chunk;
     launch_encode(w.amps.as<double2>(), nslots, g, forced, nforced, w.scratch.as<uint8_t>(),
                   w.meta.as<EncHalf>(), s);
     launch_enc_sizes(w.meta.as<EncHalf>(), nslots, g, w.sizes.as<uint64_t>(), s);
@@ -257,7 +294,7 @@ void encode_window(qzc_context *ctx, Window &w, const CodecGeom &g, uint64_t nsl
     launch_arena_alloc(w.reloff.as<uint64_t>(), w.sizes.as<uint64_t>(), nslots, used, cap,
                        w.base.as<uint64_t>(), ctx->status, s);
     if (acct && old_len) {
-        k_delta<<<(unsigned)ceil_div(nslots, 256), 256, 0, s>>>(w.sizes.as<uint64_t>(), slot_chunk,
+        k_delta<<<(unsigned)ceil_div(nslots, 256), 256, 0, s>>>(w.sizes.as<uint64_t>(), acct_map,
                                                                 old_len, nslots, w.delta.as<int64_t>());
         QZ_CHECK_LAUNCH();
         tb = w.cub.cap;
@@ -317,7 +354,9 @@ void sim_alloc(qzc_sim *sim) {
     QZ_CUDA(cudaMemGetInfo(&free_b, &total_b));
     uint64_t budget = ctx->budget ? std::min<uint64_t>(ctx->budget, free_b) : free_b;
     budget = budget > (uint64_t(3) << 30) ? budget - (uint64_t(3) << 30) : budget / 2;
-    const uint64_t per_amp = 16 + 2 * sim->geom.half_stride / sim->N + 8;  // dense + scratch + meta
+    // dense + encode scratch + metadata (+ payload staging when host-staged)
+    const uint64_t per_amp = 16 + 2 * sim->geom.half_stride / sim->N + 8 +
+                             (sim->host_res ? 2 * (payload_bound(sim->N, sim->eb) + 48) / sim->N + 1 : 0);
     const uint64_t state_amps = uint64_t(1) << sim->n;
     uint64_t wa = sim->cfg.window_amps;
     if (!wa) {
@@ -351,8 +390,27 @@ void sim_alloc(qzc_sim *sim) {
         avail = std::min<uint64_t>(avail, ctx->budget > spent ? ctx->budget - spent : 0);
     }
     sim->arena_cap = std::min<uint64_t>(worst, avail / 2);
-    if (sim->arena_cap < 4096) throw Failure(QZC_ENOMEM, "not enough HBM for the compressed store");
-    for (int i = 0; i < 2; ++i) sim->arena[i].ensure(sim->arena_cap);
+    if (!sim->host_res && sim->arena_cap < 4096)
+        throw Failure(QZC_ENOMEM, "not enough HBM for the compressed store");
+    if (sim->host_res) {
+        // page-locked, mapped host arenas (the store leaves HBM; windows
+        // stream their payloads through it).  Cap by 40% of host RAM each.
+        const uint64_t ram = uint64_t(sysconf(_SC_PHYS_PAGES)) * uint64_t(sysconf(_SC_PAGE_SIZE));
+        sim->arena_cap = std::min<uint64_t>(worst, ram * 2 / 5);
+        for (int i = 0; i < 2; ++i) {
+            void *h = nullptr, *d = nullptr;
+            QZ_CUDA(cudaHostAlloc(&h, sim->arena_cap + 64, cudaHostAllocMapped | cudaHostAllocPortable));
+            QZ_CUDA(cudaHostGetDevicePointer(&d, h, 0));
+            sim->harena[i] = static_cast<uint8_t *>(h);
+            sim->harena_dev[i] = static_cast<uint8_t *>(d);
+        }
+        sim->win.reserve_staging(sim->geom, sim->win.slots);
+        if (sim->two_windows) sim->win2.reserve_staging(sim->geom, sim->win2.slots);
+        sim->io_bytes.ensure(16);
+        QZ_CUDA(cudaMemset(sim->io_bytes.p, 0, 16));
+    } else {
+        for (int i = 0; i < 2; ++i) sim->arena[i].ensure(sim->arena_cap);
+    }
 }
 
 } // namespace
@@ -766,7 +824,7 @@ int qzc_sim_create(qzc_context *ctx, const qzc_sim_config *cfg, qzc_sim **out) {
     if (n > 40) throw Failure(QZC_ESTORE, "qubit count exceeds configured address width (40)");
     if (!(cfg->error_bound >= 0.0) || !std::isfinite(cfg->error_bound))
         throw Failure(QZC_EINVAL, "error bound must be finite and non-negative");
-    if (cfg->residency != 0) throw Failure(QZC_EINVAL, "host-staged residency not built in this version");
+    if (cfg->residency > 1) throw Failure(QZC_EINVAL, "residency must be 0 (HBM) or 1 (host-staged)");
     auto *sim = new qzc_sim;
     sim->ctx = ctx;
     sim->cfg = *cfg;
@@ -777,6 +835,7 @@ int qzc_sim_create(qzc_context *ctx, const qzc_sim_config *cfg, qzc_sim **out) {
     sim->N = uint64_t(1) << c;
     sim->nchunks = uint64_t(1) << (n - c);
     sim->geom = make_geom(sim->N, sim->eb);
+    sim->host_res = cfg->residency == 1;
     try {
         sim_alloc(sim);
     } catch (...) {
@@ -795,6 +854,9 @@ void qzc_sim_destroy(qzc_sim *sim) {
         for (DevBuf *b : {&sim->arena[i], &sim->off[i], &sim->len[i], &sim->crc[i]}) b->release();
     sim->used.release();
     sim->acct.release();
+    sim->io_bytes.release();
+    for (int i = 0; i < 2; ++i)
+        if (sim->harena[i]) cudaFreeHost(sim->harena[i]);
     sim->win.release();
     sim->win2.release();
     for (int i = 0; i < 2; ++i) {
@@ -822,7 +884,7 @@ int qzc_sim_init_basis(qzc_sim *sim) {
     const double one[2] = {1.0, 0.0};
     QZ_CUDA(cudaMemcpyAsync(w.amps.as<double2>() + N, one, 16, cudaMemcpyHostToDevice, s));
     ChunkTable t = sim->table(a);
-    encode_window(ctx, w, sim->geom, 2, nullptr, nullptr, 0, sim->arena[a].as<uint8_t>(),
+    encode_window(ctx, w, sim->geom, 2, nullptr, nullptr, 0, sim->arena_ptr(a),
                   sim->used_ptr(a), sim->arena_cap, t, nullptr, nullptr, ctx->launches);
     ctx->check_status();
     if (sim->eb > 0.0) {
@@ -832,7 +894,7 @@ int qzc_sim_init_basis(qzc_sim *sim) {
         DevBuf sc;
         sc.ensure(8);
         QZ_CUDA(cudaMemcpyAsync(sc.p, &one_slot, 8, cudaMemcpyHostToDevice, s));
-        decode_window(ctx, w, sim->geom, 1, sc.as<uint64_t>(), sim->arena[a].as<uint8_t>(), t, ctx->launches);
+        decode_window(ctx, w, sim->geom, 1, sc.as<uint64_t>(), sim->arena_ptr(a), t, ctx->launches);
         ctx->check_status();
         std::vector<double2> r(N);
         QZ_CUDA(cudaMemcpyAsync(r.data(), w.amps.p, 16 * N, cudaMemcpyDeviceToHost, s));
@@ -849,7 +911,7 @@ int qzc_sim_init_basis(qzc_sim *sim) {
             QZ_CUDA(cudaMemsetAsync(w.amps.p, 0, 16 * N, s));
             QZ_CUDA(cudaMemcpyAsync(w.amps.p, one, 16, cudaMemcpyHostToDevice, s));
             encode_window(ctx, w, sim->geom, 1, sc.as<uint64_t>(), fd.as<uint64_t>(), (uint32_t)fr.size(),
-                          sim->arena[a].as<uint8_t>(), sim->used_ptr(a), sim->arena_cap, t, nullptr,
+                          sim->arena_ptr(a), sim->used_ptr(a), sim->arena_cap, t, nullptr,
                           nullptr, ctx->launches);
             ctx->check_status();
             QZ_CUDA(cudaStreamSynchronize(s));
@@ -874,6 +936,7 @@ int qzc_sim_init_basis(qzc_sim *sim) {
     QZ_CUDA(cudaStreamSynchronize(s));
     sim->initialized = true;
     sim->stats = qzc_sim_stats{};
+    if (sim->host_res) QZ_CUDA(cudaMemset(sim->io_bytes.p, 0, 16));
     QZ_API_END
 }
 
@@ -945,16 +1008,50 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
             if (w < 2) QZ_CUDA(cudaStreamWaitEvent(S, ready, 0));
             QZ_CUDA(cudaEventRecord(ev(4 * w), S));
             launch_slot_chunks(W.slot_chunk.as<uint64_t>(), nslots, w * bpw, hs, fmask, smask, S);
-            decode_window(ctx, W, sim->geom, nslots, W.slot_chunk.as<uint64_t>(),
-                          sim->arena[a].as<uint8_t>(), sim->table(a), ctx->launches, S);
+            if (sim->host_res) {
+                // host arena -> HBM staging (zero-copy 16 B reads), then decode
+                // from the staging copy with the slot-indexed local table
+                launch_stage_sizes(sim->table(a), W.slot_chunk.as<uint64_t>(), nslots,
+                                   W.padded.as<uint64_t>(), S);
+                size_t tb = W.cub.cap;
+                QZ_CUDA(cub::DeviceScan::ExclusiveSum(W.cub.p, tb, W.padded.as<uint64_t>(),
+                                                      W.soff.as<uint64_t>(), (int)nslots, S));
+                launch_gather(sim->arena_ptr(a), sim->table(a), W.slot_chunk.as<uint64_t>(),
+                              W.soff.as<uint64_t>(), nslots, W.stage_in.as<uint8_t>(), W.local(), S);
+                k_io_count<<<1, 1, 0, S>>>(W.soff.as<uint64_t>(), W.padded.as<uint64_t>(), nslots,
+                                            sim->io_bytes.as<uint64_t>());
+                QZ_CHECK_LAUNCH();
+                ctx->launches += 5;
+                decode_window(ctx, W, sim->geom, nslots, nullptr, W.stage_in.as<uint8_t>(), W.local(),
+                              ctx->launches, S);
+            } else {
+                decode_window(ctx, W, sim->geom, nslots, W.slot_chunk.as<uint64_t>(),
+                              sim->arena_ptr(a), sim->table(a), ctx->launches, S);
+            }
             QZ_CUDA(cudaEventRecord(ev(4 * w + 1), S));
             ctx->launches += 1 + run_passes(dp, W.amps.as<double2>(), wbits, S);
             QZ_CUDA(cudaEventRecord(ev(4 * w + 2), S));
-            encode_window(ctx, W, sim->geom, nslots, W.slot_chunk.as<uint64_t>(), nullptr, 0,
-                          sim->arena[b].as<uint8_t>(), sim->used_ptr(b), sim->arena_cap,
-                          sim->table(b), sim->len[a].as<uint32_t>(), sim->acct.as<int64_t>(),
-                          ctx->launches, S, w ? sim->acct_ev[(w - 1) & 1] : nullptr,
-                          sim->acct_ev[w & 1]);
+            if (sim->host_res) {
+                QZ_CUDA(cudaMemsetAsync(W.lused.p, 0, 8, S));
+                encode_window(ctx, W, sim->geom, nslots, nullptr, nullptr, 0, W.stage_out.as<uint8_t>(),
+                              W.lused.as<uint64_t>(), W.stage_out_cap, W.local(),
+                              sim->len[a].as<uint32_t>(), sim->acct.as<int64_t>(), ctx->launches, S,
+                              w ? sim->acct_ev[(w - 1) & 1] : nullptr, sim->acct_ev[w & 1],
+                              W.slot_chunk.as<uint64_t>());
+                // HBM -> host arena (zero-copy 16 B writes) + chunk table
+                launch_copy_out(W.stage_out.as<uint8_t>(), W.lused.as<uint64_t>(), sim->used_ptr(b),
+                                sim->arena_cap, W.hbase.as<uint64_t>(), sim->arena_ptr(b), W.local(),
+                                W.slot_chunk.as<uint64_t>(), nslots, sim->table(b), ctx->status, S);
+                k_io_count_out<<<1, 1, 0, S>>>(W.lused.as<uint64_t>(), sim->io_bytes.as<uint64_t>());
+                QZ_CHECK_LAUNCH();
+                ctx->launches += 4;
+            } else {
+                encode_window(ctx, W, sim->geom, nslots, W.slot_chunk.as<uint64_t>(), nullptr, 0,
+                              sim->arena_ptr(b), sim->used_ptr(b), sim->arena_cap,
+                              sim->table(b), sim->len[a].as<uint32_t>(), sim->acct.as<int64_t>(),
+                              ctx->launches, S, w ? sim->acct_ev[(w - 1) & 1] : nullptr,
+                              sim->acct_ev[w & 1]);
+            }
             QZ_CUDA(cudaEventRecord(ev(4 * w + 3), S));
         }
         for (int i = 0; i < 2; ++i) QZ_CUDA(cudaStreamSynchronize(sim->streams[i]));
@@ -994,6 +1091,12 @@ int qzc_sim_stats_get(const qzc_sim *sim, qzc_sim_stats *out) {
     QZ_CUDA(cudaMemcpy(acct, sim->acct.p, 16, cudaMemcpyDeviceToHost));
     out->current_bytes = uint64_t(acct[0]);
     out->peak_bytes = uint64_t(acct[1]);
+    if (sim->host_res) {
+        uint64_t io[2];
+        QZ_CUDA(cudaMemcpy(io, sim->io_bytes.p, 16, cudaMemcpyDeviceToHost));
+        out->h2d_bytes += io[0];
+        out->d2h_bytes += io[1];
+    }
     out->dense_bytes = (uint64_t(1) << sim->n) * 16;
     QZ_API_END
 }
@@ -1020,7 +1123,10 @@ void pull_store(qzc_sim *sim, std::vector<uint64_t> &off, std::vector<uint32_t> 
     QZ_CUDA(cudaMemcpyAsync(&used, sim->used_ptr(a), 8, cudaMemcpyDeviceToHost, s));
     QZ_CUDA(cudaStreamSynchronize(s));
     arena.resize(used);
-    QZ_CUDA(cudaMemcpyAsync(arena.data(), sim->arena[a].p, used, cudaMemcpyDeviceToHost, s));
+    if (sim->host_res)
+        std::memcpy(arena.data(), sim->harena[a], used);
+    else
+        QZ_CUDA(cudaMemcpyAsync(arena.data(), sim->arena[a].p, used, cudaMemcpyDeviceToHost, s));
     QZ_CUDA(cudaStreamSynchronize(s));
     sim->stats.d2h_bytes += used + 16 * sim->nchunks;
 }
@@ -1083,7 +1189,10 @@ int qzc_sim_import(qzc_sim *sim, const uint8_t *payloads, const uint32_t *sizes,
     }
     if (pos > sim->arena_cap) throw Failure(QZC_ENOMEM, "store does not fit the HBM arena");
     const int a = sim->cur;
-    QZ_CUDA(cudaMemcpyAsync(sim->arena[a].p, payloads, pos, cudaMemcpyHostToDevice, s));
+    if (sim->host_res)
+        std::memcpy(sim->harena[a], payloads, pos);
+    else
+        QZ_CUDA(cudaMemcpyAsync(sim->arena[a].p, payloads, pos, cudaMemcpyHostToDevice, s));
     QZ_CUDA(cudaMemcpyAsync(sim->off[a].p, off.data(), 8 * sim->nchunks, cudaMemcpyHostToDevice, s));
     QZ_CUDA(cudaMemcpyAsync(sim->len[a].p, sizes, 4 * sim->nchunks, cudaMemcpyHostToDevice, s));
     QZ_CUDA(cudaMemcpyAsync(sim->crc[a].p, crcs, 4 * sim->nchunks, cudaMemcpyHostToDevice, s));
@@ -1108,7 +1217,7 @@ int qzc_sim_read_chunks(qzc_sim *sim, uint64_t first, uint64_t count, double *am
         const uint64_t k = std::min(per, first + count - f);
         launch_slot_chunks(sim->win.slot_chunk.as<uint64_t>(), k, f, 0, (uint64_t(1) << (sim->n - sim->c)) - 1, 0, s);
         decode_window(ctx, sim->win, sim->geom, k, sim->win.slot_chunk.as<uint64_t>(),
-                      sim->arena[sim->cur].as<uint8_t>(), sim->table(sim->cur), ctx->launches);
+                      sim->arena_ptr(sim->cur), sim->table(sim->cur), ctx->launches);
         ctx->check_status();
         QZ_CUDA(cudaMemcpyAsync(amps_out + 2 * (f - first) * sim->N, sim->win.amps.p, 16 * k * sim->N,
                                 cudaMemcpyDeviceToHost, s));
@@ -1128,7 +1237,7 @@ int qzc_sim_write_chunk(qzc_sim *sim, uint64_t index, const double *amps) {
     QZ_CUDA(cudaMemcpyAsync(sim->win.slot_chunk.p, &index, 8, cudaMemcpyHostToDevice, s));
     // the table of the live arena is updated in place; old bytes become garbage
     encode_window(ctx, sim->win, sim->geom, 1, sim->win.slot_chunk.as<uint64_t>(), nullptr, 0,
-                  sim->arena[a].as<uint8_t>(), sim->used_ptr(a), sim->arena_cap, sim->table(a),
+                  sim->arena_ptr(a), sim->used_ptr(a), sim->arena_cap, sim->table(a),
                   sim->len[a].as<uint32_t>(), sim->acct.as<int64_t>(), ctx->launches);
     ctx->check_status();
     QZ_API_END
@@ -1148,7 +1257,7 @@ int qzc_sim_norm(qzc_sim *sim, double *norm_out) {
         const uint64_t cnt = std::min(per, sim->nchunks - f);
         launch_slot_chunks(sim->win.slot_chunk.as<uint64_t>(), cnt, f, 0, (uint64_t(1) << (sim->n - sim->c)) - 1, 0, s);
         decode_window(ctx, sim->win, sim->geom, cnt, sim->win.slot_chunk.as<uint64_t>(),
-                      sim->arena[sim->cur].as<uint8_t>(), sim->table(sim->cur), ctx->launches);
+                      sim->arena_ptr(sim->cur), sim->table(sim->cur), ctx->launches);
         k_partials<<<(unsigned)ceil_div(cnt, 8), dim3(32, 8), 0, s>>>(sim->win.amps.as<double2>(), cnt, sim->N,
                                                                    nullptr, 0, part.as<double>());
         QZ_CHECK_LAUNCH();
@@ -1176,7 +1285,7 @@ int qzc_sim_fidelity_dev(qzc_sim *sim, const double *dense_dev, double *fidelity
         const uint64_t cnt = std::min(per, sim->nchunks - f);
         launch_slot_chunks(sim->win.slot_chunk.as<uint64_t>(), cnt, f, 0, (uint64_t(1) << (sim->n - sim->c)) - 1, 0, s);
         decode_window(ctx, sim->win, sim->geom, cnt, sim->win.slot_chunk.as<uint64_t>(),
-                      sim->arena[sim->cur].as<uint8_t>(), sim->table(sim->cur), ctx->launches);
+                      sim->arena_ptr(sim->cur), sim->table(sim->cur), ctx->launches);
         k_partials<<<(unsigned)ceil_div(cnt, 8), dim3(32, 8), 0, s>>>(
             sim->win.amps.as<double2>(), cnt, sim->N, reinterpret_cast<const double2 *>(dense_dev), f,
             part.as<double>());

@@ -102,6 +102,12 @@ def load_library() -> C.CDLL:
         "qzc_dense_run": (C.c_int, [C.c_void_p, C.c_uint32, P(Gate), C.c_uint64,
                                     P(C.c_void_p)]),
         "qzc_dense_free": (None, [C.c_void_p, C.c_void_p]),
+        "qzc_buffer_alloc": (C.c_int, [C.c_void_p, C.c_uint64, P(C.c_void_p)]),
+        "qzc_buffer_free": (None, [C.c_void_p, C.c_void_p]),
+        "qzc_copy_h2d": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64]),
+        "qzc_copy_d2h": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64]),
+        "qzc_host_alloc": (C.c_int, [C.c_void_p, C.c_uint64, P(C.c_void_p)]),
+        "qzc_host_free": (None, [C.c_void_p, C.c_void_p]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -161,6 +167,28 @@ class Engine:
         out = C.c_double()
         _check(self.lib.qzc_timer_end(self.h, C.byref(out)))
         return out.value
+
+    def host_link_gbps(self, nbytes: int = 1 << 30, reps: int = 5) -> dict:
+        """Pinned cudaMemcpyAsync H2D / D2H bandwidth (the host-link roofline
+        of the host-staged residency), CUDA-event timed, best of `reps`."""
+        amps = nbytes // 16
+        h, d = C.c_void_p(), C.c_void_p()
+        _check(self.lib.qzc_host_alloc(self.h, nbytes, C.byref(h)))
+        _check(self.lib.qzc_buffer_alloc(self.h, amps, C.byref(d)))
+        try:
+            out = {}
+            for name, fn, args in (("h2d", self.lib.qzc_copy_h2d, (d, 0, h, amps)),
+                                   ("d2h", self.lib.qzc_copy_d2h, (h, d, 0, amps))):
+                best = 1e30
+                for _ in range(reps):
+                    self.timer_begin()
+                    _check(fn(self.h, *args))
+                    best = min(best, self.timer_end())
+                out[name] = nbytes / best / 1e9
+            return out
+        finally:
+            self.lib.qzc_buffer_free(self.h, d)
+            self.lib.qzc_host_free(self.h, h)
 
     # ---- gates ---------------------------------------------------------------
     def gate_matrix(self, g) -> np.ndarray:
@@ -258,11 +286,12 @@ class Simulator:
     """Compressed-chunk state vector in HBM (qzc_sim) — qzsim::run's hot path."""
 
     def __init__(self, eng: Engine, n: int, c: int, m: int, eb: float, window_amps: int = 0,
-                 fuse: bool = True, init: bool = True):
+                 fuse: bool = True, init: bool = True, residency: str = "hbm"):
         self.eng, self.lib = eng, eng.lib
         self.n, self.c, self.m, self.eb = n, c, m, eb
         cfg = SimConfig(num_qubits=n, chunk_qubits=c, batch_qubits=m, error_bound=eb,
-                        window_amps=window_amps, residency=0, renormalize=0,
+                        window_amps=window_amps, residency={"hbm": 0, "host": 1}[residency],
+                        renormalize=0,
                         fuse_gates=1 if fuse else 0)
         h = C.c_void_p()
         _check(self.lib.qzc_sim_create(eng.h, C.byref(cfg), C.byref(h)))
