@@ -165,6 +165,16 @@ void qzc_event_destroy(qzc_context *ctx, void *event);
 /* 1 if the event has completed, 0 if work before it is still pending. */
 int qzc_event_done(qzc_context *ctx, void *event);
 
+/* ---- planner (plan(), planner.cpp:46-96) — host only, no context ---------- */
+/* Stage partition of a circuit: stage s covers gates [first_gate[s],
+ * first_gate[s] + stage_ngates[s]); its padded high set is
+ * high[64*s .. 64*s + nhigh[s]).  Returns the stage count in *nstages; at
+ * most `cap` stages are written. */
+int qzc_plan_export(uint32_t num_qubits, uint32_t chunk_qubits, uint32_t batch_qubits,
+                    const qzc_gate *gates, uint64_t ngates, uint64_t *nstages,
+                    uint64_t *first_gate, uint64_t *stage_ngates, uint32_t *nhigh,
+                    uint32_t *high, uint64_t cap);
+
 /* ---- simulator (replaces qzsim::run, pipeline.cpp:128-314) -------------- */
 typedef struct qzc_sim qzc_sim;
 

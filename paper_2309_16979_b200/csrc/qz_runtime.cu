@@ -940,6 +940,22 @@ int qzc_sim_init_basis(qzc_sim *sim) {
     QZ_API_END
 }
 
+int qzc_plan_export(uint32_t num_qubits, uint32_t chunk_qubits, uint32_t batch_qubits,
+                    const qzc_gate *gates, uint64_t ngates, uint64_t *nstages,
+                    uint64_t *first_gate, uint64_t *stage_ngates, uint32_t *nhigh,
+                    uint32_t *high, uint64_t cap) {
+    QZ_API_BEGIN
+    const std::vector<Stage> st = plan_stages(num_qubits, gates, ngates, chunk_qubits, batch_qubits);
+    *nstages = st.size();
+    for (size_t i = 0; i < st.size() && i < cap; ++i) {
+        first_gate[i] = st[i].first_gate;
+        stage_ngates[i] = st[i].ngates;
+        nhigh[i] = uint32_t(st[i].high.size());
+        for (size_t k = 0; k < st[i].high.size() && k < 64; ++k) high[64 * i + k] = st[i].high[k];
+    }
+    QZ_API_END
+}
+
 int qzc_sim_plan_stages(const qzc_sim *sim, const qzc_gate *gates, uint64_t ngates,
                         uint64_t *stages_out) {
     QZ_API_BEGIN

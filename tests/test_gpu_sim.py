@@ -166,3 +166,20 @@ def test_host_staged_windows_and_io(engine, oracle, golden):
         assert f"{sim.digest():016x}" == rec["digest"]
         blob, sizes, crcs = sim.export()
         assert oracle.fnv1a64(blob) == sim.digest()
+
+
+@pytest.mark.parametrize("key,g", [(("random:12:80:8", 4, 8, 1e-5), 1), (("random:12:80:8", 4, 8, 1e-5), 2),
+                                   (("qft:20", 12, 16, 1e-5), 2), (("qft:20", 12, 16, 1e-5), 1),
+                                   (("random:24:200:1", 16, 20, 1e-7), 2)])
+def test_sharded_ranks_same_digest(engine, oracle, golden, key, g):
+    """2^g ranks (in-process, one GPU) exchanging compressed chunks at stage
+    boundaries reproduce the single-GPU / reference digest."""
+    from paper_2309_16979_b200 import sharding as S
+    circ_key, c, m, eb = key
+    rec = next(r for r in golden["runs"] if r["circuit"] == circ_key and r["c"] == c
+               and r["m"] == m and r["eb"] == eb)
+    gl = circuit(golden, oracle, circ_key)
+    run = S.ShardedRun(engine, rec["n"], c, m, eb, g, range(1 << g), S.LocalGroup(1 << g))
+    run.init_basis()
+    run.run(gl)
+    assert f"{run.digest():016x}" == rec["digest"]
