@@ -339,7 +339,54 @@ GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_
                 std::memcpy(t.m, g.m, sizeof t.m);
                 plan.gates.push_back(t);
             }
+            // fast list: the same gates with macro-able runs folded
+            gd.first_fast = (uint32_t)plan.gates.size();
+            {
+                const uint32_t e0 = gd.first_gate, e1 = gd.first_gate + gd.ngates;
+                for (uint32_t i = e0; i < e1;) {
+                    const TileGate *G = &plan.gates[0];
+                    auto u1_on = [&](uint32_t k, uint32_t r) {
+                        return G[k].nq == 1 && G[k].op == OP_DIAG && G[k].r0 == r &&
+                               (uint32_t(G[k].kinds) & 15u) == CK_ONE;
+                    };
+                    auto cx_on = [&](uint32_t k, uint32_t a, uint32_t b) {
+                        return G[k].nq == 2 && G[k].op == OP_CX && G[k].r0 == a && G[k].r1 == b;
+                    };
+                    if (i + 5 <= e1 && u1_on(i, G[i].r0) && G[i + 1].nq == 2 &&
+                        cx_on(i + 1, G[i].r0, G[i + 1].r1) && u1_on(i + 2, G[i + 1].r1) &&
+                        cx_on(i + 3, G[i].r0, G[i + 1].r1) && u1_on(i + 4, G[i + 1].r1)) {
+                        TileGate mg = G[i + 1];
+                        mg.op = OP_CP5;
+                        mg.m[0] = G[i].m[3];
+                        mg.m[1] = G[i + 2].m[3];
+                        mg.m[2] = G[i + 4].m[3];
+                        mg.kinds = (uint64_t(G[i].kinds >> 12) & 15) | ((uint64_t(G[i + 2].kinds >> 12) & 15) << 4) |
+                                   ((uint64_t(G[i + 4].kinds >> 12) & 15) << 8);
+                        mg.srow = ((G[i].srow >> 1) & 1) | (((G[i + 2].srow >> 1) & 1) << 1) |
+                                  (((G[i + 4].srow >> 1) & 1) << 2);
+                        plan.gates.push_back(mg);
+                        i += 5;
+                        continue;
+                    }
+                    if (i + 3 <= e1 && G[i].nq == 2 && G[i].op == OP_CX && G[i + 1].nq == 1 &&
+                        G[i + 1].op == OP_DIAG && G[i + 1].r0 == G[i].r1 && cx_on(i + 2, G[i].r0, G[i].r1)) {
+                        TileGate mg = G[i];
+                        mg.op = OP_CXD;
+                        mg.m[0] = G[i + 1].m[0];
+                        mg.m[1] = G[i + 1].m[3];
+                        mg.kinds = (uint64_t(G[i + 1].kinds) & 15) | ((uint64_t(G[i + 1].kinds >> 12) & 15) << 4);
+                        mg.srow = G[i + 1].srow & 3;
+                        plan.gates.push_back(mg);
+                        i += 3;
+                        continue;
+                    }
+                    const TileGate same = plan.gates[i];
+                    plan.gates.push_back(same);
+                    ++i;
+                }
+            }
             plan.groups.push_back(gd);
+            plan.groups.back().nfast = (uint32_t)plan.gates.size() - gd.first_fast;
             gmembers.clear();
             gmask = 0;
         };
@@ -668,6 +715,58 @@ __device__ __forceinline__ void fast_swap(double2 (&v)[NB]) {
         }
 }
 
+// CP5 on (A, B): p01 <- m3(m2 v01), p10 <- m2(m1 v10), p11 <- m3(m1 v11)
+// (the CX swaps folded into the indexing; same products, same order).
+template <int A, int B>
+__device__ __forceinline__ void fast_cp5(double2 (&v)[NB], const TileGate &g, bool &bad) {
+    const uint32_t k1 = uint32_t(g.kinds) & 15u, k2 = uint32_t(g.kinds >> 4) & 15u,
+                   k3 = uint32_t(g.kinds >> 8) & 15u;
+    const double2 m1 = g.m[0], m2 = g.m[1], m3 = g.m[2];
+    const bool u1 = !(g.srow & 1), u2 = !(g.srow & 2), u3 = !(g.srow & 4);
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+        if (((i >> A) & 1) || ((i >> B) & 1)) continue;
+        const int i01 = i | (1 << B), i10 = i | (1 << A), i11 = i | (1 << A) | (1 << B);
+        double2 x01 = term(k2, m2, v[i01]);
+        if (u2) bad |= zc(x01);
+        x01 = term(k3, m3, x01);
+        if (u3) bad |= zc(x01);
+        double2 x10 = term(k1, m1, v[i10]);
+        if (u1) bad |= zc(x10);
+        x10 = term(k2, m2, x10);
+        if (u2) bad |= zc(x10);
+        double2 x11 = term(k1, m1, v[i11]);
+        if (u1) bad |= zc(x11);
+        x11 = term(k3, m3, x11);
+        if (u3) bad |= zc(x11);
+        v[i01] = x01;
+        v[i10] = x10;
+        v[i11] = x11;
+    }
+}
+
+// CXD on (A, B), D = diag(d0, d1) on B: p00 <- d0 v00, p01 <- d1 v01,
+// p10 <- d1 v10, p11 <- d0 v11.
+template <int A, int B>
+__device__ __forceinline__ void fast_cxd(double2 (&v)[NB], const TileGate &g, bool &bad) {
+    const uint32_t k0 = uint32_t(g.kinds) & 15u, k1 = uint32_t(g.kinds >> 4) & 15u;
+    const double2 d0 = g.m[0], d1 = g.m[1];
+    const bool u0 = !(g.srow & 1), u1 = !(g.srow & 2);
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+        if (((i >> A) & 1) || ((i >> B) & 1)) continue;
+        const int i01 = i | (1 << B), i10 = i | (1 << A), i11 = i | (1 << A) | (1 << B);
+        const double2 x00 = term(k0, d0, v[i]), x01 = term(k1, d1, v[i01]);
+        const double2 x10 = term(k1, d1, v[i10]), x11 = term(k0, d0, v[i11]);
+        if (u0) bad |= zc(x00) | zc(x11);
+        if (u1) bad |= zc(x01) | zc(x10);
+        v[i] = x00;
+        v[i01] = x01;
+        v[i10] = x10;
+        v[i11] = x11;
+    }
+}
+
 #if QZ_REG_BITS == 3
 #define QZ_PAIRS(X) X(0, 1) X(0, 2) X(1, 2)
 #else
@@ -691,7 +790,23 @@ __device__ __forceinline__ void fast_apply(double2 (&v)[NB], const TileGate &g, 
         return;
     }
     const uint32_t lo = min(g.r0, g.r1), hi = max(g.r0, g.r1);
-    if (op == OP_CX) {
+    if (op == OP_CP5) {
+        switch (g.r0 * 4 + g.r1) {
+#define X(a, b)                                                                              \
+    case a * 4 + b: fast_cp5<a, b>(v, g, bad); break;
+            QZ_R2_CASES(X)
+#undef X
+        default: break;
+        }
+    } else if (op == OP_CXD) {
+        switch (g.r0 * 4 + g.r1) {
+#define X(a, b)                                                                              \
+    case a * 4 + b: fast_cxd<a, b>(v, g, bad); break;
+            QZ_R2_CASES(X)
+#undef X
+        default: break;
+        }
+    } else if (op == OP_CX) {
         switch (g.r0 * 4 + g.r1) {
 #define X(a, b)                                                                              \
     case a * 4 + b: fast_cx<a, b>(v); break;
@@ -975,7 +1090,8 @@ __global__ void __launch_bounds__(1 << (12 - kRegBits), 1) tile_pass_reg(double2
                 }
                 bool bad = !okblk;
                 path = okblk ? 3 : 4;
-                for (uint32_t q = 0; q < G.ngates && !bad; ++q) fast_apply(v, gp[q], bad);
+                const TileGate *fp = gates + G.first_fast;
+                for (uint32_t q = 0; q < G.nfast && !bad; ++q) fast_apply(v, fp[q], bad);
                 if (bad && okblk) path = 5;
                 if (bad) {
                     // a zero is (or became) present: redo the group exactly
@@ -1005,11 +1121,13 @@ __global__ void __launch_bounds__(1 << (12 - kRegBits), 1) tile_pass_reg(double2
 
 // Buffers below 16 amplitudes: one thread, dense formula.
 __global__ void tile_pass_tiny(double2 *buf, uint32_t nbits, PassDesc pd,
+                               const GroupDesc *__restrict__ groups,
                                const TileGate *__restrict__ gates) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     const uint32_t n = 1u << nbits;
-    for (uint32_t q = 0; q < pd.ngates; ++q) {
-        const TileGate &g = gates[pd.first_gate + q];
+    for (uint32_t gi = 0; gi < pd.ngroups; ++gi)
+    for (uint32_t q = 0; q < groups[pd.first_group + gi].ngates; ++q) {
+        const TileGate &g = gates[groups[pd.first_group + gi].first_gate + q];
         if (g.nq == 1) {
             for (uint32_t p = 0; p < n / 2; ++p) {
                 const uint32_t i = insert_zero_bit32(p, g.t0), j = i | (1u << g.t0);
@@ -1071,7 +1189,7 @@ uint64_t run_passes(const DevPlan &plan, double2 *buf, uint32_t nbits, cudaStrea
     for (const PassDesc &pd : plan.host_passes) {
         if (pd.k < (uint32_t)kRegBits + 1) {
             // tile == whole buffer (nbits < 4)
-            tile_pass_tiny<<<1, 32, 0, s>>>(buf, nbits, pd, plan.gates);
+            tile_pass_tiny<<<1, 32, 0, s>>>(buf, nbits, pd, plan.groups, plan.gates);
         } else {
             const uint32_t tile = 1u << pd.k;
             const uint64_t ntiles = uint64_t(1) << (nbits - pd.k);

@@ -25,7 +25,12 @@ struct DevGate {
 // Matrix structure for the zero-free register fast path.  CX / CZ / SWAP are
 // recognised by value (their ±0 entries only ever matter for zero outputs,
 // which the fast path never produces without falling back).
-enum GateOp : uint32_t { OP_GEN1 = 0, OP_DIAG = 1, OP_CX = 2, OP_CZ = 3, OP_SWAP = 4, OP_GEN2 = 5 };
+enum GateOp : uint32_t {
+    OP_GEN1 = 0, OP_DIAG = 1, OP_CX = 2, OP_CZ = 3, OP_SWAP = 4, OP_GEN2 = 5,
+    // fast-path macros (a run of gates on one qubit pair, same operations)
+    OP_CP5 = 6,  // U1(a) CX(a,b) U1(b) CX(a,b) U1(b): m[0..2] = the U1s' phase entries
+    OP_CXD = 7,  // CX(a,b) D(b) CX(a,b), D diagonal: m[0], m[1] = D's entries
+};
 
 // A gate inside a register group: r0/r1 are the gate's qubits as bit
 // positions of the thread's 16-amplitude register block.
@@ -61,7 +66,8 @@ constexpr int kRegBits = QZ_REG_BITS;
 // Consecutive gates whose qubits fit kRegBits tile bits: applied in registers.
 struct GroupDesc {
     uint32_t gbits[4];     // tile-local bits, ascending; register bit i <-> gbits[i]
-    uint32_t first_gate, ngates;
+    uint32_t first_gate, ngates;   // exact gate list
+    uint32_t first_fast, nfast;    // fast-path list (macros folded in)
     uint32_t generic;      // 1: apply on the smem tile with the full formula
     uint32_t pz_stable;    // every gate maps an all-(+0) block to all-(+0)
 };
