@@ -385,6 +385,25 @@ GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_
                     ++i;
                 }
             }
+            for (size_t k = gd.first_fast; k < plan.gates.size(); ++k) {
+                TileGate &t = plan.gates[k];
+                const uint32_t kd = uint32_t(t.kinds);
+                auto K = [&](int e) { return (kd >> (4 * e)) & 15u; };
+                t.pad2 = 0;
+                if (t.op == OP_DIAG && (t.srow & 3) == 3) {
+                    if (K(0) == CK_ONE && K(3) == CK_CPLX) t.pad2 = 1;
+                    else if (K(0) == CK_CPLX && K(3) == CK_CPLX) t.pad2 = 2;
+                } else if (t.op == OP_GEN1 && (t.srow & 3) == 3) {
+                    if (K(0) == CK_REAL && K(1) == CK_IMAG && K(2) == CK_IMAG && K(3) == CK_REAL) t.pad2 = 3;
+                    else if (K(0) == CK_REAL && K(1) == CK_REAL && K(2) == CK_REAL && K(3) == CK_REAL) t.pad2 = 4;
+                    else if (K(0) == CK_CPLX && K(1) == CK_CPLX && K(2) == CK_CPLX && K(3) == CK_CPLX) t.pad2 = 5;
+                } else if (t.op == OP_CP5 && (t.srow & 7) == 7 && K(0) == CK_CPLX && K(1) == CK_CPLX &&
+                           K(2) == CK_CPLX) {
+                    t.pad2 = 6;
+                } else if (t.op == OP_CXD && (t.srow & 3) == 3 && K(0) == CK_CPLX && K(1) == CK_CPLX) {
+                    t.pad2 = 7;
+                }
+            }
             plan.groups.push_back(gd);
             plan.groups.back().nfast = (uint32_t)plan.gates.size() - gd.first_fast;
             gmembers.clear();
@@ -549,6 +568,25 @@ __device__ __forceinline__ double2 term(uint32_t kind, double2 m, double2 v) {
                         __dadd_rn(__dmul_rn(m.x, v.y), __dmul_rn(m.y, v.x)));
 }
 
+// Compile-time-kind term (K < 0: run-time kind).
+template <int K>
+__device__ __forceinline__ double2 termk(uint32_t kind, double2 m, double2 v) {
+    if constexpr (K < 0) {
+        return term(kind, m, v);
+    } else if constexpr (K == CK_ONE) {
+        return v;
+    } else if constexpr (K == CK_NEG) {
+        return make_double2(dneg(v.x), dneg(v.y));
+    } else if constexpr (K == CK_REAL) {
+        return make_double2(__dmul_rn(m.x, v.x), __dmul_rn(m.x, v.y));
+    } else if constexpr (K == CK_IMAG) {
+        return make_double2(dneg(__dmul_rn(m.y, v.y)), __dmul_rn(m.y, v.x));
+    } else {
+        return make_double2(__dsub_rn(__dmul_rn(m.x, v.x), __dmul_rn(m.y, v.y)),
+                            __dadd_rn(__dmul_rn(m.x, v.y), __dmul_rn(m.y, v.x)));
+    }
+}
+
 __device__ __forceinline__ double2 sum2(double2 a, double2 b) {
     return make_double2(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y));
 }
@@ -641,27 +679,31 @@ __device__ __forceinline__ void reg_apply2(double2 (&v)[NB], const TileGate &g) 
 // Valid while every component in the block is nonzero: moves are exact, and
 // the shortcut products are exact for nonzero results.  Any zero output sets
 // `bad`; the caller then redoes the whole group on the exact path.
-template <int R>
+// SPEC = 1: every row +0-safe and the kinds are the template's (no checks,
+// no kind branches); SPEC = 0: run-time kinds and safety.
+template <int R, int K0 = -1, int K1 = -1, int SPEC = 0>
 __device__ __forceinline__ void fast_diag(double2 (&v)[NB], const TileGate &g, bool &bad) {
     constexpr int sh = 1 << R;
     const uint32_t k00 = uint32_t(g.kinds) & 15u, k11 = uint32_t(g.kinds >> 12) & 15u;
     const double2 m00 = g.m[0], m11 = g.m[3];
-    const bool u0 = !(g.srow & 1), u1 = !(g.srow & 2);   // unsafe rows: check zeros
+    const bool u0 = !SPEC && !(g.srow & 1), u1 = !SPEC && !(g.srow & 2);
 #pragma unroll
     for (int p = 0; p < NB / 2; ++p) {
         const int i = izb(p, R), j = i | sh;
-        if (k00 != CK_ONE) {
-            v[i] = term(k00, m00, v[i]);
+        if (K0 == CK_ONE || (K0 < 0 && k00 == CK_ONE)) {
+        } else {
+            v[i] = termk<K0>(k00, m00, v[i]);
             if (u0) bad |= zc(v[i]);
         }
-        if (k11 != CK_ONE) {
-            v[j] = term(k11, m11, v[j]);
+        if (K1 == CK_ONE || (K1 < 0 && k11 == CK_ONE)) {
+        } else {
+            v[j] = termk<K1>(k11, m11, v[j]);
             if (u1) bad |= zc(v[j]);
         }
     }
 }
 
-template <int R>
+template <int R, int K00 = -1, int K01 = -1, int K10 = -1, int K11 = -1, int SPEC = 0>
 __device__ __forceinline__ void fast_gen1(double2 (&v)[NB], const TileGate &g, bool &bad) {
     constexpr int sh = 1 << R;
     const uint32_t kd = uint32_t(g.kinds);
@@ -671,12 +713,18 @@ __device__ __forceinline__ void fast_gen1(double2 (&v)[NB], const TileGate &g, b
     for (int p = 0; p < NB / 2; ++p) {
         const int i = izb(p, R), j = i | sh;
         const double2 a = v[i], b = v[j];
-        const double2 oi = k00 == CK_ZERO ? term(k01, m01, b)
-                         : (k01 == CK_ZERO ? term(k00, m00, a) : sum2(term(k00, m00, a), term(k01, m01, b)));
-        const double2 oj = k10 == CK_ZERO ? term(k11, m11, b)
-                         : (k11 == CK_ZERO ? term(k10, m10, a) : sum2(term(k10, m10, a), term(k11, m11, b)));
-        if (!(g.srow & 1)) bad |= zc(oi);
-        if (!(g.srow & 2)) bad |= zc(oj);
+        double2 oi, oj;
+        if constexpr (SPEC) {
+            oi = sum2(termk<K00>(k00, m00, a), termk<K01>(k01, m01, b));
+            oj = sum2(termk<K10>(k10, m10, a), termk<K11>(k11, m11, b));
+        } else {
+            oi = k00 == CK_ZERO ? term(k01, m01, b)
+               : (k01 == CK_ZERO ? term(k00, m00, a) : sum2(term(k00, m00, a), term(k01, m01, b)));
+            oj = k10 == CK_ZERO ? term(k11, m11, b)
+               : (k11 == CK_ZERO ? term(k10, m10, a) : sum2(term(k10, m10, a), term(k11, m11, b)));
+            if (!(g.srow & 1)) bad |= zc(oi);
+            if (!(g.srow & 2)) bad |= zc(oj);
+        }
         v[i] = oi;
         v[j] = oj;
     }
@@ -717,27 +765,28 @@ __device__ __forceinline__ void fast_swap(double2 (&v)[NB]) {
 
 // CP5 on (A, B): p01 <- m3(m2 v01), p10 <- m2(m1 v10), p11 <- m3(m1 v11)
 // (the CX swaps folded into the indexing; same products, same order).
-template <int A, int B>
+template <int A, int B, int SPEC = 0>
 __device__ __forceinline__ void fast_cp5(double2 (&v)[NB], const TileGate &g, bool &bad) {
     const uint32_t k1 = uint32_t(g.kinds) & 15u, k2 = uint32_t(g.kinds >> 4) & 15u,
                    k3 = uint32_t(g.kinds >> 8) & 15u;
     const double2 m1 = g.m[0], m2 = g.m[1], m3 = g.m[2];
-    const bool u1 = !(g.srow & 1), u2 = !(g.srow & 2), u3 = !(g.srow & 4);
+    const bool u1 = !SPEC && !(g.srow & 1), u2 = !SPEC && !(g.srow & 2), u3 = !SPEC && !(g.srow & 4);
+    constexpr int KC = SPEC ? int(CK_CPLX) : -1;
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
         if (((i >> A) & 1) || ((i >> B) & 1)) continue;
         const int i01 = i | (1 << B), i10 = i | (1 << A), i11 = i | (1 << A) | (1 << B);
-        double2 x01 = term(k2, m2, v[i01]);
+        double2 x01 = termk<KC>(k2, m2, v[i01]);
         if (u2) bad |= zc(x01);
-        x01 = term(k3, m3, x01);
+        x01 = termk<KC>(k3, m3, x01);
         if (u3) bad |= zc(x01);
-        double2 x10 = term(k1, m1, v[i10]);
+        double2 x10 = termk<KC>(k1, m1, v[i10]);
         if (u1) bad |= zc(x10);
-        x10 = term(k2, m2, x10);
+        x10 = termk<KC>(k2, m2, x10);
         if (u2) bad |= zc(x10);
-        double2 x11 = term(k1, m1, v[i11]);
+        double2 x11 = termk<KC>(k1, m1, v[i11]);
         if (u1) bad |= zc(x11);
-        x11 = term(k3, m3, x11);
+        x11 = termk<KC>(k3, m3, x11);
         if (u3) bad |= zc(x11);
         v[i01] = x01;
         v[i10] = x10;
@@ -747,17 +796,18 @@ __device__ __forceinline__ void fast_cp5(double2 (&v)[NB], const TileGate &g, bo
 
 // CXD on (A, B), D = diag(d0, d1) on B: p00 <- d0 v00, p01 <- d1 v01,
 // p10 <- d1 v10, p11 <- d0 v11.
-template <int A, int B>
+template <int A, int B, int SPEC = 0>
 __device__ __forceinline__ void fast_cxd(double2 (&v)[NB], const TileGate &g, bool &bad) {
     const uint32_t k0 = uint32_t(g.kinds) & 15u, k1 = uint32_t(g.kinds >> 4) & 15u;
     const double2 d0 = g.m[0], d1 = g.m[1];
-    const bool u0 = !(g.srow & 1), u1 = !(g.srow & 2);
+    const bool u0 = !SPEC && !(g.srow & 1), u1 = !SPEC && !(g.srow & 2);
+    constexpr int KC = SPEC ? int(CK_CPLX) : -1;
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
         if (((i >> A) & 1) || ((i >> B) & 1)) continue;
         const int i01 = i | (1 << B), i10 = i | (1 << A), i11 = i | (1 << A) | (1 << B);
-        const double2 x00 = term(k0, d0, v[i]), x01 = term(k1, d1, v[i01]);
-        const double2 x10 = term(k1, d1, v[i10]), x11 = term(k0, d0, v[i11]);
+        const double2 x00 = termk<KC>(k0, d0, v[i]), x01 = termk<KC>(k1, d1, v[i01]);
+        const double2 x10 = termk<KC>(k1, d1, v[i10]), x11 = termk<KC>(k0, d0, v[i11]);
         if (u0) bad |= zc(x00) | zc(x11);
         if (u1) bad |= zc(x01) | zc(x10);
         v[i] = x00;
@@ -780,8 +830,16 @@ __device__ __forceinline__ void fast_apply(double2 (&v)[NB], const TileGate &g, 
         switch (g.r0) {
 #define X(a)                                                                                 \
     case a:                                                                                  \
-        if (op == OP_DIAG) fast_diag<a>(v, g, bad);                                         \
-        else fast_gen1<a>(v, g, bad);                                                        \
+        if (op == OP_DIAG) {                                                                 \
+            if (g.pad2 == 1) fast_diag<a, CK_ONE, CK_CPLX, 1>(v, g, bad);                    \
+            else if (g.pad2 == 2) fast_diag<a, CK_CPLX, CK_CPLX, 1>(v, g, bad);              \
+            else fast_diag<a>(v, g, bad);                                                    \
+        } else {                                                                             \
+            if (g.pad2 == 3) fast_gen1<a, CK_REAL, CK_IMAG, CK_IMAG, CK_REAL, 1>(v, g, bad); \
+            else if (g.pad2 == 4) fast_gen1<a, CK_REAL, CK_REAL, CK_REAL, CK_REAL, 1>(v, g, bad); \
+            else if (g.pad2 == 5) fast_gen1<a, CK_CPLX, CK_CPLX, CK_CPLX, CK_CPLX, 1>(v, g, bad); \
+            else fast_gen1<a>(v, g, bad);                                                    \
+        }                                                                                    \
         break;
             QZ_R1_CASES(X)
 #undef X
@@ -793,7 +851,10 @@ __device__ __forceinline__ void fast_apply(double2 (&v)[NB], const TileGate &g, 
     if (op == OP_CP5) {
         switch (g.r0 * 4 + g.r1) {
 #define X(a, b)                                                                              \
-    case a * 4 + b: fast_cp5<a, b>(v, g, bad); break;
+    case a * 4 + b:                                                                          \
+        if (g.pad2 == 6) fast_cp5<a, b, 1>(v, g, bad);                                       \
+        else fast_cp5<a, b>(v, g, bad);                                                      \
+        break;
             QZ_R2_CASES(X)
 #undef X
         default: break;
@@ -801,7 +862,10 @@ __device__ __forceinline__ void fast_apply(double2 (&v)[NB], const TileGate &g, 
     } else if (op == OP_CXD) {
         switch (g.r0 * 4 + g.r1) {
 #define X(a, b)                                                                              \
-    case a * 4 + b: fast_cxd<a, b>(v, g, bad); break;
+    case a * 4 + b:                                                                          \
+        if (g.pad2 == 7) fast_cxd<a, b, 1>(v, g, bad);                                       \
+        else fast_cxd<a, b>(v, g, bad);                                                      \
+        break;
             QZ_R2_CASES(X)
 #undef X
         default: break;
@@ -982,7 +1046,7 @@ __device__ void smem_generic(double2 *s, uint32_t tile, const TileGate &g) {
 // each group is applied by 2^(k-kRegBits) threads holding NB amplitudes in
 // registers.  Every thread moves exactly NB amplitudes per tile in each
 // direction, all issued before any is consumed (cp.async in, batched stores).
-__global__ void __launch_bounds__(1 << (12 - kRegBits), 1) tile_pass_reg(double2 *__restrict__ buf, uint32_t nbits,
+__global__ void __launch_bounds__(1 << (kTileBits - kRegBits), (kTileBits >= 12 ? 1 : (kTileBits == 11 ? 2 : 4))) tile_pass_reg(double2 *__restrict__ buf, uint32_t nbits,
                                                          PassDesc pd,
                                                          const GroupDesc *__restrict__ groups,
                                                          const TileGate *__restrict__ gates,

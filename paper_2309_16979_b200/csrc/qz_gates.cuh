@@ -62,6 +62,11 @@ enum GateClass : uint32_t {
 #define QZ_REG_BITS 3
 #endif
 constexpr int kRegBits = QZ_REG_BITS;
+// Fused-pass tile: 2^kTileBits amplitudes in shared memory per CTA.
+#ifndef QZ_TILE_BITS
+#define QZ_TILE_BITS 11
+#endif
+constexpr uint32_t kTileBits = QZ_TILE_BITS;
 
 // Consecutive gates whose qubits fit kRegBits tile bits: applied in registers.
 struct GroupDesc {

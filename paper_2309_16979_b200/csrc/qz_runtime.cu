@@ -32,7 +32,6 @@ namespace {
 
 thread_local std::string g_last_error;
 
-constexpr uint32_t kTileBits = 12;           // fused-pass tile: 2^12 amplitudes (64 KB smem)
 constexpr uint64_t kPerChunkOverhead = 48;   // ChunkStore::kPerChunkOverhead (store.hpp:48)
 
 // Grow-only device buffer.
