@@ -49,6 +49,8 @@ def parse_args():
     ap.add_argument("--cpu-budget", type=float, default=20.0,
                     help="seconds of reference CPU work per sample")
     ap.add_argument("--no-fuse", action="store_true")
+    ap.add_argument("--strict-passes", action="store_true",
+                    help="every gate qubit inside the pass tile (no relaxed diagonal units)")
     ap.add_argument("--shard", action="store_true",
                     help="N>1: shard ONE circuit over the ranks by global qubits with NCCL "
                          "exchange of compressed chunks (strong scaling) instead of replicas")
@@ -235,7 +237,8 @@ def main() -> int:
     ngates = len(gates)
     if args.shard and world > 1:
         return run_sharded(args, eng, gates, dist, rank, world, local)
-    sim = eng.simulator(args.n, args.c, args.m, args.eb, init=False, fuse=not args.no_fuse,
+    sim = eng.simulator(args.n, args.c, args.m, args.eb, init=False,
+                        fuse=False if args.no_fuse else ("strict" if args.strict_passes else True),
                         residency=args.residency)
 
     for _ in range(args.warmup):
@@ -334,6 +337,7 @@ def main() -> int:
         "peak_ratio": st["dense_bytes"] / st["peak_bytes"] if st["peak_bytes"] else None,
         "digest": f"{digest:016x}",
         "phases_s": phases, "stages": st["stages"], "gate_passes": st["gate_passes"],
+        "replays": st["replays"],
         "gpu_launches": launches,
         "roofline": roofline,
         "host_link": host_link,

@@ -187,8 +187,11 @@ typedef struct qzc_sim_config {
     uint64_t window_amps;    /* dense amplitudes per device window; 0 = auto  */
     uint32_t residency;      /* 0 = compressed store in HBM, 1 = pinned host  */
     uint32_t renormalize;    /* PipelineConfig::renormalize                   */
-    uint32_t fuse_gates;     /* 1 = fused smem gate passes (default)          */
-    uint32_t reserved1;
+    uint32_t fuse_gates;     /* 0 = one pass per gate; 1 = fused passes where
+                                diagonal units may keep qubits outside the
+                                tile (default); 2 = fused, every gate qubit
+                                inside the tile                              */
+    uint32_t debug_flags;    /* bit 0: always take the strict replay (test)   */
 } qzc_sim_config;
 
 /* Per-run statistics (SimulationReport subset, pipeline.hpp:53-67, plus
@@ -212,6 +215,9 @@ typedef struct qzc_sim_stats {
     uint64_t peak_bytes;
     uint64_t dense_bytes;
     uint64_t windows;
+    uint64_t replays;            /* windows whose relaxed gate passes met a
+                                    zero and were replayed with the strict
+                                    plan (device-side, same result)         */
 } qzc_sim_stats;
 
 int qzc_sim_create(qzc_context *ctx, const qzc_sim_config *cfg,

@@ -67,7 +67,7 @@ class SimConfig(C.Structure):
                 ("batch_qubits", C.c_uint32), ("reserved0", C.c_uint32),
                 ("error_bound", C.c_double), ("window_amps", C.c_uint64),
                 ("residency", C.c_uint32), ("renormalize", C.c_uint32),
-                ("fuse_gates", C.c_uint32), ("reserved1", C.c_uint32)]
+                ("fuse_gates", C.c_uint32), ("debug_flags", C.c_uint32)]
 
 
 class SimStats(C.Structure):
@@ -77,7 +77,7 @@ class SimStats(C.Structure):
                [(name, C.c_uint64) for name in
                 ("stages", "batches", "gate_passes", "chunk_decompress_count",
                  "chunk_recompress_count", "h2d_bytes", "d2h_bytes", "kernel_launches",
-                 "current_bytes", "peak_bytes", "dense_bytes", "windows")]
+                 "current_bytes", "peak_bytes", "dense_bytes", "windows", "replays")]
 
     def as_dict(self) -> dict:
         return {name: getattr(self, name) for name, _ in self._fields_}

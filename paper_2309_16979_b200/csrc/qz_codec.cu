@@ -264,7 +264,8 @@ __device__ __forceinline__ void set_comp(double2 &v, uint32_t h, double x) {
 __global__ void __launch_bounds__(2 * kSlotsPerCta) k_dec_lossy(
     const uint8_t *__restrict__ arena, const DecIdx *__restrict__ idx,
     const uint64_t *__restrict__ slot_chunk, uint64_t nslots, CodecGeom g,
-    double2 *__restrict__ win, DevStatus *status) {
+    double2 *__restrict__ win, DevStatus *status, const uint32_t *cond) {
+    if (cond && *cond == 0) return;
     __shared__ TileSmem tile;
     const uint32_t r = threadIdx.x >> 1, h = threadIdx.x & 1;
     const uint64_t slot0 = uint64_t(blockIdx.x) * kSlotsPerCta, s = slot0 + r;
@@ -317,7 +318,8 @@ __global__ void __launch_bounds__(2 * kSlotsPerCta) k_dec_lossy(
 // Lossless decode (codec.cpp:251-263): 8 byte-plane cursors per half.
 __global__ void __launch_bounds__(2 * kSlotsPerCta) k_dec_lossless(
     const uint8_t *__restrict__ arena, const DecIdx *__restrict__ idx, uint64_t nslots,
-    CodecGeom g, double2 *__restrict__ win) {
+    CodecGeom g, double2 *__restrict__ win, const uint32_t *cond) {
+    if (cond && *cond == 0) return;
     __shared__ TileSmem tile;
     const uint32_t r = threadIdx.x >> 1, h = threadIdx.x & 1;
     const uint64_t slot0 = uint64_t(blockIdx.x) * kSlotsPerCta, s = slot0 + r;
@@ -845,13 +847,13 @@ void launch_dec_index(const uint8_t *arena, ChunkTable table, const uint64_t *sl
 
 void launch_decode(const uint8_t *arena, const DecIdx *idx, const uint64_t *slot_chunk,
                    uint64_t nslots, const CodecGeom &g, double2 *win, DevStatus *status,
-                   cudaStream_t s) {
+                   cudaStream_t s, const uint32_t *cond) {
     const unsigned grid = grid_for(nslots, kSlotsPerCta);
     if (g.lossy)
         k_dec_lossy<<<grid, 2 * kSlotsPerCta, 0, s>>>(arena, idx, slot_chunk, nslots, g, win,
-                                                       status);
+                                                       status, cond);
     else
-        k_dec_lossless<<<grid, 2 * kSlotsPerCta, 0, s>>>(arena, idx, nslots, g, win);
+        k_dec_lossless<<<grid, 2 * kSlotsPerCta, 0, s>>>(arena, idx, nslots, g, win, cond);
     QZ_CHECK_LAUNCH();
 }
 

@@ -84,10 +84,11 @@ void launch_dec_index(const uint8_t *arena, ChunkTable table, const uint64_t *sl
                       uint64_t nslots, const CodecGeom &g, DecIdx *idx, DevStatus *status,
                       cudaStream_t s);
 
-// Decode every slot into win[slot*N .. (slot+1)*N).
+// Decode every slot into win[slot*N .. (slot+1)*N).  cond != nullptr: the
+// launch does nothing unless *cond != 0 (device-side replay, see run_passes).
 void launch_decode(const uint8_t *arena, const DecIdx *idx, const uint64_t *slot_chunk,
                    uint64_t nslots, const CodecGeom &g, double2 *win, DevStatus *status,
-                   cudaStream_t s);
+                   cudaStream_t s, const uint32_t *cond = nullptr);
 
 // Sequential encoder pass: codes, RLE sub-streams and raws into scratch.
 void launch_encode(const double2 *win, uint64_t nslots, const CodecGeom &g,

@@ -225,17 +225,117 @@ static bool is_signed_perm(const DevGate &g) {
     return true;
 }
 
-GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_t kmax, bool fuse) {
+// A diagonal unit: a run of gates whose net effect is diagonal (1q diagonal,
+// CZ, or the CP5 / CXD runs) — only these may leave qubits outside a pass.
+struct Unit {
+    size_t first;
+    uint32_t count;
+    bool diag;
+    uint64_t bits;   // buffer bits of all its gates
+};
+
+static uint64_t gate_bits(const DevGate &g) {
+    uint64_t m = uint64_t(1) << g.b0;
+    if (g.nq == 2) m |= uint64_t(1) << g.b1;
+    return m;
+}
+
+static std::vector<Unit> make_units(const std::vector<DevGate> &G, bool relax) {
+    std::vector<Unit> out;
+    auto diag1 = [&](size_t i) {
+        return G[i].nq == 1 && G[i].op == OP_DIAG && (uint32_t(G[i].kinds) & 15u) != CK_ZERO &&
+               (uint32_t(G[i].kinds >> 12) & 15u) != CK_ZERO;
+    };
+    auto u1_on = [&](size_t i, uint32_t b) {
+        return diag1(i) && G[i].b0 == b && (uint32_t(G[i].kinds) & 15u) == CK_ONE;
+    };
+    auto cx_on = [&](size_t i, uint32_t a, uint32_t b) {
+        return G[i].nq == 2 && G[i].op == OP_CX && G[i].b0 == a && G[i].b1 == b;
+    };
+    for (size_t i = 0; i < G.size();) {
+        Unit u{i, 1, false, gate_bits(G[i])};
+        if (relax) {
+            if (i + 5 <= G.size() && u1_on(i, G[i].b0) && G[i + 1].nq == 2 &&
+                cx_on(i + 1, G[i].b0, G[i + 1].b1) && u1_on(i + 2, G[i + 1].b1) &&
+                cx_on(i + 3, G[i].b0, G[i + 1].b1) && u1_on(i + 4, G[i + 1].b1)) {
+                u = Unit{i, 5, true, gate_bits(G[i + 1])};
+            } else if (i + 3 <= G.size() && G[i].nq == 2 && G[i].op == OP_CX && diag1(i + 1) &&
+                       G[i + 1].b0 == G[i].b1 && cx_on(i + 2, G[i].b0, G[i].b1)) {
+                u = Unit{i, 3, true, gate_bits(G[i])};
+            } else if (diag1(i) || (G[i].nq == 2 && G[i].op == OP_CZ)) {
+                u.diag = true;
+            }
+        }
+        out.push_back(u);
+        i += u.count;
+    }
+    return out;
+}
+
+// +0-safe single step (see safe_rows): a structural coefficient of kind
+// ONE / REAL / CPLX with a real part of sign 0, no part below 2^-100.
+static bool safe_coef(uint32_t kind, double2 m) {
+    const double re = std::fabs(m.x), im = std::fabs(m.y);
+    if ((re != 0.0 && re < 0x1p-100) || (im != 0.0 && im < 0x1p-100)) return false;
+    return (kind == CK_ONE || kind == CK_REAL || kind == CK_CPLX) && !std::signbit(m.x);
+}
+
+// Per-basis-state step chain of a diagonal unit: follow the basis state
+// through the unit's gates (CX moves it, diagonal entries multiply it).
+struct Step {
+    uint32_t kind;
+    double2 m;
+};
+static std::vector<Step> unit_chain(const std::vector<DevGate> &G, const Unit &u, uint64_t state) {
+    std::vector<Step> ch;
+    const uint64_t start = state;
+    for (size_t i = u.first; i < u.first + u.count; ++i) {
+        const DevGate &g = G[i];
+        const uint32_t s0 = uint32_t(state >> g.b0) & 1;
+        if (g.nq == 1) {
+            const uint32_t e = s0 * 3;
+            const uint32_t kd = uint32_t(g.kinds >> (4 * e)) & 15u;
+            if (kd != CK_ONE) ch.push_back(Step{kd, g.m[e]});
+        } else if (g.op == OP_CX) {
+            if (s0) state ^= uint64_t(1) << g.b1;
+        } else {   // CZ
+            const uint32_t st = (s0 << 1) | (uint32_t(state >> g.b1) & 1);
+            const uint32_t e = st * 5;
+            const uint32_t kd = uint32_t(g.kinds >> (4 * e)) & 15u;
+            if (kd != CK_ONE) ch.push_back(Step{kd, g.m[e]});
+        }
+    }
+    if (state != start || ch.size() > 2) throw Failure(QZC_EDEVICE, "diagonal unit: bad chain");
+    return ch;
+}
+
+// A unit may be relaxed only if every step of every basis state's chain is
+// +0-safe: then a relaxed group needs no zero checks at all, and the only
+// way it can fail is a block with a -0 / tiny component at group entry.
+static bool unit_safe(const std::vector<DevGate> &G, const Unit &u) {
+    uint32_t q[2], nq = 0;
+    for (uint64_t r = u.bits; r; r &= r - 1) q[nq++] = (uint32_t)__builtin_ctzll(r);
+    for (uint32_t st = 0; st < (1u << nq); ++st) {
+        uint64_t state = 0;
+        for (uint32_t i = 0; i < nq; ++i)
+            if ((st >> i) & 1) state |= uint64_t(1) << q[i];
+        for (const Step &s : unit_chain(G, u, state))
+            if (!safe_coef(s.kind, s.m)) return false;
+    }
+    return true;
+}
+
+GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_t kmax, bool fuse,
+                      bool relax) {
     GatePlan plan;
     const uint32_t k = std::min(kmax, nbits);
     const uint32_t low = std::min<uint32_t>(3, k);
     const uint64_t low_mask = (uint64_t(1) << low) - 1;
-    auto bits_of = [](const DevGate &g) {
-        uint64_t m = uint64_t(1) << g.b0;
-        if (g.nq == 2) m |= uint64_t(1) << g.b1;
-        return m;
-    };
-    std::vector<size_t> members;
+    relax = relax && fuse && nbits > k;
+    std::vector<Unit> units = make_units(gates, relax);
+    for (Unit &u : units)
+        if (u.diag && !unit_safe(gates, u)) u.diag = false;
+    std::vector<size_t> members;   // unit indices of the open pass
     uint64_t tmask = low_mask;
     auto close = [&]() {
         if (members.empty()) return;
@@ -256,15 +356,41 @@ GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_
         auto local = [&](uint32_t b) {
             return (uint32_t)__builtin_popcountll(tmask & ((uint64_t(1) << b) - 1));
         };
-        // register groups: consecutive gates whose tile bits fit 4 bits
+        // register groups: consecutive gates whose tile bits fit kRegBits bits
         uint32_t gmask = 0;
-        std::vector<size_t> gmembers;
+        std::vector<int64_t> gentries;   // gate index, or -(unit + 1) for a relaxed unit
+        std::vector<size_t> gmembers;    // the group's plain gates (exact list)
         auto close_group = [&]() {
-            if (gmembers.empty()) return;
+            if (gentries.empty()) return;
             for (uint32_t b = 0; b < k && __builtin_popcount(gmask) < kRegBits; ++b) gmask |= 1u << b;
+            auto is_reg = [&](uint32_t b) {   // buffer bit b is one of the group's register bits
+                return ((tmask >> b) & 1) && ((gmask >> local(b)) & 1);
+            };
+            {
+                // diagonal units entirely on register bits stay plain gates
+                std::vector<int64_t> ents;
+                for (int64_t e : gentries) {
+                    if (e < 0) {
+                        const Unit &u = units[size_t(-(e + 1))];
+                        bool all_reg = true;
+                        for (uint64_t r = u.bits; r; r &= r - 1) all_reg &= is_reg((uint32_t)__builtin_ctzll(r));
+                        if (all_reg) {
+                            for (size_t i = u.first; i < u.first + u.count; ++i) ents.push_back(int64_t(i));
+                            continue;
+                        }
+                    }
+                    ents.push_back(e);
+                }
+                gentries.swap(ents);
+                gmembers.clear();
+                for (int64_t e : gentries)
+                    if (e >= 0) gmembers.push_back(size_t(e));
+            }
             GroupDesc gd;
+            std::memset(&gd, 0, sizeof gd);
             gd.generic = 0;
             gd.pz_stable = 1;
+            gd.relaxed = 0;
             for (size_t gi : gmembers) gd.pz_stable &= maps_pos_zero(gates[gi]) ? 1u : 0u;
             int i = 0;
             for (uint32_t b = 0; b < k; ++b)
@@ -339,10 +465,61 @@ GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_
                 std::memcpy(t.m, g.m, sizeof t.m);
                 plan.gates.push_back(t);
             }
-            // fast list: the same gates with macro-able runs folded
+            // fast list: the same gates with macro-able runs folded, relaxed
+            // units in their place in the order
             gd.first_fast = (uint32_t)plan.gates.size();
-            {
-                const uint32_t e0 = gd.first_gate, e1 = gd.first_gate + gd.ngates;
+            uint32_t exact_pos = gd.first_gate;
+            for (size_t ei = 0; ei < gentries.size();) {
+                if (gentries[ei] < 0) {
+                    const Unit &u = units[size_t(-(gentries[ei] + 1))];
+                    TileGate t;
+                    std::memset(&t, 0, sizeof t);
+                    t.op = OP_PDIAG;
+                    uint64_t in = 0;
+                    for (uint64_t r = u.bits; r; r &= r - 1)
+                        if (is_reg((uint32_t)__builtin_ctzll(r))) in |= r & (0 - r);
+                    const uint64_t outb = u.bits & ~in;
+                    t.nq = __builtin_popcountll(in);   // 0 or 1 register bits
+                    if (t.nq) {
+                        const uint32_t b = (uint32_t)__builtin_ctzll(in);
+                        t.r0 = reg(local(b));
+                        t.t0 = b;
+                    }
+                    t.ob0 = (uint32_t)__builtin_ctzll(outb);
+                    const uint64_t rest = outb & (outb - 1);
+                    t.ob1 = rest ? (uint32_t)__builtin_ctzll(rest) : 63u;
+                    bool spec = true, pz = true;
+                    for (uint32_t var = 0; var < 4; ++var) {
+                        if (!rest && var >= 2) break;
+                        for (uint32_t st = 0; st < (t.nq ? 2u : 1u); ++st) {
+                            uint64_t state = 0;
+                            if (var & 1) state |= uint64_t(1) << t.ob0;
+                            if (var & 2) state |= uint64_t(1) << t.ob1;
+                            if (t.nq && st) state |= in;
+                            const std::vector<Step> ch = unit_chain(gates, u, state);
+                            for (size_t j = 0; j < ch.size(); ++j) {
+                                const uint32_t e = 4 * var + 2 * st + (uint32_t)j;
+                                t.kinds |= uint64_t(ch[j].kind) << (4 * e);
+                                t.m[e] = ch[j].m;
+                                const bool sf = safe_coef(ch[j].kind, ch[j].m);
+                                t.srow |= uint32_t(sf) << e;
+                                spec &= sf && ch[j].kind == CK_CPLX;
+                                pz &= sf;
+                            }
+                        }
+                    }
+                    t.pad2 = spec ? 8u : 0u;
+                    gd.pz_stable &= pz ? 1u : 0u;
+                    gd.relaxed = 1;
+                    plan.gates.push_back(t);
+                    ++ei;
+                    continue;
+                }
+                size_t ej = ei;
+                while (ej < gentries.size() && gentries[ej] >= 0) ++ej;
+                const uint32_t e0 = exact_pos, e1 = exact_pos + uint32_t(ej - ei);
+                exact_pos = e1;
+                ei = ej;
                 for (uint32_t i = e0; i < e1;) {
                     const TileGate *G = &plan.gates[0];
                     auto u1_on = [&](uint32_t k, uint32_t r) {
@@ -387,6 +564,7 @@ GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_
             }
             for (size_t k = gd.first_fast; k < plan.gates.size(); ++k) {
                 TileGate &t = plan.gates[k];
+                if (t.op == OP_PDIAG) continue;
                 const uint32_t kd = uint32_t(t.kinds);
                 auto K = [&](int e) { return (kd >> (4 * e)) & 15u; };
                 t.pad2 = 0;
@@ -407,20 +585,32 @@ GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_
             plan.groups.push_back(gd);
             plan.groups.back().nfast = (uint32_t)plan.gates.size() - gd.first_fast;
             gmembers.clear();
+            gentries.clear();
             gmask = 0;
         };
-        for (size_t i : members) {
-            const DevGate &g = gates[i];
-            uint32_t need = 1u << local(g.b0);
-            if (g.nq == 2) need |= 1u << local(g.b1);
-            const bool generic = g.nq == 2 && !is_signed_perm(g);
-            if (generic || __builtin_popcount(gmask | need) > kRegBits || k <= (uint32_t)kRegBits)
-                close_group();
-            gmask |= need;
-            gmembers.push_back(i);
-            if (generic) {
-                close_group();
-                plan.groups.back().generic = 1;
+        for (size_t ui : members) {
+            const Unit &u = units[ui];
+            if (relax && u.diag) {
+                // diagonal unit: needs no register bit; at close_group its
+                // qubits outside the group's register bits become per-thread
+                // constants (OP_PDIAG), unless all of them are register bits
+                gentries.push_back(-int64_t(ui) - 1);
+                continue;
+            }
+            for (size_t i = u.first; i < u.first + u.count; ++i) {
+                const DevGate &g = gates[i];
+                uint32_t need = 1u << local(g.b0);
+                if (g.nq == 2) need |= 1u << local(g.b1);
+                const bool generic = g.nq == 2 && !is_signed_perm(g);
+                if (generic || __builtin_popcount(gmask | need) > kRegBits || k <= (uint32_t)kRegBits)
+                    close_group();
+                gmask |= need;
+                gmembers.push_back(i);
+                gentries.push_back(int64_t(i));
+                if (generic) {
+                    close_group();
+                    plan.groups.back().generic = 1;
+                }
             }
         }
         close_group();
@@ -432,33 +622,42 @@ GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_
         members.clear();
         tmask = low_mask;
     };
-    for (size_t i = 0; i < gates.size(); ++i) {
-        const uint64_t need = bits_of(gates[i]);
-        if (need >> nbits) throw Failure(QZC_EDEVICE, "gate bit outside buffer");
+    for (size_t ui = 0; ui < units.size(); ++ui) {
+        const Unit &u = units[ui];
+        if (u.bits >> nbits) throw Failure(QZC_EDEVICE, "gate bit outside buffer");
+        const uint64_t need = u.diag ? 0 : u.bits;
         const uint64_t merged = tmask | need;
         if (!fuse || (uint32_t)__builtin_popcountll(merged) > k) close();
         tmask |= need;
-        members.push_back(i);
+        members.push_back(ui);
     }
     close();
     return plan;
 }
 
 void upload_plan(const GatePlan &plan, DevPlan &out, cudaStream_t s) {
-    free_plan(out);
     out.ngates = plan.gates.size();
     out.ngroups = plan.groups.size();
     out.host_passes = plan.passes;
-    if (out.ngates) {
-        QZ_CUDA(cudaMalloc(&out.gates, sizeof(TileGate) * out.ngates));
+    out.relaxed = false;
+    for (const GroupDesc &g : plan.groups) out.relaxed |= g.relaxed != 0;
+    if (out.ngates > out.cap_gates) {
+        if (out.gates) QZ_CUDA(cudaFree(out.gates));
+        out.cap_gates = std::max<size_t>(out.ngates * 2, 256);
+        QZ_CUDA(cudaMalloc(&out.gates, sizeof(TileGate) * out.cap_gates));
+    }
+    if (out.ngroups > out.cap_groups) {
+        if (out.groups) QZ_CUDA(cudaFree(out.groups));
+        out.cap_groups = std::max<size_t>(out.ngroups * 2, 64);
+        QZ_CUDA(cudaMalloc(&out.groups, sizeof(GroupDesc) * out.cap_groups));
+    }
+    if (out.ngates)
         QZ_CUDA(cudaMemcpyAsync(out.gates, plan.gates.data(), sizeof(TileGate) * out.ngates,
                                 cudaMemcpyHostToDevice, s));
-    }
-    if (out.ngroups) {
-        QZ_CUDA(cudaMalloc(&out.groups, sizeof(GroupDesc) * out.ngroups));
+    if (out.ngroups)
         QZ_CUDA(cudaMemcpyAsync(out.groups, plan.groups.data(), sizeof(GroupDesc) * out.ngroups,
                                 cudaMemcpyHostToDevice, s));
-    }
+    // (pageable source: staged by the driver before the call returns)
 }
 
 void free_plan(DevPlan &p) {
@@ -467,7 +666,9 @@ void free_plan(DevPlan &p) {
     p.gates = nullptr;
     p.groups = nullptr;
     p.ngates = p.ngroups = 0;
+    p.cap_gates = p.cap_groups = 0;
     p.host_passes.clear();
+    p.relaxed = false;
 }
 
 // ============================================================ device math ==
@@ -817,6 +1018,34 @@ __device__ __forceinline__ void fast_cxd(double2 (&v)[NB], const TileGate &g, bo
     }
 }
 
+// OP_PDIAG resolved for this tile's outside-bit values `var`: step chains on
+// register bit R (R == kRegBits: one chain for the whole block).
+// SPEC = 1: every step CPLX and +0-safe (no kind branches, no checks).
+template <int R, int SPEC = 0>
+__device__ __forceinline__ void fast_pdiag(double2 (&v)[NB], const TileGate &g, uint32_t var,
+                                           bool &bad) {
+    const uint32_t kd = uint32_t(g.kinds >> (16 * var));
+    const uint32_t sf = g.srow >> (4 * var);
+    constexpr int KC = SPEC ? int(CK_CPLX) : -1;
+#pragma unroll
+    for (int st = 0; st < (R < kRegBits ? 2 : 1); ++st) {
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const uint32_t e = 2 * st + j;
+            const uint32_t kind = (kd >> (4 * e)) & 15u;
+            if (kind == CK_ZERO) continue;
+            const double2 m = g.m[4 * var + e];
+            const bool chk = !SPEC && !((sf >> e) & 1);
+#pragma unroll
+            for (int i = 0; i < NB; ++i) {
+                if (R < kRegBits && ((i >> R) & 1) != st) continue;
+                v[i] = termk<KC>(kind, m, v[i]);
+                if (chk) bad |= zc(v[i]);
+            }
+        }
+    }
+}
+
 #if QZ_REG_BITS == 3
 #define QZ_PAIRS(X) X(0, 1) X(0, 2) X(1, 2)
 #else
@@ -824,8 +1053,24 @@ __device__ __forceinline__ void fast_cxd(double2 (&v)[NB], const TileGate &g, bo
 #endif
 
 // Returns false if the gate could not be taken on the fast path at all.
-__device__ __forceinline__ void fast_apply(double2 (&v)[NB], const TileGate &g, bool &bad) {
+__device__ __forceinline__ void fast_apply(double2 (&v)[NB], const TileGate &g, uint64_t gidx,
+                                           bool &bad) {
     const uint32_t op = g.op;
+    if (op == OP_PDIAG) {
+        const uint32_t var = uint32_t((gidx >> g.ob0) & 1) | (uint32_t((gidx >> g.ob1) & 1) << 1);
+        switch (g.nq ? g.r0 : uint32_t(kRegBits)) {
+#define X(a)                                                                                 \
+    case a:                                                                                  \
+        if (g.pad2 == 8) fast_pdiag<a, 1>(v, g, var, bad);                                   \
+        else fast_pdiag<a>(v, g, var, bad);                                                  \
+        break;
+            QZ_R1_CASES(X)
+            X(kRegBits)
+#undef X
+        default: break;
+        }
+        return;
+    }
     if (op == OP_DIAG || op == OP_GEN1) {
         switch (g.r0) {
 #define X(a)                                                                                 \
@@ -1051,7 +1296,10 @@ __global__ void __launch_bounds__(1 << (kTileBits - kRegBits), (kTileBits >= 12 
                                                          const GroupDesc *__restrict__ groups,
                                                          const TileGate *__restrict__ gates,
                                                          uint64_t ntiles,
-                                                         unsigned long long *__restrict__ counters) {
+                                                         unsigned long long *__restrict__ counters,
+                                                         uint32_t *__restrict__ flag,
+                                                         const uint32_t *__restrict__ cond) {
+    if (cond && *cond == 0) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double2 *s = reinterpret_cast<double2 *>(smem_raw);
     const uint32_t k = pd.k, L = pd.lowbits;
@@ -1105,6 +1353,9 @@ __global__ void __launch_bounds__(1 << (kTileBits - kRegBits), (kTileBits >= 12 
                 gm |= bm[i];
             }
             const uint32_t mybase = deposit32(tid, (tile - 1) & ~gm);
+            // buffer index of the thread's register-0 amplitude: the values of
+            // every non-register bit (OP_PDIAG variants)
+            const uint64_t gidx = G.relaxed ? base + offhi[mybase >> L] + (mybase & lowmask) : 0;
             uint32_t addr[NB];
 #pragma unroll
             for (int r = 0; r < NB; ++r) {
@@ -1128,6 +1379,8 @@ __global__ void __launch_bounds__(1 << (kTileBits - kRegBits), (kTileBits >= 12 
             int path = 1;
             if (raw == 0 && G.pz_stable) {
                 // all-(+0) block, every gate keeps it all-(+0): nothing to do
+            } else if (G.relaxed && nz == 0) {
+                *flag = 1u;   // partner values outside the tile would be needed
             } else if (nz == 0) {
                 path = 2;
                 // all-zero block: stays zero, track the zero signs only
@@ -1155,9 +1408,11 @@ __global__ void __launch_bounds__(1 << (kTileBits - kRegBits), (kTileBits >= 12 
                 bool bad = !okblk;
                 path = okblk ? 3 : 4;
                 const TileGate *fp = gates + G.first_fast;
-                for (uint32_t q = 0; q < G.nfast && !bad; ++q) fast_apply(v, fp[q], bad);
+                for (uint32_t q = 0; q < G.nfast && !bad; ++q) fast_apply(v, fp[q], gidx, bad);
                 if (bad && okblk) path = 5;
-                if (bad) {
+                if (bad && G.relaxed) {
+                    *flag = 1u;   // the exact path needs partners outside the tile
+                } else if (bad) {
                     // a zero is (or became) present: redo the group exactly
 #pragma unroll
                     for (int r = 0; r < NB; ++r) v[r] = s[addr[r]];
@@ -1186,8 +1441,9 @@ __global__ void __launch_bounds__(1 << (kTileBits - kRegBits), (kTileBits >= 12 
 // Buffers below 16 amplitudes: one thread, dense formula.
 __global__ void tile_pass_tiny(double2 *buf, uint32_t nbits, PassDesc pd,
                                const GroupDesc *__restrict__ groups,
-                               const TileGate *__restrict__ gates) {
+                               const TileGate *__restrict__ gates, const uint32_t *cond) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (cond && *cond == 0) return;
     const uint32_t n = 1u << nbits;
     for (uint32_t gi = 0; gi < pd.ngroups; ++gi)
     for (uint32_t q = 0; q < groups[pd.first_group + gi].ngates; ++q) {
@@ -1242,7 +1498,9 @@ void dump_debug_counters() {
     QZ_CUDA(cudaMemset(p, 0, sizeof h));
 }
 
-uint64_t run_passes(const DevPlan &plan, double2 *buf, uint32_t nbits, cudaStream_t s) {
+uint64_t run_passes(const DevPlan &plan, double2 *buf, uint32_t nbits, cudaStream_t s,
+                    uint32_t *flag, const uint32_t *cond) {
+    if (plan.relaxed && !flag) throw Failure(QZC_EDEVICE, "relaxed plan without a replay flag");
     static bool attr_set = false;
     if (!attr_set) {
         QZ_CUDA(cudaFuncSetAttribute(tile_pass_reg, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1253,7 +1511,7 @@ uint64_t run_passes(const DevPlan &plan, double2 *buf, uint32_t nbits, cudaStrea
     for (const PassDesc &pd : plan.host_passes) {
         if (pd.k < (uint32_t)kRegBits + 1) {
             // tile == whole buffer (nbits < 4)
-            tile_pass_tiny<<<1, 32, 0, s>>>(buf, nbits, pd, plan.groups, plan.gates);
+            tile_pass_tiny<<<1, 32, 0, s>>>(buf, nbits, pd, plan.groups, plan.gates, cond);
         } else {
             const uint32_t tile = 1u << pd.k;
             const uint64_t ntiles = uint64_t(1) << (nbits - pd.k);
@@ -1261,7 +1519,8 @@ uint64_t run_passes(const DevPlan &plan, double2 *buf, uint32_t nbits, cudaStrea
             const size_t smem = sizeof(double2) * tile + sizeof(uint64_t) * (tile >> pd.lowbits);
             const uint64_t grid = std::min<uint64_t>(ntiles, uint64_t(kNumSMs) * 2 * 8);
             tile_pass_reg<<<(unsigned)grid, threads, smem, s>>>(buf, nbits, pd, plan.groups,
-                                                               plan.gates, ntiles, debug_counters());
+                                                               plan.gates, ntiles, debug_counters(),
+                                                               flag, cond);
         }
         QZ_CHECK_LAUNCH();
         ++launches;

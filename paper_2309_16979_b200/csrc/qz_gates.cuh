@@ -30,6 +30,15 @@ enum GateOp : uint32_t {
     // fast-path macros (a run of gates on one qubit pair, same operations)
     OP_CP5 = 6,  // U1(a) CX(a,b) U1(b) CX(a,b) U1(b): m[0..2] = the U1s' phase entries
     OP_CXD = 7,  // CX(a,b) D(b) CX(a,b), D diagonal: m[0], m[1] = D's entries
+    // diagonal unit (1q diagonal, CZ, CP5 or CXD run) with qubits that are not
+    // register bits of its group (outside the pass's tile set, or tile bits
+    // held constant across a thread's registers): per thread the unit reduces
+    // to a diagonal chain on <= 1 register bit.  Variant v = values of those
+    // bits in the thread's amplitude index (ob0 -> bit 0, ob1 -> bit 1); state s of the
+    // register bit (s = 0 only when nq == 0: uniform over the block); step
+    // j < 2: kinds nibble 4v+2s+j (CK_ZERO = no step), coefficient m[4v+2s+j],
+    // srow bit 4v+2s+j = step is +0-safe.
+    OP_PDIAG = 8,
 };
 
 // A gate inside a register group: r0/r1 are the gate's qubits as bit
@@ -45,7 +54,9 @@ struct TileGate {
     uint32_t op;                  // GateOp
     uint32_t pad;                 // bit r: row r maps all-(+0) inputs to (+0,+0)
     uint32_t srow;                // bit r: row r is "+0-safe" (see qz_gates.cu)
-    uint32_t pad2;
+    uint32_t pad2;                // compile-time specialisation code of the fast path
+    uint32_t ob0, ob1;            // OP_PDIAG: outside buffer bits (ob1 = 63 if unused)
+    uint32_t pad3[2];
     double2 m[16];
 };
 
@@ -75,6 +86,9 @@ struct GroupDesc {
     uint32_t first_fast, nfast;    // fast-path list (macros folded in)
     uint32_t generic;      // 1: apply on the smem tile with the full formula
     uint32_t pz_stable;    // every gate maps an all-(+0) block to all-(+0)
+    uint32_t relaxed;      // holds OP_PDIAG units: no exact path; a block that
+                           // cannot take the fast path raises the replay flag
+    uint32_t pad;
 };
 
 // A fused pass: gates whose buffer bits all lie in the tile bit set T.
@@ -103,8 +117,11 @@ uint32_t gate_nparams(uint32_t kind);
 
 // Host: greedy in-order fusion of gates (already on buffer bits) into passes
 // over a buffer of 2^nbits amplitudes with tiles of at most 2^kmax.
+// relax: diagonal units do not need their qubits in the tile set (OP_PDIAG);
+// such a plan can raise the replay flag and must then be replayed strictly
+// from the same input (see run_passes).
 GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_t kmax,
-                      bool fuse);
+                      bool fuse, bool relax = false);
 
 DevGate make_dev_gate(const qzc_gate &g);
 DevGate make_dev_gate_matrix(const double2 *m, uint32_t dim, uint32_t b0, uint32_t b1);
@@ -115,13 +132,21 @@ struct DevPlan {
     GroupDesc *groups = nullptr;
     size_t ngates = 0, ngroups = 0;
     std::vector<PassDesc> host_passes;
+    bool relaxed = false;   // some group is relaxed: may raise the replay flag
+    size_t cap_gates = 0, cap_groups = 0;   // device capacity (grow-only reuse)
 };
+// Stream-ordered upload into `out`, reusing its device buffers when they are
+// large enough (no allocator calls on the steady-state stage loop).
 void upload_plan(const GatePlan &plan, DevPlan &out, cudaStream_t s);
-void free_plan(DevPlan &p);
+void free_plan(DevPlan &p);   // releases the device buffers
 
 // Launch every pass of `plan` over buf (2^nbits amplitudes).  Returns the
-// number of kernel launches.
-uint64_t run_passes(const DevPlan &plan, double2 *buf, uint32_t nbits, cudaStream_t s);
+// number of kernel launches.  flag: set to 1 by a relaxed group that could
+// not take the fast path (the buffer is then garbage and must be rebuilt
+// from the input and replayed with a strict plan).  cond != nullptr: every
+// launch returns immediately unless *cond != 0 (device-side conditional).
+uint64_t run_passes(const DevPlan &plan, double2 *buf, uint32_t nbits, cudaStream_t s,
+                    uint32_t *flag = nullptr, const uint32_t *cond = nullptr);
 void dump_debug_counters();
 
 } // namespace qz

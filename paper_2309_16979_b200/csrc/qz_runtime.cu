@@ -71,6 +71,7 @@ const char *status_text(int code) {
 // Scratch set for one window of codec work.
 struct Window {
     DevBuf amps, scratch, meta, idx, slot_chunk, sizes, reloff, base, cub, delta, maxd;
+    DevBuf replay;   // uint32 flag raised by a relaxed gate pass
     // host-staged residency: HBM staging of the window's payloads
     DevBuf stage_in, stage_out, lt_off, lt_len, lt_crc, padded, soff, lused, hbase;
     uint64_t slots = 0, stage_in_cap = 0, stage_out_cap = 0;
@@ -102,6 +103,10 @@ struct Window {
         delta.ensure(sizeof(int64_t) * nslots);
         base.ensure(sizeof(uint64_t) * 2);
         maxd.ensure(sizeof(int64_t) * 2);
+        if (!replay.p) {
+            replay.ensure(16);
+            QZ_CUDA(cudaMemset(replay.p, 0, 16));
+        }
         size_t t1 = 0, t2 = 0;
         cub::DeviceScan::ExclusiveSum(nullptr, t1, (uint64_t *)nullptr, (uint64_t *)nullptr,
                                       (int)std::min<uint64_t>(nslots, INT32_MAX));
@@ -140,6 +145,12 @@ __global__ void k_account(int64_t *acct, const int64_t *prefix, const int64_t *m
 __global__ void k_io_count(const uint64_t *soff, const uint64_t *padded, uint64_t nslots,
                            uint64_t *io) {
     atomicAdd((unsigned long long *)&io[0], (unsigned long long)(soff[nslots - 1] + padded[nslots - 1]));
+}
+// Relaxed-plan replay bookkeeping: count the windows that were replayed and
+// clear the flag for the next window on this stream.
+__global__ void k_replay_done(uint32_t *flag, uint64_t *count) {
+    *count += *flag;
+    *flag = 0;
 }
 __global__ void k_io_count_out(const uint64_t *used_local, uint64_t *io) {
     atomicAdd((unsigned long long *)&io[1], (unsigned long long)((*used_local + 15) / 16 * 16));
@@ -251,6 +262,8 @@ struct qzc_sim {
     uint8_t *harena[2] = {nullptr, nullptr};      // host view
     uint8_t *harena_dev[2] = {nullptr, nullptr};  // device view of the same bytes
     DevBuf io_bytes;  // uint64[2]: host->HBM and HBM->host payload bytes
+    DevBuf replays;   // uint64: windows replayed with the strict plan
+    DevPlan plans[2]; // stage plans (relaxed / strict), device buffers reused
     DevBuf used;   // uint64[2] bump pointers
     DevBuf acct;   // int64[2] current / peak
     uint64_t arena_cap = 0;
@@ -259,6 +272,8 @@ struct qzc_sim {
     Window win;              // window set 0 (also used by the host entry points)
     Window win2;             // window set 1: second stream of the stage pipeline
     bool two_windows = false;
+    bool relax = true;          // fuse_gates == 1: relaxed passes + strict replay
+    bool force_replay = false;  // debug_flags bit 0
     cudaStream_t streams[2] = {nullptr, nullptr};
     cudaEvent_t acct_ev[2] = {nullptr, nullptr};
     qzc_sim_stats stats{};
@@ -824,9 +839,12 @@ int qzc_sim_create(qzc_context *ctx, const qzc_sim_config *cfg, qzc_sim **out) {
     if (!(cfg->error_bound >= 0.0) || !std::isfinite(cfg->error_bound))
         throw Failure(QZC_EINVAL, "error bound must be finite and non-negative");
     if (cfg->residency > 1) throw Failure(QZC_EINVAL, "residency must be 0 (HBM) or 1 (host-staged)");
+    if (cfg->fuse_gates > 2) throw Failure(QZC_EINVAL, "fuse_gates must be 0, 1 or 2");
     auto *sim = new qzc_sim;
     sim->ctx = ctx;
     sim->cfg = *cfg;
+    sim->relax = cfg->fuse_gates == 1;
+    sim->force_replay = (cfg->debug_flags & 1u) != 0;
     sim->n = n;
     sim->c = c;
     sim->m = cfg->batch_qubits;
@@ -854,6 +872,8 @@ void qzc_sim_destroy(qzc_sim *sim) {
     sim->used.release();
     sim->acct.release();
     sim->io_bytes.release();
+    sim->replays.release();
+    for (DevPlan &p : sim->plans) free_plan(p);
     for (int i = 0; i < 2; ++i)
         if (sim->harena[i]) cudaFreeHost(sim->harena[i]);
     sim->win.release();
@@ -936,6 +956,8 @@ int qzc_sim_init_basis(qzc_sim *sim) {
     sim->initialized = true;
     sim->stats = qzc_sim_stats{};
     if (sim->host_res) QZ_CUDA(cudaMemset(sim->io_bytes.p, 0, 16));
+    sim->replays.ensure(8);
+    QZ_CUDA(cudaMemset(sim->replays.p, 0, 8));
     QZ_API_END
 }
 
@@ -973,6 +995,7 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
     const uint64_t chunk_bits_mask = (uint64_t(1) << (n - c)) - 1;
     const uint64_t launches0 = ctx->launches;
     const double t0 = now_s();
+    static const bool trace = getenv("QZ_TRACE") && *getenv("QZ_TRACE") == '1';
     // 4 events per window, recycled per stage
     auto ev = [&](size_t i) {
         while (sim->events.size() <= i) {
@@ -1005,9 +1028,13 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
             }
             dg.push_back(make_dev_gate(g));
         }
-        GatePlan gp = build_passes(dg, wbits, kTileBits, sim->cfg.fuse_gates != 0);
-        DevPlan dp;
+        // relaxed plan (diagonal units need no tile bits) + the strict plan
+        // it is replayed with, device-side, when a window raises the flag
+        const double tp0 = now_s();
+        GatePlan gp = build_passes(dg, wbits, kTileBits, sim->cfg.fuse_gates != 0, sim->relax);
+        DevPlan &dp = sim->plans[0], &dstrict = sim->plans[1];
         upload_plan(gp, dp, s);
+        if (dp.relaxed) upload_plan(build_passes(dg, wbits, kTileBits, true, false), dstrict, s);
         const int a = sim->cur, b = 1 - sim->cur;
         QZ_CUDA(cudaMemsetAsync(sim->used_ptr(b), 0, 8, s));
         // the stage's plan upload and arena reset happen on the context
@@ -1016,6 +1043,7 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
         cudaEvent_t ready = ev(4 * nwin);
         QZ_CUDA(cudaEventRecord(ready, s));
         const uint64_t nslots = bpw << hs;
+        const double tp1 = now_s();
         for (uint64_t w = 0; w < nwin; ++w) {
             const int ws = sim->two_windows ? int(w & 1) : 0;
             Window &W = ws ? sim->win2 : sim->win;
@@ -1044,7 +1072,25 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
                               sim->arena_ptr(a), sim->table(a), ctx->launches, S);
             }
             QZ_CUDA(cudaEventRecord(ev(4 * w + 1), S));
-            ctx->launches += 1 + run_passes(dp, W.amps.as<double2>(), wbits, S);
+            if (dp.relaxed) {
+                uint32_t *flag = W.replay.as<uint32_t>();
+                if (sim->force_replay) QZ_CUDA(cudaMemsetAsync(flag, 1, 1, S));
+                ctx->launches += run_passes(dp, W.amps.as<double2>(), wbits, S, flag);
+                // replay (no-ops unless *flag): decode again from the still
+                // intact input payloads, then the strict plan
+                if (sim->host_res)
+                    launch_decode(W.stage_in.as<uint8_t>(), W.idx.as<DecIdx>(), nullptr, nslots,
+                                  sim->geom, W.amps.as<double2>(), ctx->status, S, flag);
+                else
+                    launch_decode(sim->arena_ptr(a), W.idx.as<DecIdx>(), W.slot_chunk.as<uint64_t>(),
+                                  nslots, sim->geom, W.amps.as<double2>(), ctx->status, S, flag);
+                ctx->launches += 1 + run_passes(dstrict, W.amps.as<double2>(), wbits, S, nullptr, flag);
+                k_replay_done<<<1, 1, 0, S>>>(flag, sim->replays.as<uint64_t>());
+                QZ_CHECK_LAUNCH();
+                ctx->launches += 2;
+            } else {
+                ctx->launches += 1 + run_passes(dp, W.amps.as<double2>(), wbits, S);
+            }
             QZ_CUDA(cudaEventRecord(ev(4 * w + 2), S));
             if (sim->host_res) {
                 QZ_CUDA(cudaMemsetAsync(W.lused.p, 0, 8, S));
@@ -1069,11 +1115,14 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
             }
             QZ_CUDA(cudaEventRecord(ev(4 * w + 3), S));
         }
+        const double tp2 = now_s();
         for (int i = 0; i < 2; ++i) QZ_CUDA(cudaStreamSynchronize(sim->streams[i]));
+        if (trace)
+            fprintf(stderr, "qz trace: stage %zu plan %.2f ms launch %.2f ms sync %.2f ms (%zu passes)\n", si,
+                    1e3 * (tp1 - tp0), 1e3 * (tp2 - tp1), 1e3 * (now_s() - tp2), gp.passes.size());
         try {
             ctx->check_status();
         } catch (const Failure &f) {
-            free_plan(dp);
             throw Failure(f.code, "stage " + std::to_string(si) + ": " + f.what());
         }
         for (uint64_t w = 0; w < nwin; ++w) {
@@ -1083,7 +1132,6 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
             sim->stats.gate_seconds += ms[1] * 1e-3;
             sim->stats.encode_seconds += ms[2] * 1e-3;
         }
-        free_plan(dp);
         sim->cur = b;
         sim->stats.stages += 1;
         sim->stats.batches += nbatches;
@@ -1113,6 +1161,8 @@ int qzc_sim_stats_get(const qzc_sim *sim, qzc_sim_stats *out) {
         out->d2h_bytes += io[1];
     }
     out->dense_bytes = (uint64_t(1) << sim->n) * 16;
+    out->replays = 0;
+    if (sim->replays.p) QZ_CUDA(cudaMemcpy(&out->replays, sim->replays.p, 8, cudaMemcpyDeviceToHost));
     QZ_API_END
 }
 

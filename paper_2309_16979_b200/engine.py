@@ -286,13 +286,18 @@ class Simulator:
     """Compressed-chunk state vector in HBM (qzc_sim) — qzsim::run's hot path."""
 
     def __init__(self, eng: Engine, n: int, c: int, m: int, eb: float, window_amps: int = 0,
-                 fuse: bool = True, init: bool = True, residency: str = "hbm"):
+                 fuse=True, init: bool = True, residency: str = "hbm",
+                 force_replay: bool = False):
+        """fuse: True = fused passes with relaxed diagonal units (default),
+        "strict" = fused passes with every gate qubit in the tile, False = one
+        pass per gate.  force_replay: always take the strict replay (test)."""
         self.eng, self.lib = eng, eng.lib
         self.n, self.c, self.m, self.eb = n, c, m, eb
         cfg = SimConfig(num_qubits=n, chunk_qubits=c, batch_qubits=m, error_bound=eb,
                         window_amps=window_amps, residency={"hbm": 0, "host": 1}[residency],
                         renormalize=0,
-                        fuse_gates=1 if fuse else 0)
+                        fuse_gates=2 if fuse == "strict" else (1 if fuse else 0),
+                        debug_flags=1 if force_replay else 0)
         h = C.c_void_p()
         _check(self.lib.qzc_sim_create(eng.h, C.byref(cfg), C.byref(h)))
         self.h = h

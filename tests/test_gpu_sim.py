@@ -183,3 +183,54 @@ def test_sharded_ranks_same_digest(engine, oracle, golden, key, g):
     run.init_basis()
     run.run(gl)
     assert f"{run.digest():016x}" == rec["digest"]
+
+
+def _relax_cases():
+    from paper_2309_16979_b200 import circuits as CI
+    from tests_util import diagonal_heavy_circuit
+    return [
+        ("qft16", 16, 8, 16, 1e-5, lambda: CI.qft(16)),
+        ("qft18_m14", 18, 8, 14, 1e-5, lambda: CI.qft(18)),
+        ("qaoa16", 16, 8, 16, 1e-5, lambda: CI.qaoa(16)),
+        ("supremacy16", 16, 8, 16, 1e-6, lambda: CI.supremacy(16, depth=8)),
+        ("ghz16_phases", 16, 8, 16, 0.0,
+         lambda: to_array([(g[0], g[1], g[2]) for g in
+                           [("h", (0,), ())] + [("cx", (0, k), ()) for k in range(1, 16)]
+                           + [("z", (15,), ()), ("s", (14,), ()), ("cz", (3, 12), ()),
+                              ("u1", (13,), (0.3,)), ("h", (15,), ()), ("cz", (15, 2), ())]])),
+        ("diag_heavy_a", 16, 8, 16, 0.0, lambda: to_array(diagonal_heavy_circuit(16, 300, 5))),
+        ("diag_heavy_b", 16, 6, 14, 1e-6, lambda: to_array(diagonal_heavy_circuit(16, 400, 9))),
+    ]
+
+
+@pytest.mark.parametrize("case", range(7))
+def test_relaxed_passes_match_strict_and_reference(engine, oracle, case):
+    """Diagonal units with qubits outside the pass's tile set (relaxed plan),
+    the strict plan, and a forced device-side replay all give the reference's
+    bytes (oracle digest)."""
+    name, n, c, m, eb, make = _relax_cases()[case]
+    g = make()
+    ref = oracle.run(n, g, c, m, eb)["digest"]
+    out = {}
+    for mode, kw in (("relaxed", {}), ("strict", {"fuse": "strict"}),
+                     ("replay", {"force_replay": True})):
+        sim = run_sim(engine, n, c, m, eb, g, **kw)
+        out[mode] = (sim.digest(), sim.stats())
+        sim.close()
+    for mode, (d, _) in out.items():
+        assert d == ref, (name, mode)
+    rel, strict, rep = out["relaxed"][1], out["strict"][1], out["replay"][1]
+    assert rel["gate_passes"] <= strict["gate_passes"], name
+    assert strict["replays"] == 0
+    if rel["gate_passes"] < strict["gate_passes"]:
+        assert rep["replays"] >= 1, name
+
+
+def test_relaxed_qft_needs_no_replay(engine):
+    from paper_2309_16979_b200 import circuits as CI
+    sim = run_sim(engine, 20, 10, 20, 1e-5, CI.qft(20))
+    st = sim.stats()
+    assert st["replays"] == 0
+    strict = run_sim(engine, 20, 10, 20, 1e-5, CI.qft(20), fuse="strict")
+    assert strict.digest() == sim.digest()
+    assert st["gate_passes"] * 3 < strict.stats()["gate_passes"]
