@@ -170,6 +170,14 @@ int qzc_event_done(qzc_context *ctx, void *event);
  * first_gate[s] + stage_ngates[s]); its padded high set is
  * high[64*s .. 64*s + nhigh[s]).  Returns the stage count in *nstages; at
  * most `cap` stages are written. */
+/* Fused-pass plan summary for gates already on buffer bits of a 2^nbits
+ * window (host only, no GPU): out[0] passes, [1] register groups,
+ * [2] relaxed groups, [3] gates, [4] fast-path ops (macros folded),
+ * [5] OP_PDIAG ops.  fuse_mode as qzc_sim_config.fuse_gates.
+ * (Engine-internal scheduling; no reference counterpart.) */
+int qzc_pass_plan_stats(const qzc_gate *gates, uint64_t ngates, uint32_t nbits,
+                        uint32_t fuse_mode, uint64_t *out);
+
 int qzc_plan_export(uint32_t num_qubits, uint32_t chunk_qubits, uint32_t batch_qubits,
                     const qzc_gate *gates, uint64_t ngates, uint64_t *nstages,
                     uint64_t *first_gate, uint64_t *stage_ngates, uint32_t *nhigh,

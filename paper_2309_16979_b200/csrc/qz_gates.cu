@@ -232,6 +232,7 @@ struct Unit {
     uint32_t count;
     bool diag;
     uint64_t bits;   // buffer bits of all its gates
+    bool swaps = false;   // a run of >= 2 pairwise disjoint SWAPs (PASS_SWAPS)
 };
 
 static uint64_t gate_bits(const DevGate &g) {
@@ -254,6 +255,21 @@ static std::vector<Unit> make_units(const std::vector<DevGate> &G, bool relax) {
     };
     for (size_t i = 0; i < G.size();) {
         Unit u{i, 1, false, gate_bits(G[i])};
+        if (relax && G[i].nq == 2 && G[i].op == OP_SWAP) {
+            uint64_t used = 0;
+            size_t j = i;
+            while (j < G.size() && G[j].nq == 2 && G[j].op == OP_SWAP && !(gate_bits(G[j]) & used)) {
+                used |= gate_bits(G[j]);
+                ++j;
+            }
+            if (j - i >= 2) {
+                u = Unit{i, uint32_t(j - i), false, used};
+                u.swaps = true;
+                out.push_back(u);
+                i = j;
+                continue;
+            }
+        }
         if (relax) {
             if (i + 5 <= G.size() && u1_on(i, G[i].b0) && G[i + 1].nq == 2 &&
                 cx_on(i + 1, G[i].b0, G[i + 1].b1) && u1_on(i + 2, G[i + 1].b1) &&
@@ -509,6 +525,8 @@ GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_
                         }
                     }
                     t.pad2 = spec ? 8u : 0u;
+                    for (uint32_t e = 0; e < 16; ++e)
+                        if ((t.kinds >> (4 * e)) & 15u) t.steps |= 1u << e;
                     gd.pz_stable &= pz ? 1u : 0u;
                     gd.relaxed = 1;
                     plan.gates.push_back(t);
@@ -568,18 +586,35 @@ GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_
                 const uint32_t kd = uint32_t(t.kinds);
                 auto K = [&](int e) { return (kd >> (4 * e)) & 15u; };
                 t.pad2 = 0;
-                if (t.op == OP_DIAG && (t.srow & 3) == 3) {
-                    if (K(0) == CK_ONE && K(3) == CK_CPLX) t.pad2 = 1;
-                    else if (K(0) == CK_CPLX && K(3) == CK_CPLX) t.pad2 = 2;
-                } else if (t.op == OP_GEN1 && (t.srow & 3) == 3) {
-                    if (K(0) == CK_REAL && K(1) == CK_IMAG && K(2) == CK_IMAG && K(3) == CK_REAL) t.pad2 = 3;
-                    else if (K(0) == CK_REAL && K(1) == CK_REAL && K(2) == CK_REAL && K(3) == CK_REAL) t.pad2 = 4;
-                    else if (K(0) == CK_CPLX && K(1) == CK_CPLX && K(2) == CK_CPLX && K(3) == CK_CPLX) t.pad2 = 5;
+                // 1-5: compile-time kinds, rows +0-safe (no checks);
+                // 11-15: the same kinds with run-time row checks
+                const uint32_t chk = (t.srow & 3) == 3 ? 0u : 10u;
+                if (t.op == OP_DIAG) {
+                    if (K(0) == CK_ONE && K(3) == CK_CPLX) t.pad2 = 1 + chk;
+                    else if (K(0) == CK_CPLX && K(3) == CK_CPLX) t.pad2 = 2 + chk;
+                } else if (t.op == OP_GEN1) {
+                    if (K(0) == CK_REAL && K(1) == CK_IMAG && K(2) == CK_IMAG && K(3) == CK_REAL) t.pad2 = 3 + chk;
+                    else if (K(0) == CK_REAL && K(1) == CK_REAL && K(2) == CK_REAL && K(3) == CK_REAL) t.pad2 = 4 + chk;
+                    else if (K(0) == CK_CPLX && K(1) == CK_CPLX && K(2) == CK_CPLX && K(3) == CK_CPLX) t.pad2 = 5 + chk;
                 } else if (t.op == OP_CP5 && (t.srow & 7) == 7 && K(0) == CK_CPLX && K(1) == CK_CPLX &&
                            K(2) == CK_CPLX) {
                     t.pad2 = 6;
                 } else if (t.op == OP_CXD && (t.srow & 3) == 3 && K(0) == CK_CPLX && K(1) == CK_CPLX) {
                     t.pad2 = 7;
+                }
+            }
+            // runs of specialised OP_PDIAG ops on one register selector (the
+            // kernel's tight loop)
+            for (size_t q = plan.gates.size(); q-- > gd.first_fast;) {
+                TileGate &t = plan.gates[q];
+                t.run = 0;
+                if (t.op == OP_PDIAG && t.pad2 == 8) {
+                    t.run = 1;
+                    if (q + 1 < plan.gates.size()) {
+                        const TileGate &u = plan.gates[q + 1];
+                        const uint32_t rs = t.nq ? t.r0 : kRegBits, ru = u.nq ? u.r0 : kRegBits;
+                        if (u.run && rs == ru) t.run += u.run;
+                    }
                 }
             }
             plan.groups.push_back(gd);
@@ -625,6 +660,23 @@ GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_
     for (size_t ui = 0; ui < units.size(); ++ui) {
         const Unit &u = units[ui];
         if (u.bits >> nbits) throw Failure(QZC_EDEVICE, "gate bit outside buffer");
+        if (u.swaps) {
+            // the whole swap network is one in-place bit-permutation pass
+            close();
+            PassDesc pd;
+            std::memset(&pd, 0, sizeof pd);
+            pd.kind = PASS_SWAPS;
+            pd.first_gate = (uint32_t)u.first;
+            pd.ngates = u.count;
+            for (uint32_t b = 0; b < 48; ++b) pd.perm[b] = uint8_t(b);
+            for (size_t i = u.first; i < u.first + u.count; ++i) {
+                pd.perm[gates[i].b0] = uint8_t(gates[i].b1);
+                pd.perm[gates[i].b1] = uint8_t(gates[i].b0);
+            }
+            pd.pz_stable = 1;
+            plan.passes.push_back(pd);
+            continue;
+        }
         const uint64_t need = u.diag ? 0 : u.bits;
         const uint64_t merged = tmask | need;
         if (!fuse || (uint32_t)__builtin_popcountll(merged) > k) close();
@@ -641,6 +693,7 @@ void upload_plan(const GatePlan &plan, DevPlan &out, cudaStream_t s) {
     out.host_passes = plan.passes;
     out.relaxed = false;
     for (const GroupDesc &g : plan.groups) out.relaxed |= g.relaxed != 0;
+    for (const PassDesc &pd : plan.passes) out.relaxed |= pd.kind == PASS_SWAPS;
     if (out.ngates > out.cap_gates) {
         if (out.gates) QZ_CUDA(cudaFree(out.gates));
         out.cap_gates = std::max<size_t>(out.ngates * 2, 256);
@@ -698,6 +751,12 @@ __device__ __forceinline__ double dneg(double x) {
 }
 __device__ __forceinline__ double2 pm(double2 v, uint32_t neg) {
     return neg ? make_double2(dneg(v.x), dneg(v.y)) : v;
+}
+// +0, or exponent field in [123, 2046]: no -0, tiny, inf or nan component.
+__device__ __forceinline__ uint32_t comp_ok(double x) {
+    const uint64_t b = (uint64_t)__double_as_longlong(x);
+    const uint32_t e = uint32_t(b >> 52) & 0x7ff;
+    return uint32_t(b == 0) | uint32_t(e - 123u < 1924u);
 }
 __device__ __forceinline__ uint32_t sbit(double x) {
     return uint32_t((unsigned long long)__double_as_longlong(x) >> 63);
@@ -887,7 +946,7 @@ __device__ __forceinline__ void fast_diag(double2 (&v)[NB], const TileGate &g, b
     constexpr int sh = 1 << R;
     const uint32_t k00 = uint32_t(g.kinds) & 15u, k11 = uint32_t(g.kinds >> 12) & 15u;
     const double2 m00 = g.m[0], m11 = g.m[3];
-    const bool u0 = !SPEC && !(g.srow & 1), u1 = !SPEC && !(g.srow & 2);
+    const bool u0 = SPEC != 1 && !(g.srow & 1), u1 = SPEC != 1 && !(g.srow & 2);
 #pragma unroll
     for (int p = 0; p < NB / 2; ++p) {
         const int i = izb(p, R), j = i | sh;
@@ -918,6 +977,10 @@ __device__ __forceinline__ void fast_gen1(double2 (&v)[NB], const TileGate &g, b
         if constexpr (SPEC) {
             oi = sum2(termk<K00>(k00, m00, a), termk<K01>(k01, m01, b));
             oj = sum2(termk<K10>(k10, m10, a), termk<K11>(k11, m11, b));
+            if constexpr (SPEC == 2) {   // compile-time kinds, rows not all +0-safe
+                if (!(g.srow & 1)) bad |= zc(oi);
+                if (!(g.srow & 2)) bad |= zc(oj);
+            }
         } else {
             oi = k00 == CK_ZERO ? term(k01, m01, b)
                : (k01 == CK_ZERO ? term(k00, m00, a) : sum2(term(k00, m00, a), term(k01, m01, b)));
@@ -1046,6 +1109,48 @@ __device__ __forceinline__ void fast_pdiag(double2 (&v)[NB], const TileGate &g, 
     }
 }
 
+// Run of specialised OP_PDIAG ops: every step a CPLX +0-safe product, no
+// checks; per op only the thread's variant and register bit are resolved.
+template <int R>
+__device__ __forceinline__ void pdiag_spec(double2 (&v)[NB], const double2 *__restrict__ mm,
+                                           uint32_t act) {
+#pragma unroll
+    for (int st = 0; st < (R < kRegBits ? 2 : 1); ++st) {
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int e = 2 * st + j;
+            if (!((act >> e) & 1)) continue;
+            const double2 m = mm[e];
+#pragma unroll
+            for (int i = 0; i < NB; ++i) {
+                if (R < kRegBits && ((i >> R) & 1) != st) continue;
+                v[i] = termk<CK_CPLX>(CK_CPLX, m, v[i]);
+            }
+        }
+    }
+}
+
+// n consecutive such ops on the same register selector (the switch is
+// hoisted out of the loop: one code path, no register shuffling per op).
+__device__ __forceinline__ void run_pdiag(double2 (&v)[NB], const TileGate *__restrict__ gp,
+                                          uint32_t n, uint64_t gidx) {
+    switch (gp->nq ? gp->r0 : uint32_t(kRegBits)) {
+#define X(a)                                                                                 \
+    case a:                                                                                  \
+        for (uint32_t q = 0; q < n; ++q) {                                                   \
+            const TileGate &g = gp[q];                                                       \
+            const uint32_t var =                                                             \
+                uint32_t((gidx >> g.ob0) & 1) | (uint32_t((gidx >> g.ob1) & 1) << 1);         \
+            pdiag_spec<a>(v, g.m + 4 * var, (g.steps >> (4 * var)) & 15u);                   \
+        }                                                                                    \
+        break;
+        QZ_R1_CASES(X)
+        X(kRegBits)
+#undef X
+    default: break;
+    }
+}
+
 #if QZ_REG_BITS == 3
 #define QZ_PAIRS(X) X(0, 1) X(0, 2) X(1, 2)
 #else
@@ -1075,14 +1180,19 @@ __device__ __forceinline__ void fast_apply(double2 (&v)[NB], const TileGate &g, 
         switch (g.r0) {
 #define X(a)                                                                                 \
     case a:                                                                                  \
-        if (op == OP_DIAG) {                                                                 \
-            if (g.pad2 == 1) fast_diag<a, CK_ONE, CK_CPLX, 1>(v, g, bad);                    \
-            else if (g.pad2 == 2) fast_diag<a, CK_CPLX, CK_CPLX, 1>(v, g, bad);              \
-            else fast_diag<a>(v, g, bad);                                                    \
-        } else {                                                                             \
-            if (g.pad2 == 3) fast_gen1<a, CK_REAL, CK_IMAG, CK_IMAG, CK_REAL, 1>(v, g, bad); \
-            else if (g.pad2 == 4) fast_gen1<a, CK_REAL, CK_REAL, CK_REAL, CK_REAL, 1>(v, g, bad); \
-            else if (g.pad2 == 5) fast_gen1<a, CK_CPLX, CK_CPLX, CK_CPLX, CK_CPLX, 1>(v, g, bad); \
+        switch (g.pad2) {                                                                    \
+        case 1: fast_diag<a, CK_ONE, CK_CPLX, 1>(v, g, bad); break;                          \
+        case 2: fast_diag<a, CK_CPLX, CK_CPLX, 1>(v, g, bad); break;                         \
+        case 11: fast_diag<a, CK_ONE, CK_CPLX, 2>(v, g, bad); break;                         \
+        case 12: fast_diag<a, CK_CPLX, CK_CPLX, 2>(v, g, bad); break;                        \
+        case 3: fast_gen1<a, CK_REAL, CK_IMAG, CK_IMAG, CK_REAL, 1>(v, g, bad); break;       \
+        case 4: fast_gen1<a, CK_REAL, CK_REAL, CK_REAL, CK_REAL, 1>(v, g, bad); break;       \
+        case 5: fast_gen1<a, CK_CPLX, CK_CPLX, CK_CPLX, CK_CPLX, 1>(v, g, bad); break;       \
+        case 13: fast_gen1<a, CK_REAL, CK_IMAG, CK_IMAG, CK_REAL, 2>(v, g, bad); break;      \
+        case 14: fast_gen1<a, CK_REAL, CK_REAL, CK_REAL, CK_REAL, 2>(v, g, bad); break;      \
+        case 15: fast_gen1<a, CK_CPLX, CK_CPLX, CK_CPLX, CK_CPLX, 2>(v, g, bad); break;      \
+        default:                                                                             \
+            if (op == OP_DIAG) fast_diag<a>(v, g, bad);                                      \
             else fast_gen1<a>(v, g, bad);                                                    \
         }                                                                                    \
         break;
@@ -1243,16 +1353,6 @@ __device__ __forceinline__ void mask_apply(uint32_t &SR, uint32_t &SI, const Til
 // Bank-conflict swizzle of the 16 B shared-memory slots inside each 128 B row.
 __device__ __forceinline__ uint32_t swz(uint32_t l) { return l ^ ((l >> 3) & 7u); }
 
-__device__ __forceinline__ uint32_t deposit32(uint32_t v, uint32_t mask) {
-    uint32_t out = 0;
-    while (mask) {
-        const uint32_t low = mask & (0u - mask);
-        if (v & 1) out |= low;
-        v >>= 1;
-        mask &= mask - 1;
-    }
-    return out;
-}
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
     const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
@@ -1313,8 +1413,12 @@ __global__ void __launch_bounds__(1 << (kTileBits - kRegBits), (kTileBits >= 12 
     const uint32_t tid = threadIdx.x, nth = blockDim.x;   // nth == tile / NB
     for (uint32_t h = tid; h < nhi; h += nth) offhi[h] = deposit_bits(h, himask);
     __syncthreads();
-    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const uint64_t base = deposit_bits(t, ntmask);
+    // tile bases: deposit(t) advanced by deposit(gridDim.x) with the carry
+    // running through the tile-bit positions
+    const uint64_t dstep = deposit_bits(gridDim.x, ntmask);
+    uint64_t base = deposit_bits(blockIdx.x, ntmask);
+    for (uint64_t t = blockIdx.x; t < ntiles;
+         t += gridDim.x, base = ((base | ~ntmask) + dstep) & ntmask) {
 #pragma unroll
         for (int i = 0; i < NB; ++i) {
             const uint32_t l = tid + i * nth;
@@ -1322,20 +1426,24 @@ __global__ void __launch_bounds__(1 << (kTileBits - kRegBits), (kTileBits >= 12 
         }
         cp_async_wait_all();
         __syncthreads();
-        if (pd.pz_stable) {
-            // an all-(+0) tile is a fixed point of the whole pass: skip it
-            unsigned long long any = 0;
+        // tile census: any nonzero bit (all-(+0) skip) and "clean" = no -0,
+        // tiny, inf or nan component (the fast path's precondition, then
+        // kept by every group that stays on the fast path)
+        unsigned long long any = 0;
+        uint32_t okv = 1;
 #pragma unroll
-            for (int i = 0; i < NB; ++i) {
-                const double2 x = s[swz(tid + i * nth)];
-                any |= (unsigned long long)__double_as_longlong(x.x) |
-                       (unsigned long long)__double_as_longlong(x.y);
-            }
-            if (!__syncthreads_or(any != 0)) {
-                if (counters && tid == 0) atomicAdd(&counters[0], 1ull);
-                continue;
-            }
+        for (int i = 0; i < NB; ++i) {
+            const double2 x = s[swz(tid + i * nth)];
+            any |= (unsigned long long)__double_as_longlong(x.x) |
+                   (unsigned long long)__double_as_longlong(x.y);
+            okv &= comp_ok(x.x) & comp_ok(x.y);
         }
+        if (pd.pz_stable && !__syncthreads_or(any != 0)) {
+            // an all-(+0) tile is a fixed point of the whole pass: skip it
+            if (counters && tid == 0) atomicAdd(&counters[0], 1ull);
+            continue;
+        }
+        bool clean = __syncthreads_and(okv) != 0;
         for (uint32_t gi = 0; gi < pd.ngroups; ++gi) {
             const GroupDesc &G = groups[pd.first_group + gi];
             const TileGate *gp = gates + G.first_gate;
@@ -1344,6 +1452,7 @@ __global__ void __launch_bounds__(1 << (kTileBits - kRegBits), (kTileBits >= 12 
                     smem_generic(s, tile, gp[q]);
                     __syncthreads();
                 }
+                clean = false;
                 continue;
             }
             uint32_t bm[kRegBits], gm = 0;
@@ -1352,7 +1461,14 @@ __global__ void __launch_bounds__(1 << (kTileBits - kRegBits), (kTileBits >= 12 
                 bm[i] = 1u << G.gbits[i];
                 gm |= bm[i];
             }
-            const uint32_t mybase = deposit32(tid, (tile - 1) & ~gm);
+            // tid with zeros inserted at the (ascending) register bits ==
+            // deposit of tid into the tile bits outside gm
+            uint32_t mybase = tid;
+#pragma unroll
+            for (int i = 0; i < kRegBits; ++i) {
+                const uint32_t b = G.gbits[i];
+                mybase = ((mybase >> b) << (b + 1)) | (mybase & ((1u << b) - 1));
+            }
             // buffer index of the thread's register-0 amplitude: the values of
             // every non-register bit (OP_PDIAG variants)
             const uint64_t gidx = G.relaxed ? base + offhi[mybase >> L] + (mybase & lowmask) : 0;
@@ -1397,18 +1513,25 @@ __global__ void __launch_bounds__(1 << (kTileBits - kRegBits), (kTileBits >= 12 
             } else {
                 // fast path precondition: no -0 component and every nonzero
                 // component in [2^-900, 2^1023] (no underflow, no inf/nan)
-                bool okblk = true;
+                uint32_t okg = 1;
+                if (!clean) {
 #pragma unroll
-                for (int r = 0; r < NB; ++r) {
-                    const uint64_t xr = (uint64_t)__double_as_longlong(v[r].x);
-                    const uint64_t xi = (uint64_t)__double_as_longlong(v[r].y);
-                    const uint32_t er = uint32_t(xr >> 52) & 0x7ff, ei = uint32_t(xi >> 52) & 0x7ff;
-                    okblk &= (xr == 0 || (er >= 123 && er < 2047)) && (xi == 0 || (ei >= 123 && ei < 2047));
+                    for (int r = 0; r < NB; ++r) okg &= comp_ok(v[r].x) & comp_ok(v[r].y);
                 }
+                const bool okblk = okg != 0;
                 bool bad = !okblk;
                 path = okblk ? 3 : 4;
                 const TileGate *fp = gates + G.first_fast;
-                for (uint32_t q = 0; q < G.nfast && !bad; ++q) fast_apply(v, fp[q], gidx, bad);
+                for (uint32_t q = 0; q < G.nfast && !bad;) {
+                    const uint32_t run = fp[q].run;
+                    if (run) {
+                        run_pdiag(v, fp + q, run, gidx);
+                        q += run;
+                    } else {
+                        fast_apply(v, fp[q], gidx, bad);
+                        ++q;
+                    }
+                }
                 if (bad && okblk) path = 5;
                 if (bad && G.relaxed) {
                     *flag = 1u;   // the exact path needs partners outside the tile
@@ -1424,7 +1547,8 @@ __global__ void __launch_bounds__(1 << (kTileBits - kRegBits), (kTileBits >= 12 
                 for (int r = 0; r < NB; ++r) s[addr[r]] = v[r];
             }
             if (counters) atomicAdd(&counters[path], 1ull);
-            __syncthreads();
+            // the sign-mask and exact paths may leave -0 behind
+            clean = __syncthreads_and(path == 1 || path == 3) != 0;
         }
         double2 out[NB];
 #pragma unroll
@@ -1433,6 +1557,87 @@ __global__ void __launch_bounds__(1 << (kTileBits - kRegBits), (kTileBits >= 12 
         for (int i = 0; i < NB; ++i) {
             const uint32_t l = tid + i * nth;
             __stcs(buf + base + offhi[l >> L] + (l & lowmask), out[i]);
+        }
+        __syncthreads();
+    }
+}
+
+// PASS_SWAPS: a run of pairwise disjoint SWAPs applied as the bit permutation
+// pi (an involution): psi'[j] = psi[pi(j)].  Each SWAP row is 1*v + 0*(others)
+// (kernels.cpp:49-50), which equals v exactly unless v has a -0 component;
+// a tile pair holding a -0 raises the replay flag instead.
+// Tile = buffer bits S = {0..4} u pi({0..4}) (512 B contiguous segments on
+// both the read and the write side); tiles pair up as (base, pi(base)) and
+// one CTA moves both, in place.
+constexpr uint32_t kSwapLow = 5;
+
+__device__ __forceinline__ uint64_t permute_bits(uint64_t x, const uint8_t *perm, uint32_t nbits) {
+    uint64_t y = 0;
+    for (uint32_t b = 0; b < nbits; ++b) y |= ((x >> b) & 1) << perm[b];
+    return y;
+}
+
+__global__ void __launch_bounds__(256) tile_swaps(double2 *__restrict__ buf, uint32_t nbits,
+                                                  PassDesc pd, uint32_t *__restrict__ flag,
+                                                  const uint32_t *__restrict__ cond) {
+    if (cond && *cond == 0) return;
+    __shared__ uint8_t perm[48];
+    __shared__ uint16_t lperm[1u << (2 * kSwapLow)];
+    __shared__ uint64_t loff[1u << (2 * kSwapLow)];
+    __shared__ __align__(16) double2 ta[1u << (2 * kSwapLow)], tb[1u << (2 * kSwapLow)];
+    const uint32_t tid = threadIdx.x, nth = blockDim.x;
+    const uint32_t L = min(kSwapLow, nbits);
+    uint64_t smask = (uint64_t(1) << L) - 1;
+    for (uint32_t b = 0; b < L; ++b) smask |= uint64_t(1) << pd.perm[b];
+    const uint32_t ks = __popcll(smask), tile = 1u << ks;
+    const uint64_t cmask = ((uint64_t(1) << nbits) - 1) & ~smask;
+    if (tid < 48) perm[tid] = pd.perm[tid];
+    __syncthreads();
+    // local bit permutation induced on S
+    for (uint32_t l = tid; l < tile; l += nth) {
+        const uint64_t off = deposit_bits(l, smask);
+        const uint64_t img = permute_bits(off, perm, nbits);
+        // compress img back to local bits
+        uint32_t li = 0, i = 0;
+        for (uint64_t m = smask; m; m &= m - 1, ++i)
+            if (img & (m & (0 - m))) li |= 1u << i;
+        lperm[l] = uint16_t(li);
+        loff[l] = off;
+    }
+    __syncthreads();
+    const uint64_t ntiles = uint64_t(1) << (nbits - ks);
+    const uint64_t dstep = deposit_bits(gridDim.x, cmask);
+    uint64_t base = deposit_bits(blockIdx.x, cmask);
+    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, base = ((base | ~cmask) + dstep) & cmask) {
+        const uint64_t pbase = permute_bits(base, perm, nbits);
+        if (pbase < base) continue;   // the partner tile's CTA moves this pair
+        const bool pair = pbase != base;
+        uint32_t neg0 = 0;
+        for (uint32_t l = tid; l < tile; l += nth) {
+            const uint64_t off = loff[l];
+            const double2 a = __ldcs(buf + base + off);
+            ta[l] = a;
+            neg0 |= uint32_t(__double_as_longlong(a.x) == (long long)0x8000000000000000ULL) |
+                    uint32_t(__double_as_longlong(a.y) == (long long)0x8000000000000000ULL);
+            if (pair) {
+                const double2 b = __ldcs(buf + pbase + off);
+                tb[l] = b;
+                neg0 |= uint32_t(__double_as_longlong(b.x) == (long long)0x8000000000000000ULL) |
+                        uint32_t(__double_as_longlong(b.y) == (long long)0x8000000000000000ULL);
+            }
+        }
+        if (__syncthreads_or(neg0)) {
+            if (tid == 0) *flag = 1u;
+        }
+        for (uint32_t l = tid; l < tile; l += nth) {
+            const uint64_t off = loff[l];
+            const uint32_t src = lperm[l];
+            if (pair) {
+                __stcs(buf + base + off, tb[src]);
+                __stcs(buf + pbase + off, ta[src]);
+            } else {
+                __stcs(buf + base + off, ta[src]);
+            }
         }
         __syncthreads();
     }
@@ -1509,7 +1714,12 @@ uint64_t run_passes(const DevPlan &plan, double2 *buf, uint32_t nbits, cudaStrea
     }
     uint64_t launches = 0;
     for (const PassDesc &pd : plan.host_passes) {
-        if (pd.k < (uint32_t)kRegBits + 1) {
+        if (pd.kind == PASS_SWAPS) {
+            if (!flag && !cond) throw Failure(QZC_EDEVICE, "swap-network pass without a replay flag");
+            const uint64_t tiles = uint64_t(1) << (nbits > 2 * kSwapLow ? nbits - 2 * kSwapLow : 0);
+            const uint64_t grid = std::min<uint64_t>(std::max<uint64_t>(tiles, 1), uint64_t(kNumSMs) * 8);
+            tile_swaps<<<(unsigned)grid, 256, 0, s>>>(buf, nbits, pd, flag, cond);
+        } else if (pd.k < (uint32_t)kRegBits + 1) {
             // tile == whole buffer (nbits < 4)
             tile_pass_tiny<<<1, 32, 0, s>>>(buf, nbits, pd, plan.groups, plan.gates, cond);
         } else {

@@ -56,7 +56,9 @@ struct TileGate {
     uint32_t srow;                // bit r: row r is "+0-safe" (see qz_gates.cu)
     uint32_t pad2;                // compile-time specialisation code of the fast path
     uint32_t ob0, ob1;            // OP_PDIAG: outside buffer bits (ob1 = 63 if unused)
-    uint32_t pad3[2];
+    uint32_t run;                 // OP_PDIAG, all steps CPLX and +0-safe: length of the
+                                  // run of such ops starting here (0 otherwise)
+    uint32_t steps;               // OP_PDIAG: bit 4v+e set = step e of variant v present
     double2 m[16];
 };
 
@@ -101,8 +103,12 @@ struct PassDesc {
     uint32_t ngates;
     uint64_t tmask;        // T as a bit mask over buffer bits
     uint32_t pz_stable;    // all groups pz_stable: an all-(+0) tile is left untouched
-    uint32_t pad;
+    uint32_t kind;         // PASS_TILE, or PASS_SWAPS: a run of disjoint SWAPs as one
+                           // bit permutation (perm[b] = image of buffer bit b)
+    uint8_t perm[48];
 };
+
+enum PassKind : uint32_t { PASS_TILE = 0, PASS_SWAPS = 1 };
 
 struct GatePlan {
     std::vector<PassDesc> passes;

@@ -352,6 +352,8 @@ uint32_t log2u(uint64_t x) {
 void sim_alloc(qzc_sim *sim) {
     qzc_context *ctx = sim->ctx;
     const uint64_t tbl_entries = std::max<uint64_t>(sim->nchunks, 2);
+    sim->replays.ensure(8);
+    QZ_CUDA(cudaMemset(sim->replays.p, 0, 8));
     for (int i = 0; i < 2; ++i) {
         sim->off[i].ensure(8 * tbl_entries);
         sim->len[i].ensure(4 * tbl_entries);
@@ -956,8 +958,31 @@ int qzc_sim_init_basis(qzc_sim *sim) {
     sim->initialized = true;
     sim->stats = qzc_sim_stats{};
     if (sim->host_res) QZ_CUDA(cudaMemset(sim->io_bytes.p, 0, 16));
-    sim->replays.ensure(8);
     QZ_CUDA(cudaMemset(sim->replays.p, 0, 8));
+    QZ_API_END
+}
+
+int qzc_pass_plan_stats(const qzc_gate *gates, uint64_t ngates, uint32_t nbits,
+                        uint32_t fuse_mode, uint64_t *out) {
+    QZ_API_BEGIN
+    if (fuse_mode > 2 || nbits > 40) throw Failure(QZC_EINVAL, "bad fuse mode / buffer width");
+    const std::string err = validate_gates(nbits, gates, ngates);
+    if (!err.empty()) throw Failure(QZC_EINVAL, err);
+    std::vector<DevGate> dg;
+    for (uint64_t i = 0; i < ngates; ++i) dg.push_back(make_dev_gate(gates[i]));
+    const GatePlan p = build_passes(dg, nbits, kTileBits, fuse_mode != 0, fuse_mode == 1);
+    uint64_t relaxed = 0, fast = 0, pdiag = 0;
+    for (const GroupDesc &g : p.groups) {
+        relaxed += g.relaxed;
+        fast += g.nfast;
+        for (uint32_t q = 0; q < g.nfast; ++q) pdiag += p.gates[g.first_fast + q].op == OP_PDIAG;
+    }
+    out[0] = p.passes.size();
+    out[1] = p.groups.size();
+    out[2] = relaxed;
+    out[3] = ngates;
+    out[4] = fast;
+    out[5] = pdiag;
     QZ_API_END
 }
 

@@ -108,6 +108,7 @@ def load_library() -> C.CDLL:
         "qzc_copy_d2h": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64]),
         "qzc_host_alloc": (C.c_int, [C.c_void_p, C.c_uint64, P(C.c_void_p)]),
         "qzc_host_free": (None, [C.c_void_p, C.c_void_p]),
+        "qzc_pass_plan_stats": (C.c_int, [P(Gate), C.c_uint64, C.c_uint32, C.c_uint32, u64p]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -115,6 +116,18 @@ def load_library() -> C.CDLL:
         f.argtypes = args
     _lib = lib
     return lib
+
+
+def pass_plan_stats(gates, nbits: int, fuse="relaxed") -> dict:
+    """Fused-pass plan summary for gates on buffer bits of a 2^nbits window
+    (host-only planning, no GPU needed)."""
+    lib = load_library()
+    arr = to_array(gates)
+    out = (C.c_uint64 * 6)()
+    mode = {"none": 0, "relaxed": 1, "strict": 2}[fuse]
+    _check(lib.qzc_pass_plan_stats(arr.ctypes.data_as(P(Gate)), arr.size, nbits, mode, out))
+    keys = ("passes", "groups", "relaxed_groups", "gates", "fast_ops", "pdiag_ops")
+    return dict(zip(keys, (int(x) for x in out)))
 
 
 def exported_symbols() -> list[str]:

@@ -234,3 +234,50 @@ def test_relaxed_qft_needs_no_replay(engine):
     strict = run_sim(engine, 20, 10, 20, 1e-5, CI.qft(20), fuse="strict")
     assert strict.digest() == sim.digest()
     assert st["gate_passes"] * 3 < strict.stats()["gate_passes"]
+
+
+def _load_state(engine, oracle, n, c, m, state):
+    """Lossless store holding `state` exactly (payloads from the oracle codec)."""
+    sim = engine.simulator(n, c, m, 0.0, init=False)
+    blobs, sizes, crcs = [], [], []
+    for k in range(1 << (n - c)):
+        p, crc = oracle.compress(state[k << c:(k + 1) << c], 0.0)
+        blobs.append(p)
+        sizes.append(len(p))
+        crcs.append(crc)
+    sim.import_(b"".join(blobs), np.array(sizes, np.uint32), np.array(crcs, np.uint32))
+    return sim
+
+
+def _random_state(rng, n, neg_zero: bool):
+    st = (rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)) / (1 << (n // 2))
+    st[rng.random(1 << n) < 0.1] = 0.0                         # +0 components
+    if neg_zero:
+        z = rng.random(1 << n) < 0.02
+        st.real[z] = -0.0
+    return st
+
+
+@pytest.mark.parametrize("seed", range(4))
+@pytest.mark.parametrize("neg_zero", [False, True])
+def test_swap_network_pass_bit_exact(engine, oracle, seed, neg_zero):
+    """Runs of disjoint SWAPs become one in-place bit-permutation pass; the
+    result equals the reference kernels bit for bit, and a -0 component makes
+    the pass replay strictly (still bit-exact)."""
+    rng = np.random.default_rng(100 + seed)
+    n, c = 14, 4
+    q = rng.permutation(n)
+    npairs = int(rng.integers(2, n // 2 + 1))
+    gates = [("swap", (int(q[2 * i]), int(q[2 * i + 1])), ()) for i in range(npairs)]
+    if seed % 2:
+        gates = [("h", (int(q[0]),), ()), ("t", (int(q[1]),), ())] + gates + [("rx", (3,), (0.4,))]
+    state = _random_state(rng, n, neg_zero)
+    want = oracle.apply_gates(state.copy(), gates)
+    sim = _load_state(engine, oracle, n, c, n, state)
+    sim.run(gates)
+    got = sim.state()
+    assert got.view(np.uint64).tobytes() == want.view(np.uint64).tobytes()
+    if neg_zero:
+        assert sim.stats()["replays"] >= 1
+    elif seed % 2 == 0:
+        assert sim.stats()["replays"] == 0
