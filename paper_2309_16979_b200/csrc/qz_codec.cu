@@ -230,18 +230,27 @@ __device__ __forceinline__ uint32_t cur_next(Cursor &c, const uint8_t *p) {
     return c.byte;
 }
 
+// Tile width for a CTA holding `rows` chunks: kTileElems for a full CTA, wider
+// when only a few chunks are coded (init, read-back), so the serial per-chunk
+// loop crosses fewer barriers.  rows * (te + 1) <= kSlotsPerCta * (kTileElems + 1).
+__device__ __forceinline__ uint32_t tile_width(uint32_t rows, uint64_t N) {
+    uint32_t rp = 1;
+    while (rp < rows) rp <<= 1;
+    return uint32_t(umin64(uint64_t(kTileElems) * (kSlotsPerCta / rp), N));
+}
+
 // Tile of kSlotsPerCta rows x kTileElems amplitudes (+1 pad element per row).
 struct TileSmem {
-    double2 v[kSlotsPerCta][kTileElems + 1];
+    double2 f[kSlotsPerCta * (kTileElems + 1)];   // row r at r * (te + 1)
 };
 
 __device__ __forceinline__ void store_tile(TileSmem &t, double2 *win, uint64_t slot0,
                                            uint64_t nslots, uint64_t N, uint64_t e0,
-                                           uint32_t te) {
+                                           uint32_t te, uint32_t stride) {
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (uint32_t r = warp; r < kSlotsPerCta; r += nw) {
         if (slot0 + r >= nslots) break;
-        if (lane < te) win[(slot0 + r) * N + e0 + lane] = t.v[r][lane];
+        for (uint32_t e = lane; e < te; e += 32) win[(slot0 + r) * N + e0 + e] = t.f[r * stride + e];
     }
 }
 
@@ -251,7 +260,7 @@ __device__ __forceinline__ void load_tile(TileSmem &t, const double2 *win, uint6
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (uint32_t r = warp; r < kSlotsPerCta; r += nw) {
         if (slot0 + r >= nslots) break;
-        if (lane < te) t.v[r][lane] = __ldcs(win + (slot0 + r) * N + e0 + lane);
+        for (uint32_t e = lane; e < te; e += 32) t.f[r * (te + 1) + e] = __ldcs(win + (slot0 + r) * N + e0 + e);
     }
 }
 
@@ -260,7 +269,9 @@ __device__ __forceinline__ void set_comp(double2 &v, uint32_t h, double x) {
     if (h) v.y = x; else v.x = x;
 }
 
-// Lossy decode (codec.cpp:217-249): thread = (slot, half).
+// Lossy decode (codec.cpp:217-249): thread = (slot, half).  WIDE: a launch
+// with fewer chunks than one CTA row set uses wide tiles (tile_width).
+template <bool WIDE>
 __global__ void __launch_bounds__(2 * kSlotsPerCta) k_dec_lossy(
     const uint8_t *__restrict__ arena, const DecIdx *__restrict__ idx,
     const uint64_t *__restrict__ slot_chunk, uint64_t nslots, CodecGeom g,
@@ -285,10 +296,34 @@ __global__ void __launch_bounds__(2 * kSlotsPerCta) k_dec_lossy(
         twoeb = 2.0 * d->eb;
     }
     const uint64_t N = g.N;
-    const uint32_t te = uint32_t(umin64(kTileElems, N));
+    const uint32_t rows = uint32_t(umin64(kSlotsPerCta, nslots - slot0));
+    const uint32_t te = WIDE ? tile_width(rows, N) : uint32_t(umin64(kTileElems, N));
+    // rows past the CTA's chunk count have no tile storage (wide tiles)
+    double2 *row = tile.f + (WIDE ? min(r, rows - 1) * (te + 1) : r * (kTileElems + 1));
+    const bool has_row = !WIDE || r < rows;
     for (uint64_t e0 = 0; e0 < N; e0 += te) {
-        for (uint32_t e = 0; e < te; ++e) {
+        for (uint32_t e = 0; e < te && has_row; ++e) {
             if (active) {
+                if (lo.rem == 0) {
+                    lo.pos += 2;
+                    lo.byte = p[lo.pos];
+                    lo.rem = p[lo.pos + 1];
+                }
+                if (hi.rem == 0) {
+                    hi.pos += 2;
+                    hi.byte = p[hi.pos];
+                    hi.rem = p[hi.pos + 1];
+                }
+                if ((lo.byte | hi.byte) == 0) {
+                    // a stretch of code 0: pred + (+0) = pred (a -0 becomes +0)
+                    const uint32_t k = min(min(lo.rem, hi.rem), te - e);
+                    if (__double_as_longlong(pred) << 1 == 0) pred = 0.0;
+                    for (uint32_t j = 0; j < k; ++j) set_comp(row[e + j], h, pred);
+                    lo.rem -= k;
+                    hi.rem -= k;
+                    e += k - 1;
+                    continue;
+                }
                 const uint32_t z = cur_next(lo, p) | (cur_next(hi, p) << 8);
                 if (z == 0xFFFFu) {
                     if (raw_i >= raw_count) {
@@ -303,10 +338,10 @@ __global__ void __launch_bounds__(2 * kSlotsPerCta) k_dec_lossy(
                     pred = __dadd_rn(pred, __dmul_rn(double(code), twoeb));
                 }
             }
-            set_comp(tile.v[r][e], h, pred);
+            set_comp(row[e], h, pred);
         }
         __syncthreads();
-        store_tile(tile, win, slot0, nslots, N, e0, te);
+        store_tile(tile, win, slot0, nslots, N, e0, te, WIDE ? te + 1 : kTileElems + 1);
         __syncthreads();
     }
     if (active) {
@@ -334,6 +369,7 @@ __global__ void __launch_bounds__(2 * kSlotsPerCta) k_dec_lossless(
     }
     const uint64_t N = g.N;
     const uint32_t te = uint32_t(umin64(kTileElems, N));
+    double2 *row = tile.f + r * (kTileElems + 1);
     for (uint64_t e0 = 0; e0 < N; e0 += te) {
         for (uint32_t e = 0; e < te; ++e) {
             uint64_t bits = 0;
@@ -341,10 +377,10 @@ __global__ void __launch_bounds__(2 * kSlotsPerCta) k_dec_lossless(
 #pragma unroll
                 for (int k = 0; k < 8; ++k) bits |= uint64_t(cur_next(cur[k], p)) << (8 * k);
             }
-            set_comp(tile.v[r][e], h, __longlong_as_double((long long)bits));
+            set_comp(row[e], h, __longlong_as_double((long long)bits));
         }
         __syncthreads();
-        store_tile(tile, win, slot0, nslots, N, e0, te);
+        store_tile(tile, win, slot0, nslots, N, e0, te, kTileElems + 1);
         __syncthreads();
     }
 }
@@ -407,6 +443,25 @@ __device__ __forceinline__ void rle_push(Rle &s, uint32_t x) {
     }
 }
 
+// n pushes of byte x (the same run state as n calls of rle_push).
+__device__ __forceinline__ void rle_push_n(Rle &s, uint32_t x, uint32_t n) {
+    if (n == 0) return;
+    if (x != s.cur) {
+        rle_push(s, x);
+        --n;
+    }
+    if (s.hold) {
+        s.cnt += n;
+        return;
+    }
+    uint32_t tot = s.cnt + n;
+    while (tot >= 255) {
+        rle_emit(s, x, 255);
+        tot -= 255;
+    }
+    s.cnt = tot;
+}
+
 // Close a half: real half keeps (cur, cnt) as its open tail; imaginary half
 // emits its last run (or, if still holding, reports the whole half as head).
 __device__ __forceinline__ void rle_finish(Rle &s, uint32_t h, EncHalf &m, int k) {
@@ -434,7 +489,7 @@ __device__ __forceinline__ uint8_t *scratch_half(uint8_t *scratch, const CodecGe
 
 // Double-buffered tile of kSlotsPerCta rows x kTileElems amplitudes.
 struct EncTiles {
-    double2 v[2][kSlotsPerCta][kTileElems + 1];
+    double2 f[2][kSlotsPerCta * (kTileElems + 1)];   // row r at r * (te + 1)
 };
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
@@ -484,13 +539,15 @@ __global__ void __launch_bounds__(2 * kSlotsPerCta) k_enc_lossy(
     while (fc < nforced && forced[fc] < h * N) ++fc;
     uint64_t next_forced = fc < nforced ? forced[fc] : ~uint64_t(0);
     const double eb = g.eb, twoeb = g.twoeb;
+    const double thr = __dmul_rn(0.99, eb);
     double pred = 0.0;
-    const uint32_t te = uint32_t(umin64(kTileElems, N));
     const uint32_t rows = uint32_t(umin64(kSlotsPerCta, nslots - slot0));
+    const uint32_t te = tile_width(rows, N), lte = 31 - __clz(te);
+    auto at = [&](int buf, uint32_t rr, uint32_t e) -> double2 & { return tiles.f[buf][rr * (te + 1) + e]; };
     auto issue = [&](int buf, uint64_t e0) {
         for (uint32_t i = threadIdx.x; i < rows * te; i += blockDim.x) {
-            const uint32_t rr = i / te, e = i - rr * te;
-            cp_async16(&tiles.v[buf][rr][e], win + (slot0 + rr) * N + e0 + e);
+            const uint32_t rr = i >> lte, e = i & (te - 1);
+            cp_async16(&at(buf, rr, e), win + (slot0 + rr) * N + e0 + e);
         }
         cp_async_commit();
     };
@@ -504,9 +561,28 @@ __global__ void __launch_bounds__(2 * kSlotsPerCta) k_enc_lossy(
             cp_async_wait<0>();
         }
         __syncthreads();
-        if (active) {
+        // fast-forward: if every value of the tile is within 0.99 eb of the
+        // predictor, every element quantises to code 0 (|d / 2eb| < 0.495
+        // rounds to 0 in any rounding of the quotient), reconstructs to
+        // rec = pred + (+0) = pred (a -0 predictor becomes +0) and passes the
+        // error check — the predictor never moves, so the tile is two runs of
+        // byte 0 (zero runs of sparse states, slowly varying amplitudes)
+        bool ff = active && next_forced >= h * N + e0 + te;
+        if (ff) {
+            bool all = true;
+#pragma unroll 8
+            for (uint32_t e = 0; e < te; ++e)
+                all &= fabs(__dsub_rn(comp(at(buf, r, e), h), pred)) < thr;
+            ff = all;
+            if (ff) {
+                rle_push_n(lo, 0, te);
+                rle_push_n(hi, 0, te);
+                pred = __dadd_rn(pred, 0.0);
+            }
+        }
+        if (active && !ff) {
             for (uint32_t e = 0; e < te; ++e) {
-                const double v = comp(tiles.v[buf][r][e], h);
+                const double v = comp(at(buf, r, e), h);
                 const uint64_t flat = h * N + e0 + e;
                 bool raw = false;
                 int32_t code = 0;
@@ -849,9 +925,12 @@ void launch_decode(const uint8_t *arena, const DecIdx *idx, const uint64_t *slot
                    uint64_t nslots, const CodecGeom &g, double2 *win, DevStatus *status,
                    cudaStream_t s, const uint32_t *cond) {
     const unsigned grid = grid_for(nslots, kSlotsPerCta);
-    if (g.lossy)
-        k_dec_lossy<<<grid, 2 * kSlotsPerCta, 0, s>>>(arena, idx, slot_chunk, nslots, g, win,
-                                                       status, cond);
+    if (g.lossy && nslots < uint64_t(kSlotsPerCta))
+        k_dec_lossy<true><<<grid, 2 * kSlotsPerCta, 0, s>>>(arena, idx, slot_chunk, nslots, g, win,
+                                                             status, cond);
+    else if (g.lossy)
+        k_dec_lossy<false><<<grid, 2 * kSlotsPerCta, 0, s>>>(arena, idx, slot_chunk, nslots, g, win,
+                                                              status, cond);
     else
         k_dec_lossless<<<grid, 2 * kSlotsPerCta, 0, s>>>(arena, idx, nslots, g, win, cond);
     QZ_CHECK_LAUNCH();

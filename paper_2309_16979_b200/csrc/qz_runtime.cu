@@ -263,6 +263,7 @@ struct qzc_sim {
     uint8_t *harena_dev[2] = {nullptr, nullptr};  // device view of the same bytes
     DevBuf io_bytes;  // uint64[2]: host->HBM and HBM->host payload bytes
     DevBuf replays;   // uint64: windows replayed with the strict plan
+    DevBuf small;     // uint64[4] scratch for init_basis (slot / forced lists)
     DevPlan plans[2]; // stage plans (relaxed / strict), device buffers reused
     DevBuf used;   // uint64[2] bump pointers
     DevBuf acct;   // int64[2] current / peak
@@ -354,6 +355,7 @@ void sim_alloc(qzc_sim *sim) {
     const uint64_t tbl_entries = std::max<uint64_t>(sim->nchunks, 2);
     sim->replays.ensure(8);
     QZ_CUDA(cudaMemset(sim->replays.p, 0, 8));
+    sim->small.ensure(64);
     for (int i = 0; i < 2; ++i) {
         sim->off[i].ensure(8 * tbl_entries);
         sim->len[i].ensure(4 * tbl_entries);
@@ -875,6 +877,7 @@ void qzc_sim_destroy(qzc_sim *sim) {
     sim->acct.release();
     sim->io_bytes.release();
     sim->replays.release();
+    sim->small.release();
     for (DevPlan &p : sim->plans) free_plan(p);
     for (int i = 0; i < 2; ++i)
         if (sim->harena[i]) cudaFreeHost(sim->harena[i]);
@@ -899,6 +902,8 @@ int qzc_sim_init_basis(qzc_sim *sim) {
     Window &w = sim->win;
     const uint64_t N = sim->N;
     const int a = sim->cur;
+    static const bool trace = getenv("QZ_TRACE") && *getenv("QZ_TRACE") == '1';
+    const double ti0 = now_s();
     QZ_CUDA(cudaMemsetAsync(sim->used.p, 0, 16, s));
     // slot 0 = zero chunk, slot 1 = basis chunk (store.cpp:46-51)
     QZ_CUDA(cudaMemsetAsync(w.amps.p, 0, 32 * N, s));
@@ -908,14 +913,14 @@ int qzc_sim_init_basis(qzc_sim *sim) {
     encode_window(ctx, w, sim->geom, 2, nullptr, nullptr, 0, sim->arena_ptr(a),
                   sim->used_ptr(a), sim->arena_cap, t, nullptr, nullptr, ctx->launches);
     ctx->check_status();
+    const double ti1 = now_s();
     if (sim->eb > 0.0) {
         // decode the basis chunk; route {0,1} through the raw path if the
         // quantiser perturbed it (store.cpp:52-67)
-        uint64_t one_slot = 1;
-        DevBuf sc;
-        sc.ensure(8);
-        QZ_CUDA(cudaMemcpyAsync(sc.p, &one_slot, 8, cudaMemcpyHostToDevice, s));
-        decode_window(ctx, w, sim->geom, 1, sc.as<uint64_t>(), sim->arena_ptr(a), t, ctx->launches);
+        static const uint64_t kSmall[4] = {1, 0, 1, 0};   // slot list {1}, forced list {0, 1}
+        QZ_CUDA(cudaMemcpyAsync(sim->small.p, kSmall, sizeof kSmall, cudaMemcpyHostToDevice, s));
+        const uint64_t *sc = sim->small.as<uint64_t>();
+        decode_window(ctx, w, sim->geom, 1, sc, sim->arena_ptr(a), t, ctx->launches);
         ctx->check_status();
         std::vector<double2> r(N);
         QZ_CUDA(cudaMemcpyAsync(r.data(), w.amps.p, 16 * N, cudaMemcpyDeviceToHost, s));
@@ -924,22 +929,13 @@ int qzc_sim_init_basis(qzc_sim *sim) {
         for (uint64_t i = 0; exact && i < N; ++i)
             if (r[i].y != 0.0 || (i > 0 && r[i].x != 0.0)) exact = false;
         if (!exact) {
-            std::vector<uint64_t> fr{0};
-            if (N > 1) fr.push_back(1);
-            DevBuf fd;
-            fd.ensure(16);
-            QZ_CUDA(cudaMemcpyAsync(fd.p, fr.data(), 8 * fr.size(), cudaMemcpyHostToDevice, s));
             QZ_CUDA(cudaMemsetAsync(w.amps.p, 0, 16 * N, s));
             QZ_CUDA(cudaMemcpyAsync(w.amps.p, one, 16, cudaMemcpyHostToDevice, s));
-            encode_window(ctx, w, sim->geom, 1, sc.as<uint64_t>(), fd.as<uint64_t>(), (uint32_t)fr.size(),
+            encode_window(ctx, w, sim->geom, 1, sc, sc + 1, N > 1 ? 2u : 1u,
                           sim->arena_ptr(a), sim->used_ptr(a), sim->arena_cap, t, nullptr,
                           nullptr, ctx->launches);
             ctx->check_status();
-            QZ_CUDA(cudaStreamSynchronize(s));
-            fd.release();
         }
-        QZ_CUDA(cudaStreamSynchronize(s));
-        sc.release();
     }
     uint64_t off2[2];
     uint32_t len2[2], crc2[2];
@@ -959,6 +955,9 @@ int qzc_sim_init_basis(qzc_sim *sim) {
     sim->stats = qzc_sim_stats{};
     if (sim->host_res) QZ_CUDA(cudaMemset(sim->io_bytes.p, 0, 16));
     QZ_CUDA(cudaMemset(sim->replays.p, 0, 8));
+    if (trace)
+        fprintf(stderr, "qz trace: init encode %.2f ms total %.2f ms\n", 1e3 * (ti1 - ti0),
+                1e3 * (now_s() - ti0));
     QZ_API_END
 }
 

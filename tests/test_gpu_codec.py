@@ -156,3 +156,36 @@ def test_quantiser_half_integer_boundaries(engine, oracle, eb):
     assert got == want
     back = engine.decompress(got[0], got[1], n)
     assert back.tobytes() == oracle.decompress(want[0], want[1], n).tobytes()
+
+
+@pytest.mark.parametrize("eb", [1e-5, 1e-7, 0.01])
+def test_fast_forward_tiles_match_oracle(engine, oracle, eb):
+    """Tiles that never move the predictor (zero runs, values within 0.99 eb of
+    it, -0/+0 mixtures, values straddling the 0.99 eb threshold, forced raws
+    inside such runs) take the encoder's and decoder's run fast-forward; the
+    bytes must still be the reference's."""
+    rng = np.random.default_rng(int(eb * 1e9) + 5)
+    n = 1 << 12
+    rows = []
+    z = np.zeros(n, complex)
+    rows.append(z.copy())                                        # all zeros
+    a = z.copy(); a[::517] = 0.3 + 0.1j; rows.append(a)          # sparse spikes
+    a = np.full(n, 0.25 + 0.0j) + rng.uniform(-0.9, 0.9, n) * eb; rows.append(a)   # smooth
+    a = np.full(n, -0.5 + 0.5j); a[1000:1100] += 0.989 * eb; a[2000] += 0.991 * eb
+    rows.append(a)                                               # threshold straddle
+    a = rng.uniform(-0.98, 0.98, n) * eb + 1j * rng.uniform(-0.98, 0.98, n) * eb
+    rows.append(a)                                               # noise below eb
+    a = z.copy(); a.real[::3] = -0.0; a.imag[1::5] = -0.0; rows.append(a)   # signed zeros
+    a = z.copy(); a[7] = 1.0; a[8] = -1.0; rows.append(a)        # basis-like escapes
+    arr = np.array(rows)
+    got = engine.compress_many(arr, eb)
+    for k in range(len(rows)):
+        assert got[k] == oracle.compress(arr[k], eb), k
+    back = engine.decompress_many([g[0] for g in got], [g[1] for g in got], n)
+    for k in range(len(rows)):
+        ref = oracle.decompress(got[k][0], got[k][1], n)
+        assert back[k].tobytes() == ref.tobytes(), k
+    # forced raws (flat indices) landing inside zero runs
+    forced = [5, 64, 4095, n + 33, 2 * n - 1]
+    p = engine.compress(z, eb, forced=forced)
+    assert p == oracle.compress(z, eb, forced=forced)
