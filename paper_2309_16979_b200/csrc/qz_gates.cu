@@ -684,6 +684,19 @@ GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_
         members.push_back(ui);
     }
     close();
+    if (getenv("QZ_TRACE") && getenv("QZ_TRACE")[0] == '2') {
+        for (const PassDesc &pd : plan.passes) {
+            uint32_t nf = 0, npd = 0, nrel = 0;
+            for (uint32_t gi = pd.first_group; gi < pd.first_group + pd.ngroups; ++gi) {
+                nf += plan.groups[gi].nfast;
+                nrel += plan.groups[gi].relaxed;
+                for (uint32_t q = 0; q < plan.groups[gi].nfast; ++q)
+                    npd += plan.gates[plan.groups[gi].first_fast + q].op == OP_PDIAG;
+            }
+            fprintf(stderr, "qz plan: kind %u tmask %#llx groups %u (relaxed %u) fast ops %u pdiag %u gates %u\n",
+                    pd.kind, (unsigned long long)pd.tmask, pd.ngroups, nrel, nf, npd, pd.ngates);
+        }
+    }
     return plan;
 }
 
@@ -1577,14 +1590,21 @@ __device__ __forceinline__ uint64_t permute_bits(uint64_t x, const uint8_t *perm
     return y;
 }
 
+// smem slot of local index l in a swap tile: XOR the low 5 bits with the next
+// 5 so both the contiguous fill and the permuted gather spread over banks
+__device__ __forceinline__ uint32_t swz10(uint32_t l) { return l ^ ((l >> kSwapLow) & 31u); }
+
 __global__ void __launch_bounds__(256) tile_swaps(double2 *__restrict__ buf, uint32_t nbits,
                                                   PassDesc pd, uint32_t *__restrict__ flag,
                                                   const uint32_t *__restrict__ cond) {
     if (cond && *cond == 0) return;
+    constexpr uint32_t kMaxTile = 1u << (2 * kSwapLow);
+    constexpr uint32_t kChunks = 8;   // tile index split in 5-bit chunks (<= 40 bits)
     __shared__ uint8_t perm[48];
-    __shared__ uint16_t lperm[1u << (2 * kSwapLow)];
-    __shared__ uint64_t loff[1u << (2 * kSwapLow)];
-    __shared__ __align__(16) double2 ta[1u << (2 * kSwapLow)], tb[1u << (2 * kSwapLow)];
+    __shared__ uint16_t lperm[kMaxTile];
+    __shared__ uint64_t loff[kMaxTile];
+    __shared__ uint64_t dtab[kChunks][32], ptab[kChunks][32];   // deposit / permuted deposit
+    __shared__ __align__(16) double2 ta[kMaxTile], tb[kMaxTile];
     const uint32_t tid = threadIdx.x, nth = blockDim.x;
     const uint32_t L = min(kSwapLow, nbits);
     uint64_t smask = (uint64_t(1) << L) - 1;
@@ -1597,41 +1617,50 @@ __global__ void __launch_bounds__(256) tile_swaps(double2 *__restrict__ buf, uin
     for (uint32_t l = tid; l < tile; l += nth) {
         const uint64_t off = deposit_bits(l, smask);
         const uint64_t img = permute_bits(off, perm, nbits);
-        // compress img back to local bits
         uint32_t li = 0, i = 0;
         for (uint64_t m = smask; m; m &= m - 1, ++i)
             if (img & (m & (0 - m))) li |= 1u << i;
         lperm[l] = uint16_t(li);
         loff[l] = off;
     }
+    // tile index -> base / partner base, 5 index bits per table (GF(2)-linear)
+    for (uint32_t e = tid; e < kChunks * 32; e += nth) {
+        const uint32_t c = e >> 5, v = e & 31;
+        const uint64_t dep = deposit_bits(uint64_t(v) << (5 * c), cmask);
+        dtab[c][v] = dep;
+        ptab[c][v] = permute_bits(dep, perm, nbits);
+    }
     __syncthreads();
     const uint64_t ntiles = uint64_t(1) << (nbits - ks);
-    const uint64_t dstep = deposit_bits(gridDim.x, cmask);
-    uint64_t base = deposit_bits(blockIdx.x, cmask);
-    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, base = ((base | ~cmask) + dstep) & cmask) {
-        const uint64_t pbase = permute_bits(base, perm, nbits);
+    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        uint64_t base = 0, pbase = 0;
+#pragma unroll
+        for (uint32_t c = 0; c < kChunks; ++c) {
+            const uint32_t v = uint32_t(t >> (5 * c)) & 31u;
+            base |= dtab[c][v];
+            pbase |= ptab[c][v];
+        }
         if (pbase < base) continue;   // the partner tile's CTA moves this pair
         const bool pair = pbase != base;
         uint32_t neg0 = 0;
         for (uint32_t l = tid; l < tile; l += nth) {
             const uint64_t off = loff[l];
             const double2 a = __ldcs(buf + base + off);
-            ta[l] = a;
+            double2 b = make_double2(0.0, 0.0);
+            if (pair) b = __ldcs(buf + pbase + off);
+            ta[swz10(l)] = a;
+            tb[swz10(l)] = b;
             neg0 |= uint32_t(__double_as_longlong(a.x) == (long long)0x8000000000000000ULL) |
-                    uint32_t(__double_as_longlong(a.y) == (long long)0x8000000000000000ULL);
-            if (pair) {
-                const double2 b = __ldcs(buf + pbase + off);
-                tb[l] = b;
-                neg0 |= uint32_t(__double_as_longlong(b.x) == (long long)0x8000000000000000ULL) |
-                        uint32_t(__double_as_longlong(b.y) == (long long)0x8000000000000000ULL);
-            }
+                    uint32_t(__double_as_longlong(a.y) == (long long)0x8000000000000000ULL) |
+                    uint32_t(__double_as_longlong(b.x) == (long long)0x8000000000000000ULL) |
+                    uint32_t(__double_as_longlong(b.y) == (long long)0x8000000000000000ULL);
         }
         if (__syncthreads_or(neg0)) {
             if (tid == 0) *flag = 1u;
         }
         for (uint32_t l = tid; l < tile; l += nth) {
             const uint64_t off = loff[l];
-            const uint32_t src = lperm[l];
+            const uint32_t src = swz10(lperm[l]);
             if (pair) {
                 __stcs(buf + base + off, tb[src]);
                 __stcs(buf + pbase + off, ta[src]);
