@@ -142,6 +142,19 @@ __global__ void k_account(int64_t *acct, const int64_t *prefix, const int64_t *m
     acct[0] = cur + prefix[nslots - 1];
 }
 
+// Export: copy every chunk's payload to its place in chunk order (warp per
+// chunk, 16 B vector stores where aligned).
+__global__ void k_pack_payloads(const uint8_t *__restrict__ arena, ChunkTable t, const uint64_t *__restrict__ dst_off,
+                                uint64_t nchunks, uint8_t *__restrict__ out) {
+    const uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    if (w >= nchunks) return;
+    const uint8_t *src = arena + t.off[w];
+    uint8_t *dst = out + dst_off[w];
+    const uint32_t n = t.len[w];
+    for (uint32_t i = lane; i < n; i += 32) dst[i] = src[i];
+}
+
 __global__ void k_io_count(const uint64_t *soff, const uint64_t *padded, uint64_t nslots,
                            uint64_t *io) {
     atomicAdd((unsigned long long *)&io[0], (unsigned long long)(soff[nslots - 1] + padded[nslots - 1]));
@@ -1246,20 +1259,45 @@ int qzc_sim_payload_bytes(qzc_sim *sim, uint64_t *total_out) {
 
 int qzc_sim_export(qzc_sim *sim, uint8_t *payload_out, uint64_t cap, uint32_t *sizes, uint32_t *crcs) {
     QZ_API_BEGIN
-    QZ_CUDA(cudaSetDevice(sim->ctx->device));
-    std::vector<uint64_t> off;
-    std::vector<uint32_t> len, crc;
-    std::vector<uint8_t> arena;
-    pull_store(sim, off, len, crc, arena);
-    uint64_t pos = 0;
-    for (uint64_t i = 0; i < sim->nchunks; ++i) {
-        if (payload_out) {
-            if (pos + len[i] > cap) throw Failure(QZC_EINVAL, "export buffer too small");
-            std::memcpy(payload_out + pos, arena.data() + off[i], len[i]);
-        }
-        pos += len[i];
-        if (sizes) sizes[i] = len[i];
-        if (crcs) crcs[i] = crc[i];
+    qzc_context *ctx = sim->ctx;
+    QZ_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    const int a = sim->cur;
+    const uint64_t nc = sim->nchunks;
+    std::vector<uint32_t> len(nc), crc(nc);
+    QZ_CUDA(cudaMemcpyAsync(len.data(), sim->len[a].p, 4 * nc, cudaMemcpyDeviceToHost, s));
+    QZ_CUDA(cudaMemcpyAsync(crc.data(), sim->crc[a].p, 4 * nc, cudaMemcpyDeviceToHost, s));
+    QZ_CUDA(cudaStreamSynchronize(s));
+    std::vector<uint64_t> dst(nc);
+    uint64_t total = 0;
+    for (uint64_t i = 0; i < nc; ++i) {
+        dst[i] = total;
+        total += len[i];
+    }
+    if (sizes) std::memcpy(sizes, len.data(), 4 * nc);
+    if (crcs) std::memcpy(crcs, crc.data(), 4 * nc);
+    if (payload_out && total > cap) throw Failure(QZC_EINVAL, "export buffer too small");
+    if (payload_out && sim->host_res) {
+        // the store already lives in host memory
+        std::vector<uint64_t> off(nc);
+        QZ_CUDA(cudaMemcpy(off.data(), sim->off[a].p, 8 * nc, cudaMemcpyDeviceToHost));
+        for (uint64_t i = 0; i < nc; ++i) std::memcpy(payload_out + dst[i], sim->harena[a] + off[i], len[i]);
+    } else if (payload_out) {
+        // pack the payloads in chunk order in HBM (the idle window's encode
+        // scratch when it is large enough), then one device->host copy
+        DevBuf tmp;
+        const uint64_t need = ((total + 15) & ~uint64_t(15)) + 8 * nc;
+        uint8_t *stage = sim->win.scratch.cap >= need ? sim->win.scratch.as<uint8_t>()
+                                                      : (tmp.ensure(need), tmp.as<uint8_t>());
+        uint64_t *doff = reinterpret_cast<uint64_t *>(stage + ((total + 15) & ~uint64_t(15)));
+        QZ_CUDA(cudaMemcpyAsync(doff, dst.data(), 8 * nc, cudaMemcpyHostToDevice, s));
+        k_pack_payloads<<<(unsigned)ceil_div(nc * 32, 256), 256, 0, s>>>(sim->arena_ptr(a), sim->table(a), doff,
+                                                                          nc, stage);
+        QZ_CHECK_LAUNCH();
+        ++ctx->launches;
+        QZ_CUDA(cudaMemcpyAsync(payload_out, stage, total, cudaMemcpyDeviceToHost, s));
+        QZ_CUDA(cudaStreamSynchronize(s));
+        sim->stats.d2h_bytes += total + 8 * nc;
     }
     QZ_API_END
 }

@@ -181,6 +181,18 @@ class Engine:
         _check(self.lib.qzc_timer_end(self.h, C.byref(out)))
         return out.value
 
+    def pinned(self, nbytes: int, dtype=np.uint8) -> np.ndarray:
+        """Page-locked host array (qzc_host_alloc), freed with the array."""
+        h = C.c_void_p()
+        _check(self.lib.qzc_host_alloc(self.h, max(int(nbytes), 1), C.byref(h)))
+        count = max(int(nbytes), 1) // np.dtype(dtype).itemsize
+        raw = (C.c_uint8 * max(int(nbytes), 1)).from_address(h.value)
+        arr = np.frombuffer(raw, dtype=dtype, count=count)
+        lib, eh, ptr = self.lib, self.h, h.value
+        import weakref
+        weakref.finalize(raw, lib.qzc_host_free, eh, C.c_void_p(ptr))
+        return arr
+
     def host_link_gbps(self, nbytes: int = 1 << 30, reps: int = 5) -> dict:
         """Pinned cudaMemcpyAsync H2D / D2H bandwidth (the host-link roofline
         of the host-staged residency), CUDA-event timed, best of `reps`."""
@@ -367,14 +379,20 @@ class Simulator:
         _check(self.lib.qzc_sim_payload_bytes(self.h, C.byref(out)))
         return out.value
 
-    def export(self):
+    def export(self, out=None, sizes=None, crcs=None):
+        """The store's payloads in chunk order, sizes and CRCs.  Without `out`
+        the payloads come back as bytes; with `out` (a writable uint8 array,
+        e.g. Engine.pinned(...), reused across calls) they are written into it
+        and a view of the used prefix is returned — no host-side copy."""
         total = self.payload_bytes()
-        buf = np.zeros(max(total, 1), dtype=np.uint8)
-        sizes = np.zeros(self.chunk_count, dtype=np.uint32)
-        crcs = np.zeros(self.chunk_count, dtype=np.uint32)
+        buf = np.empty(max(total, 1), dtype=np.uint8) if out is None else out
+        if buf.size < total:
+            raise ValueError(f"export buffer holds {buf.size} bytes, the store needs {total}")
+        sizes = np.empty(self.chunk_count, dtype=np.uint32) if sizes is None else sizes
+        crcs = np.empty(self.chunk_count, dtype=np.uint32) if crcs is None else crcs
         _check(self.lib.qzc_sim_export(self.h, buf.ctypes.data_as(u8p), buf.size,
                                        sizes.ctypes.data_as(u32p), crcs.ctypes.data_as(u32p)))
-        return buf[:total].tobytes(), sizes, crcs
+        return (buf[:total].tobytes() if out is None else buf[:total]), sizes, crcs
 
     def import_(self, payload: bytes, sizes, crcs) -> None:
         buf = np.frombuffer(payload, dtype=np.uint8).copy() if payload else np.zeros(1, np.uint8)

@@ -281,3 +281,16 @@ def test_swap_network_pass_bit_exact(engine, oracle, seed, neg_zero):
         assert sim.stats()["replays"] >= 1
     elif seed % 2 == 0:
         assert sim.stats()["replays"] == 0
+
+
+def test_export_into_pinned_buffer(engine, oracle, golden):
+    rec = golden["runs"][0]
+    g = circuit(golden, oracle, rec["circuit"])
+    sim = run_sim(engine, rec["n"], rec["c"], rec["m"], rec["eb"], g)
+    blob, sizes, crcs = sim.export()
+    out = engine.pinned(len(blob) + 100)
+    view, s2, c2 = sim.export(out, engine.pinned(4 * sim.chunk_count, np.uint32),
+                              engine.pinned(4 * sim.chunk_count, np.uint32))
+    assert view.tobytes() == blob and (s2 == sizes).all() and (c2 == crcs).all()
+    with pytest.raises(ValueError):
+        sim.export(engine.pinned(8))
