@@ -596,6 +596,11 @@ GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_
                     if (K(0) == CK_REAL && K(1) == CK_IMAG && K(2) == CK_IMAG && K(3) == CK_REAL) t.pad2 = 3 + chk;
                     else if (K(0) == CK_REAL && K(1) == CK_REAL && K(2) == CK_REAL && K(3) == CK_REAL) t.pad2 = 4 + chk;
                     else if (K(0) == CK_CPLX && K(1) == CK_CPLX && K(2) == CK_CPLX && K(3) == CK_CPLX) t.pad2 = 5 + chk;
+                    // X, Y, U3 / U2 shapes
+                    else if (K(0) == CK_ZERO && K(1) == CK_ONE && K(2) == CK_ONE && K(3) == CK_ZERO) t.pad2 = 21 + chk;
+                    else if (K(0) == CK_ZERO && K(1) == CK_IMAG && K(2) == CK_IMAG && K(3) == CK_ZERO) t.pad2 = 22 + chk;
+                    else if (K(0) == CK_REAL && K(1) == CK_CPLX && K(2) == CK_CPLX && K(3) == CK_CPLX) t.pad2 = 23 + chk;
+                    else if (K(0) == CK_REAL && K(1) == CK_CPLX && K(2) == CK_REAL && K(3) == CK_CPLX) t.pad2 = 24 + chk;
                 } else if (t.op == OP_CP5 && (t.srow & 7) == 7 && K(0) == CK_CPLX && K(1) == CK_CPLX &&
                            K(2) == CK_CPLX) {
                     t.pad2 = 6;
@@ -759,6 +764,11 @@ constexpr int NB = 1 << kRegBits;   // amplitudes per thread register block
 
 __device__ __forceinline__ bool dz(double x) { return (__double_as_longlong(x) << 1) == 0; }
 __device__ __forceinline__ bool zc(double2 v) { return dz(v.x) | dz(v.y); }
+// a -0 component: the fast path's +0-safe rows may not see it (group redo)
+__device__ __forceinline__ bool nz0(double2 v) {
+    return (__double_as_longlong(v.x) == (long long)0x8000000000000000ULL) |
+           (__double_as_longlong(v.y) == (long long)0x8000000000000000ULL);
+}
 __device__ __forceinline__ double dneg(double x) {
     return __longlong_as_double(__double_as_longlong(x) ^ (long long)0x8000000000000000ULL);
 }
@@ -963,15 +973,25 @@ __device__ __forceinline__ void fast_diag(double2 (&v)[NB], const TileGate &g, b
 #pragma unroll
     for (int p = 0; p < NB / 2; ++p) {
         const int i = izb(p, R), j = i | sh;
+        const double2 a = v[i], b = v[j];
+        // a zero in a row that is not +0-safe: that row's exact value
         if (K0 == CK_ONE || (K0 < 0 && k00 == CK_ONE)) {
         } else {
-            v[i] = termk<K0>(k00, m00, v[i]);
-            if (u0) bad |= zc(v[i]);
+            double2 o = termk<K0>(k00, m00, a);
+            if (u0 && zc(o)) {
+                o = slow2(g, 0, a, b);
+                bad |= nz0(o);
+            }
+            v[i] = o;
         }
         if (K1 == CK_ONE || (K1 < 0 && k11 == CK_ONE)) {
         } else {
-            v[j] = termk<K1>(k11, m11, v[j]);
-            if (u1) bad |= zc(v[j]);
+            double2 o = termk<K1>(k11, m11, b);
+            if (u1 && zc(o)) {
+                o = slow2(g, 1, a, b);
+                bad |= nz0(o);
+            }
+            v[j] = o;
         }
     }
 }
@@ -988,19 +1008,35 @@ __device__ __forceinline__ void fast_gen1(double2 (&v)[NB], const TileGate &g, b
         const double2 a = v[i], b = v[j];
         double2 oi, oj;
         if constexpr (SPEC) {
-            oi = sum2(termk<K00>(k00, m00, a), termk<K01>(k01, m01, b));
-            oj = sum2(termk<K10>(k10, m10, a), termk<K11>(k11, m11, b));
+            if constexpr (K00 == CK_ZERO) oi = termk<K01>(k01, m01, b);
+            else if constexpr (K01 == CK_ZERO) oi = termk<K00>(k00, m00, a);
+            else oi = sum2(termk<K00>(k00, m00, a), termk<K01>(k01, m01, b));
+            if constexpr (K10 == CK_ZERO) oj = termk<K11>(k11, m11, b);
+            else if constexpr (K11 == CK_ZERO) oj = termk<K10>(k10, m10, a);
+            else oj = sum2(termk<K10>(k10, m10, a), termk<K11>(k11, m11, b));
             if constexpr (SPEC == 2) {   // compile-time kinds, rows not all +0-safe
-                if (!(g.srow & 1)) bad |= zc(oi);
-                if (!(g.srow & 2)) bad |= zc(oj);
+                if (!(g.srow & 1) && zc(oi)) {
+                    oi = slow2(g, 0, a, b);
+                    bad |= nz0(oi);
+                }
+                if (!(g.srow & 2) && zc(oj)) {
+                    oj = slow2(g, 1, a, b);
+                    bad |= nz0(oj);
+                }
             }
         } else {
             oi = k00 == CK_ZERO ? term(k01, m01, b)
                : (k01 == CK_ZERO ? term(k00, m00, a) : sum2(term(k00, m00, a), term(k01, m01, b)));
             oj = k10 == CK_ZERO ? term(k11, m11, b)
                : (k11 == CK_ZERO ? term(k10, m10, a) : sum2(term(k10, m10, a), term(k11, m11, b)));
-            if (!(g.srow & 1)) bad |= zc(oi);
-            if (!(g.srow & 2)) bad |= zc(oj);
+            if (!(g.srow & 1) && zc(oi)) {
+                oi = slow2(g, 0, a, b);
+                bad |= nz0(oi);
+            }
+            if (!(g.srow & 2) && zc(oj)) {
+                oj = slow2(g, 1, a, b);
+                bad |= nz0(oj);
+            }
         }
         v[i] = oi;
         v[j] = oj;
@@ -1019,12 +1055,20 @@ __device__ __forceinline__ void fast_cx(double2 (&v)[NB]) {
 }
 
 template <int A, int B>
-__device__ __forceinline__ void fast_cz(double2 (&v)[NB], bool &bad) {
+__device__ __forceinline__ void fast_cz(double2 (&v)[NB], const TileGate &g, bool &bad) {
 #pragma unroll
     for (int i = 0; i < NB; ++i)
         if (((i >> A) & 1) && ((i >> B) & 1)) {
-            v[i] = make_double2(dneg(v[i].x), dneg(v[i].y));
-            bad |= zc(v[i]);   // the -1 row is not +0-safe
+            const double2 o = make_double2(dneg(v[i].x), dneg(v[i].y));
+            if (zc(o)) {
+                // the -1 row is not +0-safe: its exact value (the other three
+                // products are +-0; their order does not matter for zeros)
+                const int i00 = i & ~((1 << A) | (1 << B));
+                v[i] = slow4(g, 3, v[i00], v[i00 | (1 << A)], v[i00 | (1 << B)], v[i]);
+                bad |= nz0(v[i]);
+            } else {
+                v[i] = o;
+            }
         }
 }
 
@@ -1204,6 +1248,14 @@ __device__ __forceinline__ void fast_apply(double2 (&v)[NB], const TileGate &g, 
         case 13: fast_gen1<a, CK_REAL, CK_IMAG, CK_IMAG, CK_REAL, 2>(v, g, bad); break;      \
         case 14: fast_gen1<a, CK_REAL, CK_REAL, CK_REAL, CK_REAL, 2>(v, g, bad); break;      \
         case 15: fast_gen1<a, CK_CPLX, CK_CPLX, CK_CPLX, CK_CPLX, 2>(v, g, bad); break;      \
+        case 21: fast_gen1<a, CK_ZERO, CK_ONE, CK_ONE, CK_ZERO, 1>(v, g, bad); break;        \
+        case 22: fast_gen1<a, CK_ZERO, CK_IMAG, CK_IMAG, CK_ZERO, 1>(v, g, bad); break;      \
+        case 23: fast_gen1<a, CK_REAL, CK_CPLX, CK_CPLX, CK_CPLX, 1>(v, g, bad); break;      \
+        case 24: fast_gen1<a, CK_REAL, CK_CPLX, CK_REAL, CK_CPLX, 1>(v, g, bad); break;      \
+        case 31: fast_gen1<a, CK_ZERO, CK_ONE, CK_ONE, CK_ZERO, 2>(v, g, bad); break;        \
+        case 32: fast_gen1<a, CK_ZERO, CK_IMAG, CK_IMAG, CK_ZERO, 2>(v, g, bad); break;      \
+        case 33: fast_gen1<a, CK_REAL, CK_CPLX, CK_CPLX, CK_CPLX, 2>(v, g, bad); break;      \
+        case 34: fast_gen1<a, CK_REAL, CK_CPLX, CK_REAL, CK_CPLX, 2>(v, g, bad); break;      \
         default:                                                                             \
             if (op == OP_DIAG) fast_diag<a>(v, g, bad);                                      \
             else fast_gen1<a>(v, g, bad);                                                    \
@@ -1249,7 +1301,7 @@ __device__ __forceinline__ void fast_apply(double2 (&v)[NB], const TileGate &g, 
     } else if (op == OP_CZ) {
         switch (lo * 4 + hi) {
 #define X(a, b)                                                                              \
-    case a * 4 + b: fast_cz<a, b>(v, bad); break;
+    case a * 4 + b: fast_cz<a, b>(v, g, bad); break;
             QZ_PAIRS(X)
 #undef X
         default: break;
