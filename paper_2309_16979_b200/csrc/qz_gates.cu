@@ -341,6 +341,42 @@ static bool unit_safe(const std::vector<DevGate> &G, const Unit &u) {
     return true;
 }
 
+// Case id of a fast-list op: mirrors the device switch in fast_case().
+static uint32_t case_id(const TileGate &t) {
+    static const uint32_t gen_codes[14] = {3, 4, 5, 13, 14, 15, 21, 22, 23, 24, 31, 32, 33, 34};
+    auto pair_idx = [](uint32_t a, uint32_t b) {
+        static const uint32_t P[3][3] = {{99, 0, 1}, {2, 99, 3}, {4, 5, 99}};
+        return P[a][b];
+    };
+    auto lohi_idx = [](uint32_t a, uint32_t b) {
+        const uint32_t lo = std::min(a, b), hi = std::max(a, b);
+        return lo == 0 ? (hi == 1 ? 0u : 1u) : 2u;
+    };
+    switch (t.op) {
+    case OP_PDIAG: {
+        const uint32_t R = t.nq ? t.r0 : 3;
+        if (t.run) return R;
+        return 4 + R * 2 + (t.pad2 == 8 ? 1 : 0);
+    }
+    case OP_DIAG: {
+        const uint32_t vi = t.pad2 == 1 ? 0 : t.pad2 == 2 ? 1 : t.pad2 == 11 ? 2 : t.pad2 == 12 ? 3 : 4;
+        return 12 + t.r0 * 5 + vi;
+    }
+    case OP_GEN1: {
+        uint32_t gi = 14;
+        for (uint32_t i = 0; i < 14; ++i)
+            if (t.pad2 == gen_codes[i]) gi = i;
+        return 27 + t.r0 * 15 + gi;
+    }
+    case OP_CP5: return 72 + pair_idx(t.r0, t.r1) * 2 + (t.pad2 == 6 ? 1 : 0);
+    case OP_CXD: return 84 + pair_idx(t.r0, t.r1) * 2 + (t.pad2 == 7 ? 1 : 0);
+    case OP_CX: return 96 + pair_idx(t.r0, t.r1);
+    case OP_CZ: return 102 + lohi_idx(t.r0, t.r1);
+    case OP_SWAP: return 105 + lohi_idx(t.r0, t.r1);
+    default: return 1000;   // exact path only
+    }
+}
+
 GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_t kmax, bool fuse,
                       bool relax) {
     GatePlan plan;
@@ -622,6 +658,7 @@ GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_
                     }
                 }
             }
+            for (size_t q = gd.first_fast; q < plan.gates.size(); ++q) plan.gates[q].cid = case_id(plan.gates[q]);
             plan.groups.push_back(gd);
             plan.groups.back().nfast = (uint32_t)plan.gates.size() - gd.first_fast;
             gmembers.clear();
@@ -1187,137 +1224,148 @@ __device__ __forceinline__ void pdiag_spec(double2 (&v)[NB], const double2 *__re
     }
 }
 
-// n consecutive such ops on the same register selector (the switch is
-// hoisted out of the loop: one code path, no register shuffling per op).
-__device__ __forceinline__ void run_pdiag(double2 (&v)[NB], const TileGate *__restrict__ gp,
-                                          uint32_t n, uint64_t gidx) {
-    switch (gp->nq ? gp->r0 : uint32_t(kRegBits)) {
-#define X(a)                                                                                 \
-    case a:                                                                                  \
-        for (uint32_t q = 0; q < n; ++q) {                                                   \
-            const TileGate &g = gp[q];                                                       \
-            const uint32_t var =                                                             \
-                uint32_t((gidx >> g.ob0) & 1) | (uint32_t((gidx >> g.ob1) & 1) << 1);         \
-            pdiag_spec<a>(v, g.m + 4 * var, (g.steps >> (4 * var)) & 15u);                   \
-        }                                                                                    \
-        break;
-        QZ_R1_CASES(X)
-        X(kRegBits)
-#undef X
-    default: break;
-    }
-}
-
 #if QZ_REG_BITS == 3
 #define QZ_PAIRS(X) X(0, 1) X(0, 2) X(1, 2)
 #else
 #define QZ_PAIRS(X) X(0, 1) X(0, 2) X(0, 3) X(1, 2) X(1, 3) X(2, 3)
 #endif
 
-// Returns false if the gate could not be taken on the fast path at all.
-__device__ __forceinline__ void fast_apply(double2 (&v)[NB], const TileGate &g, uint64_t gidx,
-                                           bool &bad) {
-    const uint32_t op = g.op;
-    if (op == OP_PDIAG) {
-        const uint32_t var = uint32_t((gidx >> g.ob0) & 1) | (uint32_t((gidx >> g.ob1) & 1) << 1);
-        switch (g.nq ? g.r0 : uint32_t(kRegBits)) {
-#define X(a)                                                                                 \
-    case a:                                                                                  \
-        if (g.pad2 == 8) fast_pdiag<a, 1>(v, g, var, bad);                                   \
-        else fast_pdiag<a>(v, g, var, bad);                                                  \
-        break;
-            QZ_R1_CASES(X)
-            X(kRegBits)
-#undef X
-        default: break;
-        }
-        return;
-    }
-    if (op == OP_DIAG || op == OP_GEN1) {
-        switch (g.r0) {
-#define X(a)                                                                                 \
-    case a:                                                                                  \
-        switch (g.pad2) {                                                                    \
-        case 1: fast_diag<a, CK_ONE, CK_CPLX, 1>(v, g, bad); break;                          \
-        case 2: fast_diag<a, CK_CPLX, CK_CPLX, 1>(v, g, bad); break;                         \
-        case 11: fast_diag<a, CK_ONE, CK_CPLX, 2>(v, g, bad); break;                         \
-        case 12: fast_diag<a, CK_CPLX, CK_CPLX, 2>(v, g, bad); break;                        \
-        case 3: fast_gen1<a, CK_REAL, CK_IMAG, CK_IMAG, CK_REAL, 1>(v, g, bad); break;       \
-        case 4: fast_gen1<a, CK_REAL, CK_REAL, CK_REAL, CK_REAL, 1>(v, g, bad); break;       \
-        case 5: fast_gen1<a, CK_CPLX, CK_CPLX, CK_CPLX, CK_CPLX, 1>(v, g, bad); break;       \
-        case 13: fast_gen1<a, CK_REAL, CK_IMAG, CK_IMAG, CK_REAL, 2>(v, g, bad); break;      \
-        case 14: fast_gen1<a, CK_REAL, CK_REAL, CK_REAL, CK_REAL, 2>(v, g, bad); break;      \
-        case 15: fast_gen1<a, CK_CPLX, CK_CPLX, CK_CPLX, CK_CPLX, 2>(v, g, bad); break;      \
-        case 21: fast_gen1<a, CK_ZERO, CK_ONE, CK_ONE, CK_ZERO, 1>(v, g, bad); break;        \
-        case 22: fast_gen1<a, CK_ZERO, CK_IMAG, CK_IMAG, CK_ZERO, 1>(v, g, bad); break;      \
-        case 23: fast_gen1<a, CK_REAL, CK_CPLX, CK_CPLX, CK_CPLX, 1>(v, g, bad); break;      \
-        case 24: fast_gen1<a, CK_REAL, CK_CPLX, CK_REAL, CK_CPLX, 1>(v, g, bad); break;      \
-        case 31: fast_gen1<a, CK_ZERO, CK_ONE, CK_ONE, CK_ZERO, 2>(v, g, bad); break;        \
-        case 32: fast_gen1<a, CK_ZERO, CK_IMAG, CK_IMAG, CK_ZERO, 2>(v, g, bad); break;      \
-        case 33: fast_gen1<a, CK_REAL, CK_CPLX, CK_CPLX, CK_CPLX, 2>(v, g, bad); break;      \
-        case 34: fast_gen1<a, CK_REAL, CK_CPLX, CK_REAL, CK_CPLX, 2>(v, g, bad); break;      \
-        default:                                                                             \
-            if (op == OP_DIAG) fast_diag<a>(v, g, bad);                                      \
-            else fast_gen1<a>(v, g, bad);                                                    \
-        }                                                                                    \
-        break;
-            QZ_R1_CASES(X)
-#undef X
-        default: break;
-        }
-        return;
-    }
-    const uint32_t lo = min(g.r0, g.r1), hi = max(g.r0, g.r1);
-    if (op == OP_CP5) {
-        switch (g.r0 * 4 + g.r1) {
-#define X(a, b)                                                                              \
-    case a * 4 + b:                                                                          \
-        if (g.pad2 == 6) fast_cp5<a, b, 1>(v, g, bad);                                       \
-        else fast_cp5<a, b>(v, g, bad);                                                      \
-        break;
-            QZ_R2_CASES(X)
-#undef X
-        default: break;
-        }
-    } else if (op == OP_CXD) {
-        switch (g.r0 * 4 + g.r1) {
-#define X(a, b)                                                                              \
-    case a * 4 + b:                                                                          \
-        if (g.pad2 == 7) fast_cxd<a, b, 1>(v, g, bad);                                       \
-        else fast_cxd<a, b>(v, g, bad);                                                      \
-        break;
-            QZ_R2_CASES(X)
-#undef X
-        default: break;
-        }
-    } else if (op == OP_CX) {
-        switch (g.r0 * 4 + g.r1) {
-#define X(a, b)                                                                              \
-    case a * 4 + b: fast_cx<a, b>(v); break;
-            QZ_R2_CASES(X)
-#undef X
-        default: break;
-        }
-    } else if (op == OP_CZ) {
-        switch (lo * 4 + hi) {
-#define X(a, b)                                                                              \
-    case a * 4 + b: fast_cz<a, b>(v, g, bad); break;
-            QZ_PAIRS(X)
-#undef X
-        default: break;
-        }
-    } else if (op == OP_SWAP) {
-        switch (lo * 4 + hi) {
-#define X(a, b)                                                                              \
-    case a * 4 + b: fast_swap<a, b>(v); break;
-            QZ_PAIRS(X)
-#undef X
-        default: break;
-        }
-    } else {
-        bad = true;  // other 2q matrices: exact path only
+// Flat dispatch: one jump table over a host-computed case id (case_id(),
+// which mirrors this switch), so every op leaves the register block in the
+// same registers.  Returns the number of fast-list entries consumed.
+__device__ __forceinline__ uint32_t pdiag_var(const TileGate &g, uint64_t gidx) {
+    return uint32_t((gidx >> g.ob0) & 1) | (uint32_t((gidx >> g.ob1) & 1) << 1);
+}
+
+template <int R>
+__device__ __forceinline__ void run_pdiag_r(double2 (&v)[NB], const TileGate *__restrict__ gp,
+                                            uint32_t n, uint64_t gidx) {
+    for (uint32_t q = 0; q < n; ++q) {
+        const TileGate &g = gp[q];
+        const uint32_t var = pdiag_var(g, gidx);
+        pdiag_spec<R>(v, g.m + 4 * var, (g.steps >> (4 * var)) & 15u);
     }
 }
+
+__device__ __forceinline__ uint32_t fast_case(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q,
+                                              uint64_t gidx, bool &bad) {
+    const TileGate &g = fp[q];
+    switch (g.cid) {
+    case 0: run_pdiag_r<0>(v, fp + q, g.run, gidx); return g.run;
+    case 1: run_pdiag_r<1>(v, fp + q, g.run, gidx); return g.run;
+    case 2: run_pdiag_r<2>(v, fp + q, g.run, gidx); return g.run;
+    case 3: run_pdiag_r<3>(v, fp + q, g.run, gidx); return g.run;
+    case 4: fast_pdiag<0, 0>(v, g, pdiag_var(g, gidx), bad); return 1;
+    case 5: fast_pdiag<0, 1>(v, g, pdiag_var(g, gidx), bad); return 1;
+    case 6: fast_pdiag<1, 0>(v, g, pdiag_var(g, gidx), bad); return 1;
+    case 7: fast_pdiag<1, 1>(v, g, pdiag_var(g, gidx), bad); return 1;
+    case 8: fast_pdiag<2, 0>(v, g, pdiag_var(g, gidx), bad); return 1;
+    case 9: fast_pdiag<2, 1>(v, g, pdiag_var(g, gidx), bad); return 1;
+    case 10: fast_pdiag<3, 0>(v, g, pdiag_var(g, gidx), bad); return 1;
+    case 11: fast_pdiag<3, 1>(v, g, pdiag_var(g, gidx), bad); return 1;
+    case 12: fast_diag<0, CK_ONE, CK_CPLX, 1>(v, g, bad); return 1;
+    case 13: fast_diag<0, CK_CPLX, CK_CPLX, 1>(v, g, bad); return 1;
+    case 14: fast_diag<0, CK_ONE, CK_CPLX, 2>(v, g, bad); return 1;
+    case 15: fast_diag<0, CK_CPLX, CK_CPLX, 2>(v, g, bad); return 1;
+    case 16: fast_diag<0>(v, g, bad); return 1;
+    case 17: fast_diag<1, CK_ONE, CK_CPLX, 1>(v, g, bad); return 1;
+    case 18: fast_diag<1, CK_CPLX, CK_CPLX, 1>(v, g, bad); return 1;
+    case 19: fast_diag<1, CK_ONE, CK_CPLX, 2>(v, g, bad); return 1;
+    case 20: fast_diag<1, CK_CPLX, CK_CPLX, 2>(v, g, bad); return 1;
+    case 21: fast_diag<1>(v, g, bad); return 1;
+    case 22: fast_diag<2, CK_ONE, CK_CPLX, 1>(v, g, bad); return 1;
+    case 23: fast_diag<2, CK_CPLX, CK_CPLX, 1>(v, g, bad); return 1;
+    case 24: fast_diag<2, CK_ONE, CK_CPLX, 2>(v, g, bad); return 1;
+    case 25: fast_diag<2, CK_CPLX, CK_CPLX, 2>(v, g, bad); return 1;
+    case 26: fast_diag<2>(v, g, bad); return 1;
+    case 27: fast_gen1<0, CK_REAL, CK_IMAG, CK_IMAG, CK_REAL, 1>(v, g, bad); return 1;
+    case 28: fast_gen1<0, CK_REAL, CK_REAL, CK_REAL, CK_REAL, 1>(v, g, bad); return 1;
+    case 29: fast_gen1<0, CK_CPLX, CK_CPLX, CK_CPLX, CK_CPLX, 1>(v, g, bad); return 1;
+    case 30: fast_gen1<0, CK_REAL, CK_IMAG, CK_IMAG, CK_REAL, 2>(v, g, bad); return 1;
+    case 31: fast_gen1<0, CK_REAL, CK_REAL, CK_REAL, CK_REAL, 2>(v, g, bad); return 1;
+    case 32: fast_gen1<0, CK_CPLX, CK_CPLX, CK_CPLX, CK_CPLX, 2>(v, g, bad); return 1;
+    case 33: fast_gen1<0, CK_ZERO, CK_ONE, CK_ONE, CK_ZERO, 1>(v, g, bad); return 1;
+    case 34: fast_gen1<0, CK_ZERO, CK_IMAG, CK_IMAG, CK_ZERO, 1>(v, g, bad); return 1;
+    case 35: fast_gen1<0, CK_REAL, CK_CPLX, CK_CPLX, CK_CPLX, 1>(v, g, bad); return 1;
+    case 36: fast_gen1<0, CK_REAL, CK_CPLX, CK_REAL, CK_CPLX, 1>(v, g, bad); return 1;
+    case 37: fast_gen1<0, CK_ZERO, CK_ONE, CK_ONE, CK_ZERO, 2>(v, g, bad); return 1;
+    case 38: fast_gen1<0, CK_ZERO, CK_IMAG, CK_IMAG, CK_ZERO, 2>(v, g, bad); return 1;
+    case 39: fast_gen1<0, CK_REAL, CK_CPLX, CK_CPLX, CK_CPLX, 2>(v, g, bad); return 1;
+    case 40: fast_gen1<0, CK_REAL, CK_CPLX, CK_REAL, CK_CPLX, 2>(v, g, bad); return 1;
+    case 41: fast_gen1<0>(v, g, bad); return 1;
+    case 42: fast_gen1<1, CK_REAL, CK_IMAG, CK_IMAG, CK_REAL, 1>(v, g, bad); return 1;
+    case 43: fast_gen1<1, CK_REAL, CK_REAL, CK_REAL, CK_REAL, 1>(v, g, bad); return 1;
+    case 44: fast_gen1<1, CK_CPLX, CK_CPLX, CK_CPLX, CK_CPLX, 1>(v, g, bad); return 1;
+    case 45: fast_gen1<1, CK_REAL, CK_IMAG, CK_IMAG, CK_REAL, 2>(v, g, bad); return 1;
+    case 46: fast_gen1<1, CK_REAL, CK_REAL, CK_REAL, CK_REAL, 2>(v, g, bad); return 1;
+    case 47: fast_gen1<1, CK_CPLX, CK_CPLX, CK_CPLX, CK_CPLX, 2>(v, g, bad); return 1;
+    case 48: fast_gen1<1, CK_ZERO, CK_ONE, CK_ONE, CK_ZERO, 1>(v, g, bad); return 1;
+    case 49: fast_gen1<1, CK_ZERO, CK_IMAG, CK_IMAG, CK_ZERO, 1>(v, g, bad); return 1;
+    case 50: fast_gen1<1, CK_REAL, CK_CPLX, CK_CPLX, CK_CPLX, 1>(v, g, bad); return 1;
+    case 51: fast_gen1<1, CK_REAL, CK_CPLX, CK_REAL, CK_CPLX, 1>(v, g, bad); return 1;
+    case 52: fast_gen1<1, CK_ZERO, CK_ONE, CK_ONE, CK_ZERO, 2>(v, g, bad); return 1;
+    case 53: fast_gen1<1, CK_ZERO, CK_IMAG, CK_IMAG, CK_ZERO, 2>(v, g, bad); return 1;
+    case 54: fast_gen1<1, CK_REAL, CK_CPLX, CK_CPLX, CK_CPLX, 2>(v, g, bad); return 1;
+    case 55: fast_gen1<1, CK_REAL, CK_CPLX, CK_REAL, CK_CPLX, 2>(v, g, bad); return 1;
+    case 56: fast_gen1<1>(v, g, bad); return 1;
+    case 57: fast_gen1<2, CK_REAL, CK_IMAG, CK_IMAG, CK_REAL, 1>(v, g, bad); return 1;
+    case 58: fast_gen1<2, CK_REAL, CK_REAL, CK_REAL, CK_REAL, 1>(v, g, bad); return 1;
+    case 59: fast_gen1<2, CK_CPLX, CK_CPLX, CK_CPLX, CK_CPLX, 1>(v, g, bad); return 1;
+    case 60: fast_gen1<2, CK_REAL, CK_IMAG, CK_IMAG, CK_REAL, 2>(v, g, bad); return 1;
+    case 61: fast_gen1<2, CK_REAL, CK_REAL, CK_REAL, CK_REAL, 2>(v, g, bad); return 1;
+    case 62: fast_gen1<2, CK_CPLX, CK_CPLX, CK_CPLX, CK_CPLX, 2>(v, g, bad); return 1;
+    case 63: fast_gen1<2, CK_ZERO, CK_ONE, CK_ONE, CK_ZERO, 1>(v, g, bad); return 1;
+    case 64: fast_gen1<2, CK_ZERO, CK_IMAG, CK_IMAG, CK_ZERO, 1>(v, g, bad); return 1;
+    case 65: fast_gen1<2, CK_REAL, CK_CPLX, CK_CPLX, CK_CPLX, 1>(v, g, bad); return 1;
+    case 66: fast_gen1<2, CK_REAL, CK_CPLX, CK_REAL, CK_CPLX, 1>(v, g, bad); return 1;
+    case 67: fast_gen1<2, CK_ZERO, CK_ONE, CK_ONE, CK_ZERO, 2>(v, g, bad); return 1;
+    case 68: fast_gen1<2, CK_ZERO, CK_IMAG, CK_IMAG, CK_ZERO, 2>(v, g, bad); return 1;
+    case 69: fast_gen1<2, CK_REAL, CK_CPLX, CK_CPLX, CK_CPLX, 2>(v, g, bad); return 1;
+    case 70: fast_gen1<2, CK_REAL, CK_CPLX, CK_REAL, CK_CPLX, 2>(v, g, bad); return 1;
+    case 71: fast_gen1<2>(v, g, bad); return 1;
+    case 72: fast_cp5<0, 1>(v, g, bad); return 1;
+    case 73: fast_cp5<0, 1, 1>(v, g, bad); return 1;
+    case 74: fast_cp5<0, 2>(v, g, bad); return 1;
+    case 75: fast_cp5<0, 2, 1>(v, g, bad); return 1;
+    case 76: fast_cp5<1, 0>(v, g, bad); return 1;
+    case 77: fast_cp5<1, 0, 1>(v, g, bad); return 1;
+    case 78: fast_cp5<1, 2>(v, g, bad); return 1;
+    case 79: fast_cp5<1, 2, 1>(v, g, bad); return 1;
+    case 80: fast_cp5<2, 0>(v, g, bad); return 1;
+    case 81: fast_cp5<2, 0, 1>(v, g, bad); return 1;
+    case 82: fast_cp5<2, 1>(v, g, bad); return 1;
+    case 83: fast_cp5<2, 1, 1>(v, g, bad); return 1;
+    case 84: fast_cxd<0, 1>(v, g, bad); return 1;
+    case 85: fast_cxd<0, 1, 1>(v, g, bad); return 1;
+    case 86: fast_cxd<0, 2>(v, g, bad); return 1;
+    case 87: fast_cxd<0, 2, 1>(v, g, bad); return 1;
+    case 88: fast_cxd<1, 0>(v, g, bad); return 1;
+    case 89: fast_cxd<1, 0, 1>(v, g, bad); return 1;
+    case 90: fast_cxd<1, 2>(v, g, bad); return 1;
+    case 91: fast_cxd<1, 2, 1>(v, g, bad); return 1;
+    case 92: fast_cxd<2, 0>(v, g, bad); return 1;
+    case 93: fast_cxd<2, 0, 1>(v, g, bad); return 1;
+    case 94: fast_cxd<2, 1>(v, g, bad); return 1;
+    case 95: fast_cxd<2, 1, 1>(v, g, bad); return 1;
+    case 96: fast_cx<0, 1>(v); return 1;
+    case 97: fast_cx<0, 2>(v); return 1;
+    case 98: fast_cx<1, 0>(v); return 1;
+    case 99: fast_cx<1, 2>(v); return 1;
+    case 100: fast_cx<2, 0>(v); return 1;
+    case 101: fast_cx<2, 1>(v); return 1;
+    case 102: fast_cz<0, 1>(v, g, bad); return 1;
+    case 103: fast_cz<0, 2>(v, g, bad); return 1;
+    case 104: fast_cz<1, 2>(v, g, bad); return 1;
+    case 105: fast_swap<0, 1>(v); return 1;
+    case 106: fast_swap<0, 2>(v); return 1;
+    case 107: fast_swap<1, 2>(v); return 1;
+    default: bad = true; return 1;   // other 2q matrices: exact path only
+    }
+}
+
+#if QZ_REG_BITS != 3
+#error "the flat fast-path dispatch (fast_case / case_id) is generated for QZ_REG_BITS == 3"
+#endif
 
 // ---- sign-mask mode for all-zero register blocks ----
 __host__ __device__ constexpr uint32_t low_positions(int R) {
@@ -1587,16 +1635,7 @@ __global__ void __launch_bounds__(1 << (kTileBits - kRegBits), (kTileBits >= 12 
                 bool bad = !okblk;
                 path = okblk ? 3 : 4;
                 const TileGate *fp = gates + G.first_fast;
-                for (uint32_t q = 0; q < G.nfast && !bad;) {
-                    const uint32_t run = fp[q].run;
-                    if (run) {
-                        run_pdiag(v, fp + q, run, gidx);
-                        q += run;
-                    } else {
-                        fast_apply(v, fp[q], gidx, bad);
-                        ++q;
-                    }
-                }
+                for (uint32_t q = 0; q < G.nfast && !bad;) q += fast_case(v, fp, q, gidx, bad);
                 if (bad && okblk) path = 5;
                 if (bad && G.relaxed) {
                     *flag = 1u;   // the exact path needs partners outside the tile

@@ -59,6 +59,8 @@ struct TileGate {
     uint32_t run;                 // OP_PDIAG, all steps CPLX and +0-safe: length of the
                                   // run of such ops starting here (0 otherwise)
     uint32_t steps;               // OP_PDIAG: bit 4v+e set = step e of variant v present
+    uint32_t cid;                 // fast-path case id (the kernel's jump table)
+    uint32_t pad4[3];
     double2 m[16];
 };
 
