@@ -37,7 +37,7 @@ PEAKS = ROOT / "MEASURED_PEAKS.json"
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
     ap.add_argument("--circuit", default="qft")
@@ -300,9 +300,17 @@ def main() -> int:
     payload = len(blob)
     dec_bytes = st["stages"] * (16 * (1 << args.n) + payload)   # approx: final payload size
     enc_bytes = dec_bytes
-    roofline = {"bound": "hbm", "kernel": "tile_pass_kernel (fused gate pass)",
+    # measured DRAM bytes per launch of the dominant kernel from the committed
+    # `ncu --set full` capture (profiles/traffic.json, written by
+    # tools/profile_round.sh) for this workload, when present
+    traffic = None
+    tfile = ROOT / "profiles" / "traffic.json"
+    if tfile.exists():
+        t = json.loads(tfile.read_text()).get(f"{args.circuit}-{args.n}-m{args.m}")
+        traffic = t["dram_bytes_per_launch"] if t else None
+    roofline = {"bound": "hbm", "kernel": "tile_pass_reg + tile_swaps (fused gate passes)",
                 "achieved": gate_ach, "peak": hbm_peak, "unit": "GB/s",
-                "frac": gate_ach / hbm_peak, "traffic": None,
+                "frac": gate_ach / hbm_peak, "traffic": traffic,
                 "bytes_per_launch": pass_bytes, "avg_launch_s": avg_pass,
                 "launches": st["gate_passes"],
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
