@@ -1734,22 +1734,35 @@ __global__ void __launch_bounds__(256) tile_swaps(double2 *__restrict__ buf, uin
         if (pbase < base) continue;   // the partner tile's CTA moves this pair
         const bool pair = pbase != base;
         uint32_t neg0 = 0;
-        for (uint32_t l = tid; l < tile; l += nth) {
-            const uint64_t off = loff[l];
-            const double2 a = __ldcs(buf + base + off);
-            double2 b = make_double2(0.0, 0.0);
-            if (pair) b = __ldcs(buf + pbase + off);
-            ta[swz10(l)] = a;
-            tb[swz10(l)] = b;
-            neg0 |= uint32_t(__double_as_longlong(a.x) == (long long)0x8000000000000000ULL) |
-                    uint32_t(__double_as_longlong(a.y) == (long long)0x8000000000000000ULL) |
-                    uint32_t(__double_as_longlong(b.x) == (long long)0x8000000000000000ULL) |
-                    uint32_t(__double_as_longlong(b.y) == (long long)0x8000000000000000ULL);
+        // all loads of the pair issued before any is consumed (8 x 16 B per thread)
+        constexpr uint32_t kPer = kMaxTile / 256;
+        double2 ra[kPer], rb[kPer];
+#pragma unroll
+        for (uint32_t i = 0; i < kPer; ++i) {
+            const uint32_t l = tid + i * nth;
+            ra[i] = rb[i] = make_double2(0.0, 0.0);
+            if (l < tile) {
+                const uint64_t off = loff[l];
+                ra[i] = __ldcs(buf + base + off);
+                if (pair) rb[i] = __ldcs(buf + pbase + off);
+            }
+        }
+#pragma unroll
+        for (uint32_t i = 0; i < kPer; ++i) {
+            const uint32_t l = tid + i * nth;
+            if (l < tile) {
+                ta[swz10(l)] = ra[i];
+                tb[swz10(l)] = rb[i];
+            }
+            neg0 |= uint32_t(nz0(ra[i])) | uint32_t(nz0(rb[i]));
         }
         if (__syncthreads_or(neg0)) {
             if (tid == 0) *flag = 1u;
         }
-        for (uint32_t l = tid; l < tile; l += nth) {
+#pragma unroll
+        for (uint32_t i = 0; i < kPer; ++i) {
+            const uint32_t l = tid + i * nth;
+            if (l >= tile) break;
             const uint64_t off = loff[l];
             const uint32_t src = swz10(lperm[l]);
             if (pair) {
