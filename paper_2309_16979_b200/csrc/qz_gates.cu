@@ -355,7 +355,7 @@ static uint32_t case_id(const TileGate &t) {
     switch (t.op) {
     case OP_PDIAG: {
         const uint32_t R = t.nq ? t.r0 : 3;
-        if (t.run) return R;
+        if (t.run) return t.pad4[0];
         return 4 + R * 2 + (t.pad2 == 8 ? 1 : 0);
     }
     case OP_DIAG: {
@@ -644,17 +644,23 @@ GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_
                     t.pad2 = 7;
                 }
             }
-            // runs of specialised OP_PDIAG ops on one register selector (the
-            // kernel's tight loop)
+            // runs of specialised OP_PDIAG ops whose register selectors are
+            // "uniform" or one common bit R (the kernel's tight loop); the
+            // run's selector is kept in pad4[0]
             for (size_t q = plan.gates.size(); q-- > gd.first_fast;) {
                 TileGate &t = plan.gates[q];
                 t.run = 0;
                 if (t.op == OP_PDIAG && t.pad2 == 8) {
+                    const uint32_t rs = t.nq ? t.r0 : kRegBits;
                     t.run = 1;
+                    t.pad4[0] = rs;
                     if (q + 1 < plan.gates.size()) {
                         const TileGate &u = plan.gates[q + 1];
-                        const uint32_t rs = t.nq ? t.r0 : kRegBits, ru = u.nq ? u.r0 : kRegBits;
-                        if (u.run && rs == ru) t.run += u.run;
+                        const uint32_t ru = u.pad4[0];
+                        if (u.run && (rs == kRegBits || ru == kRegBits || rs == ru)) {
+                            t.run += u.run;
+                            t.pad4[0] = rs == kRegBits ? ru : rs;
+                        }
                     }
                 }
             }
@@ -1237,13 +1243,16 @@ __device__ __forceinline__ uint32_t pdiag_var(const TileGate &g, uint64_t gidx) 
     return uint32_t((gidx >> g.ob0) & 1) | (uint32_t((gidx >> g.ob1) & 1) << 1);
 }
 
+// A run mixes uniform ops (no register bit) with ops on register bit R.
 template <int R>
 __device__ __forceinline__ void run_pdiag_r(double2 (&v)[NB], const TileGate *__restrict__ gp,
                                             uint32_t n, uint64_t gidx) {
     for (uint32_t q = 0; q < n; ++q) {
         const TileGate &g = gp[q];
         const uint32_t var = pdiag_var(g, gidx);
-        pdiag_spec<R>(v, g.m + 4 * var, (g.steps >> (4 * var)) & 15u);
+        const uint32_t act = (g.steps >> (4 * var)) & 15u;
+        if (R == kRegBits || g.nq == 0) pdiag_spec<kRegBits>(v, g.m + 4 * var, act);
+        else pdiag_spec<R>(v, g.m + 4 * var, act);
     }
 }
 
