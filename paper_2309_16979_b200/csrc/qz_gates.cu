@@ -1509,11 +1509,15 @@ __device__ void smem_generic(double2 *s, uint32_t tile, const TileGate &g) {
     }
 }
 
+#ifndef QZ_MIN_CTAS
+#define QZ_MIN_CTAS 3
+#endif
+
 // One fused pass: tile of 2^k amplitudes (k >= kRegBits) in shared memory;
 // each group is applied by 2^(k-kRegBits) threads holding NB amplitudes in
 // registers.  Every thread moves exactly NB amplitudes per tile in each
 // direction, all issued before any is consumed (cp.async in, batched stores).
-__global__ void __launch_bounds__(1 << (kTileBits - kRegBits), (kTileBits >= 12 ? 1 : (kTileBits == 11 ? 2 : 4))) tile_pass_reg(double2 *__restrict__ buf, uint32_t nbits,
+__global__ void __launch_bounds__(1 << (kTileBits - kRegBits), (kTileBits >= 12 ? 1 : (kTileBits == 11 ? QZ_MIN_CTAS : 4))) tile_pass_reg(double2 *__restrict__ buf, uint32_t nbits,
                                                          PassDesc pd,
                                                          const GroupDesc *__restrict__ groups,
                                                          const TileGate *__restrict__ gates,

@@ -15,7 +15,8 @@ import numpy as np
 
 from .abi import GATE_DTYPE, Gate, SimConfig, SimStats, gate_ptr, to_array
 
-LIB_PATH = Path(__file__).resolve().parent / "lib" / "libqzcuda.so"
+# QZC_LIB: an alternative build of the same library (tuning experiments)
+LIB_PATH = Path(os.environ.get("QZC_LIB", Path(__file__).resolve().parent / "lib" / "libqzcuda.so"))
 
 P = C.POINTER
 u8p, u32p, u64p, f64p = P(C.c_uint8), P(C.c_uint32), P(C.c_uint64), P(C.c_double)
