@@ -142,6 +142,177 @@ struct Cursor {
     uint32_t pos, rem, byte;
 };
 
+// Warp per chunk.  Each plane's RLE stream is walked 256 pairs per step
+// (8 per lane, warp scan of the run sums): validation, the pair / skip where
+// the plane's element count crosses N (start of the imaginary half) and the
+// per-step element counts (smem) from which every lane then locates its
+// 1/32 of the real half and merges the two byte planes there to count the
+// sentinel (raw) codes of the real half.  Same results as a sequential walk.
+constexpr uint32_t kIdxWarps = 4;
+constexpr uint32_t kIdxMaxSteps = 1040;   // >= 4N / 256 + 1 for c <= 17 (lossy: <= 2N pairs per plane)
+
+__global__ void __launch_bounds__(32 * kIdxWarps) k_dec_index_warp(
+    const uint8_t *__restrict__ arena, ChunkTable table, const uint64_t *__restrict__ slot_chunk,
+    uint64_t nslots, CodecGeom g, DecIdx *__restrict__ out, DevStatus *status) {
+    __shared__ uint32_t step_prod[kIdxWarps][2][kIdxMaxSteps];   // elements before step j
+    const uint32_t lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+    const uint64_t s = uint64_t(blockIdx.x) * kIdxWarps + wq;
+    if (s >= nslots) return;
+    const uint64_t chunk = slot_chunk ? slot_chunk[s] : s;
+    DecIdx d;
+    d.base = table.off[chunk];
+    d.len = 0;
+    const uint32_t len = table.len[chunk];
+    const uint8_t *p = arena + d.base;
+    const uint64_t N = g.N, total = 2 * N;
+    int err = 0;
+    uint32_t count = 0;
+    if (len < kHdr) err = QZS_HEADER;
+    if (!err) {
+        const uint32_t id = ld_u8(p);
+        d.eb = __longlong_as_double((long long)ld_u64(p + 1));
+        count = ld_u32(p + 9);
+        d.raw_count = ld_u32(p + 13);
+        if ((id != 1 && id != 2) || id != (g.lossy ? 1u : 2u) || count != N) err = QZS_HEADER;
+    }
+    uint32_t pos = kHdr;
+    uint32_t nsteps[2] = {0, 0}, start[2] = {0, 0};
+    for (uint32_t k = 0; k < g.planes && !err; ++k) {
+        uint64_t produced = 0;
+        d.pos[k][0] = pos;
+        d.skip[k][0] = 0;
+        start[k < 2 ? k : 1] = pos;
+        bool done = false, found = false;
+        uint32_t step = 0;
+        while (!done && !err) {
+            if (k < 2 && step < kIdxMaxSteps && lane == 0) step_prod[wq][k][step] = uint32_t(produced);
+            // this lane's 8 pairs
+            const uint32_t p0 = pos + 16 * lane;
+            uint32_t runs[8];
+            uint32_t mysum = 0, avail = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const uint32_t q = p0 + 2 * j;
+                runs[j] = q + 2 <= len ? uint32_t(__ldg(p + q + 1)) : 0u;
+                avail += q + 2 <= len ? 1u : 0u;
+                mysum += runs[j];
+            }
+            // inclusive scan of the lane sums
+            uint64_t incl = mysum;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint64_t t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= uint32_t(o)) incl += t;
+            }
+            const uint64_t excl = produced + incl - mysum;
+            // the pair that completes the plane, the pair holding element N,
+            // the first zero run before the end, the first missing pair
+            uint32_t end_pair = ~0u, half_pair = ~0u, half_skip = 0, bad_pair = ~0u;
+            uint64_t c = excl;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const uint32_t idx = 8 * lane + j;
+                if (j >= int(avail)) { if (bad_pair == ~0u && c < total) bad_pair = idx; continue; }
+                if (c >= total) continue;
+                const uint32_t r = runs[j];
+                if (bad_pair == ~0u && (r == 0 || c + r > total)) bad_pair = idx;
+                if (half_pair == ~0u && c <= N && N < c + r) { half_pair = idx; half_skip = uint32_t(N - c); }
+                if (end_pair == ~0u && c + r == total) end_pair = idx;
+                c += r;
+            }
+            // warp-wide minima (first occurrence in stream order)
+            uint32_t e_end = end_pair, e_half = half_pair, e_bad = bad_pair;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                e_end = min(e_end, __shfl_xor_sync(0xffffffffu, e_end, o));
+                e_half = min(e_half, __shfl_xor_sync(0xffffffffu, e_half, o));
+                e_bad = min(e_bad, __shfl_xor_sync(0xffffffffu, e_bad, o));
+            }
+            if (e_half != ~0u && !found) {
+                const uint32_t src = e_half >> 3;
+                const uint32_t sk = __shfl_sync(0xffffffffu, half_skip, src);
+                if (e_bad == ~0u || e_half < e_bad) {
+                    d.pos[k][1] = pos + 2 * e_half;
+                    d.skip[k][1] = sk;
+                    found = true;
+                }
+            }
+            if (e_bad != ~0u && (e_end == ~0u || e_bad <= e_end)) {
+                // a zero / overlong run, or the stream ends before 2N elements
+                const uint32_t q = pos + 2 * e_bad;
+                err = q + 2 > len ? QZS_RLE_TRUNC : QZS_RLE_RUN;
+                break;
+            }
+            if (e_end != ~0u) {
+                pos += 2 * (e_end + 1);
+                done = true;
+            } else {
+                produced += __shfl_sync(0xffffffffu, incl, 31);
+                pos += 512;
+            }
+            ++step;
+        }
+        if (k < 2) nsteps[k] = step;
+    }
+    if (!err && g.lossy) {
+        d.raw_pos = pos;
+        if (uint64_t(pos) + uint64_t(d.raw_count) * 8 > len) err = QZS_RAW_MISSING;
+    }
+    if (!err && g.lossy && (nsteps[0] > kIdxMaxSteps || nsteps[1] > kIdxMaxSteps)) err = QZS_RLE_RUN;
+    __syncwarp();
+    if (!err && g.lossy) {
+        // sentinel codes in [lane * N/32, (lane+1) * N/32): locate both planes'
+        // cursors at the segment start, then merge the two run streams
+        const uint64_t seg = N / 32 ? N / 32 : 1;
+        const uint64_t e0 = uint64_t(lane) * seg, e1 = lane == 31 ? N : umin64(N, e0 + seg);
+        uint64_t cnt = 0;
+        if (e0 < e1) {
+            uint32_t pp[2], rr[2];
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                // last step whose start count <= e0, then walk its pairs
+                uint32_t lo = 0, hi = nsteps[k] - 1;
+                while (lo < hi) {
+                    const uint32_t mid = (lo + hi + 1) >> 1;
+                    if (step_prod[wq][k][mid] <= e0) lo = mid;
+                    else hi = mid - 1;
+                }
+                uint32_t q = start[k] + 512 * lo;
+                uint64_t c = step_prod[wq][k][lo];
+                uint32_t r = p[q + 1];
+                while (c + r <= e0) {
+                    c += r;
+                    q += 2;
+                    r = p[q + 1];
+                }
+                pp[k] = q;
+                rr[k] = uint32_t(c + r - e0);   // elements of this run at/after e0
+            }
+            uint64_t i = e0;
+            while (i < e1) {
+                const uint64_t st = umin64(umin32(rr[0], rr[1]), e1 - i);
+                if (p[pp[0]] == 0xFF && p[pp[1]] == 0xFF) cnt += st;
+                i += st;
+                rr[0] -= uint32_t(st);
+                rr[1] -= uint32_t(st);
+                if (i < e1) {
+                    if (rr[0] == 0) { pp[0] += 2; rr[0] = p[pp[0] + 1]; }
+                    if (rr[1] == 0) { pp[1] += 2; rr[1] = p[pp[1] + 1]; }
+                }
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        if (cnt > d.raw_count) err = QZS_RAW_UNDER;
+        d.raw_re = uint32_t(cnt);
+    }
+    if (lane == 0) {
+        if (err) dev_fail(status, err, chunk);
+        else d.len = len;
+        out[s] = d;
+    }
+}
+
 __global__ void k_dec_index(const uint8_t *__restrict__ arena, ChunkTable table,
                             const uint64_t *__restrict__ slot_chunk, uint64_t nslots,
                             CodecGeom g, DecIdx *__restrict__ out, DevStatus *status) {
@@ -254,15 +425,6 @@ __device__ __forceinline__ void store_tile(TileSmem &t, double2 *win, uint64_t s
     }
 }
 
-__device__ __forceinline__ void load_tile(TileSmem &t, const double2 *win, uint64_t slot0,
-                                          uint64_t nslots, uint64_t N, uint64_t e0,
-                                          uint32_t te) {
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (uint32_t r = warp; r < kSlotsPerCta; r += nw) {
-        if (slot0 + r >= nslots) break;
-        for (uint32_t e = lane; e < te; e += 32) t.f[r * (te + 1) + e] = __ldcs(win + (slot0 + r) * N + e0 + e);
-    }
-}
 
 __device__ __forceinline__ double comp(const double2 &v, uint32_t h) { return h ? v.y : v.x; }
 __device__ __forceinline__ void set_comp(double2 &v, uint32_t h, double x) {
@@ -916,8 +1078,12 @@ void launch_crc(const CodecTables &tabs, const uint8_t *arena, ChunkTable table,
 void launch_dec_index(const uint8_t *arena, ChunkTable table, const uint64_t *slot_chunk,
                       uint64_t nslots, const CodecGeom &g, DecIdx *idx, DevStatus *status,
                       cudaStream_t s) {
-    k_dec_index<<<grid_for(nslots, 64), 64, 0, s>>>(arena, table, slot_chunk, nslots, g, idx,
-                                                    status);
+    if (g.lossy && g.N >= 64 && 4 * g.N / 256 + 1 <= kIdxMaxSteps)
+        k_dec_index_warp<<<grid_for(nslots, kIdxWarps), 32 * kIdxWarps, 0, s>>>(arena, table, slot_chunk,
+                                                                              nslots, g, idx, status);
+    else
+        k_dec_index<<<grid_for(nslots, 64), 64, 0, s>>>(arena, table, slot_chunk, nslots, g, idx,
+                                                        status);
     QZ_CHECK_LAUNCH();
 }
 
