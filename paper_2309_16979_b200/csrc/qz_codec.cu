@@ -385,6 +385,54 @@ __global__ void k_dec_index(const uint8_t *__restrict__ arena, ChunkTable table,
 
 // ----------------------------------------------------------------- decode --
 
+// Buffered RLE reader for the lossy decoder: 8 (byte, run) pairs are fetched
+// at a time (16 independent byte loads, up to 15 bytes past the stream —
+// arenas and staging buffers keep >= 64 bytes of slack), so the dependent
+// load latency is paid once per 8 pairs instead of once per pair.
+struct BCursor {
+    uint32_t bpos;      // byte offset of the buffered pairs
+    uint32_t k;         // next pair in the buffer (0..8)
+    uint32_t byte, rem; // current run
+    uint64_t b0, b1;    // pairs 0-3, 4-7
+};
+
+__device__ __forceinline__ void bc_fill(BCursor &c, const uint8_t *p) {
+    uint64_t x0 = 0, x1 = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        x0 |= uint64_t(__ldg(p + c.bpos + i)) << (8 * i);
+        x1 |= uint64_t(__ldg(p + c.bpos + 8 + i)) << (8 * i);
+    }
+    c.b0 = x0;
+    c.b1 = x1;
+    c.k = 0;
+}
+
+__device__ __forceinline__ void bc_take(BCursor &c, const uint8_t *p) {
+    if (c.k == 8) {
+        c.bpos += 16;
+        bc_fill(c, p);
+    }
+    const uint64_t w = c.k < 4 ? c.b0 : c.b1;
+    const uint32_t sh = 16 * (c.k & 3);
+    c.byte = uint32_t(w >> sh) & 0xffu;
+    c.rem = uint32_t(w >> (sh + 8)) & 0xffu;
+    ++c.k;
+}
+
+__device__ __forceinline__ void bc_init(BCursor &c, const uint8_t *p, uint32_t pos, uint32_t skip) {
+    c.bpos = pos;
+    bc_fill(c, p);
+    bc_take(c, p);
+    c.rem -= skip;
+}
+
+__device__ __forceinline__ uint32_t bc_next(BCursor &c, const uint8_t *p) {
+    if (c.rem == 0) bc_take(c, p);
+    --c.rem;
+    return c.byte;
+}
+
 __device__ __forceinline__ void cur_init(Cursor &c, const uint8_t *p, uint32_t pos, uint32_t skip) {
     c.pos = pos;
     c.byte = p[pos];
@@ -445,13 +493,13 @@ __global__ void __launch_bounds__(2 * kSlotsPerCta) k_dec_lossy(
     const bool active = s < nslots && idx[min(s, nslots - 1)].len != 0;
     const DecIdx *d = &idx[min(s, nslots - 1)];
     const uint8_t *p = arena + d->base;
-    Cursor lo{0, 0, 0}, hi{0, 0, 0};
+    BCursor lo{0, 8, 0, 0, 0, 0}, hi{0, 8, 0, 0, 0, 0};
     uint32_t raw_i = 0, raw_count = 0, raw_pos = 0;
     double twoeb = 0.0, pred = 0.0;
     bool bad = false;
     if (active) {
-        cur_init(lo, p, d->pos[0][h], d->skip[0][h]);
-        cur_init(hi, p, d->pos[1][h], d->skip[1][h]);
+        bc_init(lo, p, d->pos[0][h], d->skip[0][h]);
+        bc_init(hi, p, d->pos[1][h], d->skip[1][h]);
         raw_i = h ? d->raw_re : 0;
         raw_count = d->raw_count;
         raw_pos = d->raw_pos;
@@ -466,16 +514,8 @@ __global__ void __launch_bounds__(2 * kSlotsPerCta) k_dec_lossy(
     for (uint64_t e0 = 0; e0 < N; e0 += te) {
         for (uint32_t e = 0; e < te && has_row; ++e) {
             if (active) {
-                if (lo.rem == 0) {
-                    lo.pos += 2;
-                    lo.byte = p[lo.pos];
-                    lo.rem = p[lo.pos + 1];
-                }
-                if (hi.rem == 0) {
-                    hi.pos += 2;
-                    hi.byte = p[hi.pos];
-                    hi.rem = p[hi.pos + 1];
-                }
+                if (lo.rem == 0) bc_take(lo, p);
+                if (hi.rem == 0) bc_take(hi, p);
                 if ((lo.byte | hi.byte) == 0) {
                     // a stretch of code 0: pred + (+0) = pred (a -0 becomes +0)
                     const uint32_t k = min(min(lo.rem, hi.rem), te - e);
@@ -486,7 +526,7 @@ __global__ void __launch_bounds__(2 * kSlotsPerCta) k_dec_lossy(
                     e += k - 1;
                     continue;
                 }
-                const uint32_t z = cur_next(lo, p) | (cur_next(hi, p) << 8);
+                const uint32_t z = bc_next(lo, p) | (bc_next(hi, p) << 8);
                 if (z == 0xFFFFu) {
                     if (raw_i >= raw_count) {
                         bad = true;

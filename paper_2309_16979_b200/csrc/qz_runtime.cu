@@ -440,7 +440,8 @@ void sim_alloc(qzc_sim *sim) {
         sim->io_bytes.ensure(16);
         QZ_CUDA(cudaMemset(sim->io_bytes.p, 0, 16));
     } else {
-        for (int i = 0; i < 2; ++i) sim->arena[i].ensure(sim->arena_cap);
+        // +64: the decoder's RLE readers fetch 16 bytes ahead
+        for (int i = 0; i < 2; ++i) sim->arena[i].ensure(sim->arena_cap + 64);
     }
 }
 
