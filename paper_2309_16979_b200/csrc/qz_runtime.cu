@@ -78,12 +78,38 @@ struct Window {
     ChunkTable local() {
         return ChunkTable{lt_off.as<uint64_t>(), lt_len.as<uint32_t>(), lt_crc.as<uint32_t>()};
     }
+    // host-staged pipeline: the second input set (slot map, staged
+    // payloads, slot-indexed table, decode cursors) of a single window
+    void reserve_input(const CodecGeom &g, uint64_t nslots) {
+        const uint64_t bound = payload_bound(g.N, g.lossy ? 1.0 : 0.0);
+        slots = nslots;
+        stage_in_cap = nslots * (bound + 48) + 64;
+        stage_in.ensure(stage_in_cap);
+        lt_off.ensure(8 * nslots);
+        lt_len.ensure(4 * nslots);
+        lt_crc.ensure(4 * nslots);
+        padded.ensure(8 * nslots);
+        soff.ensure(8 * nslots);
+        slot_chunk.ensure(sizeof(uint64_t) * nslots);
+        idx.ensure(sizeof(DecIdx) * nslots);
+        size_t t1 = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, t1, (uint64_t *)nullptr, (uint64_t *)nullptr,
+                                      (int)std::min<uint64_t>(nslots, INT32_MAX));
+        cub.ensure(t1 + 256);
+    }
+    DevBuf out_off, out_len, out_crc;   // encode output table (pipelined host-staged)
+    ChunkTable out_local() {
+        return ChunkTable{out_off.as<uint64_t>(), out_len.as<uint32_t>(), out_crc.as<uint32_t>()};
+    }
     void reserve_staging(const CodecGeom &g, uint64_t nslots) {
         const uint64_t bound = payload_bound(g.N, g.lossy ? 1.0 : 0.0);
         stage_in_cap = nslots * (bound + 48) + 64;
         stage_out_cap = nslots * bound + 64;
         stage_in.ensure(stage_in_cap);
         stage_out.ensure(stage_out_cap);
+        out_off.ensure(8 * nslots);
+        out_len.ensure(4 * nslots);
+        out_crc.ensure(4 * nslots);
         lt_off.ensure(8 * nslots);
         lt_len.ensure(4 * nslots);
         lt_crc.ensure(4 * nslots);
@@ -121,7 +147,7 @@ struct Window {
     void release() {
         for (DevBuf *b : {&amps, &scratch, &meta, &idx, &slot_chunk, &sizes, &reloff, &base, &cub,
                           &delta, &maxd, &stage_in, &stage_out, &lt_off, &lt_len, &lt_crc, &padded,
-                          &soff, &lused, &hbase})
+                          &soff, &lused, &hbase, &out_off, &out_len, &out_crc, &replay})
             b->release();
     }
 };
@@ -288,7 +314,10 @@ struct qzc_sim {
     bool two_windows = false;
     bool relax = true;          // fuse_gates == 1: relaxed passes + strict replay
     bool force_replay = false;  // debug_flags bit 0
-    cudaStream_t streams[2] = {nullptr, nullptr};
+    cudaStream_t streams[3] = {nullptr, nullptr, nullptr};   // [2]: host-staged write-back
+    bool pipelined = false;   // host-staged, one window: gather / compute / write-back streams
+    DevBuf gcub;              // scan scratch of the gather stream
+    std::vector<cudaEvent_t> pevents;
     cudaEvent_t acct_ev[2] = {nullptr, nullptr};
     qzc_sim_stats stats{};
     bool initialized = false;
@@ -357,6 +386,16 @@ void decode_window(qzc_context *ctx, Window &w, const CodecGeom &g, uint64_t nsl
     launches += 3;
 }
 
+// decode_window with an explicit cursor array and target window
+void decode_into(qzc_context *ctx, DecIdx *idx, double2 *amps, const CodecGeom &g, uint64_t nslots,
+                 const uint64_t *slot_chunk, const uint8_t *arena, ChunkTable t, uint64_t &launches,
+                 cudaStream_t s) {
+    launch_crc(ctx->tabs, arena, t, slot_chunk, nslots, true, ctx->status, s);
+    launch_dec_index(arena, t, slot_chunk, nslots, g, idx, ctx->status, s);
+    launch_decode(arena, idx, slot_chunk, nslots, g, amps, ctx->status, s);
+    launches += 3;
+}
+
 uint32_t log2u(uint64_t x) {
     uint32_t r = 0;
     while ((uint64_t(1) << r) < x) ++r;
@@ -385,13 +424,15 @@ void sim_alloc(qzc_sim *sim) {
     QZ_CUDA(cudaMemGetInfo(&free_b, &total_b));
     uint64_t budget = ctx->budget ? std::min<uint64_t>(ctx->budget, free_b) : free_b;
     budget = budget > (uint64_t(3) << 30) ? budget - (uint64_t(3) << 30) : budget / 2;
-    // dense + encode scratch + metadata (+ payload staging when host-staged)
+    // dense + encode scratch + metadata (+ payload staging when host-staged:
+    // two input sets and one output)
     const uint64_t per_amp = 16 + 2 * sim->geom.half_stride / sim->N + 8 +
-                             (sim->host_res ? 2 * (payload_bound(sim->N, sim->eb) + 48) / sim->N + 1 : 0);
+                             (sim->host_res ? 3 * (payload_bound(sim->N, sim->eb) + 48) / sim->N + 1 : 0);
     const uint64_t state_amps = uint64_t(1) << sim->n;
     uint64_t wa = sim->cfg.window_amps;
     if (!wa) {
-        const uint64_t cap_amps = std::max<uint64_t>(budget / 2 / per_amp, sim->N);
+        // HBM-resident: half the budget stays for the arenas
+        const uint64_t cap_amps = std::max<uint64_t>(budget / (sim->host_res ? 1 : 2) / per_amp, sim->N);
         wa = uint64_t(1) << (63 - __builtin_clzll(cap_amps));
         wa = std::min(wa, state_amps);
     }
@@ -411,6 +452,7 @@ void sim_alloc(qzc_sim *sim) {
         QZ_CUDA(cudaStreamCreateWithFlags(&sim->streams[i], cudaStreamNonBlocking));
         QZ_CUDA(cudaEventCreateWithFlags(&sim->acct_ev[i], cudaEventDisableTiming));
     }
+    QZ_CUDA(cudaStreamCreateWithFlags(&sim->streams[2], cudaStreamNonBlocking));
 
     // arenas: worst case if it fits, else what is left
     QZ_CUDA(cudaMemGetInfo(&free_b, &total_b));
@@ -436,7 +478,18 @@ void sim_alloc(qzc_sim *sim) {
             sim->harena_dev[i] = static_cast<uint8_t *>(d);
         }
         sim->win.reserve_staging(sim->geom, sim->win.slots);
-        if (sim->two_windows) sim->win2.reserve_staging(sim->geom, sim->win2.slots);
+        if (sim->two_windows) {
+            sim->win2.reserve_staging(sim->geom, sim->win2.slots);
+        } else {
+            // one window: overlap the next window's gather and this window's
+            // write-back with its decode / passes / encode
+            sim->pipelined = true;
+            sim->win2.reserve_input(sim->geom, sim->win.slots);
+            size_t t1 = 0;
+            cub::DeviceScan::ExclusiveSum(nullptr, t1, (uint64_t *)nullptr, (uint64_t *)nullptr,
+                                          (int)std::min<uint64_t>(sim->win.slots, INT32_MAX));
+            sim->gcub.ensure(t1 + 256);
+        }
         sim->io_bytes.ensure(16);
         QZ_CUDA(cudaMemset(sim->io_bytes.p, 0, 16));
     } else {
@@ -885,6 +938,8 @@ void qzc_sim_destroy(qzc_sim *sim) {
     if (!sim) return;
     cudaSetDevice(sim->ctx->device);
     cudaStreamSynchronize(sim->ctx->stream);
+    for (int i = 0; i < 3; ++i)
+        if (sim->streams[i]) cudaStreamSynchronize(sim->streams[i]);
     for (int i = 0; i < 2; ++i)
         for (DevBuf *b : {&sim->arena[i], &sim->off[i], &sim->len[i], &sim->crc[i]}) b->release();
     sim->used.release();
@@ -892,19 +947,22 @@ void qzc_sim_destroy(qzc_sim *sim) {
     sim->io_bytes.release();
     sim->replays.release();
     sim->small.release();
+    sim->gcub.release();
     for (DevPlan &p : sim->plans) free_plan(p);
     for (int i = 0; i < 2; ++i)
         if (sim->harena[i]) cudaFreeHost(sim->harena[i]);
     sim->win.release();
     sim->win2.release();
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 3; ++i) {
         if (sim->streams[i]) {
             cudaStreamSynchronize(sim->streams[i]);
             cudaStreamDestroy(sim->streams[i]);
         }
-        if (sim->acct_ev[i]) cudaEventDestroy(sim->acct_ev[i]);
     }
+    for (int i = 0; i < 2; ++i)
+        if (sim->acct_ev[i]) cudaEventDestroy(sim->acct_ev[i]);
     for (cudaEvent_t e : sim->events) cudaEventDestroy(e);
+    for (cudaEvent_t e : sim->pevents) cudaEventDestroy(e);
     delete sim;
 }
 
@@ -1082,7 +1140,79 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
         QZ_CUDA(cudaEventRecord(ready, s));
         const uint64_t nslots = bpw << hs;
         const double tp1 = now_s();
-        for (uint64_t w = 0; w < nwin; ++w) {
+        // pipeline events: 3 per window (gathered, encoded, written back)
+        auto pev = [&](uint64_t i) {
+            while (sim->pevents.size() <= i) {
+                cudaEvent_t e;
+                QZ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                sim->pevents.push_back(e);
+            }
+            return sim->pevents[i];
+        };
+        for (uint64_t w = 0; w < nwin && sim->pipelined; ++w) {
+            // host-staged, one window: input set w&1 (slot map, staged payloads,
+            // slot table, cursors) cycles gather -> decode -> write-back; the
+            // window, scratch and output staging are shared and serialised
+            Window &W = sim->win;
+            Window &In = (w & 1) ? sim->win2 : sim->win;
+            cudaStream_t SG = sim->streams[1], S = sim->streams[0], SO = sim->streams[2];
+            // gather (H2D) of window w on SG, after the write-back of window
+            // w-2 released this input set
+            if (w < 2) QZ_CUDA(cudaStreamWaitEvent(SG, ready, 0));
+            else QZ_CUDA(cudaStreamWaitEvent(SG, pev(3 * (w - 2) + 2), 0));
+            launch_slot_chunks(In.slot_chunk.as<uint64_t>(), nslots, w * bpw, hs, fmask, smask, SG);
+            launch_stage_sizes(sim->table(a), In.slot_chunk.as<uint64_t>(), nslots, In.padded.as<uint64_t>(), SG);
+            size_t tb = sim->gcub.cap;
+            QZ_CUDA(cub::DeviceScan::ExclusiveSum(sim->gcub.p, tb, In.padded.as<uint64_t>(), In.soff.as<uint64_t>(),
+                                                  (int)nslots, SG));
+            launch_gather(sim->arena_ptr(a), sim->table(a), In.slot_chunk.as<uint64_t>(), In.soff.as<uint64_t>(),
+                          nslots, In.stage_in.as<uint8_t>(), In.local(), SG);
+            k_io_count<<<1, 1, 0, SG>>>(In.soff.as<uint64_t>(), In.padded.as<uint64_t>(), nslots,
+                                         sim->io_bytes.as<uint64_t>());
+            QZ_CHECK_LAUNCH();
+            ctx->launches += 5;
+            QZ_CUDA(cudaEventRecord(pev(3 * w), SG));
+            // decode / passes / encode of window w on S
+            if (w == 0) QZ_CUDA(cudaStreamWaitEvent(S, ready, 0));
+            QZ_CUDA(cudaStreamWaitEvent(S, pev(3 * w), 0));
+            QZ_CUDA(cudaEventRecord(ev(4 * w), S));
+            decode_into(ctx, In.idx.as<DecIdx>(), W.amps.as<double2>(), sim->geom, nslots, nullptr,
+                        In.stage_in.as<uint8_t>(), In.local(), ctx->launches, S);
+            QZ_CUDA(cudaEventRecord(ev(4 * w + 1), S));
+            if (dp.relaxed) {
+                uint32_t *flag = W.replay.as<uint32_t>();
+                if (sim->force_replay) QZ_CUDA(cudaMemsetAsync(flag, 1, 1, S));
+                ctx->launches += run_passes(dp, W.amps.as<double2>(), wbits, S, flag);
+                launch_decode(In.stage_in.as<uint8_t>(), In.idx.as<DecIdx>(), nullptr, nslots, sim->geom,
+                              W.amps.as<double2>(), ctx->status, S, flag);
+                ctx->launches += 1 + run_passes(dstrict, W.amps.as<double2>(), wbits, S, nullptr, flag);
+                k_replay_done<<<1, 1, 0, S>>>(flag, sim->replays.as<uint64_t>());
+                QZ_CHECK_LAUNCH();
+                ctx->launches += 2;
+            } else {
+                ctx->launches += 1 + run_passes(dp, W.amps.as<double2>(), wbits, S);
+            }
+            QZ_CUDA(cudaEventRecord(ev(4 * w + 2), S));
+            // the output staging / table of window w-1 must be written back
+            if (w) QZ_CUDA(cudaStreamWaitEvent(S, pev(3 * (w - 1) + 2), 0));
+            QZ_CUDA(cudaMemsetAsync(W.lused.p, 0, 8, S));
+            encode_window(ctx, W, sim->geom, nslots, nullptr, nullptr, 0, W.stage_out.as<uint8_t>(),
+                          W.lused.as<uint64_t>(), W.stage_out_cap, W.out_local(), sim->len[a].as<uint32_t>(),
+                          sim->acct.as<int64_t>(), ctx->launches, S, nullptr, nullptr,
+                          In.slot_chunk.as<uint64_t>());
+            QZ_CUDA(cudaEventRecord(ev(4 * w + 3), S));
+            QZ_CUDA(cudaEventRecord(pev(3 * w + 1), S));
+            // write-back (D2H) of window w on SO
+            QZ_CUDA(cudaStreamWaitEvent(SO, pev(3 * w + 1), 0));
+            launch_copy_out(W.stage_out.as<uint8_t>(), W.lused.as<uint64_t>(), sim->used_ptr(b), sim->arena_cap,
+                            W.hbase.as<uint64_t>(), sim->arena_ptr(b), W.out_local(), In.slot_chunk.as<uint64_t>(),
+                            nslots, sim->table(b), ctx->status, SO);
+            k_io_count_out<<<1, 1, 0, SO>>>(W.lused.as<uint64_t>(), sim->io_bytes.as<uint64_t>());
+            QZ_CHECK_LAUNCH();
+            ctx->launches += 4;
+            QZ_CUDA(cudaEventRecord(pev(3 * w + 2), SO));
+        }
+        for (uint64_t w = 0; w < nwin && !sim->pipelined; ++w) {
             const int ws = sim->two_windows ? int(w & 1) : 0;
             Window &W = ws ? sim->win2 : sim->win;
             cudaStream_t S = sim->streams[ws];
@@ -1154,7 +1284,7 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
             QZ_CUDA(cudaEventRecord(ev(4 * w + 3), S));
         }
         const double tp2 = now_s();
-        for (int i = 0; i < 2; ++i) QZ_CUDA(cudaStreamSynchronize(sim->streams[i]));
+        for (int i = 0; i < 3; ++i) QZ_CUDA(cudaStreamSynchronize(sim->streams[i]));
         if (trace)
             fprintf(stderr, "qz trace: stage %zu plan %.2f ms launch %.2f ms sync %.2f ms (%zu passes)\n", si,
                     1e3 * (tp1 - tp0), 1e3 * (tp2 - tp1), 1e3 * (now_s() - tp2), gp.passes.size());
