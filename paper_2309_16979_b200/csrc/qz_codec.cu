@@ -1006,7 +1006,17 @@ __global__ void __launch_bounds__(256) k_gather(const uint8_t *__restrict__ host
         const uint64_t words = (uint64_t((src & 15) + len) + 15) / 16;
         const uint4 *in = reinterpret_cast<const uint4 *>(host_arena + (src & ~uint64_t(15)));
         uint4 *out = reinterpret_cast<uint4 *>(stage + soff[s]);
-        for (uint64_t w = lane; w < words; w += 32) out[w] = in[w];
+        // 8 x 16 B zero-copy reads in flight per lane: a few CTAs keep the
+        // host link busy and leave the SMs to the decode / gate kernels
+        uint64_t w = lane;
+        for (; w + 7 * 32 < words; w += 8 * 32) {
+            uint4 r[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) r[j] = in[w + 32 * j];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) out[w + 32 * j] = r[j];
+        }
+        for (; w < words; w += 32) out[w] = in[w];
         if (lane == 0) {
             local.off[s] = soff[s] + (src & 15);
             local.len[s] = len;
@@ -1035,9 +1045,16 @@ __global__ void k_copy_out(const uint8_t *__restrict__ stage, const uint64_t *__
     const uint64_t words = round_up(*used_local, 16) / 16;
     const uint4 *in = reinterpret_cast<const uint4 *>(stage);
     uint4 *out = reinterpret_cast<uint4 *>(host_arena + *base);
-    for (uint64_t w = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; w < words;
-         w += uint64_t(gridDim.x) * blockDim.x)
-        out[w] = in[w];
+    const uint64_t nth = uint64_t(gridDim.x) * blockDim.x;
+    uint64_t w = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    for (; w + 7 * nth < words; w += 8 * nth) {
+        uint4 r[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = in[w + nth * j];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) out[w + nth * j] = r[j];
+    }
+    for (; w < words; w += nth) out[w] = in[w];
 }
 
 // Publish the window's entries in the global (chunk-indexed) table.
@@ -1186,7 +1203,8 @@ void launch_stage_sizes(ChunkTable table, const uint64_t *slot_chunk, uint64_t n
 void launch_gather(const uint8_t *host_arena, ChunkTable table, const uint64_t *slot_chunk,
                    const uint64_t *soff, uint64_t nslots, uint8_t *stage, ChunkTable local,
                    cudaStream_t s) {
-    const unsigned grid = (unsigned)std::min<uint64_t>(ceil_div(nslots, 8), kNumSMs * 32);
+    // a small grid: the transfer is link-bound, the SMs stay with the compute stream
+    const unsigned grid = (unsigned)std::min<uint64_t>(ceil_div(nslots, 8), 64);
     k_gather<<<grid, 256, 0, s>>>(host_arena, table, slot_chunk, soff, nslots, stage, local);
     QZ_CHECK_LAUNCH();
 }
@@ -1197,7 +1215,7 @@ void launch_copy_out(const uint8_t *stage, const uint64_t *used_local, uint64_t 
                      DevStatus *status, cudaStream_t s) {
     k_host_alloc<<<1, 1, 0, s>>>(used_local, host_used, cap, base, status);
     QZ_CHECK_LAUNCH();
-    k_copy_out<<<kNumSMs * 8, 256, 0, s>>>(stage, used_local, base, host_arena);
+    k_copy_out<<<64, 256, 0, s>>>(stage, used_local, base, host_arena);
     QZ_CHECK_LAUNCH();
     k_table_out<<<grid_for(nslots, 256), 256, 0, s>>>(local, slot_chunk, base, nslots, table);
     QZ_CHECK_LAUNCH();
