@@ -479,6 +479,154 @@ __device__ __forceinline__ void set_comp(double2 &v, uint32_t h, double x) {
     if (h) v.y = x; else v.x = x;
 }
 
+// Lossy decode, warp per (slot, half): 32 elements per step.  Each lane
+// expands one element's code from the two byte planes (32 pairs fetched per
+// plane, warp scan of the runs, binary search by shuffles), raw escapes are
+// ranked by ballot and fetched in parallel, d = code * 2eb is formed per lane,
+// and only the predictor chain itself — pred = raw ? value : pred + d, the
+// reference's sequence of roundings (codec.cpp:217-249) — runs serially over
+// the 32 lanes' values.  One chain per warp instead of per thread: enough
+// warps to hide latency when a window holds few chunks.
+struct PlaneRd {
+    uint32_t pp;    // byte offset of the current pair
+    uint32_t rem;   // elements left in it
+};
+
+__device__ __forceinline__ uint32_t plane_block(PlaneRd &c, const uint8_t *p, uint32_t lane) {
+    if (c.rem >= 32) {
+        // the whole block lies in the current run
+        const uint32_t byte = __ldg(p + c.pp);
+        c.rem -= 32;
+        if (c.rem == 0) {
+            c.pp += 2;
+            c.rem = __ldg(p + c.pp + 1);
+        }
+        return byte;
+    }
+    const uint32_t q = c.pp + 2 * lane;
+    const uint32_t b = __ldg(p + q);
+    uint32_t r = __ldg(p + q + 1);
+    if (lane == 0) r = c.rem;
+    uint32_t S = r;   // inclusive scan of the runs
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, S, o);
+        if (lane >= uint32_t(o)) S += t;
+    }
+    // pair of element `lane`: number of pairs whose scan is <= lane
+    uint32_t j = 0;
+#pragma unroll
+    for (uint32_t step = 16; step; step >>= 1) {
+        const uint32_t sv = __shfl_sync(0xffffffffu, S, j + step - 1);
+        if (sv <= lane) j += step;
+    }
+    const uint32_t byte = __shfl_sync(0xffffffffu, b, j);
+    // advance past 32 elements
+    const uint32_t j31 = __shfl_sync(0xffffffffu, j, 31);
+    const uint32_t s31 = __shfl_sync(0xffffffffu, S, j31);
+    const uint32_t rnext = __shfl_sync(0xffffffffu, r, (j31 + 1) & 31);
+    if (s31 > 32) {
+        c.pp += 2 * j31;
+        c.rem = s31 - 32;
+    } else {
+        c.pp += 2 * (j31 + 1);
+        c.rem = j31 + 1 < 32 ? rnext : uint32_t(__ldg(p + c.pp + 1));
+    }
+    return byte;
+}
+
+__global__ void __launch_bounds__(256) k_dec_lossy_warp(
+    const uint8_t *__restrict__ arena, const DecIdx *__restrict__ idx,
+    const uint64_t *__restrict__ slot_chunk, uint64_t nslots, CodecGeom g,
+    double2 *__restrict__ win, DevStatus *status, const uint32_t *cond) {
+    if (cond && *cond == 0) return;
+    __shared__ double chain[8][64];   // per warp: 32 inputs, 32 predictor values
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t wg = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t s = wg >> 1;
+    const uint32_t h = uint32_t(wg & 1);
+    if (s >= nslots) return;
+    const DecIdx &d = idx[s];
+    const uint64_t N = g.N;
+    double *out = reinterpret_cast<double *>(win) + 2 * s * N + h;
+    if (d.len == 0) {
+        for (uint64_t e = lane; e < N; e += 32) __stcs(out + 2 * e, 0.0);
+        return;
+    }
+    const uint8_t *p = arena + d.base;
+    PlaneRd lo{d.pos[0][h], 0}, hi{d.pos[1][h], 0};
+    lo.rem = uint32_t(__ldg(p + lo.pp + 1)) - d.skip[0][h];
+    hi.rem = uint32_t(__ldg(p + hi.pp + 1)) - d.skip[1][h];
+    // a zero remainder: the half starts at the next pair
+    if (lo.rem == 0) { lo.pp += 2; lo.rem = __ldg(p + lo.pp + 1); }
+    if (hi.rem == 0) { hi.pp += 2; hi.rem = __ldg(p + hi.pp + 1); }
+    const double twoeb = 2.0 * d.eb;
+    uint32_t raw_i = h ? d.raw_re : 0;
+    const uint32_t raw_count = d.raw_count, raw_pos = d.raw_pos;
+    double pred = 0.0;
+    bool bad = false;
+    for (uint64_t e0 = 0; e0 < N; e0 += 32) {
+        // runs of code 0 in both planes: pred + (+0) = pred (a -0 becomes
+        // +0), so whole 32-element blocks are value fills
+        if (lo.rem >= 32 && hi.rem >= 32 && (__ldg(p + lo.pp) | __ldg(p + hi.pp)) == 0) {
+            const uint32_t nb = uint32_t(umin64(min(lo.rem, hi.rem) / 32, (N - e0) / 32));
+            pred = __dadd_rn(pred, 0.0);
+            for (uint32_t k = 0; k < nb; ++k) __stcs(out + 2 * (e0 + 32 * k + lane), pred);
+            lo.rem -= 32 * nb;
+            hi.rem -= 32 * nb;
+            if (lo.rem == 0) { lo.pp += 2; lo.rem = __ldg(p + lo.pp + 1); }
+            if (hi.rem == 0) { hi.pp += 2; hi.rem = __ldg(p + hi.pp + 1); }
+            e0 += 32 * uint64_t(nb) - 32;
+            continue;
+        }
+        const uint32_t z = plane_block(lo, p, lane) | (plane_block(hi, p, lane) << 8);
+        if (__all_sync(0xffffffffu, z == 0)) {
+            // a block of code 0 across pair boundaries: a value fill
+            pred = __dadd_rn(pred, 0.0);
+            __stcs(out + 2 * (e0 + lane), pred);
+            continue;
+        }
+        const bool raw = z == 0xFFFFu;
+        const uint32_t rm = __ballot_sync(0xffffffffu, raw);
+        double val;
+        if (raw) {
+            const uint32_t k = raw_i + __popc(rm & ((1u << lane) - 1));
+            val = k < raw_count ? __longlong_as_double((long long)ld_u64(p + raw_pos + 8ull * k)) : 0.0;
+        } else {
+            // ((double)code * 2.0) * eb == (double)code * (2 eb) exactly
+            val = __dmul_rn(double(unzigzag16(z)), twoeb);
+        }
+        raw_i += __popc(rm);
+        bad |= raw_i > raw_count;
+        // the chain through shared memory: broadcast reads of the inputs,
+        // uniform writes of the running predictor
+        double *cv = chain[threadIdx.x >> 5];
+        cv[lane] = val;
+        __syncwarp();
+        if (rm == 0) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                pred = __dadd_rn(pred, cv[i]);
+                cv[32 + i] = pred;
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                const double x = cv[i];
+                pred = ((rm >> i) & 1) ? x : __dadd_rn(pred, x);
+                cv[32 + i] = pred;
+            }
+        }
+        __syncwarp();
+        __stcs(out + 2 * (e0 + lane), cv[32 + lane]);
+        __syncwarp();
+    }
+    if (lane == 0) {
+        if (bad) dev_fail(status, QZS_RAW_UNDER, slot_chunk ? slot_chunk[s] : s);
+        else if (h == 1 && raw_i != raw_count) dev_fail(status, QZS_RAW_UNUSED, slot_chunk ? slot_chunk[s] : s);
+    }
+}
+
 // Lossy decode (codec.cpp:217-249): thread = (slot, half).  WIDE: a launch
 // with fewer chunks than one CTA row set uses wide tiles (tile_width).
 template <bool WIDE>
@@ -1146,9 +1294,16 @@ void launch_dec_index(const uint8_t *arena, ChunkTable table, const uint64_t *sl
 
 void launch_decode(const uint8_t *arena, const DecIdx *idx, const uint64_t *slot_chunk,
                    uint64_t nslots, const CodecGeom &g, double2 *win, DevStatus *status,
-                   cudaStream_t s, const uint32_t *cond) {
+                   cudaStream_t s, const uint32_t *cond, bool sparse) {
     const unsigned grid = grid_for(nslots, kSlotsPerCta);
-    if (g.lossy && nslots < uint64_t(kSlotsPerCta))
+    // dense payloads: warp per chunk-half (parallel RLE expansion, serial
+    // predictor chain only); a store known to be mostly zero runs (right
+    // after init): thread per chunk-half with run fills
+    if (g.lossy && g.N >= 32 && !sparse) {
+        // warp per (slot, half): 4 slots per 256-thread CTA
+        k_dec_lossy_warp<<<grid_for(nslots, 4), 256, 0, s>>>(arena, idx, slot_chunk, nslots, g, win,
+                                                              status, cond);
+    } else if (g.lossy && nslots < uint64_t(kSlotsPerCta))
         k_dec_lossy<true><<<grid, 2 * kSlotsPerCta, 0, s>>>(arena, idx, slot_chunk, nslots, g, win,
                                                              status, cond);
     else if (g.lossy)

@@ -88,7 +88,7 @@ void launch_dec_index(const uint8_t *arena, ChunkTable table, const uint64_t *sl
 // launch does nothing unless *cond != 0 (device-side replay, see run_passes).
 void launch_decode(const uint8_t *arena, const DecIdx *idx, const uint64_t *slot_chunk,
                    uint64_t nslots, const CodecGeom &g, double2 *win, DevStatus *status,
-                   cudaStream_t s, const uint32_t *cond = nullptr);
+                   cudaStream_t s, const uint32_t *cond = nullptr, bool sparse = false);
 
 // Sequential encoder pass: codes, RLE sub-streams and raws into scratch.
 void launch_encode(const double2 *win, uint64_t nslots, const CodecGeom &g,

@@ -316,6 +316,7 @@ struct qzc_sim {
     bool force_replay = false;  // debug_flags bit 0
     cudaStream_t streams[3] = {nullptr, nullptr, nullptr};   // [2]: host-staged write-back
     bool pipelined = false;   // host-staged, one window: gather / compute / write-back streams
+    bool sparse_store = false;   // store = the init state (zero-chunk aliases): decode with run fills
     DevBuf gcub;              // scan scratch of the gather stream
     std::vector<cudaEvent_t> pevents;
     cudaEvent_t acct_ev[2] = {nullptr, nullptr};
@@ -377,22 +378,22 @@ void encode_window(qzc_context *ctx, Window &w, const CodecGeom &g, uint64_t nsl
 
 void decode_window(qzc_context *ctx, Window &w, const CodecGeom &g, uint64_t nslots,
                    const uint64_t *slot_chunk, const uint8_t *arena, ChunkTable t,
-                   uint64_t &launches, cudaStream_t s = nullptr) {
+                   uint64_t &launches, cudaStream_t s = nullptr, bool sparse = false) {
     if (!s) s = ctx->stream;
     launch_crc(ctx->tabs, arena, t, slot_chunk, nslots, true, ctx->status, s);
     launch_dec_index(arena, t, slot_chunk, nslots, g, w.idx.as<DecIdx>(), ctx->status, s);
     launch_decode(arena, w.idx.as<DecIdx>(), slot_chunk, nslots, g, w.amps.as<double2>(),
-                  ctx->status, s);
+                  ctx->status, s, nullptr, sparse);
     launches += 3;
 }
 
 // decode_window with an explicit cursor array and target window
 void decode_into(qzc_context *ctx, DecIdx *idx, double2 *amps, const CodecGeom &g, uint64_t nslots,
                  const uint64_t *slot_chunk, const uint8_t *arena, ChunkTable t, uint64_t &launches,
-                 cudaStream_t s) {
+                 cudaStream_t s, bool sparse = false) {
     launch_crc(ctx->tabs, arena, t, slot_chunk, nslots, true, ctx->status, s);
     launch_dec_index(arena, t, slot_chunk, nslots, g, idx, ctx->status, s);
-    launch_decode(arena, idx, slot_chunk, nslots, g, amps, ctx->status, s);
+    launch_decode(arena, idx, slot_chunk, nslots, g, amps, ctx->status, s, nullptr, sparse);
     launches += 3;
 }
 
@@ -1024,6 +1025,7 @@ int qzc_sim_init_basis(qzc_sim *sim) {
     QZ_CUDA(cudaMemcpyAsync(sim->acct.p, acct, 16, cudaMemcpyHostToDevice, s));
     QZ_CUDA(cudaStreamSynchronize(s));
     sim->initialized = true;
+    sim->sparse_store = true;
     sim->stats = qzc_sim_stats{};
     if (sim->host_res) QZ_CUDA(cudaMemset(sim->io_bytes.p, 0, 16));
     QZ_CUDA(cudaMemset(sim->replays.p, 0, 8));
@@ -1177,14 +1179,14 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
             QZ_CUDA(cudaStreamWaitEvent(S, pev(3 * w), 0));
             QZ_CUDA(cudaEventRecord(ev(4 * w), S));
             decode_into(ctx, In.idx.as<DecIdx>(), W.amps.as<double2>(), sim->geom, nslots, nullptr,
-                        In.stage_in.as<uint8_t>(), In.local(), ctx->launches, S);
+                        In.stage_in.as<uint8_t>(), In.local(), ctx->launches, S, sim->sparse_store);
             QZ_CUDA(cudaEventRecord(ev(4 * w + 1), S));
             if (dp.relaxed) {
                 uint32_t *flag = W.replay.as<uint32_t>();
                 if (sim->force_replay) QZ_CUDA(cudaMemsetAsync(flag, 1, 1, S));
                 ctx->launches += run_passes(dp, W.amps.as<double2>(), wbits, S, flag);
                 launch_decode(In.stage_in.as<uint8_t>(), In.idx.as<DecIdx>(), nullptr, nslots, sim->geom,
-                              W.amps.as<double2>(), ctx->status, S, flag);
+                              W.amps.as<double2>(), ctx->status, S, flag, sim->sparse_store);
                 ctx->launches += 1 + run_passes(dstrict, W.amps.as<double2>(), wbits, S, nullptr, flag);
                 k_replay_done<<<1, 1, 0, S>>>(flag, sim->replays.as<uint64_t>());
                 QZ_CHECK_LAUNCH();
@@ -1234,10 +1236,10 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
                 QZ_CHECK_LAUNCH();
                 ctx->launches += 5;
                 decode_window(ctx, W, sim->geom, nslots, nullptr, W.stage_in.as<uint8_t>(), W.local(),
-                              ctx->launches, S);
+                              ctx->launches, S, sim->sparse_store);
             } else {
                 decode_window(ctx, W, sim->geom, nslots, W.slot_chunk.as<uint64_t>(),
-                              sim->arena_ptr(a), sim->table(a), ctx->launches, S);
+                              sim->arena_ptr(a), sim->table(a), ctx->launches, S, sim->sparse_store);
             }
             QZ_CUDA(cudaEventRecord(ev(4 * w + 1), S));
             if (dp.relaxed) {
@@ -1248,10 +1250,11 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
                 // intact input payloads, then the strict plan
                 if (sim->host_res)
                     launch_decode(W.stage_in.as<uint8_t>(), W.idx.as<DecIdx>(), nullptr, nslots,
-                                  sim->geom, W.amps.as<double2>(), ctx->status, S, flag);
+                                  sim->geom, W.amps.as<double2>(), ctx->status, S, flag, sim->sparse_store);
                 else
                     launch_decode(sim->arena_ptr(a), W.idx.as<DecIdx>(), W.slot_chunk.as<uint64_t>(),
-                                  nslots, sim->geom, W.amps.as<double2>(), ctx->status, S, flag);
+                                  nslots, sim->geom, W.amps.as<double2>(), ctx->status, S, flag,
+                                  sim->sparse_store);
                 ctx->launches += 1 + run_passes(dstrict, W.amps.as<double2>(), wbits, S, nullptr, flag);
                 k_replay_done<<<1, 1, 0, S>>>(flag, sim->replays.as<uint64_t>());
                 QZ_CHECK_LAUNCH();
@@ -1301,6 +1304,7 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
             sim->stats.encode_seconds += ms[2] * 1e-3;
         }
         sim->cur = b;
+        sim->sparse_store = false;   // after a stage the payload density is unknown
         sim->stats.stages += 1;
         sim->stats.batches += nbatches;
         sim->stats.windows += nwin;
@@ -1435,6 +1439,7 @@ int qzc_sim_export(qzc_sim *sim, uint8_t *payload_out, uint64_t cap, uint32_t *s
 
 int qzc_sim_import(qzc_sim *sim, const uint8_t *payloads, const uint32_t *sizes, const uint32_t *crcs) {
     QZ_API_BEGIN
+    sim->sparse_store = false;
     qzc_context *ctx = sim->ctx;
     QZ_CUDA(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
@@ -1486,6 +1491,7 @@ int qzc_sim_read_chunks(qzc_sim *sim, uint64_t first, uint64_t count, double *am
 
 int qzc_sim_write_chunk(qzc_sim *sim, uint64_t index, const double *amps) {
     QZ_API_BEGIN
+    sim->sparse_store = false;
     qzc_context *ctx = sim->ctx;
     QZ_CUDA(cudaSetDevice(ctx->device));
     if (index >= sim->nchunks) throw Failure(QZC_ESTORE, "chunk index out of range: " + std::to_string(index));
