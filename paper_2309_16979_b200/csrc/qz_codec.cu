@@ -177,6 +177,7 @@ __global__ void __launch_bounds__(32 * kIdxWarps) k_dec_index_warp(
     }
     uint32_t pos = kHdr;
     uint32_t nsteps[2] = {0, 0}, start[2] = {0, 0};
+    bool ff_real[2] = {false, false};   // a 0xFF run touches the real half
     for (uint32_t k = 0; k < g.planes && !err; ++k) {
         uint64_t produced = 0;
         d.pos[k][0] = pos;
@@ -209,17 +210,20 @@ __global__ void __launch_bounds__(32 * kIdxWarps) k_dec_index_warp(
             // the first zero run before the end, the first missing pair
             uint32_t end_pair = ~0u, half_pair = ~0u, half_skip = 0, bad_pair = ~0u;
             uint64_t c = excl;
+            bool ff = false;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 const uint32_t idx = 8 * lane + j;
                 if (j >= int(avail)) { if (bad_pair == ~0u && c < total) bad_pair = idx; continue; }
                 if (c >= total) continue;
                 const uint32_t r = runs[j];
+                ff |= c < N && __ldg(p + p0 + 2 * j) == 0xFF;
                 if (bad_pair == ~0u && (r == 0 || c + r > total)) bad_pair = idx;
                 if (half_pair == ~0u && c <= N && N < c + r) { half_pair = idx; half_skip = uint32_t(N - c); }
                 if (end_pair == ~0u && c + r == total) end_pair = idx;
                 c += r;
             }
+            if (k < 2 && __any_sync(0xffffffffu, ff)) ff_real[k] = true;
             // warp-wide minima (first occurrence in stream order)
             uint32_t e_end = end_pair, e_half = half_pair, e_bad = bad_pair;
 #pragma unroll
@@ -266,7 +270,9 @@ __global__ void __launch_bounds__(32 * kIdxWarps) k_dec_index_warp(
         const uint64_t seg = N / 32 ? N / 32 : 1;
         const uint64_t e0 = uint64_t(lane) * seg, e1 = lane == 31 ? N : umin64(N, e0 + seg);
         uint64_t cnt = 0;
-        if (e0 < e1) {
+        // a sentinel needs 0xFF in both planes: without 0xFF runs in the real
+        // half of either plane there is none (the common dense case)
+        if (e0 < e1 && ff_real[0] && ff_real[1]) {
             uint32_t pp[2], rr[2];
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
