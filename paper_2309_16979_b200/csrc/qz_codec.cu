@@ -746,8 +746,7 @@ __global__ void __launch_bounds__(2 * kSlotsPerCta) k_dec_lossless(
 // One RLE sub-stream of one half, written to scratch 8 bytes at a time.
 struct Rle {
     uint8_t *out;
-    uint64_t word;
-    uint32_t nb, written, npairs;
+    uint32_t npairs;
     uint32_t cur, cnt;   // open run
     uint32_t hold;       // imaginary half: first run not emitted yet
     uint32_t head_byte, head_len;
@@ -755,8 +754,7 @@ struct Rle {
 
 __device__ __forceinline__ void rle_init(Rle &s, uint8_t *out, uint32_t hold) {
     s.out = out;
-    s.word = 0;
-    s.nb = s.written = s.npairs = 0;
+    s.npairs = 0;
     s.cur = 0x100;
     s.cnt = 0;
     s.hold = hold;
@@ -765,15 +763,10 @@ __device__ __forceinline__ void rle_init(Rle &s, uint8_t *out, uint32_t hold) {
 }
 
 __device__ __forceinline__ void rle_emit(Rle &s, uint32_t b, uint32_t run) {
-    s.word |= uint64_t(b | (run << 8)) << (8 * s.nb);
-    s.nb += 2;
+    // one 16-bit (byte, run) store per pair (fire-and-forget; L2 merges the
+    // consecutive pairs of a stream)
+    reinterpret_cast<uint16_t *>(s.out)[s.npairs] = uint16_t(b | (run << 8));
     ++s.npairs;
-    if (s.nb == 8) {
-        *reinterpret_cast<uint64_t *>(s.out + s.written) = s.word;
-        s.written += 8;
-        s.word = 0;
-        s.nb = 0;
-    }
 }
 
 // rle_encode (codec.cpp:52-63) restated as a streaming state machine.
@@ -834,7 +827,6 @@ __device__ __forceinline__ void rle_finish(Rle &s, uint32_t h, EncHalf &m, int k
         m.edge_byte[k] = uint8_t(s.head_byte);
         m.edge_len[k] = s.head_len;
     }
-    if (s.nb) *reinterpret_cast<uint64_t *>(s.out + s.written) = s.word;
     m.npairs[k] = s.npairs;
 }
 
@@ -937,15 +929,21 @@ __global__ void __launch_bounds__(2 * kSlotsPerCta) k_enc_lossy(
             }
         }
         if (active && !ff) {
+            // this half's component of the row, and the next forced index
+            // relative to the tile (~0 when beyond it)
+            const double *rowc = reinterpret_cast<const double *>(&at(buf, r, 0)) + h;
+            const uint64_t tile0 = h * N + e0;
+            uint32_t fr = next_forced - tile0 < te ? uint32_t(next_forced - tile0) : ~0u;
             for (uint32_t e = 0; e < te; ++e) {
-                const double v = comp(at(buf, r, e), h);
-                const uint64_t flat = h * N + e0 + e;
+                const double v = rowc[2 * e];
                 bool raw = false;
                 int32_t code = 0;
-                if (flat == next_forced) {
+                if (e == fr) {
+                    const uint64_t flat = tile0 + e;
                     raw = true;
                     do { ++fc; } while (fc < nforced && forced[fc] == flat);
                     next_forced = fc < nforced ? forced[fc] : ~uint64_t(0);
+                    fr = next_forced - tile0 < te ? uint32_t(next_forced - tile0) : ~0u;
                 } else {
                     const double q = quantise(__dsub_rn(v, pred), g);
                     if (!(fabs(q) < 32768.0)) {
