@@ -46,6 +46,8 @@ def parse_args():
     ap.add_argument("--m", type=int, default=30)
     ap.add_argument("--eb", type=float, default=1e-5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-fidelity", action="store_true",
+                    help="skip the uncompressed fp64 reference run used for the fidelity figure")
     ap.add_argument("--cpu-budget", type=float, default=20.0,
                     help="seconds of reference CPU work per sample")
     ap.add_argument("--no-fuse", action="store_true")
@@ -63,13 +65,22 @@ def parse_args():
 class ClockSampler:
     """nvidia-smi sampling DURING the timed region (B200_PROFILING.md)."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    Q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, device: int):
         self.device = device
         self.proc = None
+        self.t0 = self.t1 = None
+
+    def mark_begin(self):
+        import datetime
+        self.t0 = datetime.datetime.now()
+
+    def mark_end(self):
+        import datetime
+        self.t1 = datetime.datetime.now()
 
     def start(self):
         try:
@@ -85,12 +96,23 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
         out, _ = self.proc.communicate(timeout=10)
+        import datetime
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in out.strip().splitlines():
             f = [x.strip() for x in line.split(",")]
-            if len(f) < 9:
+            if len(f) < 10:
                 continue
+            try:
+                ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f")
+            except ValueError:
+                ts = None
+            # samples inside the timed region only (plus one sampling period)
+            if ts and self.t0 and self.t1 and not (
+                    self.t0 - datetime.timedelta(milliseconds=100) <= ts
+                    <= self.t1 + datetime.timedelta(milliseconds=100)):
+                continue
+            f = f[1:]
             try:
                 sm.append(float(f[1]))
                 mx.append(float(f[2]))
@@ -247,16 +269,19 @@ def main() -> int:
 
     # ---- timed region: K steps, device time (CUDA events on the engine stream)
     clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(1.0)   # nvidia-smi's first samples arrive before the timed region
     barrier()
     eng.timer_begin()
     eng.timer_end()
-    clocks.start()
     launches0 = eng.kernel_launches
+    clocks.mark_begin()
     eng.timer_begin()
     for _ in range(args.steps):
         sim.init_basis()
         sim.run(gates)
     t_dev = eng.timer_end()
+    clocks.mark_end()
     launches = eng.kernel_launches - launches0
     clk = clocks.stop()
     t_max = max_over_ranks(t_dev)
@@ -286,6 +311,17 @@ def main() -> int:
 
     if rank != 0:
         return 0
+
+    # ---- fidelity of the compressed run against an uncompressed fp64 run of
+    # the same circuit on the GPU (outside the timed region; BASELINE metric)
+    fidelity = None
+    if not args.no_fidelity:
+        try:
+            dense = eng.dense_state(args.n, gates)
+            fidelity = sim.fidelity(dense)
+            dense.free()
+        except Exception as e:  # not enough HBM for the dense state next to the store
+            fidelity = f"unavailable: {e}"
 
     value = world * ngates * args.steps / t_max
     # ---- roofline of the dominant kernel (from the engine's event timers)
@@ -347,6 +383,7 @@ def main() -> int:
                                             gates=ngates),
         "circuit_seconds": t_max / args.steps,
         "compression_ratio": st["ratio"],
+        "fidelity": fidelity,
         "peak_ratio": st["dense_bytes"] / st["peak_bytes"] if st["peak_bytes"] else None,
         "digest": f"{digest:016x}",
         "phases_s": phases, "stages": st["stages"], "gate_passes": st["gate_passes"],
