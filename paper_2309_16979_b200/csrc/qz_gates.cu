@@ -381,7 +381,9 @@ GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_
                       bool relax) {
     GatePlan plan;
     const uint32_t k = std::min(kmax, nbits);
-    const uint32_t low = std::min<uint32_t>(3, k);
+    // bits always in the tile (global segments of 2^low amplitudes)
+    static const uint32_t kLow = getenv("QZ_TILE_LOW") ? uint32_t(atoi(getenv("QZ_TILE_LOW"))) : 3u;
+    const uint32_t low = std::min<uint32_t>(kLow, k);
     const uint64_t low_mask = (uint64_t(1) << low) - 1;
     relax = relax && fuse && nbits > k;
     std::vector<Unit> units = make_units(gates, relax);

@@ -294,3 +294,22 @@ def test_export_into_pinned_buffer(engine, oracle, golden):
     assert view.tobytes() == blob and (s2 == sizes).all() and (c2 == crcs).all()
     with pytest.raises(ValueError):
         sim.export(engine.pinned(8))
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_random_circuits_relaxed_vs_reference(engine, oracle, seed):
+    """Seeded random circuits over the whole gate set plus diagonal-unit runs,
+    windows wider than one tile (relaxed passes, swap networks, replays):
+    final store digest equals the reference's."""
+    from tests_util import diagonal_heavy_circuit, random_circuit
+    rng = np.random.default_rng(1000 + seed)
+    n = 14
+    g = random_circuit(n, 60, 2000 + seed) + diagonal_heavy_circuit(n, 80, 3000 + seed)
+    q = rng.permutation(n)
+    g += [("swap", (int(q[2 * i]), int(q[2 * i + 1])), ()) for i in range(int(rng.integers(2, 6)))]
+    g += random_circuit(n, 20, 4000 + seed)
+    eb = [0.0, 1e-7, 1e-5][seed % 3]
+    c, m = (4, 14) if seed % 2 else (6, 12)
+    ref = oracle.run(n, g, c, m, eb)["digest"]
+    sim = run_sim(engine, n, c, m, eb, g)
+    assert sim.digest() == ref
