@@ -313,3 +313,55 @@ def test_random_circuits_relaxed_vs_reference(engine, oracle, seed):
     ref = oracle.run(n, g, c, m, eb)["digest"]
     sim = run_sim(engine, n, c, m, eb, g)
     assert sim.digest() == ref
+
+
+def test_qft30_full_size_parity(engine, oracle):
+    """Beyond the oracle's reach: at the bench size the relaxed
+    plan (5 passes) and the strict plan (54 passes) give the same store bytes,
+    and sampled chunks decode through the C oracle to the GPU's values."""
+    from paper_2309_16979_b200 import circuits as CI
+    g = CI.qft(30)
+    sim = run_sim(engine, 30, 16, 30, 1e-5, g)
+    d_rel = sim.digest()
+    blob, sizes, crcs = sim.export()
+    offs = np.concatenate([[0], np.cumsum(sizes.astype(np.int64))])
+    rng = np.random.default_rng(30)
+    for k in [0, 1, sim.chunk_count - 1] + list(rng.integers(0, sim.chunk_count, 5)):
+        k = int(k)
+        p = blob[offs[k]:offs[k + 1]]
+        assert oracle.crc32(p) == int(crcs[k])
+        want = oracle.decompress(p, int(crcs[k]), 1 << 16)
+        got = sim.read_chunks(k, 1)
+        assert got.tobytes() == want.tobytes(), k
+    assert sim.stats()["gate_passes"] == 5
+    sim.close()
+    strict = run_sim(engine, 30, 16, 30, 1e-5, g, fuse="strict")
+    assert strict.digest() == d_rel
+    assert f"{d_rel:016x}" == "983d82375d9c6325"   # the bench's digest (both plans agree)
+    strict.close()
+
+
+def _large_cases():
+    import json
+    from pathlib import Path
+    f = Path(__file__).parent / "golden" / "golden_large.json"
+    return json.loads(f.read_text()) if f.exists() else []
+
+
+@pytest.mark.parametrize("idx", range(4))
+def test_large_runs_vs_reference(engine, idx):
+    """Reference digests at 2^26..2^28 (tests/golden/make_golden_large.py):
+    relaxed passes, swap networks and multi-stage windows at scale."""
+    from paper_2309_16979_b200 import circuits as CI
+    cases = _large_cases()
+    if idx >= len(cases):
+        pytest.skip("golden_large.json not generated")
+    rec = cases[idx]
+    n = rec["n"]
+    g = CI.supremacy(n, **rec["kw"]) if rec["circuit"] == "supremacy" else CI.make(rec["circuit"], n)
+    sim = run_sim(engine, n, rec["c"], rec["m"], rec["eb"], g)
+    st = sim.stats()
+    assert f"{sim.digest():016x}" == rec["digest"], rec
+    assert st["stages"] == rec["stages"]
+    assert st["current_bytes"] == rec["current_bytes"]
+    sim.close()
