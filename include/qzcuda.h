@@ -223,9 +223,11 @@ typedef struct qzc_sim_stats {
     uint64_t peak_bytes;
     uint64_t dense_bytes;
     uint64_t windows;
-    uint64_t replays;            /* windows whose relaxed gate passes met a
-                                    zero and were replayed with the strict
-                                    plan (device-side, same result)         */
+    uint64_t replays;            /* relaxed gate passes that met a zero / -0
+                                    they could not evaluate without amplitudes
+                                    outside their tile and were re-applied by
+                                    their strict sub-plan (device-side, same
+                                    bytes)                                    */
 } qzc_sim_stats;
 
 int qzc_sim_create(qzc_context *ctx, const qzc_sim_config *cfg,

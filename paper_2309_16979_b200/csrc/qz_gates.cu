@@ -387,8 +387,9 @@ GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_
     const uint64_t low_mask = (uint64_t(1) << low) - 1;
     relax = relax && fuse && nbits > k;
     std::vector<Unit> units = make_units(gates, relax);
-    for (Unit &u : units)
-        if (u.diag && !unit_safe(gates, u)) u.diag = false;
+    // units with steps that are not +0-safe are relaxed too: their steps are
+    // zero-checked and a zero raises the replay flag of the pass
+    (void)unit_safe;
     std::vector<size_t> members;   // unit indices of the open pass
     uint64_t tmask = low_mask;
     auto close = [&]() {
@@ -406,6 +407,8 @@ GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_
         pd.tmask = tmask;
         pd.first_gate = (uint32_t)plan.gates.size();
         pd.ngates = (uint32_t)members.size();
+        pd.dg0 = (uint32_t)units[members.front()].first;
+        pd.dg1 = (uint32_t)(units[members.back()].first + units[members.back()].count);
         pd.first_group = (uint32_t)plan.groups.size();
         auto local = [&](uint32_t b) {
             return (uint32_t)__builtin_popcountll(tmask & ((uint64_t(1) << b) - 1));
@@ -566,6 +569,7 @@ GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_
                     for (uint32_t e = 0; e < 16; ++e)
                         if ((t.kinds >> (4 * e)) & 15u) t.steps |= 1u << e;
                     gd.pz_stable &= pz ? 1u : 0u;
+                    gd.unsafe |= pz ? 0u : 1u;
                     gd.relaxed = 1;
                     plan.gates.push_back(t);
                     ++ei;
@@ -701,8 +705,10 @@ GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_
         close_group();
         pd.ngroups = (uint32_t)plan.groups.size() - pd.first_group;
         pd.pz_stable = 1;
-        for (uint32_t gi = pd.first_group; gi < pd.first_group + pd.ngroups; ++gi)
+        for (uint32_t gi = pd.first_group; gi < pd.first_group + pd.ngroups; ++gi) {
             pd.pz_stable &= plan.groups[gi].pz_stable;
+            if (plan.groups[gi].relaxed) pd.relaxed = std::max<uint32_t>(pd.relaxed, plan.groups[gi].unsafe ? 2u : 1u);
+        }
         plan.passes.push_back(pd);
         members.clear();
         tmask = low_mask;
@@ -718,6 +724,9 @@ GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_
             pd.kind = PASS_SWAPS;
             pd.first_gate = (uint32_t)u.first;
             pd.ngates = u.count;
+            pd.dg0 = (uint32_t)u.first;
+            pd.dg1 = (uint32_t)(u.first + u.count);
+            pd.relaxed = 1;
             for (uint32_t b = 0; b < 48; ++b) pd.perm[b] = uint8_t(b);
             for (size_t i = u.first; i < u.first + u.count; ++i) {
                 pd.perm[gates[i].b0] = uint8_t(gates[i].b1);
@@ -755,8 +764,8 @@ void upload_plan(const GatePlan &plan, DevPlan &out, cudaStream_t s) {
     out.ngroups = plan.groups.size();
     out.host_passes = plan.passes;
     out.relaxed = false;
-    for (const GroupDesc &g : plan.groups) out.relaxed |= g.relaxed != 0;
-    for (const PassDesc &pd : plan.passes) out.relaxed |= pd.kind == PASS_SWAPS;
+    for (const PassDesc &pd : plan.passes) out.relaxed |= pd.relaxed != 0;
+    out.replay_range.clear();
     if (out.ngates > out.cap_gates) {
         if (out.gates) QZ_CUDA(cudaFree(out.gates));
         out.cap_gates = std::max<size_t>(out.ngates * 2, 256);
@@ -1519,7 +1528,7 @@ __device__ void smem_generic(double2 *s, uint32_t tile, const TileGate &g) {
 // each group is applied by 2^(k-kRegBits) threads holding NB amplitudes in
 // registers.  Every thread moves exactly NB amplitudes per tile in each
 // direction, all issued before any is consumed (cp.async in, batched stores).
-__global__ void __launch_bounds__(1 << (kTileBits - kRegBits), (kTileBits >= 12 ? 1 : (kTileBits == 11 ? QZ_MIN_CTAS : 4))) tile_pass_reg(double2 *__restrict__ buf, uint32_t nbits,
+__global__ void __launch_bounds__(1 << (kTileBits - kRegBits), (kTileBits >= 12 ? 1 : (kTileBits == 11 ? QZ_MIN_CTAS : 4))) tile_pass_reg(const double2 *__restrict__ src, double2 *__restrict__ dst, uint32_t nbits,
                                                          PassDesc pd,
                                                          const GroupDesc *__restrict__ groups,
                                                          const TileGate *__restrict__ gates,
@@ -1550,7 +1559,7 @@ __global__ void __launch_bounds__(1 << (kTileBits - kRegBits), (kTileBits >= 12 
 #pragma unroll
         for (int i = 0; i < NB; ++i) {
             const uint32_t l = tid + i * nth;
-            cp_async16(s + swz(l), buf + base + offhi[l >> L] + (l & lowmask));
+            cp_async16(s + swz(l), src + base + offhi[l >> L] + (l & lowmask));
         }
         cp_async_wait_all();
         __syncthreads();
@@ -1568,7 +1577,15 @@ __global__ void __launch_bounds__(1 << (kTileBits - kRegBits), (kTileBits >= 12 
         }
         if (pd.pz_stable && !__syncthreads_or(any != 0)) {
             // an all-(+0) tile is a fixed point of the whole pass: skip it
+            // (out of place: the output still needs the zeros)
             if (counters && tid == 0) atomicAdd(&counters[0], 1ull);
+            if (src != dst) {
+#pragma unroll
+                for (int i = 0; i < NB; ++i) {
+                    const uint32_t l = tid + i * nth;
+                    __stcs(dst + base + offhi[l >> L] + (l & lowmask), make_double2(0.0, 0.0));
+                }
+            }
             continue;
         }
         bool clean = __syncthreads_and(okv) != 0;
@@ -1675,7 +1692,7 @@ __global__ void __launch_bounds__(1 << (kTileBits - kRegBits), (kTileBits >= 12 
 #pragma unroll
         for (int i = 0; i < NB; ++i) {
             const uint32_t l = tid + i * nth;
-            __stcs(buf + base + offhi[l >> L] + (l & lowmask), out[i]);
+            __stcs(dst + base + offhi[l >> L] + (l & lowmask), out[i]);
         }
         __syncthreads();
     }
@@ -1700,7 +1717,8 @@ __device__ __forceinline__ uint64_t permute_bits(uint64_t x, const uint8_t *perm
 // 5 so both the contiguous fill and the permuted gather spread over banks
 __device__ __forceinline__ uint32_t swz10(uint32_t l) { return l ^ ((l >> kSwapLow) & 31u); }
 
-__global__ void __launch_bounds__(256) tile_swaps(double2 *__restrict__ buf, uint32_t nbits,
+__global__ void __launch_bounds__(256) tile_swaps(const double2 *__restrict__ src, double2 *__restrict__ dst,
+                                                  uint32_t nbits,
                                                   PassDesc pd, uint32_t *__restrict__ flag,
                                                   const uint32_t *__restrict__ cond) {
     if (cond && *cond == 0) return;
@@ -1758,8 +1776,8 @@ __global__ void __launch_bounds__(256) tile_swaps(double2 *__restrict__ buf, uin
             ra[i] = rb[i] = make_double2(0.0, 0.0);
             if (l < tile) {
                 const uint64_t off = loff[l];
-                ra[i] = __ldcs(buf + base + off);
-                if (pair) rb[i] = __ldcs(buf + pbase + off);
+                ra[i] = __ldcs(src + base + off);
+                if (pair) rb[i] = __ldcs(src + pbase + off);
             }
         }
 #pragma unroll
@@ -1779,12 +1797,12 @@ __global__ void __launch_bounds__(256) tile_swaps(double2 *__restrict__ buf, uin
             const uint32_t l = tid + i * nth;
             if (l >= tile) break;
             const uint64_t off = loff[l];
-            const uint32_t src = swz10(lperm[l]);
+            const uint32_t srcl = swz10(lperm[l]);
             if (pair) {
-                __stcs(buf + base + off, tb[src]);
-                __stcs(buf + pbase + off, ta[src]);
+                __stcs(dst + base + off, tb[srcl]);
+                __stcs(dst + pbase + off, ta[srcl]);
             } else {
-                __stcs(buf + base + off, ta[src]);
+                __stcs(dst + base + off, ta[srcl]);
             }
         }
         __syncthreads();
@@ -1851,39 +1869,114 @@ void dump_debug_counters() {
     QZ_CUDA(cudaMemset(p, 0, sizeof h));
 }
 
-uint64_t run_passes(const DevPlan &plan, double2 *buf, uint32_t nbits, cudaStream_t s,
-                    uint32_t *flag, const uint32_t *cond) {
-    if (plan.relaxed && !flag) throw Failure(QZC_EDEVICE, "relaxed plan without a replay flag");
+namespace {
+
+// Count a replayed pass and clear the flag for the next relaxed pass.
+__global__ void k_flag_done(uint32_t *flag, uint64_t *count) {
+    if (count) *count += *flag;
+    *flag = 0;
+}
+
+void set_attrs() {
     static bool attr_set = false;
     if (!attr_set) {
         QZ_CUDA(cudaFuncSetAttribute(tile_pass_reg, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      110 * 1024));
         attr_set = true;
     }
-    uint64_t launches = 0;
-    for (const PassDesc &pd : plan.host_passes) {
-        if (pd.kind == PASS_SWAPS) {
-            if (!flag && !cond) throw Failure(QZC_EDEVICE, "swap-network pass without a replay flag");
-            const uint64_t tiles = uint64_t(1) << (nbits > 2 * kSwapLow ? nbits - 2 * kSwapLow : 0);
-            const uint64_t grid = std::min<uint64_t>(std::max<uint64_t>(tiles, 1), uint64_t(kNumSMs) * 8);
-            tile_swaps<<<(unsigned)grid, 256, 0, s>>>(buf, nbits, pd, flag, cond);
-        } else if (pd.k < (uint32_t)kRegBits + 1) {
-            // tile == whole buffer (nbits < 4)
-            tile_pass_tiny<<<1, 32, 0, s>>>(buf, nbits, pd, plan.groups, plan.gates, cond);
-        } else {
-            const uint32_t tile = 1u << pd.k;
-            const uint64_t ntiles = uint64_t(1) << (nbits - pd.k);
-            const uint32_t threads = tile >> kRegBits;
-            const size_t smem = sizeof(double2) * tile + sizeof(uint64_t) * (tile >> pd.lowbits);
-            const uint64_t grid = std::min<uint64_t>(ntiles, uint64_t(kNumSMs) * 2 * 8);
-            tile_pass_reg<<<(unsigned)grid, threads, smem, s>>>(buf, nbits, pd, plan.groups,
-                                                               plan.gates, ntiles, debug_counters(),
-                                                               flag, cond);
-        }
-        QZ_CHECK_LAUNCH();
-        ++launches;
+}
+
+void launch_pass(const DevPlan &plan, const PassDesc &pd, const double2 *src, double2 *dst,
+                 uint32_t nbits, cudaStream_t s, uint32_t *flag, const uint32_t *cond) {
+    if (pd.kind == PASS_SWAPS) {
+        const uint64_t tiles = uint64_t(1) << (nbits > 2 * kSwapLow ? nbits - 2 * kSwapLow : 0);
+        const uint64_t grid = std::min<uint64_t>(std::max<uint64_t>(tiles, 1), uint64_t(kNumSMs) * 8);
+        tile_swaps<<<(unsigned)grid, 256, 0, s>>>(src, dst, nbits, pd, flag, cond);
+    } else if (pd.k < (uint32_t)kRegBits + 1) {
+        // tile == whole buffer (nbits < 4): never relaxed, in place
+        if (src != dst) throw Failure(QZC_EDEVICE, "tiny pass out of place");
+        tile_pass_tiny<<<1, 32, 0, s>>>(dst, nbits, pd, plan.groups, plan.gates, cond);
+    } else {
+        const uint32_t tile = 1u << pd.k;
+        const uint64_t ntiles = uint64_t(1) << (nbits - pd.k);
+        const uint32_t threads = tile >> kRegBits;
+        const size_t smem = sizeof(double2) * tile + sizeof(uint64_t) * (tile >> pd.lowbits);
+        const uint64_t grid = std::min<uint64_t>(ntiles, uint64_t(kNumSMs) * 2 * 8);
+        tile_pass_reg<<<(unsigned)grid, threads, smem, s>>>(src, dst, nbits, pd, plan.groups, plan.gates,
+                                                           ntiles, debug_counters(), flag, cond);
     }
-    return launches;
+    QZ_CHECK_LAUNCH();
+}
+
+} // namespace
+
+uint64_t run_passes(const DevPlan &plan, double2 *buf, uint32_t nbits, cudaStream_t s,
+                    const uint32_t *cond) {
+    if (plan.relaxed) throw Failure(QZC_EDEVICE, "relaxed plan run without its replay plan");
+    set_attrs();
+    for (const PassDesc &pd : plan.host_passes) launch_pass(plan, pd, buf, buf, nbits, s, nullptr, cond);
+    return plan.host_passes.size();
+}
+
+void flag_done(uint32_t *flag, uint64_t *replays, cudaStream_t s) {
+    k_flag_done<<<1, 1, 0, s>>>(flag, replays);
+    QZ_CHECK_LAUNCH();
+}
+
+double2 *run_relaxed(const DevPlan &plan, const DevPlan &replay, double2 *buf, double2 *alt,
+                     uint32_t nbits, cudaStream_t s, uint32_t *flag, uint32_t *win_flag,
+                     uint64_t *replays, bool force_replay, uint64_t &launches) {
+    set_attrs();
+    double2 *cur = buf, *oth = alt;
+    for (size_t p = 0; p < plan.host_passes.size(); ++p) {
+        const PassDesc &pd = plan.host_passes[p];
+        if (pd.relaxed != 2) {
+            if (pd.relaxed && force_replay) QZ_CUDA(cudaMemsetAsync(win_flag, 1, 1, s));
+            launch_pass(plan, pd, cur, cur, nbits, s, pd.relaxed ? win_flag : nullptr, nullptr);
+            ++launches;
+            continue;
+        }
+        if (force_replay) QZ_CUDA(cudaMemsetAsync(flag, 1, 1, s));
+        launch_pass(plan, pd, cur, oth, nbits, s, flag, nullptr);
+        // strict replay of this pass from its untouched input (no-ops unless flagged)
+        const auto &rr = plan.replay_range.at(p);
+        for (uint32_t q = rr.first; q < rr.second; ++q)
+            launch_pass(replay, replay.host_passes[q], q == rr.first ? cur : oth, oth, nbits, s, nullptr, flag);
+        k_flag_done<<<1, 1, 0, s>>>(flag, replays);
+        QZ_CHECK_LAUNCH();
+        launches += 2 + (rr.second - rr.first);
+        std::swap(cur, oth);
+    }
+    return cur;
+}
+
+void upload_replay(const std::vector<DevGate> &gates, uint32_t nbits, uint32_t kmax,
+                   DevPlan &relaxed_dev, DevPlan &out, cudaStream_t s) {
+    GatePlan all;
+    relaxed_dev.replay_range.assign(relaxed_dev.host_passes.size(), {0u, 0u});
+    for (size_t p = 0; p < relaxed_dev.host_passes.size(); ++p) {
+        const PassDesc &pd = relaxed_dev.host_passes[p];
+        if (pd.relaxed != 2) continue;
+        const std::vector<DevGate> sub(gates.begin() + pd.dg0, gates.begin() + pd.dg1);
+        const GatePlan gp = build_passes(sub, nbits, kmax, true, false);
+        const uint32_t goff = (uint32_t)all.gates.size(), groff = (uint32_t)all.groups.size();
+        relaxed_dev.replay_range[p].first = (uint32_t)all.passes.size();
+        for (PassDesc q : gp.passes) {
+            q.first_group += groff;
+            q.first_gate += goff;
+            q.dg0 += pd.dg0;
+            q.dg1 += pd.dg0;
+            all.passes.push_back(q);
+        }
+        relaxed_dev.replay_range[p].second = (uint32_t)all.passes.size();
+        for (GroupDesc g : gp.groups) {
+            g.first_gate += goff;
+            g.first_fast += goff;
+            all.groups.push_back(g);
+        }
+        all.gates.insert(all.gates.end(), gp.gates.begin(), gp.gates.end());
+    }
+    upload_plan(all, out, s);
 }
 
 } // namespace qz

@@ -92,7 +92,7 @@ struct GroupDesc {
     uint32_t pz_stable;    // every gate maps an all-(+0) block to all-(+0)
     uint32_t relaxed;      // holds OP_PDIAG units: no exact path; a block that
                            // cannot take the fast path raises the replay flag
-    uint32_t pad;
+    uint32_t unsafe;       // some of its OP_PDIAG steps are not +0-safe (checked)
 };
 
 // A fused pass: gates whose buffer bits all lie in the tile bit set T.
@@ -107,6 +107,11 @@ struct PassDesc {
     uint32_t pz_stable;    // all groups pz_stable: an all-(+0) tile is left untouched
     uint32_t kind;         // PASS_TILE, or PASS_SWAPS: a run of disjoint SWAPs as one
                            // bit permutation (perm[b] = image of buffer bit b)
+    uint32_t dg0, dg1;     // the stage gates [dg0, dg1) this pass applies
+    uint32_t relaxed;      // 0 strict; 1 relaxed, +0-safe units / swap network: in place,
+                           // a flag replays the whole window; 2 relaxed with checked
+                           // units: out of place, replayed pass by pass
+    uint32_t pad5;
     uint8_t perm[48];
 };
 
@@ -140,21 +145,41 @@ struct DevPlan {
     GroupDesc *groups = nullptr;
     size_t ngates = 0, ngroups = 0;
     std::vector<PassDesc> host_passes;
-    bool relaxed = false;   // some group is relaxed: may raise the replay flag
+    bool relaxed = false;   // some pass may raise the replay flag
     size_t cap_gates = 0, cap_groups = 0;   // device capacity (grow-only reuse)
+    // strict replay plan: passes [replay_range[p].first, .second) of `replay`
+    // re-apply relaxed pass p's gates with every qubit in the tile
+    std::vector<std::pair<uint32_t, uint32_t>> replay_range;
 };
 // Stream-ordered upload into `out`, reusing its device buffers when they are
 // large enough (no allocator calls on the steady-state stage loop).
 void upload_plan(const GatePlan &plan, DevPlan &out, cudaStream_t s);
 void free_plan(DevPlan &p);   // releases the device buffers
 
-// Launch every pass of `plan` over buf (2^nbits amplitudes).  Returns the
-// number of kernel launches.  flag: set to 1 by a relaxed group that could
-// not take the fast path (the buffer is then garbage and must be rebuilt
-// from the input and replayed with a strict plan).  cond != nullptr: every
-// launch returns immediately unless *cond != 0 (device-side conditional).
+// Launch every pass of a strict `plan` in place over buf (2^nbits
+// amplitudes).  Returns the number of kernel launches.
 uint64_t run_passes(const DevPlan &plan, double2 *buf, uint32_t nbits, cudaStream_t s,
-                    uint32_t *flag = nullptr, const uint32_t *cond = nullptr);
+                    const uint32_t *cond = nullptr);
+// Count a replay and clear the flag (stream-ordered).
+void flag_done(uint32_t *flag, uint64_t *replays, cudaStream_t s);
+
+// Relaxed plan (built with relax = true) and its strict replay plan (upload_replay):
+// relaxed passes run out of place, buf -> alt, and raise *flag when a tile
+// cannot be evaluated exactly (a zero / -0 where partners outside the tile
+// would decide the bytes, or -0 under a swap network); the pass is then
+// re-applied from its untouched input by the strict sub-plan (launches that
+// are no-ops unless *flag), and *flag is cleared (replays counted in
+// *replays).  Returns the buffer holding the result (buf or alt).
+// Passes with relaxed == 1 run in place and raise *win_flag (sticky; the
+// caller replays the whole window from its payloads when set).
+double2 *run_relaxed(const DevPlan &plan, const DevPlan &replay, double2 *buf, double2 *alt,
+                     uint32_t nbits, cudaStream_t s, uint32_t *flag, uint32_t *win_flag,
+                     uint64_t *replays, bool force_replay, uint64_t &launches);
+
+// Strict sub-plans of every relaxed pass of `relaxed`, concatenated into
+// `out` (ranges recorded in relaxed_dev.replay_range).
+void upload_replay(const std::vector<DevGate> &gates, uint32_t nbits, uint32_t kmax,
+                   DevPlan &relaxed_dev, DevPlan &out, cudaStream_t s);
 void dump_debug_counters();
 
 } // namespace qz

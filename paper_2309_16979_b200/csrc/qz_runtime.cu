@@ -20,6 +20,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <functional>
 #include <vector>
 
 #include "qz_codec.cuh"
@@ -72,6 +73,7 @@ const char *status_text(int code) {
 struct Window {
     DevBuf amps, scratch, meta, idx, slot_chunk, sizes, reloff, base, cub, delta, maxd;
     DevBuf replay;   // uint32 flag raised by a relaxed gate pass
+    DevBuf alt;      // second dense buffer: relaxed passes run out of place
     // host-staged residency: HBM staging of the window's payloads
     DevBuf stage_in, stage_out, lt_off, lt_len, lt_crc, padded, soff, lused, hbase;
     uint64_t slots = 0, stage_in_cap = 0, stage_out_cap = 0;
@@ -147,7 +149,7 @@ struct Window {
     void release() {
         for (DevBuf *b : {&amps, &scratch, &meta, &idx, &slot_chunk, &sizes, &reloff, &base, &cub,
                           &delta, &maxd, &stage_in, &stage_out, &lt_off, &lt_len, &lt_crc, &padded,
-                          &soff, &lused, &hbase, &out_off, &out_len, &out_crc, &replay})
+                          &soff, &lused, &hbase, &out_off, &out_len, &out_crc, &replay, &alt})
             b->release();
     }
 };
@@ -184,12 +186,6 @@ __global__ void k_pack_payloads(const uint8_t *__restrict__ arena, ChunkTable t,
 __global__ void k_io_count(const uint64_t *soff, const uint64_t *padded, uint64_t nslots,
                            uint64_t *io) {
     atomicAdd((unsigned long long *)&io[0], (unsigned long long)(soff[nslots - 1] + padded[nslots - 1]));
-}
-// Relaxed-plan replay bookkeeping: count the windows that were replayed and
-// clear the flag for the next window on this stream.
-__global__ void k_replay_done(uint32_t *flag, uint64_t *count) {
-    *count += *flag;
-    *flag = 0;
 }
 __global__ void k_io_count_out(const uint64_t *used_local, uint64_t *io) {
     atomicAdd((unsigned long long *)&io[1], (unsigned long long)((*used_local + 15) / 16 * 16));
@@ -303,7 +299,7 @@ struct qzc_sim {
     DevBuf io_bytes;  // uint64[2]: host->HBM and HBM->host payload bytes
     DevBuf replays;   // uint64: windows replayed with the strict plan
     DevBuf small;     // uint64[4] scratch for init_basis (slot / forced lists)
-    DevPlan plans[2]; // stage plans (relaxed / strict), device buffers reused
+    DevPlan plans[3]; // stage plans (relaxed / per-pass replay / whole strict), device buffers reused
     DevBuf used;   // uint64[2] bump pointers
     DevBuf acct;   // int64[2] current / peak
     uint64_t arena_cap = 0;
@@ -397,6 +393,13 @@ void decode_into(qzc_context *ctx, DecIdx *idx, double2 *amps, const CodecGeom &
     launches += 3;
 }
 
+// The stage's fused passes over window W: relaxed passes run out of place
+// between W.amps and W.alt with their per-pass strict replay; the result is
+// left in W.amps (the two buffers swap roles when needed).
+void run_window_passes(qzc_sim *sim, Window &W, const DevPlan &dp, const DevPlan &dsub, const DevPlan &dfull,
+                       uint32_t wbits, cudaStream_t S,
+                       const std::function<void(double2 *, const uint32_t *)> &redecode);
+
 uint32_t log2u(uint64_t x) {
     uint32_t r = 0;
     while ((uint64_t(1) << r) < x) ++r;
@@ -427,7 +430,7 @@ void sim_alloc(qzc_sim *sim) {
     budget = budget > (uint64_t(3) << 30) ? budget - (uint64_t(3) << 30) : budget / 2;
     // dense + encode scratch + metadata (+ payload staging when host-staged:
     // two input sets and one output)
-    const uint64_t per_amp = 16 + 2 * sim->geom.half_stride / sim->N + 8 +
+    const uint64_t per_amp = 16 + (sim->relax ? 16 : 0) + 2 * sim->geom.half_stride / sim->N + 8 +
                              (sim->host_res ? 3 * (payload_bound(sim->N, sim->eb) + 48) / sim->N + 1 : 0);
     const uint64_t state_amps = uint64_t(1) << sim->n;
     uint64_t wa = sim->cfg.window_amps;
@@ -449,6 +452,10 @@ void sim_alloc(qzc_sim *sim) {
     const uint64_t win_slots = std::max<uint64_t>(wa / sim->N, 2);
     sim->win.reserve(sim->geom, win_slots);
     if (sim->two_windows) sim->win2.reserve(sim->geom, win_slots);
+    if (sim->relax) {
+        sim->win.alt.ensure(sizeof(double2) * win_slots * sim->N);
+        if (sim->two_windows) sim->win2.alt.ensure(sizeof(double2) * win_slots * sim->N);
+    }
     for (int i = 0; i < 2; ++i) {
         QZ_CUDA(cudaStreamCreateWithFlags(&sim->streams[i], cudaStreamNonBlocking));
         QZ_CUDA(cudaEventCreateWithFlags(&sim->acct_ev[i], cudaEventDisableTiming));
@@ -497,6 +504,28 @@ void sim_alloc(qzc_sim *sim) {
         // +64: the decoder's RLE readers fetch 16 bytes ahead
         for (int i = 0; i < 2; ++i) sim->arena[i].ensure(sim->arena_cap + 64);
     }
+}
+
+void run_window_passes(qzc_sim *sim, Window &W, const DevPlan &dp, const DevPlan &dsub, const DevPlan &dfull,
+                       uint32_t wbits, cudaStream_t S,
+                       const std::function<void(double2 *, const uint32_t *)> &redecode) {
+    qzc_context *ctx = sim->ctx;
+    if (!dp.relaxed) {
+        ctx->launches += run_passes(dp, W.amps.as<double2>(), wbits, S);
+        return;
+    }
+    uint32_t *pflag = W.replay.as<uint32_t>(), *wflag = pflag + 1;
+    double2 *res = run_relaxed(dp, dsub, W.amps.as<double2>(), W.alt.p ? W.alt.as<double2>() : nullptr, wbits, S,
+                               pflag, wflag, sim->replays.as<uint64_t>(), sim->force_replay, ctx->launches);
+    if (!dfull.host_passes.empty()) {
+        // a +0-safe relaxed pass flagged: decode the window again from its
+        // untouched payloads and run the strict plan (no-ops unless flagged)
+        redecode(res, wflag);
+        ctx->launches += 1 + run_passes(dfull, res, wbits, S, wflag);
+        flag_done(wflag, sim->replays.as<uint64_t>(), S);
+        ++ctx->launches;
+    }
+    if (res != W.amps.as<double2>()) std::swap(W.amps, W.alt);   // stream-ordered: later kernels see the swap
 }
 
 } // namespace
@@ -1130,9 +1159,16 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
         // it is replayed with, device-side, when a window raises the flag
         const double tp0 = now_s();
         GatePlan gp = build_passes(dg, wbits, kTileBits, sim->cfg.fuse_gates != 0, sim->relax);
-        DevPlan &dp = sim->plans[0], &dstrict = sim->plans[1];
+        DevPlan &dp = sim->plans[0], &dsub = sim->plans[1], &dfull = sim->plans[2];
         upload_plan(gp, dp, s);
-        if (dp.relaxed) upload_plan(build_passes(dg, wbits, kTileBits, true, false), dstrict, s);
+        dsub.host_passes.clear();
+        dfull.host_passes.clear();
+        if (dp.relaxed) {
+            upload_replay(dg, wbits, kTileBits, dp, dsub, s);
+            bool any_inplace = false;
+            for (const PassDesc &pd : dp.host_passes) any_inplace |= pd.relaxed == 1;
+            if (any_inplace) upload_plan(build_passes(dg, wbits, kTileBits, true, false), dfull, s);
+        }
         const int a = sim->cur, b = 1 - sim->cur;
         QZ_CUDA(cudaMemsetAsync(sim->used_ptr(b), 0, 8, s));
         // the stage's plan upload and arena reset happen on the context
@@ -1181,19 +1217,10 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
             decode_into(ctx, In.idx.as<DecIdx>(), W.amps.as<double2>(), sim->geom, nslots, nullptr,
                         In.stage_in.as<uint8_t>(), In.local(), ctx->launches, S, sim->sparse_store);
             QZ_CUDA(cudaEventRecord(ev(4 * w + 1), S));
-            if (dp.relaxed) {
-                uint32_t *flag = W.replay.as<uint32_t>();
-                if (sim->force_replay) QZ_CUDA(cudaMemsetAsync(flag, 1, 1, S));
-                ctx->launches += run_passes(dp, W.amps.as<double2>(), wbits, S, flag);
-                launch_decode(In.stage_in.as<uint8_t>(), In.idx.as<DecIdx>(), nullptr, nslots, sim->geom,
-                              W.amps.as<double2>(), ctx->status, S, flag, sim->sparse_store);
-                ctx->launches += 1 + run_passes(dstrict, W.amps.as<double2>(), wbits, S, nullptr, flag);
-                k_replay_done<<<1, 1, 0, S>>>(flag, sim->replays.as<uint64_t>());
-                QZ_CHECK_LAUNCH();
-                ctx->launches += 2;
-            } else {
-                ctx->launches += 1 + run_passes(dp, W.amps.as<double2>(), wbits, S);
-            }
+            run_window_passes(sim, W, dp, dsub, dfull, wbits, S, [&](double2 *dst, const uint32_t *cond) {
+                launch_decode(In.stage_in.as<uint8_t>(), In.idx.as<DecIdx>(), nullptr, nslots, sim->geom, dst,
+                              ctx->status, S, cond, sim->sparse_store);
+            });
             QZ_CUDA(cudaEventRecord(ev(4 * w + 2), S));
             // the output staging / table of window w-1 must be written back
             if (w) QZ_CUDA(cudaStreamWaitEvent(S, pev(3 * (w - 1) + 2), 0));
@@ -1242,26 +1269,14 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
                               sim->arena_ptr(a), sim->table(a), ctx->launches, S, sim->sparse_store);
             }
             QZ_CUDA(cudaEventRecord(ev(4 * w + 1), S));
-            if (dp.relaxed) {
-                uint32_t *flag = W.replay.as<uint32_t>();
-                if (sim->force_replay) QZ_CUDA(cudaMemsetAsync(flag, 1, 1, S));
-                ctx->launches += run_passes(dp, W.amps.as<double2>(), wbits, S, flag);
-                // replay (no-ops unless *flag): decode again from the still
-                // intact input payloads, then the strict plan
+            run_window_passes(sim, W, dp, dsub, dfull, wbits, S, [&](double2 *dst, const uint32_t *cond) {
                 if (sim->host_res)
-                    launch_decode(W.stage_in.as<uint8_t>(), W.idx.as<DecIdx>(), nullptr, nslots,
-                                  sim->geom, W.amps.as<double2>(), ctx->status, S, flag, sim->sparse_store);
+                    launch_decode(W.stage_in.as<uint8_t>(), W.idx.as<DecIdx>(), nullptr, nslots, sim->geom, dst,
+                                  ctx->status, S, cond, sim->sparse_store);
                 else
-                    launch_decode(sim->arena_ptr(a), W.idx.as<DecIdx>(), W.slot_chunk.as<uint64_t>(),
-                                  nslots, sim->geom, W.amps.as<double2>(), ctx->status, S, flag,
-                                  sim->sparse_store);
-                ctx->launches += 1 + run_passes(dstrict, W.amps.as<double2>(), wbits, S, nullptr, flag);
-                k_replay_done<<<1, 1, 0, S>>>(flag, sim->replays.as<uint64_t>());
-                QZ_CHECK_LAUNCH();
-                ctx->launches += 2;
-            } else {
-                ctx->launches += 1 + run_passes(dp, W.amps.as<double2>(), wbits, S);
-            }
+                    launch_decode(sim->arena_ptr(a), W.idx.as<DecIdx>(), W.slot_chunk.as<uint64_t>(), nslots,
+                                  sim->geom, dst, ctx->status, S, cond, sim->sparse_store);
+            });
             QZ_CUDA(cudaEventRecord(ev(4 * w + 2), S));
             if (sim->host_res) {
                 QZ_CUDA(cudaMemsetAsync(W.lused.p, 0, 8, S));
