@@ -173,7 +173,7 @@ int qzc_event_done(qzc_context *ctx, void *event);
 /* Fused-pass plan summary for gates already on buffer bits of a 2^nbits
  * window (host only, no GPU): out[0] passes, [1] register groups,
  * [2] relaxed groups, [3] gates, [4] fast-path ops (macros folded),
- * [5] OP_PDIAG ops.  fuse_mode as qzc_sim_config.fuse_gates.
+ * [5] OP_PDIAG ops.  fuse_mode as qzc_sim_config.fuse_gates (0..3).
  * (Engine-internal scheduling; no reference counterpart.) */
 int qzc_pass_plan_stats(const qzc_gate *gates, uint64_t ngates, uint32_t nbits,
                         uint32_t fuse_mode, uint64_t *out);
@@ -196,9 +196,11 @@ typedef struct qzc_sim_config {
     uint32_t residency;      /* 0 = compressed store in HBM, 1 = pinned host  */
     uint32_t renormalize;    /* PipelineConfig::renormalize                   */
     uint32_t fuse_gates;     /* 0 = one pass per gate; 1 = fused passes where
-                                diagonal units may keep qubits outside the
-                                tile (default); 2 = fused, every gate qubit
-                                inside the tile                              */
+                                +0-safe diagonal units may keep qubits outside
+                                the tile (default); 2 = fused, every gate
+                                qubit inside the tile; 3 = as 1, plus checked
+                                diagonal units (Z, S, CZ ...) in out-of-place
+                                passes replayed pass by pass on a zero        */
     uint32_t debug_flags;    /* bit 0: always take the strict replay (test)   */
 } qzc_sim_config;
 

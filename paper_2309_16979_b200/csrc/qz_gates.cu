@@ -378,7 +378,8 @@ static uint32_t case_id(const TileGate &t) {
 }
 
 GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_t kmax, bool fuse,
-                      bool relax) {
+                      int relax_level) {
+    bool relax = relax_level > 0;
     GatePlan plan;
     const uint32_t k = std::min(kmax, nbits);
     // bits always in the tile (global segments of 2^low amplitudes)
@@ -387,9 +388,12 @@ GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_
     const uint64_t low_mask = (uint64_t(1) << low) - 1;
     relax = relax && fuse && nbits > k;
     std::vector<Unit> units = make_units(gates, relax);
-    // units with steps that are not +0-safe are relaxed too: their steps are
-    // zero-checked and a zero raises the replay flag of the pass
-    (void)unit_safe;
+    // level 2: units with steps that are not +0-safe are relaxed too (their
+    // steps are zero-checked and a zero raises the pass's replay flag) — a
+    // win for zero-free states, a loss where lossy coding leaves exact zeros
+    if (relax_level < 2)
+        for (Unit &u : units)
+            if (u.diag && !unit_safe(gates, u)) u.diag = false;
     std::vector<size_t> members;   // unit indices of the open pass
     uint64_t tmask = low_mask;
     auto close = [&]() {

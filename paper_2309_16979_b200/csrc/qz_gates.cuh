@@ -134,7 +134,7 @@ uint32_t gate_nparams(uint32_t kind);
 // such a plan can raise the replay flag and must then be replayed strictly
 // from the same input (see run_passes).
 GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_t kmax,
-                      bool fuse, bool relax = false);
+                      bool fuse, int relax_level = 0);
 
 DevGate make_dev_gate(const qzc_gate &g);
 DevGate make_dev_gate_matrix(const double2 *m, uint32_t dim, uint32_t b0, uint32_t b1);

@@ -308,7 +308,7 @@ struct qzc_sim {
     Window win;              // window set 0 (also used by the host entry points)
     Window win2;             // window set 1: second stream of the stage pipeline
     bool two_windows = false;
-    bool relax = true;          // fuse_gates == 1: relaxed passes + strict replay
+    int relax = 1;              // 1: +0-safe diagonal units relaxed; 2: checked units too
     bool force_replay = false;  // debug_flags bit 0
     cudaStream_t streams[3] = {nullptr, nullptr, nullptr};   // [2]: host-staged write-back
     bool pipelined = false;   // host-staged, one window: gather / compute / write-back streams
@@ -430,7 +430,7 @@ void sim_alloc(qzc_sim *sim) {
     budget = budget > (uint64_t(3) << 30) ? budget - (uint64_t(3) << 30) : budget / 2;
     // dense + encode scratch + metadata (+ payload staging when host-staged:
     // two input sets and one output)
-    const uint64_t per_amp = 16 + (sim->relax ? 16 : 0) + 2 * sim->geom.half_stride / sim->N + 8 +
+    const uint64_t per_amp = 16 + (sim->relax == 2 ? 16 : 0) + 2 * sim->geom.half_stride / sim->N + 8 +
                              (sim->host_res ? 3 * (payload_bound(sim->N, sim->eb) + 48) / sim->N + 1 : 0);
     const uint64_t state_amps = uint64_t(1) << sim->n;
     uint64_t wa = sim->cfg.window_amps;
@@ -452,7 +452,8 @@ void sim_alloc(qzc_sim *sim) {
     const uint64_t win_slots = std::max<uint64_t>(wa / sim->N, 2);
     sim->win.reserve(sim->geom, win_slots);
     if (sim->two_windows) sim->win2.reserve(sim->geom, win_slots);
-    if (sim->relax) {
+    if (sim->relax == 2) {
+        // out-of-place passes for checked units
         sim->win.alt.ensure(sizeof(double2) * win_slots * sim->N);
         if (sim->two_windows) sim->win2.alt.ensure(sizeof(double2) * win_slots * sim->N);
     }
@@ -940,11 +941,11 @@ int qzc_sim_create(qzc_context *ctx, const qzc_sim_config *cfg, qzc_sim **out) {
     if (!(cfg->error_bound >= 0.0) || !std::isfinite(cfg->error_bound))
         throw Failure(QZC_EINVAL, "error bound must be finite and non-negative");
     if (cfg->residency > 1) throw Failure(QZC_EINVAL, "residency must be 0 (HBM) or 1 (host-staged)");
-    if (cfg->fuse_gates > 2) throw Failure(QZC_EINVAL, "fuse_gates must be 0, 1 or 2");
+    if (cfg->fuse_gates > 3) throw Failure(QZC_EINVAL, "fuse_gates must be 0, 1, 2 or 3");
     auto *sim = new qzc_sim;
     sim->ctx = ctx;
     sim->cfg = *cfg;
-    sim->relax = cfg->fuse_gates == 1;
+    sim->relax = cfg->fuse_gates == 1 ? 1 : (cfg->fuse_gates == 3 ? 2 : 0);
     sim->force_replay = (cfg->debug_flags & 1u) != 0;
     sim->n = n;
     sim->c = c;
@@ -1067,12 +1068,13 @@ int qzc_sim_init_basis(qzc_sim *sim) {
 int qzc_pass_plan_stats(const qzc_gate *gates, uint64_t ngates, uint32_t nbits,
                         uint32_t fuse_mode, uint64_t *out) {
     QZ_API_BEGIN
-    if (fuse_mode > 2 || nbits > 40) throw Failure(QZC_EINVAL, "bad fuse mode / buffer width");
+    if (fuse_mode > 3 || nbits > 40) throw Failure(QZC_EINVAL, "bad fuse mode / buffer width");
     const std::string err = validate_gates(nbits, gates, ngates);
     if (!err.empty()) throw Failure(QZC_EINVAL, err);
     std::vector<DevGate> dg;
     for (uint64_t i = 0; i < ngates; ++i) dg.push_back(make_dev_gate(gates[i]));
-    const GatePlan p = build_passes(dg, nbits, kTileBits, fuse_mode != 0, fuse_mode == 1);
+    const GatePlan p = build_passes(dg, nbits, kTileBits, fuse_mode != 0,
+                                    fuse_mode == 1 ? 1 : (fuse_mode == 3 ? 2 : 0));
     uint64_t relaxed = 0, fast = 0, pdiag = 0;
     for (const GroupDesc &g : p.groups) {
         relaxed += g.relaxed;

@@ -125,7 +125,7 @@ def pass_plan_stats(gates, nbits: int, fuse="relaxed") -> dict:
     lib = load_library()
     arr = to_array(gates)
     out = (C.c_uint64 * 6)()
-    mode = {"none": 0, "relaxed": 1, "strict": 2}[fuse]
+    mode = {"none": 0, "relaxed": 1, "strict": 2, "checked": 3}[fuse]
     _check(lib.qzc_pass_plan_stats(arr.ctypes.data_as(P(Gate)), arr.size, nbits, mode, out))
     keys = ("passes", "groups", "relaxed_groups", "gates", "fast_ops", "pdiag_ops")
     return dict(zip(keys, (int(x) for x in out)))
@@ -314,15 +314,17 @@ class Simulator:
     def __init__(self, eng: Engine, n: int, c: int, m: int, eb: float, window_amps: int = 0,
                  fuse=True, init: bool = True, residency: str = "hbm",
                  force_replay: bool = False):
-        """fuse: True = fused passes with relaxed diagonal units (default),
-        "strict" = fused passes with every gate qubit in the tile, False = one
-        pass per gate.  force_replay: always take the strict replay (test)."""
+        """fuse: True = fused passes with relaxed +0-safe diagonal units
+        (default), "checked" = also checked diagonal units (out-of-place
+        passes, per-pass replay), "strict" = every gate qubit in the tile,
+        False = one pass per gate.  force_replay: always take the strict
+        replay (test)."""
         self.eng, self.lib = eng, eng.lib
         self.n, self.c, self.m, self.eb = n, c, m, eb
         cfg = SimConfig(num_qubits=n, chunk_qubits=c, batch_qubits=m, error_bound=eb,
                         window_amps=window_amps, residency={"hbm": 0, "host": 1}[residency],
                         renormalize=0,
-                        fuse_gates=2 if fuse == "strict" else (1 if fuse else 0),
+                        fuse_gates={"strict": 2, "checked": 3}.get(fuse, 1 if fuse else 0),
                         debug_flags=1 if force_replay else 0)
         h = C.c_void_p()
         _check(self.lib.qzc_sim_create(eng.h, C.byref(cfg), C.byref(h)))

@@ -213,7 +213,8 @@ def test_relaxed_passes_match_strict_and_reference(engine, oracle, case):
     ref = oracle.run(n, g, c, m, eb)["digest"]
     out = {}
     for mode, kw in (("relaxed", {}), ("strict", {"fuse": "strict"}),
-                     ("replay", {"force_replay": True})):
+                     ("replay", {"force_replay": True}), ("checked", {"fuse": "checked"}),
+                     ("checked_replay", {"fuse": "checked", "force_replay": True})):
         sim = run_sim(engine, n, c, m, eb, g, **kw)
         out[mode] = (sim.digest(), sim.stats())
         sim.close()
@@ -311,8 +312,10 @@ def test_random_circuits_relaxed_vs_reference(engine, oracle, seed):
     eb = [0.0, 1e-7, 1e-5][seed % 3]
     c, m = (4, 14) if seed % 2 else (6, 12)
     ref = oracle.run(n, g, c, m, eb)["digest"]
-    sim = run_sim(engine, n, c, m, eb, g)
-    assert sim.digest() == ref
+    for fuse in (True, "checked"):
+        sim = run_sim(engine, n, c, m, eb, g, fuse=fuse)
+        assert sim.digest() == ref, fuse
+        sim.close()
 
 
 def test_qft30_full_size_parity(engine, oracle):

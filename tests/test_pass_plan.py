@@ -40,16 +40,17 @@ def test_small_buffers_never_relax():
     assert st["relaxed_groups"] == 0 and st["pdiag_ops"] == 0
 
 
-def test_unsafe_diagonals_relaxed_with_checks():
-    # Z / S / CZ rows are not +0-safe: they are still relaxed (their steps
-    # are zero-checked; a zero raises the pass's replay flag)
+def test_unsafe_diagonals_relaxed_only_when_checked():
+    # Z / S / CZ rows are not +0-safe: the default plan keeps their qubits in
+    # the tile; the "checked" plan relaxes them (zero-checked steps, a zero
+    # raises the pass's replay flag)
     g = [("h", (q,), ()) for q in range(20)] + [("z", (19,), ()), ("s", (18,), ()),
                                                ("cz", (0, 19), ())]
-    st = E.pass_plan_stats(g, 20, "relaxed")
-    assert st["pdiag_ops"] >= 1
+    assert E.pass_plan_stats(g, 20, "relaxed")["pdiag_ops"] == 0
+    assert E.pass_plan_stats(g, 20, "checked")["pdiag_ops"] >= 1
     # supremacy layers: the CZ bricks no longer force their qubits into tiles
     sup = CI.supremacy(30)
-    assert E.pass_plan_stats(sup, 30, "relaxed")["passes"] * 3 < E.pass_plan_stats(sup, 30, "strict")["passes"] * 2
+    assert E.pass_plan_stats(sup, 30, "checked")["passes"] * 3 < E.pass_plan_stats(sup, 30, "strict")["passes"] * 2
 
 
 def test_invalid_plan_inputs():
