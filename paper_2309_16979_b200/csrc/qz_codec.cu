@@ -153,7 +153,7 @@ constexpr uint32_t kIdxMaxSteps = 1040;   // >= 4N / 256 + 1 for c <= 17 (lossy:
 
 __global__ void __launch_bounds__(32 * kIdxWarps) k_dec_index_warp(
     const uint8_t *__restrict__ arena, ChunkTable table, const uint64_t *__restrict__ slot_chunk,
-    uint64_t nslots, CodecGeom g, DecIdx *__restrict__ out, DevStatus *status) {
+    uint64_t nslots, CodecGeom g, DecIdx *__restrict__ out, DevStatus *status, uint32_t *nzslot) {
     __shared__ uint32_t step_prod[kIdxWarps][2][kIdxMaxSteps];   // elements before step j
     const uint32_t lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
     const uint64_t s = uint64_t(blockIdx.x) * kIdxWarps + wq;
@@ -178,6 +178,7 @@ __global__ void __launch_bounds__(32 * kIdxWarps) k_dec_index_warp(
     uint32_t pos = kHdr;
     uint32_t nsteps[2] = {0, 0}, start[2] = {0, 0};
     bool ff_real[2] = {false, false};   // a 0xFF run touches the real half
+    bool nonzero_byte = false;          // some run of plane 0/1 has a byte != 0
     for (uint32_t k = 0; k < g.planes && !err; ++k) {
         uint64_t produced = 0;
         d.pos[k][0] = pos;
@@ -210,20 +211,23 @@ __global__ void __launch_bounds__(32 * kIdxWarps) k_dec_index_warp(
             // the first zero run before the end, the first missing pair
             uint32_t end_pair = ~0u, half_pair = ~0u, half_skip = 0, bad_pair = ~0u;
             uint64_t c = excl;
-            bool ff = false;
+            bool ff = false, nz = false;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 const uint32_t idx = 8 * lane + j;
                 if (j >= int(avail)) { if (bad_pair == ~0u && c < total) bad_pair = idx; continue; }
                 if (c >= total) continue;
                 const uint32_t r = runs[j];
-                ff |= c < N && __ldg(p + p0 + 2 * j) == 0xFF;
+                const uint32_t bj = __ldg(p + p0 + 2 * j);
+                ff |= c < N && bj == 0xFF;
+                nz |= bj != 0;
                 if (bad_pair == ~0u && (r == 0 || c + r > total)) bad_pair = idx;
                 if (half_pair == ~0u && c <= N && N < c + r) { half_pair = idx; half_skip = uint32_t(N - c); }
                 if (end_pair == ~0u && c + r == total) end_pair = idx;
                 c += r;
             }
             if (k < 2 && __any_sync(0xffffffffu, ff)) ff_real[k] = true;
+            if (__any_sync(0xffffffffu, nz)) nonzero_byte = true;
             // warp-wide minima (first occurrence in stream order)
             uint32_t e_end = end_pair, e_half = half_pair, e_bad = bad_pair;
 #pragma unroll
@@ -316,6 +320,11 @@ __global__ void __launch_bounds__(32 * kIdxWarps) k_dec_index_warp(
         if (err) dev_fail(status, err, chunk);
         else d.len = len;
         out[s] = d;
+        if (nzslot) {
+            const bool nzs = err || nonzero_byte || d.raw_count != 0;
+            nzslot[s] = nzs ? 1u : 0u;
+            if (!nzs) atomicAdd(&nzslot[nslots], 1u);
+        }
     }
 }
 
@@ -1286,13 +1295,16 @@ void launch_crc(const CodecTables &tabs, const uint8_t *arena, ChunkTable table,
 
 void launch_dec_index(const uint8_t *arena, ChunkTable table, const uint64_t *slot_chunk,
                       uint64_t nslots, const CodecGeom &g, DecIdx *idx, DevStatus *status,
-                      cudaStream_t s) {
+                      cudaStream_t s, uint32_t *nzslot) {
+    if (nzslot) QZ_CUDA(cudaMemsetAsync(nzslot + nslots, 0, 4, s));
     if (g.lossy && g.N >= 64 && 4 * g.N / 256 + 1 <= kIdxMaxSteps)
         k_dec_index_warp<<<grid_for(nslots, kIdxWarps), 32 * kIdxWarps, 0, s>>>(arena, table, slot_chunk,
-                                                                              nslots, g, idx, status);
-    else
+                                                                              nslots, g, idx, status, nzslot);
+    else {
         k_dec_index<<<grid_for(nslots, 64), 64, 0, s>>>(arena, table, slot_chunk, nslots, g, idx,
                                                         status);
+        if (nzslot) QZ_CUDA(cudaMemsetAsync(nzslot, 1, 4 * nslots, s));   // unknown: nonzero
+    }
     QZ_CHECK_LAUNCH();
 }
 

@@ -80,9 +80,12 @@ void launch_crc(const CodecTables &tabs, const uint8_t *arena, ChunkTable table,
                 DevStatus *status, cudaStream_t s);
 
 // Parse payload headers / RLE streams into decode cursors.
+// nzslot (optional, nslots + 1 words): per slot 0 when the payload is known
+// to decode to all (+0) (lossy, no raws, both byte planes only byte-0 runs),
+// else nonzero; nzslot[nslots] = number of zero slots.
 void launch_dec_index(const uint8_t *arena, ChunkTable table, const uint64_t *slot_chunk,
                       uint64_t nslots, const CodecGeom &g, DecIdx *idx, DevStatus *status,
-                      cudaStream_t s);
+                      cudaStream_t s, uint32_t *nzslot = nullptr);
 
 // Decode every slot into win[slot*N .. (slot+1)*N).  cond != nullptr: the
 // launch does nothing unless *cond != 0 (device-side replay, see run_passes).

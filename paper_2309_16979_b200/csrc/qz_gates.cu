@@ -1539,7 +1539,8 @@ __global__ void __launch_bounds__(1 << (kTileBits - kRegBits), (kTileBits >= 12 
                                                          uint64_t ntiles,
                                                          unsigned long long *__restrict__ counters,
                                                          uint32_t *__restrict__ flag,
-                                                         const uint32_t *__restrict__ cond) {
+                                                         const uint32_t *__restrict__ cond,
+                                                         uint32_t *__restrict__ nzslot, uint32_t cbits) {
     if (cond && *cond == 0) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double2 *s = reinterpret_cast<double2 *>(smem_raw);
@@ -1553,13 +1554,29 @@ __global__ void __launch_bounds__(1 << (kTileBits - kRegBits), (kTileBits >= 12 
     const uint32_t lowmask = (1u << L) - 1;
     const uint32_t tid = threadIdx.x, nth = blockDim.x;   // nth == tile / NB
     for (uint32_t h = tid; h < nhi; h += nth) offhi[h] = deposit_bits(h, himask);
+    // the zero-slot count, read once per CTA (other CTAs update it)
+    __shared__ uint32_t s_zc;
+    if (tid == 0) s_zc = nzslot ? nzslot[uint64_t(1) << (nbits - cbits)] : 0u;
     __syncthreads();
     // tile bases: deposit(t) advanced by deposit(gridDim.x) with the carry
     // running through the tile-bit positions
     const uint64_t dstep = deposit_bits(gridDim.x, ntmask);
     uint64_t base = deposit_bits(blockIdx.x, ntmask);
+    // known all-(+0) chunk slots: tiles made only of them are fixed points of
+    // a pz_stable in-place pass (no load, no store)
+    // the map is consulted / maintained only while it still holds zero slots
+    if (s_zc == 0) nzslot = nullptr;
+    const bool use_nz = nzslot && pd.pz_stable && src == dst && L <= cbits;
     for (uint64_t t = blockIdx.x; t < ntiles;
          t += gridDim.x, base = ((base | ~ntmask) + dstep) & ntmask) {
+        if (use_nz) {
+            uint32_t nzt = 0;
+            for (uint32_t h = tid; h < nhi; h += nth) nzt |= nzslot[(base + offhi[h]) >> cbits];
+            if (!__syncthreads_or(nzt)) {
+                if (counters && tid == 0) atomicAdd(&counters[0], 1ull);
+                continue;
+            }
+        }
 #pragma unroll
         for (int i = 0; i < NB; ++i) {
             const uint32_t l = tid + i * nth;
@@ -1697,6 +1714,16 @@ __global__ void __launch_bounds__(1 << (kTileBits - kRegBits), (kTileBits >= 12 
         for (int i = 0; i < NB; ++i) {
             const uint32_t l = tid + i * nth;
             __stcs(dst + base + offhi[l >> L] + (l & lowmask), out[i]);
+        }
+        if (nzslot) {
+            // every slot the tile covers (the low tile bits span 2^(L - cbits)
+            // consecutive slots when L > cbits)
+            const uint32_t span = L > cbits ? 1u << (L - cbits) : 1u;
+            uint32_t *zcount = nzslot + (uint64_t(1) << (nbits - cbits));
+            for (uint32_t i = tid; i < nhi * span; i += nth) {
+                uint32_t *w = nzslot + ((base + offhi[i / span]) >> cbits) + (i % span);
+                if (*w == 0 && atomicExch(w, 1u) == 0) atomicSub(zcount, 1u);
+            }
         }
         __syncthreads();
     }
@@ -1891,11 +1918,17 @@ void set_attrs() {
 }
 
 void launch_pass(const DevPlan &plan, const PassDesc &pd, const double2 *src, double2 *dst,
-                 uint32_t nbits, cudaStream_t s, uint32_t *flag, const uint32_t *cond) {
+                 uint32_t nbits, cudaStream_t s, uint32_t *flag, const uint32_t *cond, NzMap nz) {
     if (pd.kind == PASS_SWAPS) {
         const uint64_t tiles = uint64_t(1) << (nbits > 2 * kSwapLow ? nbits - 2 * kSwapLow : 0);
         const uint64_t grid = std::min<uint64_t>(std::max<uint64_t>(tiles, 1), uint64_t(kNumSMs) * 8);
         tile_swaps<<<(unsigned)grid, 256, 0, s>>>(src, dst, nbits, pd, flag, cond);
+        // chunks moved: the zero map no longer describes the slots
+        if (nz.slot && nbits > nz.cbits) {
+            const size_t ns = size_t(1) << (nbits - nz.cbits);
+            QZ_CUDA(cudaMemsetAsync(nz.slot, 1, 4 * ns, s));
+            QZ_CUDA(cudaMemsetAsync(nz.slot + ns, 0, 4, s));
+        }
     } else if (pd.k < (uint32_t)kRegBits + 1) {
         // tile == whole buffer (nbits < 4): never relaxed, in place
         if (src != dst) throw Failure(QZC_EDEVICE, "tiny pass out of place");
@@ -1906,8 +1939,12 @@ void launch_pass(const DevPlan &plan, const PassDesc &pd, const double2 *src, do
         const uint32_t threads = tile >> kRegBits;
         const size_t smem = sizeof(double2) * tile + sizeof(uint64_t) * (tile >> pd.lowbits);
         const uint64_t grid = std::min<uint64_t>(ntiles, uint64_t(kNumSMs) * 2 * 8);
+        // the map is only used for passes inside one window of whole slots
+        static const bool off = getenv("QZ_NO_NZMAP") != nullptr;
+        const bool usable = nz.slot && nbits > nz.cbits && !off;
         tile_pass_reg<<<(unsigned)grid, threads, smem, s>>>(src, dst, nbits, pd, plan.groups, plan.gates,
-                                                           ntiles, debug_counters(), flag, cond);
+                                                           ntiles, debug_counters(), flag, cond,
+                                                           usable ? nz.slot : nullptr, nz.cbits);
     }
     QZ_CHECK_LAUNCH();
 }
@@ -1915,10 +1952,10 @@ void launch_pass(const DevPlan &plan, const PassDesc &pd, const double2 *src, do
 } // namespace
 
 uint64_t run_passes(const DevPlan &plan, double2 *buf, uint32_t nbits, cudaStream_t s,
-                    const uint32_t *cond) {
+                    const uint32_t *cond, NzMap nz) {
     if (plan.relaxed) throw Failure(QZC_EDEVICE, "relaxed plan run without its replay plan");
     set_attrs();
-    for (const PassDesc &pd : plan.host_passes) launch_pass(plan, pd, buf, buf, nbits, s, nullptr, cond);
+    for (const PassDesc &pd : plan.host_passes) launch_pass(plan, pd, buf, buf, nbits, s, nullptr, cond, nz);
     return plan.host_passes.size();
 }
 
@@ -1929,23 +1966,23 @@ void flag_done(uint32_t *flag, uint64_t *replays, cudaStream_t s) {
 
 double2 *run_relaxed(const DevPlan &plan, const DevPlan &replay, double2 *buf, double2 *alt,
                      uint32_t nbits, cudaStream_t s, uint32_t *flag, uint32_t *win_flag,
-                     uint64_t *replays, bool force_replay, uint64_t &launches) {
+                     uint64_t *replays, bool force_replay, uint64_t &launches, NzMap nz) {
     set_attrs();
     double2 *cur = buf, *oth = alt;
     for (size_t p = 0; p < plan.host_passes.size(); ++p) {
         const PassDesc &pd = plan.host_passes[p];
         if (pd.relaxed != 2) {
             if (pd.relaxed && force_replay) QZ_CUDA(cudaMemsetAsync(win_flag, 1, 1, s));
-            launch_pass(plan, pd, cur, cur, nbits, s, pd.relaxed ? win_flag : nullptr, nullptr);
+            launch_pass(plan, pd, cur, cur, nbits, s, pd.relaxed ? win_flag : nullptr, nullptr, nz);
             ++launches;
             continue;
         }
         if (force_replay) QZ_CUDA(cudaMemsetAsync(flag, 1, 1, s));
-        launch_pass(plan, pd, cur, oth, nbits, s, flag, nullptr);
+        launch_pass(plan, pd, cur, oth, nbits, s, flag, nullptr, nz);
         // strict replay of this pass from its untouched input (no-ops unless flagged)
         const auto &rr = plan.replay_range.at(p);
         for (uint32_t q = rr.first; q < rr.second; ++q)
-            launch_pass(replay, replay.host_passes[q], q == rr.first ? cur : oth, oth, nbits, s, nullptr, flag);
+            launch_pass(replay, replay.host_passes[q], q == rr.first ? cur : oth, oth, nbits, s, nullptr, flag, nz);
         k_flag_done<<<1, 1, 0, s>>>(flag, replays);
         QZ_CHECK_LAUNCH();
         launches += 2 + (rr.second - rr.first);

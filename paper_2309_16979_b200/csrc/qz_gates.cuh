@@ -156,10 +156,20 @@ struct DevPlan {
 void upload_plan(const GatePlan &plan, DevPlan &out, cudaStream_t s);
 void free_plan(DevPlan &p);   // releases the device buffers
 
+// Per-chunk-slot "may be nonzero" words of a window (slot = amplitude >> cbits):
+// 0 = known all-(+0) (from the decode index), so in-place passes whose groups
+// keep all-(+0) blocks fixed skip such tiles without loading them; every
+// processed tile marks its slots (keeping the zero-slot count exact, and a
+// pass that starts with no zero slot does no map work); a swap pass resets it.
+struct NzMap {
+    uint32_t *slot = nullptr;   // nslots words + the zero-slot count
+    uint32_t cbits = 0;
+};
+
 // Launch every pass of a strict `plan` in place over buf (2^nbits
 // amplitudes).  Returns the number of kernel launches.
 uint64_t run_passes(const DevPlan &plan, double2 *buf, uint32_t nbits, cudaStream_t s,
-                    const uint32_t *cond = nullptr);
+                    const uint32_t *cond = nullptr, NzMap nz = {});
 // Count a replay and clear the flag (stream-ordered).
 void flag_done(uint32_t *flag, uint64_t *replays, cudaStream_t s);
 
@@ -174,7 +184,7 @@ void flag_done(uint32_t *flag, uint64_t *replays, cudaStream_t s);
 // caller replays the whole window from its payloads when set).
 double2 *run_relaxed(const DevPlan &plan, const DevPlan &replay, double2 *buf, double2 *alt,
                      uint32_t nbits, cudaStream_t s, uint32_t *flag, uint32_t *win_flag,
-                     uint64_t *replays, bool force_replay, uint64_t &launches);
+                     uint64_t *replays, bool force_replay, uint64_t &launches, NzMap nz = {});
 
 // Strict sub-plans of every relaxed pass of `relaxed`, concatenated into
 // `out` (ranges recorded in relaxed_dev.replay_range).

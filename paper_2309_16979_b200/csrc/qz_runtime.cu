@@ -74,6 +74,7 @@ struct Window {
     DevBuf amps, scratch, meta, idx, slot_chunk, sizes, reloff, base, cub, delta, maxd;
     DevBuf replay;   // uint32 flag raised by a relaxed gate pass
     DevBuf alt;      // second dense buffer: relaxed passes run out of place
+    DevBuf nzslot;   // per slot: may be nonzero (0 = known all-(+0) after decode)
     // host-staged residency: HBM staging of the window's payloads
     DevBuf stage_in, stage_out, lt_off, lt_len, lt_crc, padded, soff, lused, hbase;
     uint64_t slots = 0, stage_in_cap = 0, stage_out_cap = 0;
@@ -122,6 +123,8 @@ struct Window {
     }
     void reserve(const CodecGeom &g, uint64_t nslots) {
         amps.ensure(sizeof(double2) * nslots * g.N);
+        nzslot.ensure(4 * (nslots + 1) + 16);
+        QZ_CUDA(cudaMemset(nzslot.p, 0, 4 * (nslots + 1)));   // count 0: map unused until a decode
         scratch.ensure(2 * nslots * g.half_stride);
         meta.ensure(sizeof(EncHalf) * 2 * nslots);
         idx.ensure(sizeof(DecIdx) * nslots);
@@ -149,7 +152,7 @@ struct Window {
     void release() {
         for (DevBuf *b : {&amps, &scratch, &meta, &idx, &slot_chunk, &sizes, &reloff, &base, &cub,
                           &delta, &maxd, &stage_in, &stage_out, &lt_off, &lt_len, &lt_crc, &padded,
-                          &soff, &lused, &hbase, &out_off, &out_len, &out_crc, &replay, &alt})
+                          &soff, &lused, &hbase, &out_off, &out_len, &out_crc, &replay, &alt, &nzslot})
             b->release();
     }
 };
@@ -377,7 +380,8 @@ void decode_window(qzc_context *ctx, Window &w, const CodecGeom &g, uint64_t nsl
                    uint64_t &launches, cudaStream_t s = nullptr, bool sparse = false) {
     if (!s) s = ctx->stream;
     launch_crc(ctx->tabs, arena, t, slot_chunk, nslots, true, ctx->status, s);
-    launch_dec_index(arena, t, slot_chunk, nslots, g, w.idx.as<DecIdx>(), ctx->status, s);
+    launch_dec_index(arena, t, slot_chunk, nslots, g, w.idx.as<DecIdx>(), ctx->status, s,
+                     w.nzslot.as<uint32_t>());
     launch_decode(arena, w.idx.as<DecIdx>(), slot_chunk, nslots, g, w.amps.as<double2>(),
                   ctx->status, s, nullptr, sparse);
     launches += 3;
@@ -386,9 +390,9 @@ void decode_window(qzc_context *ctx, Window &w, const CodecGeom &g, uint64_t nsl
 // decode_window with an explicit cursor array and target window
 void decode_into(qzc_context *ctx, DecIdx *idx, double2 *amps, const CodecGeom &g, uint64_t nslots,
                  const uint64_t *slot_chunk, const uint8_t *arena, ChunkTable t, uint64_t &launches,
-                 cudaStream_t s, bool sparse = false) {
+                 cudaStream_t s, bool sparse = false, uint32_t *nzslot = nullptr) {
     launch_crc(ctx->tabs, arena, t, slot_chunk, nslots, true, ctx->status, s);
-    launch_dec_index(arena, t, slot_chunk, nslots, g, idx, ctx->status, s);
+    launch_dec_index(arena, t, slot_chunk, nslots, g, idx, ctx->status, s, nzslot);
     launch_decode(arena, idx, slot_chunk, nslots, g, amps, ctx->status, s, nullptr, sparse);
     launches += 3;
 }
@@ -511,13 +515,14 @@ void run_window_passes(qzc_sim *sim, Window &W, const DevPlan &dp, const DevPlan
                        uint32_t wbits, cudaStream_t S,
                        const std::function<void(double2 *, const uint32_t *)> &redecode) {
     qzc_context *ctx = sim->ctx;
+    const NzMap nz{W.nzslot.as<uint32_t>(), sim->c};
     if (!dp.relaxed) {
-        ctx->launches += run_passes(dp, W.amps.as<double2>(), wbits, S);
+        ctx->launches += run_passes(dp, W.amps.as<double2>(), wbits, S, nullptr, nz);
         return;
     }
     uint32_t *pflag = W.replay.as<uint32_t>(), *wflag = pflag + 1;
     double2 *res = run_relaxed(dp, dsub, W.amps.as<double2>(), W.alt.p ? W.alt.as<double2>() : nullptr, wbits, S,
-                               pflag, wflag, sim->replays.as<uint64_t>(), sim->force_replay, ctx->launches);
+                               pflag, wflag, sim->replays.as<uint64_t>(), sim->force_replay, ctx->launches, nz);
     if (!dfull.host_passes.empty()) {
         // a +0-safe relaxed pass flagged: decode the window again from its
         // untouched payloads and run the strict plan (no-ops unless flagged)
@@ -1217,7 +1222,8 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
             QZ_CUDA(cudaStreamWaitEvent(S, pev(3 * w), 0));
             QZ_CUDA(cudaEventRecord(ev(4 * w), S));
             decode_into(ctx, In.idx.as<DecIdx>(), W.amps.as<double2>(), sim->geom, nslots, nullptr,
-                        In.stage_in.as<uint8_t>(), In.local(), ctx->launches, S, sim->sparse_store);
+                        In.stage_in.as<uint8_t>(), In.local(), ctx->launches, S, sim->sparse_store,
+                        W.nzslot.as<uint32_t>());
             QZ_CUDA(cudaEventRecord(ev(4 * w + 1), S));
             run_window_passes(sim, W, dp, dsub, dfull, wbits, S, [&](double2 *dst, const uint32_t *cond) {
                 launch_decode(In.stage_in.as<uint8_t>(), In.idx.as<DecIdx>(), nullptr, nslots, sim->geom, dst,
