@@ -1744,9 +1744,13 @@ __device__ __forceinline__ uint64_t permute_bits(uint64_t x, const uint8_t *perm
     return y;
 }
 
-// smem slot of local index l in a swap tile: XOR the low 5 bits with the next
-// 5 so both the contiguous fill and the permuted gather spread over banks
-__device__ __forceinline__ uint32_t swz10(uint32_t l) { return l ^ ((l >> kSwapLow) & 31u); }
+// smem slot of local index l in a swap tile: XOR the low 5 bits with the
+// bit-reversed next 5, so the contiguous fill and the gather of a
+// bit-reversal-type permutation (low <-> high tile bits, the QFT's swap
+// network) both hit 8 distinct 16-byte bank groups per phase
+__device__ __forceinline__ uint32_t swz10(uint32_t l) {
+    return l ^ (__brev((l >> kSwapLow) & 31u) >> 27);
+}
 
 __global__ void __launch_bounds__(256) tile_swaps(const double2 *__restrict__ src, double2 *__restrict__ dst,
                                                   uint32_t nbits,
