@@ -368,3 +368,17 @@ def test_large_runs_vs_reference(engine, idx):
     assert st["stages"] == rec["stages"]
     assert st["current_bytes"] == rec["current_bytes"]
     sim.close()
+
+
+@pytest.mark.parametrize("fuse,force", [(True, True), ("checked", False), ("checked", True)])
+def test_host_staged_replay_modes(engine, oracle, fuse, force):
+    """Host-staged pipeline (gather / compute / write-back streams) with the
+    window-level and the per-pass replays forced or taken: reference bytes."""
+    from tests_util import diagonal_heavy_circuit
+    n, c, m, eb = 15, 6, 14, 1e-6
+    g = to_array(diagonal_heavy_circuit(n, 200, 77))
+    ref = oracle.run(n, g, c, m, eb)["digest"]
+    sim = run_sim(engine, n, c, m, eb, g, residency="host", fuse=fuse, force_replay=force)
+    assert sim.digest() == ref
+    if force:
+        assert sim.stats()["replays"] >= 1
