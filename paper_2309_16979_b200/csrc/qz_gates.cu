@@ -767,6 +767,19 @@ void upload_plan(const GatePlan &plan, DevPlan &out, cudaStream_t s) {
     out.ngates = plan.gates.size();
     out.ngroups = plan.groups.size();
     out.host_passes = plan.passes;
+    // kernel case set per pass: the narrow one when every fast-list entry of
+    // every group is in it (and no group needs the shared-memory generic path)
+    static const bool narrow_off = getenv("QZ_NO_NARROW") != nullptr;
+    for (PassDesc &pd : out.host_passes) {
+        bool narrow = !narrow_off && pd.kind != PASS_SWAPS;
+        for (uint32_t gi = 0; narrow && gi < pd.ngroups; ++gi) {
+            const GroupDesc &G = plan.groups[pd.first_group + gi];
+            if (G.generic) narrow = false;
+            for (uint32_t q = 0; narrow && q < G.nfast; ++q)
+                narrow = case_on(kPassDiagH, plan.gates[G.first_fast + q].cid);
+        }
+        pd.variant = narrow ? kPassDiagH : kPassAll;
+    }
     out.relaxed = false;
     for (const PassDesc &pd : plan.passes) out.relaxed |= pd.relaxed != 0;
     out.replay_range.clear();
@@ -1271,118 +1284,119 @@ __device__ __forceinline__ void run_pdiag_r(double2 (&v)[NB], const TileGate *__
     }
 }
 
+template <int S>
 __device__ __forceinline__ uint32_t fast_case(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q,
                                               uint64_t gidx, bool &bad) {
     const TileGate &g = fp[q];
     switch (g.cid) {
-    case 0: run_pdiag_r<0>(v, fp + q, g.run, gidx); return g.run;
-    case 1: run_pdiag_r<1>(v, fp + q, g.run, gidx); return g.run;
-    case 2: run_pdiag_r<2>(v, fp + q, g.run, gidx); return g.run;
-    case 3: run_pdiag_r<3>(v, fp + q, g.run, gidx); return g.run;
-    case 4: fast_pdiag<0, 0>(v, g, pdiag_var(g, gidx), bad); return 1;
-    case 5: fast_pdiag<0, 1>(v, g, pdiag_var(g, gidx), bad); return 1;
-    case 6: fast_pdiag<1, 0>(v, g, pdiag_var(g, gidx), bad); return 1;
-    case 7: fast_pdiag<1, 1>(v, g, pdiag_var(g, gidx), bad); return 1;
-    case 8: fast_pdiag<2, 0>(v, g, pdiag_var(g, gidx), bad); return 1;
-    case 9: fast_pdiag<2, 1>(v, g, pdiag_var(g, gidx), bad); return 1;
-    case 10: fast_pdiag<3, 0>(v, g, pdiag_var(g, gidx), bad); return 1;
-    case 11: fast_pdiag<3, 1>(v, g, pdiag_var(g, gidx), bad); return 1;
-    case 12: fast_diag<0, CK_ONE, CK_CPLX, 1>(v, g, bad); return 1;
-    case 13: fast_diag<0, CK_CPLX, CK_CPLX, 1>(v, g, bad); return 1;
-    case 14: fast_diag<0, CK_ONE, CK_CPLX, 2>(v, g, bad); return 1;
-    case 15: fast_diag<0, CK_CPLX, CK_CPLX, 2>(v, g, bad); return 1;
-    case 16: fast_diag<0>(v, g, bad); return 1;
-    case 17: fast_diag<1, CK_ONE, CK_CPLX, 1>(v, g, bad); return 1;
-    case 18: fast_diag<1, CK_CPLX, CK_CPLX, 1>(v, g, bad); return 1;
-    case 19: fast_diag<1, CK_ONE, CK_CPLX, 2>(v, g, bad); return 1;
-    case 20: fast_diag<1, CK_CPLX, CK_CPLX, 2>(v, g, bad); return 1;
-    case 21: fast_diag<1>(v, g, bad); return 1;
-    case 22: fast_diag<2, CK_ONE, CK_CPLX, 1>(v, g, bad); return 1;
-    case 23: fast_diag<2, CK_CPLX, CK_CPLX, 1>(v, g, bad); return 1;
-    case 24: fast_diag<2, CK_ONE, CK_CPLX, 2>(v, g, bad); return 1;
-    case 25: fast_diag<2, CK_CPLX, CK_CPLX, 2>(v, g, bad); return 1;
-    case 26: fast_diag<2>(v, g, bad); return 1;
-    case 27: fast_gen1<0, CK_REAL, CK_IMAG, CK_IMAG, CK_REAL, 1>(v, g, bad); return 1;
-    case 28: fast_gen1<0, CK_REAL, CK_REAL, CK_REAL, CK_REAL, 1>(v, g, bad); return 1;
-    case 29: fast_gen1<0, CK_CPLX, CK_CPLX, CK_CPLX, CK_CPLX, 1>(v, g, bad); return 1;
-    case 30: fast_gen1<0, CK_REAL, CK_IMAG, CK_IMAG, CK_REAL, 2>(v, g, bad); return 1;
-    case 31: fast_gen1<0, CK_REAL, CK_REAL, CK_REAL, CK_REAL, 2>(v, g, bad); return 1;
-    case 32: fast_gen1<0, CK_CPLX, CK_CPLX, CK_CPLX, CK_CPLX, 2>(v, g, bad); return 1;
-    case 33: fast_gen1<0, CK_ZERO, CK_ONE, CK_ONE, CK_ZERO, 1>(v, g, bad); return 1;
-    case 34: fast_gen1<0, CK_ZERO, CK_IMAG, CK_IMAG, CK_ZERO, 1>(v, g, bad); return 1;
-    case 35: fast_gen1<0, CK_REAL, CK_CPLX, CK_CPLX, CK_CPLX, 1>(v, g, bad); return 1;
-    case 36: fast_gen1<0, CK_REAL, CK_CPLX, CK_REAL, CK_CPLX, 1>(v, g, bad); return 1;
-    case 37: fast_gen1<0, CK_ZERO, CK_ONE, CK_ONE, CK_ZERO, 2>(v, g, bad); return 1;
-    case 38: fast_gen1<0, CK_ZERO, CK_IMAG, CK_IMAG, CK_ZERO, 2>(v, g, bad); return 1;
-    case 39: fast_gen1<0, CK_REAL, CK_CPLX, CK_CPLX, CK_CPLX, 2>(v, g, bad); return 1;
-    case 40: fast_gen1<0, CK_REAL, CK_CPLX, CK_REAL, CK_CPLX, 2>(v, g, bad); return 1;
-    case 41: fast_gen1<0>(v, g, bad); return 1;
-    case 42: fast_gen1<1, CK_REAL, CK_IMAG, CK_IMAG, CK_REAL, 1>(v, g, bad); return 1;
-    case 43: fast_gen1<1, CK_REAL, CK_REAL, CK_REAL, CK_REAL, 1>(v, g, bad); return 1;
-    case 44: fast_gen1<1, CK_CPLX, CK_CPLX, CK_CPLX, CK_CPLX, 1>(v, g, bad); return 1;
-    case 45: fast_gen1<1, CK_REAL, CK_IMAG, CK_IMAG, CK_REAL, 2>(v, g, bad); return 1;
-    case 46: fast_gen1<1, CK_REAL, CK_REAL, CK_REAL, CK_REAL, 2>(v, g, bad); return 1;
-    case 47: fast_gen1<1, CK_CPLX, CK_CPLX, CK_CPLX, CK_CPLX, 2>(v, g, bad); return 1;
-    case 48: fast_gen1<1, CK_ZERO, CK_ONE, CK_ONE, CK_ZERO, 1>(v, g, bad); return 1;
-    case 49: fast_gen1<1, CK_ZERO, CK_IMAG, CK_IMAG, CK_ZERO, 1>(v, g, bad); return 1;
-    case 50: fast_gen1<1, CK_REAL, CK_CPLX, CK_CPLX, CK_CPLX, 1>(v, g, bad); return 1;
-    case 51: fast_gen1<1, CK_REAL, CK_CPLX, CK_REAL, CK_CPLX, 1>(v, g, bad); return 1;
-    case 52: fast_gen1<1, CK_ZERO, CK_ONE, CK_ONE, CK_ZERO, 2>(v, g, bad); return 1;
-    case 53: fast_gen1<1, CK_ZERO, CK_IMAG, CK_IMAG, CK_ZERO, 2>(v, g, bad); return 1;
-    case 54: fast_gen1<1, CK_REAL, CK_CPLX, CK_CPLX, CK_CPLX, 2>(v, g, bad); return 1;
-    case 55: fast_gen1<1, CK_REAL, CK_CPLX, CK_REAL, CK_CPLX, 2>(v, g, bad); return 1;
-    case 56: fast_gen1<1>(v, g, bad); return 1;
-    case 57: fast_gen1<2, CK_REAL, CK_IMAG, CK_IMAG, CK_REAL, 1>(v, g, bad); return 1;
-    case 58: fast_gen1<2, CK_REAL, CK_REAL, CK_REAL, CK_REAL, 1>(v, g, bad); return 1;
-    case 59: fast_gen1<2, CK_CPLX, CK_CPLX, CK_CPLX, CK_CPLX, 1>(v, g, bad); return 1;
-    case 60: fast_gen1<2, CK_REAL, CK_IMAG, CK_IMAG, CK_REAL, 2>(v, g, bad); return 1;
-    case 61: fast_gen1<2, CK_REAL, CK_REAL, CK_REAL, CK_REAL, 2>(v, g, bad); return 1;
-    case 62: fast_gen1<2, CK_CPLX, CK_CPLX, CK_CPLX, CK_CPLX, 2>(v, g, bad); return 1;
-    case 63: fast_gen1<2, CK_ZERO, CK_ONE, CK_ONE, CK_ZERO, 1>(v, g, bad); return 1;
-    case 64: fast_gen1<2, CK_ZERO, CK_IMAG, CK_IMAG, CK_ZERO, 1>(v, g, bad); return 1;
-    case 65: fast_gen1<2, CK_REAL, CK_CPLX, CK_CPLX, CK_CPLX, 1>(v, g, bad); return 1;
-    case 66: fast_gen1<2, CK_REAL, CK_CPLX, CK_REAL, CK_CPLX, 1>(v, g, bad); return 1;
-    case 67: fast_gen1<2, CK_ZERO, CK_ONE, CK_ONE, CK_ZERO, 2>(v, g, bad); return 1;
-    case 68: fast_gen1<2, CK_ZERO, CK_IMAG, CK_IMAG, CK_ZERO, 2>(v, g, bad); return 1;
-    case 69: fast_gen1<2, CK_REAL, CK_CPLX, CK_CPLX, CK_CPLX, 2>(v, g, bad); return 1;
-    case 70: fast_gen1<2, CK_REAL, CK_CPLX, CK_REAL, CK_CPLX, 2>(v, g, bad); return 1;
-    case 71: fast_gen1<2>(v, g, bad); return 1;
-    case 72: fast_cp5<0, 1>(v, g, bad); return 1;
-    case 73: fast_cp5<0, 1, 1>(v, g, bad); return 1;
-    case 74: fast_cp5<0, 2>(v, g, bad); return 1;
-    case 75: fast_cp5<0, 2, 1>(v, g, bad); return 1;
-    case 76: fast_cp5<1, 0>(v, g, bad); return 1;
-    case 77: fast_cp5<1, 0, 1>(v, g, bad); return 1;
-    case 78: fast_cp5<1, 2>(v, g, bad); return 1;
-    case 79: fast_cp5<1, 2, 1>(v, g, bad); return 1;
-    case 80: fast_cp5<2, 0>(v, g, bad); return 1;
-    case 81: fast_cp5<2, 0, 1>(v, g, bad); return 1;
-    case 82: fast_cp5<2, 1>(v, g, bad); return 1;
-    case 83: fast_cp5<2, 1, 1>(v, g, bad); return 1;
-    case 84: fast_cxd<0, 1>(v, g, bad); return 1;
-    case 85: fast_cxd<0, 1, 1>(v, g, bad); return 1;
-    case 86: fast_cxd<0, 2>(v, g, bad); return 1;
-    case 87: fast_cxd<0, 2, 1>(v, g, bad); return 1;
-    case 88: fast_cxd<1, 0>(v, g, bad); return 1;
-    case 89: fast_cxd<1, 0, 1>(v, g, bad); return 1;
-    case 90: fast_cxd<1, 2>(v, g, bad); return 1;
-    case 91: fast_cxd<1, 2, 1>(v, g, bad); return 1;
-    case 92: fast_cxd<2, 0>(v, g, bad); return 1;
-    case 93: fast_cxd<2, 0, 1>(v, g, bad); return 1;
-    case 94: fast_cxd<2, 1>(v, g, bad); return 1;
-    case 95: fast_cxd<2, 1, 1>(v, g, bad); return 1;
-    case 96: fast_cx<0, 1>(v); return 1;
-    case 97: fast_cx<0, 2>(v); return 1;
-    case 98: fast_cx<1, 0>(v); return 1;
-    case 99: fast_cx<1, 2>(v); return 1;
-    case 100: fast_cx<2, 0>(v); return 1;
-    case 101: fast_cx<2, 1>(v); return 1;
-    case 102: fast_cz<0, 1>(v, g, bad); return 1;
-    case 103: fast_cz<0, 2>(v, g, bad); return 1;
-    case 104: fast_cz<1, 2>(v, g, bad); return 1;
-    case 105: fast_swap<0, 1>(v); return 1;
-    case 106: fast_swap<0, 2>(v); return 1;
-    case 107: fast_swap<1, 2>(v); return 1;
+    case 0: if constexpr (case_on(S, 0)) { run_pdiag_r<0>(v, fp + q, g.run, gidx); return g.run; } else { bad = true; return 1; }
+    case 1: if constexpr (case_on(S, 1)) { run_pdiag_r<1>(v, fp + q, g.run, gidx); return g.run; } else { bad = true; return 1; }
+    case 2: if constexpr (case_on(S, 2)) { run_pdiag_r<2>(v, fp + q, g.run, gidx); return g.run; } else { bad = true; return 1; }
+    case 3: if constexpr (case_on(S, 3)) { run_pdiag_r<3>(v, fp + q, g.run, gidx); return g.run; } else { bad = true; return 1; }
+    case 4: if constexpr (case_on(S, 4)) { fast_pdiag<0, 0>(v, g, pdiag_var(g, gidx), bad); return 1; } else { bad = true; return 1; }
+    case 5: if constexpr (case_on(S, 5)) { fast_pdiag<0, 1>(v, g, pdiag_var(g, gidx), bad); return 1; } else { bad = true; return 1; }
+    case 6: if constexpr (case_on(S, 6)) { fast_pdiag<1, 0>(v, g, pdiag_var(g, gidx), bad); return 1; } else { bad = true; return 1; }
+    case 7: if constexpr (case_on(S, 7)) { fast_pdiag<1, 1>(v, g, pdiag_var(g, gidx), bad); return 1; } else { bad = true; return 1; }
+    case 8: if constexpr (case_on(S, 8)) { fast_pdiag<2, 0>(v, g, pdiag_var(g, gidx), bad); return 1; } else { bad = true; return 1; }
+    case 9: if constexpr (case_on(S, 9)) { fast_pdiag<2, 1>(v, g, pdiag_var(g, gidx), bad); return 1; } else { bad = true; return 1; }
+    case 10: if constexpr (case_on(S, 10)) { fast_pdiag<3, 0>(v, g, pdiag_var(g, gidx), bad); return 1; } else { bad = true; return 1; }
+    case 11: if constexpr (case_on(S, 11)) { fast_pdiag<3, 1>(v, g, pdiag_var(g, gidx), bad); return 1; } else { bad = true; return 1; }
+    case 12: if constexpr (case_on(S, 12)) { fast_diag<0, CK_ONE, CK_CPLX, 1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 13: if constexpr (case_on(S, 13)) { fast_diag<0, CK_CPLX, CK_CPLX, 1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 14: if constexpr (case_on(S, 14)) { fast_diag<0, CK_ONE, CK_CPLX, 2>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 15: if constexpr (case_on(S, 15)) { fast_diag<0, CK_CPLX, CK_CPLX, 2>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 16: if constexpr (case_on(S, 16)) { fast_diag<0>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 17: if constexpr (case_on(S, 17)) { fast_diag<1, CK_ONE, CK_CPLX, 1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 18: if constexpr (case_on(S, 18)) { fast_diag<1, CK_CPLX, CK_CPLX, 1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 19: if constexpr (case_on(S, 19)) { fast_diag<1, CK_ONE, CK_CPLX, 2>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 20: if constexpr (case_on(S, 20)) { fast_diag<1, CK_CPLX, CK_CPLX, 2>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 21: if constexpr (case_on(S, 21)) { fast_diag<1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 22: if constexpr (case_on(S, 22)) { fast_diag<2, CK_ONE, CK_CPLX, 1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 23: if constexpr (case_on(S, 23)) { fast_diag<2, CK_CPLX, CK_CPLX, 1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 24: if constexpr (case_on(S, 24)) { fast_diag<2, CK_ONE, CK_CPLX, 2>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 25: if constexpr (case_on(S, 25)) { fast_diag<2, CK_CPLX, CK_CPLX, 2>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 26: if constexpr (case_on(S, 26)) { fast_diag<2>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 27: if constexpr (case_on(S, 27)) { fast_gen1<0, CK_REAL, CK_IMAG, CK_IMAG, CK_REAL, 1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 28: if constexpr (case_on(S, 28)) { fast_gen1<0, CK_REAL, CK_REAL, CK_REAL, CK_REAL, 1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 29: if constexpr (case_on(S, 29)) { fast_gen1<0, CK_CPLX, CK_CPLX, CK_CPLX, CK_CPLX, 1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 30: if constexpr (case_on(S, 30)) { fast_gen1<0, CK_REAL, CK_IMAG, CK_IMAG, CK_REAL, 2>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 31: if constexpr (case_on(S, 31)) { fast_gen1<0, CK_REAL, CK_REAL, CK_REAL, CK_REAL, 2>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 32: if constexpr (case_on(S, 32)) { fast_gen1<0, CK_CPLX, CK_CPLX, CK_CPLX, CK_CPLX, 2>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 33: if constexpr (case_on(S, 33)) { fast_gen1<0, CK_ZERO, CK_ONE, CK_ONE, CK_ZERO, 1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 34: if constexpr (case_on(S, 34)) { fast_gen1<0, CK_ZERO, CK_IMAG, CK_IMAG, CK_ZERO, 1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 35: if constexpr (case_on(S, 35)) { fast_gen1<0, CK_REAL, CK_CPLX, CK_CPLX, CK_CPLX, 1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 36: if constexpr (case_on(S, 36)) { fast_gen1<0, CK_REAL, CK_CPLX, CK_REAL, CK_CPLX, 1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 37: if constexpr (case_on(S, 37)) { fast_gen1<0, CK_ZERO, CK_ONE, CK_ONE, CK_ZERO, 2>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 38: if constexpr (case_on(S, 38)) { fast_gen1<0, CK_ZERO, CK_IMAG, CK_IMAG, CK_ZERO, 2>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 39: if constexpr (case_on(S, 39)) { fast_gen1<0, CK_REAL, CK_CPLX, CK_CPLX, CK_CPLX, 2>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 40: if constexpr (case_on(S, 40)) { fast_gen1<0, CK_REAL, CK_CPLX, CK_REAL, CK_CPLX, 2>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 41: if constexpr (case_on(S, 41)) { fast_gen1<0>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 42: if constexpr (case_on(S, 42)) { fast_gen1<1, CK_REAL, CK_IMAG, CK_IMAG, CK_REAL, 1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 43: if constexpr (case_on(S, 43)) { fast_gen1<1, CK_REAL, CK_REAL, CK_REAL, CK_REAL, 1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 44: if constexpr (case_on(S, 44)) { fast_gen1<1, CK_CPLX, CK_CPLX, CK_CPLX, CK_CPLX, 1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 45: if constexpr (case_on(S, 45)) { fast_gen1<1, CK_REAL, CK_IMAG, CK_IMAG, CK_REAL, 2>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 46: if constexpr (case_on(S, 46)) { fast_gen1<1, CK_REAL, CK_REAL, CK_REAL, CK_REAL, 2>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 47: if constexpr (case_on(S, 47)) { fast_gen1<1, CK_CPLX, CK_CPLX, CK_CPLX, CK_CPLX, 2>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 48: if constexpr (case_on(S, 48)) { fast_gen1<1, CK_ZERO, CK_ONE, CK_ONE, CK_ZERO, 1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 49: if constexpr (case_on(S, 49)) { fast_gen1<1, CK_ZERO, CK_IMAG, CK_IMAG, CK_ZERO, 1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 50: if constexpr (case_on(S, 50)) { fast_gen1<1, CK_REAL, CK_CPLX, CK_CPLX, CK_CPLX, 1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 51: if constexpr (case_on(S, 51)) { fast_gen1<1, CK_REAL, CK_CPLX, CK_REAL, CK_CPLX, 1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 52: if constexpr (case_on(S, 52)) { fast_gen1<1, CK_ZERO, CK_ONE, CK_ONE, CK_ZERO, 2>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 53: if constexpr (case_on(S, 53)) { fast_gen1<1, CK_ZERO, CK_IMAG, CK_IMAG, CK_ZERO, 2>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 54: if constexpr (case_on(S, 54)) { fast_gen1<1, CK_REAL, CK_CPLX, CK_CPLX, CK_CPLX, 2>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 55: if constexpr (case_on(S, 55)) { fast_gen1<1, CK_REAL, CK_CPLX, CK_REAL, CK_CPLX, 2>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 56: if constexpr (case_on(S, 56)) { fast_gen1<1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 57: if constexpr (case_on(S, 57)) { fast_gen1<2, CK_REAL, CK_IMAG, CK_IMAG, CK_REAL, 1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 58: if constexpr (case_on(S, 58)) { fast_gen1<2, CK_REAL, CK_REAL, CK_REAL, CK_REAL, 1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 59: if constexpr (case_on(S, 59)) { fast_gen1<2, CK_CPLX, CK_CPLX, CK_CPLX, CK_CPLX, 1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 60: if constexpr (case_on(S, 60)) { fast_gen1<2, CK_REAL, CK_IMAG, CK_IMAG, CK_REAL, 2>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 61: if constexpr (case_on(S, 61)) { fast_gen1<2, CK_REAL, CK_REAL, CK_REAL, CK_REAL, 2>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 62: if constexpr (case_on(S, 62)) { fast_gen1<2, CK_CPLX, CK_CPLX, CK_CPLX, CK_CPLX, 2>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 63: if constexpr (case_on(S, 63)) { fast_gen1<2, CK_ZERO, CK_ONE, CK_ONE, CK_ZERO, 1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 64: if constexpr (case_on(S, 64)) { fast_gen1<2, CK_ZERO, CK_IMAG, CK_IMAG, CK_ZERO, 1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 65: if constexpr (case_on(S, 65)) { fast_gen1<2, CK_REAL, CK_CPLX, CK_CPLX, CK_CPLX, 1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 66: if constexpr (case_on(S, 66)) { fast_gen1<2, CK_REAL, CK_CPLX, CK_REAL, CK_CPLX, 1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 67: if constexpr (case_on(S, 67)) { fast_gen1<2, CK_ZERO, CK_ONE, CK_ONE, CK_ZERO, 2>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 68: if constexpr (case_on(S, 68)) { fast_gen1<2, CK_ZERO, CK_IMAG, CK_IMAG, CK_ZERO, 2>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 69: if constexpr (case_on(S, 69)) { fast_gen1<2, CK_REAL, CK_CPLX, CK_CPLX, CK_CPLX, 2>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 70: if constexpr (case_on(S, 70)) { fast_gen1<2, CK_REAL, CK_CPLX, CK_REAL, CK_CPLX, 2>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 71: if constexpr (case_on(S, 71)) { fast_gen1<2>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 72: if constexpr (case_on(S, 72)) { fast_cp5<0, 1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 73: if constexpr (case_on(S, 73)) { fast_cp5<0, 1, 1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 74: if constexpr (case_on(S, 74)) { fast_cp5<0, 2>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 75: if constexpr (case_on(S, 75)) { fast_cp5<0, 2, 1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 76: if constexpr (case_on(S, 76)) { fast_cp5<1, 0>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 77: if constexpr (case_on(S, 77)) { fast_cp5<1, 0, 1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 78: if constexpr (case_on(S, 78)) { fast_cp5<1, 2>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 79: if constexpr (case_on(S, 79)) { fast_cp5<1, 2, 1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 80: if constexpr (case_on(S, 80)) { fast_cp5<2, 0>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 81: if constexpr (case_on(S, 81)) { fast_cp5<2, 0, 1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 82: if constexpr (case_on(S, 82)) { fast_cp5<2, 1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 83: if constexpr (case_on(S, 83)) { fast_cp5<2, 1, 1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 84: if constexpr (case_on(S, 84)) { fast_cxd<0, 1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 85: if constexpr (case_on(S, 85)) { fast_cxd<0, 1, 1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 86: if constexpr (case_on(S, 86)) { fast_cxd<0, 2>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 87: if constexpr (case_on(S, 87)) { fast_cxd<0, 2, 1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 88: if constexpr (case_on(S, 88)) { fast_cxd<1, 0>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 89: if constexpr (case_on(S, 89)) { fast_cxd<1, 0, 1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 90: if constexpr (case_on(S, 90)) { fast_cxd<1, 2>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 91: if constexpr (case_on(S, 91)) { fast_cxd<1, 2, 1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 92: if constexpr (case_on(S, 92)) { fast_cxd<2, 0>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 93: if constexpr (case_on(S, 93)) { fast_cxd<2, 0, 1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 94: if constexpr (case_on(S, 94)) { fast_cxd<2, 1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 95: if constexpr (case_on(S, 95)) { fast_cxd<2, 1, 1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 96: if constexpr (case_on(S, 96)) { fast_cx<0, 1>(v); return 1; } else { bad = true; return 1; }
+    case 97: if constexpr (case_on(S, 97)) { fast_cx<0, 2>(v); return 1; } else { bad = true; return 1; }
+    case 98: if constexpr (case_on(S, 98)) { fast_cx<1, 0>(v); return 1; } else { bad = true; return 1; }
+    case 99: if constexpr (case_on(S, 99)) { fast_cx<1, 2>(v); return 1; } else { bad = true; return 1; }
+    case 100: if constexpr (case_on(S, 100)) { fast_cx<2, 0>(v); return 1; } else { bad = true; return 1; }
+    case 101: if constexpr (case_on(S, 101)) { fast_cx<2, 1>(v); return 1; } else { bad = true; return 1; }
+    case 102: if constexpr (case_on(S, 102)) { fast_cz<0, 1>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 103: if constexpr (case_on(S, 103)) { fast_cz<0, 2>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 104: if constexpr (case_on(S, 104)) { fast_cz<1, 2>(v, g, bad); return 1; } else { bad = true; return 1; }
+    case 105: if constexpr (case_on(S, 105)) { fast_swap<0, 1>(v); return 1; } else { bad = true; return 1; }
+    case 106: if constexpr (case_on(S, 106)) { fast_swap<0, 2>(v); return 1; } else { bad = true; return 1; }
+    case 107: if constexpr (case_on(S, 107)) { fast_swap<1, 2>(v); return 1; } else { bad = true; return 1; }
     default: bad = true; return 1;   // other 2q matrices: exact path only
     }
 }
@@ -1532,6 +1546,7 @@ __device__ void smem_generic(double2 *s, uint32_t tile, const TileGate &g) {
 // each group is applied by 2^(k-kRegBits) threads holding NB amplitudes in
 // registers.  Every thread moves exactly NB amplitudes per tile in each
 // direction, all issued before any is consumed (cp.async in, batched stores).
+template <int S>
 __global__ void __launch_bounds__(1 << (kTileBits - kRegBits), (kTileBits >= 12 ? 1 : (kTileBits == 11 ? QZ_MIN_CTAS : 4))) tile_pass_reg(const double2 *__restrict__ src, double2 *__restrict__ dst, uint32_t nbits,
                                                          PassDesc pd,
                                                          const GroupDesc *__restrict__ groups,
@@ -1688,7 +1703,7 @@ __global__ void __launch_bounds__(1 << (kTileBits - kRegBits), (kTileBits >= 12 
                 bool bad = !okblk;
                 path = okblk ? 3 : 4;
                 const TileGate *fp = gates + G.first_fast;
-                for (uint32_t q = 0; q < G.nfast && !bad;) q += fast_case(v, fp, q, gidx, bad);
+                for (uint32_t q = 0; q < G.nfast && !bad;) q += fast_case<S>(v, fp, q, gidx, bad);
                 if (bad && okblk) path = 5;
                 if (bad && G.relaxed) {
                     *flag = 1u;   // the exact path needs partners outside the tile
@@ -1915,8 +1930,10 @@ __global__ void k_flag_done(uint32_t *flag, uint64_t *count) {
 void set_attrs() {
     static bool attr_set = false;
     if (!attr_set) {
-        QZ_CUDA(cudaFuncSetAttribute(tile_pass_reg, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     110 * 1024));
+        QZ_CUDA(cudaFuncSetAttribute(tile_pass_reg<kPassAll>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
+        QZ_CUDA(cudaFuncSetAttribute(tile_pass_reg<kPassDiagH>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
         attr_set = true;
     }
 }
@@ -1946,9 +1963,10 @@ void launch_pass(const DevPlan &plan, const PassDesc &pd, const double2 *src, do
         // the map is only used for passes inside one window of whole slots
         static const bool off = getenv("QZ_NO_NZMAP") != nullptr;
         const bool usable = nz.slot && nbits > nz.cbits && !off;
-        tile_pass_reg<<<(unsigned)grid, threads, smem, s>>>(src, dst, nbits, pd, plan.groups, plan.gates,
-                                                           ntiles, debug_counters(), flag, cond,
-                                                           usable ? nz.slot : nullptr, nz.cbits);
+        auto kern = pd.variant == kPassDiagH ? tile_pass_reg<kPassDiagH> : tile_pass_reg<kPassAll>;
+        kern<<<(unsigned)grid, threads, smem, s>>>(src, dst, nbits, pd, plan.groups, plan.gates, ntiles,
+                                                   debug_counters(), flag, cond,
+                                                   usable ? nz.slot : nullptr, nz.cbits);
     }
     QZ_CHECK_LAUNCH();
 }

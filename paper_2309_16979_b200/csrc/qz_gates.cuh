@@ -96,6 +96,17 @@ struct GroupDesc {
 };
 
 // A fused pass: gates whose buffer bits all lie in the tile bit set T.
+// Case sets of the fused pass kernel: a pass whose fast lists only hold
+// diagonal runs, 1q diagonals, real 1q matrices (H) and CP5 ops gets a kernel
+// (tile_pass_reg<kPassDiagH>)
+// whose jump table has only those cases (anything else would go to the
+// exact path, so the set only affects speed, never results).
+constexpr int kPassAll = 0, kPassDiagH = 1;
+__host__ __device__ constexpr bool case_on(int S, uint32_t c) {
+    return S == kPassAll || c <= 26 || c == 28 || c == 31 || c == 43 || c == 46 || c == 58 ||
+           c == 61 || (c >= 72 && c <= 83);
+}
+
 struct PassDesc {
     uint32_t k;            // tile bits (|T|)
     uint32_t lowbits;      // T ⊇ {0..lowbits-1}
@@ -111,7 +122,7 @@ struct PassDesc {
     uint32_t relaxed;      // 0 strict; 1 relaxed, +0-safe units / swap network: in place,
                            // a flag replays the whole window; 2 relaxed with checked
                            // units: out of place, replayed pass by pass
-    uint32_t pad5;
+    uint32_t variant;      // kernel case set (host side: kPassAll or kPassDiagH)
     uint8_t perm[48];
 };
 
