@@ -771,14 +771,32 @@ void upload_plan(const GatePlan &plan, DevPlan &out, cudaStream_t s) {
     // every group is in it (and no group needs the shared-memory generic path)
     static const bool narrow_off = getenv("QZ_NO_NARROW") != nullptr;
     for (PassDesc &pd : out.host_passes) {
-        bool narrow = !narrow_off && pd.kind != PASS_SWAPS;
-        for (uint32_t gi = 0; narrow && gi < pd.ngroups; ++gi) {
-            const GroupDesc &G = plan.groups[pd.first_group + gi];
-            if (G.generic) narrow = false;
-            for (uint32_t q = 0; narrow && q < G.nfast; ++q)
-                narrow = case_on(kPassDiagH, plan.gates[G.first_fast + q].cid);
+        pd.variant = kPassAll;
+        for (int S : {kPassDiagH, kPassGen}) {
+            bool narrow = !narrow_off && pd.kind != PASS_SWAPS;
+            for (uint32_t gi = 0; narrow && gi < pd.ngroups; ++gi) {
+                const GroupDesc &G = plan.groups[pd.first_group + gi];
+                if (G.generic) narrow = false;
+                for (uint32_t q = 0; narrow && q < G.nfast; ++q)
+                    narrow = case_on(S, plan.gates[G.first_fast + q].cid);
+            }
+            if (narrow) {
+                pd.variant = uint32_t(S);
+                break;
+            }
         }
-        pd.variant = narrow ? kPassDiagH : kPassAll;
+        static const bool dump = getenv("QZ_CID_DUMP") != nullptr;
+        if (dump && pd.kind != PASS_SWAPS) {
+            uint32_t hist[128] = {0};
+            for (uint32_t gi = 0; gi < pd.ngroups; ++gi) {
+                const GroupDesc &G = plan.groups[pd.first_group + gi];
+                for (uint32_t q = 0; q < G.nfast; ++q) ++hist[plan.gates[G.first_fast + q].cid & 127];
+            }
+            fprintf(stderr, "qz pass k=%u groups=%u variant=%u cids:", pd.k, pd.ngroups, pd.variant);
+            for (int c = 0; c < 128; ++c)
+                if (hist[c]) fprintf(stderr, " %d:%u", c, hist[c]);
+            fprintf(stderr, "\n");
+        }
     }
     out.relaxed = false;
     for (const PassDesc &pd : plan.passes) out.relaxed |= pd.relaxed != 0;
@@ -1934,6 +1952,8 @@ void set_attrs() {
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
         QZ_CUDA(cudaFuncSetAttribute(tile_pass_reg<kPassDiagH>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
+        QZ_CUDA(cudaFuncSetAttribute(tile_pass_reg<kPassGen>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
         attr_set = true;
     }
 }
@@ -1963,7 +1983,9 @@ void launch_pass(const DevPlan &plan, const PassDesc &pd, const double2 *src, do
         // the map is only used for passes inside one window of whole slots
         static const bool off = getenv("QZ_NO_NZMAP") != nullptr;
         const bool usable = nz.slot && nbits > nz.cbits && !off;
-        auto kern = pd.variant == kPassDiagH ? tile_pass_reg<kPassDiagH> : tile_pass_reg<kPassAll>;
+        auto kern = pd.variant == kPassDiagH ? tile_pass_reg<kPassDiagH>
+                    : pd.variant == kPassGen ? tile_pass_reg<kPassGen>
+                                             : tile_pass_reg<kPassAll>;
         kern<<<(unsigned)grid, threads, smem, s>>>(src, dst, nbits, pd, plan.groups, plan.gates, ntiles,
                                                    debug_counters(), flag, cond,
                                                    usable ? nz.slot : nullptr, nz.cbits);

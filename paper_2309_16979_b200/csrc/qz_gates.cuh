@@ -101,10 +101,15 @@ struct GroupDesc {
 // (tile_pass_reg<kPassDiagH>)
 // whose jump table has only those cases (anything else would go to the
 // exact path, so the set only affects speed, never results).
-constexpr int kPassAll = 0, kPassDiagH = 1;
+// kPassGen: diagonal runs, every 1q case, CX and CX-diagonal ops (QAOA /
+// supremacy-style layers).
+constexpr int kPassAll = 0, kPassDiagH = 1, kPassGen = 2;
 __host__ __device__ constexpr bool case_on(int S, uint32_t c) {
-    return S == kPassAll || c <= 26 || c == 28 || c == 31 || c == 43 || c == 46 || c == 58 ||
-           c == 61 || (c >= 72 && c <= 83);
+    if (S == kPassDiagH)
+        return c <= 26 || c == 28 || c == 31 || c == 43 || c == 46 || c == 58 || c == 61 ||
+               (c >= 72 && c <= 83);
+    if (S == kPassGen) return c <= 71 || (c >= 84 && c <= 101);
+    return true;
 }
 
 struct PassDesc {
@@ -122,7 +127,7 @@ struct PassDesc {
     uint32_t relaxed;      // 0 strict; 1 relaxed, +0-safe units / swap network: in place,
                            // a flag replays the whole window; 2 relaxed with checked
                            // units: out of place, replayed pass by pass
-    uint32_t variant;      // kernel case set (host side: kPassAll or kPassDiagH)
+    uint32_t variant;      // kernel case set (host side: kPassAll / kPassDiagH / kPassGen)
     uint8_t perm[48];
 };
 
