@@ -106,7 +106,7 @@ struct GroupDesc {
 constexpr int kPassAll = 0, kPassDiagH = 1, kPassGen = 2;
 __host__ __device__ constexpr bool case_on(int S, uint32_t c) {
     if (S == kPassDiagH)
-        return c <= 26 || c == 28 || c == 31 || c == 43 || c == 46 || c == 58 || c == 61 ||
+        return c <= 11 || c == 28 || c == 31 || c == 43 || c == 46 || c == 58 || c == 61 ||
                (c >= 72 && c <= 83);
     if (S == kPassGen) return c <= 71 || (c >= 84 && c <= 101);
     return true;
