@@ -382,3 +382,40 @@ def test_host_staged_replay_modes(engine, oracle, fuse, force):
     assert sim.digest() == ref
     if force:
         assert sim.stats()["replays"] >= 1
+
+
+
+def test_full_case_set_same_digest(engine, golden, oracle, tmp_path):
+    """The per-pass case-set choice (tile_pass_reg<kPassDiagH / kPassGen>) only
+    changes speed: with QZ_NO_NARROW=1 (every pass on the full jump table) the
+    reference-generated digests hold too.  Fresh process: the switch is read
+    once per process."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    recs = [r for r in golden["runs"] if r["circuit"].startswith(("qft:", "ghz:"))][:3]
+    recs += [r for r in golden["runs"] if not r["circuit"].startswith(("qft:", "ghz:"))][:2]
+    for i, rec in enumerate(recs):
+        np.save(tmp_path / f"g{i}.npy", circuit(golden, oracle, rec["circuit"]))
+    script = (
+        "import json, sys\n"
+        "import numpy as np\n"
+        "from paper_2309_16979_b200 import engine as E\n"
+        "recs, d = json.loads(sys.argv[1]), sys.argv[2]\n"
+        "eng = E.Engine()\n"
+        "out = []\n"
+        "for i, rec in enumerate(recs):\n"
+        "    sim = eng.simulator(rec['n'], rec['c'], rec['m'], rec['eb'])\n"
+        "    sim.run(np.load(f'{d}/g{i}.npy'))\n"
+        "    out.append(f'{sim.digest():016x}')\n"
+        "    sim.close()\n"
+        "print(json.dumps(out))\n")
+    env = dict(os.environ, QZ_NO_NARROW="1", PYTHONPATH=str(root))
+    res = subprocess.run([sys.executable, "-c", script, json.dumps(recs), str(tmp_path)],
+                         cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    assert json.loads(res.stdout.strip().splitlines()[-1]) == [r["digest"] for r in recs]
