@@ -2,7 +2,7 @@
 """bench.py — MEMQSim hot path on B200: gates/s and circuit time at n qubits.
 
 Default workload (BASELINE.json configs[1]): 30-qubit QFT (2220 gates) from
-|0...0>, compressed-chunk store fully resident in HBM, c=16, eb=1e-5.
+|0...0>, compressed-chunk store fully resident in HBM, c=16, m=30, eb=1e-5.
 A step = one circuit execution through the staged pipeline: store init
 (store.cpp:26-81) + every stage's decode → fused gate passes → encode
 (pipeline.cpp:128-314), ending with the final compressed store in HBM.
@@ -10,9 +10,21 @@ A step = one circuit execution through the staged pipeline: store init
   python bench.py [--gpus N --steps K --warmup W]          engine arm
   python bench.py --impl reference [...]                   reference CPU arm
 
-Multi-GPU (torchrun, one rank per GPU): in this round every rank runs its
-own replica of the workload ("replicas only" until the sharded
-exchange lands), value = all ranks' gates / max-over-ranks device time.
+Roofline: every engine kernel launch inside the timed region is bracketed by
+CUDA events on its own stream (qzc_kprof_*); `roofline` is the DOMINANT
+launch (largest share of the step) with its algorithmic bytes (SURVEY §8d:
+32 B per window amplitude for a gate pass), and `roofline.kernels` lists
+every kernel family (codec families with their payload bytes added).
+
+Companions (N=1, extra key `companions`): dense workloads the headline QFT
+does not exercise — supremacy-30 depth 20 at eb=1e-7 (codec on dense
+chunks, fidelity < 1) and QFT-30 at m=20 (37 stages, codec-dominated).
+
+Multi-GPU (torchrun, one rank per GPU; `--gpus N` without torchrun
+re-launches itself under torchrun): `--mode shard` (default for N>1) runs
+ONE circuit over all ranks with compressed chunks exchanged device to
+device over NCCL at ownership changes (strong scaling); `--mode replicas`
+runs an independent replica per rank (weak scaling).
 """
 from __future__ import annotations
 
@@ -32,9 +44,10 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "gates/sec and circuit time at n qubits (1/2/4/8 B200); comp. ratio; fidelity"
 PEAKS = ROOT / "MEASURED_PEAKS.json"
+FALLBACK_HBM = 6650.0   # B200_PROFILING.md fallback when MEASURED_PEAKS.json is absent
 
 
-def parse_args():
+def parse_args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
@@ -45,20 +58,19 @@ def parse_args():
     ap.add_argument("--c", type=int, default=16)
     ap.add_argument("--m", type=int, default=30)
     ap.add_argument("--eb", type=float, default=1e-5)
+    ap.add_argument("--depth", type=int, default=20, help="supremacy depth")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fidelity", action="store_true",
                     help="skip the uncompressed fp64 reference run used for the fidelity figure")
-    ap.add_argument("--cpu-budget", type=float, default=20.0,
-                    help="seconds of reference CPU work per sample")
-    ap.add_argument("--no-fuse", action="store_true")
-    ap.add_argument("--strict-passes", action="store_true",
-                    help="every gate qubit inside the pass tile (no relaxed diagonal units)")
-    ap.add_argument("--shard", action="store_true",
-                    help="N>1: shard ONE circuit over the ranks by global qubits with NCCL "
-                         "exchange of compressed chunks (strong scaling) instead of replicas")
+    ap.add_argument("--no-companions", action="store_true")
+    ap.add_argument("--no-kprof", action="store_true",
+                    help="no per-launch events in the timed region (roofline from phase totals)")
+    ap.add_argument("--fuse", default="relaxed", choices=["relaxed", "strict", "checked", "none"])
+    ap.add_argument("--mode", default=None, choices=["shard", "replicas"],
+                    help="N>1: shard one circuit over the ranks (default) or run replicas")
     ap.add_argument("--residency", default="hbm", choices=["hbm", "host"],
                     help="compressed store in HBM (config 2) or pinned host memory (config 3)")
-    return ap.parse_args()
+    return ap.parse_args(argv)
 
 
 # ----------------------------------------------------------------- clocks --
@@ -127,57 +139,6 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------- reference --
-def reference_sample(circuit, n, c, m, eb, budget_s, workers=0):
-    """Time the UNMODIFIED reference qzsim::run (oracle/_ref/libqzref.so) on a
-    bounded sample of the same workload.  At n=30 one reference stage sweep
-    alone takes ~40 s on 16 cores, so the sample is the same circuit family
-    run in full at the largest n_s <= n whose run fits budget_s, with the
-    same c, m (capped at n_s) and eb; gates/s is then scaled by 2^(n_s - n)
-    (every gate and codec sweep touches 2^n amplitudes).  The time is the
-    reference's own report.wall_seconds (pipeline.cpp:158-290)."""
-    sys.path.insert(0, str(ROOT / "tests"))
-    from oracles import Reference  # baseline infrastructure only
-    from paper_2309_16979_b200 import circuits
-    ref = Reference()
-    ns = max(c + 2, min(n, 20))
-    last = None
-    while True:
-        gates = circuits.make(circuit, ns)
-        t = time.time()
-        r = ref.run(ns, gates, c, min(m, ns), eb, workers=workers, depth=2, strategy=2)
-        el = time.time() - t
-        last = {"n_sample": ns, "gates": len(gates), "wall_seconds": r["wall_seconds"],
-                "elapsed": el, "gates_per_s_sample": len(gates) / r["wall_seconds"],
-                "gates_per_s": len(gates) / r["wall_seconds"] * 2.0 ** (ns - n),
-                "digest": r["digest"], "stages": r["stages"]}
-        if ns >= n or el * 4.5 > budget_s:
-            return last
-        ns += 2
-
-
-def reference_sample_fixed(args, first):
-    """Repeat the sample at the n_s chosen by the first step."""
-    sys.path.insert(0, str(ROOT / "tests"))
-    from oracles import Reference
-    from paper_2309_16979_b200 import circuits
-    ns = first["n_sample"]
-    gates = circuits.make(args.circuit, ns)
-    t = time.time()
-    r = Reference().run(ns, gates, args.c, min(args.m, ns), args.eb, workers=0, depth=2, strategy=2)
-    return {"n_sample": ns, "gates": len(gates), "wall_seconds": r["wall_seconds"],
-            "elapsed": time.time() - t, "gates_per_s_sample": len(gates) / r["wall_seconds"],
-            "gates_per_s": len(gates) / r["wall_seconds"] * 2.0 ** (ns - args.n),
-            "digest": r["digest"], "stages": r["stages"]}
-
-
-def sample_text(args, s, cores) -> str:
-    return (f"{args.circuit}-{s['n_sample']} full circuit ({s['gates']} gates, c={args.c} "
-            f"m={min(args.m, s['n_sample'])} eb={args.eb}, {s['stages']} stages) through the "
-            f"unmodified reference qzsim::run with {cores} decompress/recompress/kernel workers, "
-            f"{s['wall_seconds']:.2f} s = {s['gates_per_s_sample']:.2f} gates/s, scaled by "
-            f"2^({s['n_sample']}-{args.n}) to n={args.n}; host {cpu_info()}")
-
-
 def cpu_info() -> str:
     try:
         for line in open("/proc/cpuinfo"):
@@ -188,49 +149,285 @@ def cpu_info() -> str:
     return "unknown"
 
 
-def run_reference_arm(args, gates):
+def make_circuit(name: str, n: int, depth: int = 20):
+    from paper_2309_16979_b200 import circuits
+    if name == "supremacy":
+        return circuits.supremacy(n, depth=depth)
+    return circuits.make(name, n)
+
+
+def prefix_lengths(name: str, n: int) -> tuple[int, int]:
+    """Two gate-prefix lengths of the circuit for the reference sample: whole
+    controlled-phase blocks for the QFT (H + 1 or 2 CP5 runs), one and two
+    single-qubit layers' worth of gates otherwise."""
+    if name == "qft":
+        return 6, 11
+    return max(2, n // 6), max(4, n // 3)
+
+
+class ReferenceSampler:
+    """The UNMODIFIED reference qzsim::run (oracle/_ref/libqzref.so) on a
+    bounded sample of the SAME workload: the circuit's first k1 and k2 gates
+    at the full n, c, m and eb, on every host core.  Its own report
+    wall_seconds (pipeline.cpp:158-290) is T(k) = T0 + k * t_gate (T0 =
+    init + one codec sweep of the 2^n state, t_gate = one reference gate
+    pass over 2^n amplitudes), so the full circuit's time is estimated as
+    T(k1) + (G - k1) * (T(k2) - T(k1)) / (k2 - k1)."""
+
+    def __init__(self, args):
+        sys.path.insert(0, str(ROOT / "tests"))
+        from oracles import Reference  # baseline infrastructure only
+        self.ref = Reference()
+        self.args = args
+        self.gates = make_circuit(args.circuit, args.n, args.depth)
+        self.k1, self.k2 = prefix_lengths(args.circuit, args.n)
+        self.times = {self.k1: [], self.k2: []}
+        self.cores = os.cpu_count() or 1
+
+    def sample(self, k: int) -> float:
+        a = self.args
+        # Synchronous strategy: the reference's device bound is 2^m x 16 B
+        # instead of twice that (results are strategy-invariant, SPEC.md:366)
+        r = self.ref.run(a.n, self.gates[:k], a.c, min(a.m, a.n), a.eb, workers=0, depth=2,
+                         strategy=0)
+        self.times[k].append(r["wall_seconds"])
+        return r["wall_seconds"]
+
+    def estimate(self) -> dict:
+        from paper_2309_16979_b200.sharding import global_stages
+        a = self.args
+        t1 = statistics.median(self.times[self.k1])
+        t2 = statistics.median(self.times[self.k2])
+        per_gate = max((t2 - t1) / (self.k2 - self.k1), 1e-9)
+        g = len(self.gates)
+        # both prefixes are one stage; every further stage adds one codec
+        # sweep T0 = T(k1) - k1 * per_gate (pipeline.cpp:159-276)
+        self.stages = len(global_stages(a.n, a.c, min(a.m, a.n), self.gates))
+        t0 = max(t1 - self.k1 * per_gate, 0.0)
+        full = self.stages * t0 + g * per_gate
+        return {"t_k1": t1, "t_k2": t2, "per_gate_s": per_gate, "sweep_s": t0,
+                "stages": self.stages, "full_circuit_s": full, "gates_per_s": g / full}
+
+    def text(self, est) -> str:
+        a = self.args
+        return (f"{a.circuit}-{a.n} (c={a.c} m={a.m} eb={a.eb}, the engine arm's config): the "
+                f"unmodified reference qzsim::run on its first {self.k1} and {self.k2} gates with "
+                f"{self.cores} decompress/recompress/kernel workers (Synchronous strategy), "
+                f"{est['t_k1']:.2f} s / {est['t_k2']:.2f} s -> {est['per_gate_s']:.3f} s per gate, "
+                f"{est['sweep_s']:.2f} s per stage sweep; full {len(self.gates)}-gate circuit "
+                f"({est['stages']} stages) estimated at {est['full_circuit_s']:.1f} s "
+                f"(stages x sweep + G x per-gate); host {cpu_info()}")
+
+
+def run_reference_arm(args) -> int:
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    cores = os.cpu_count() or 1
-    cfg = workload_config(args)
-    vals, samples = [], []
-    first = reference_sample(args.circuit, args.n, args.c, args.m, args.eb, args.cpu_budget)
-    for i in range(args.warmup + args.steps):
-        s = first if i == 0 else reference_sample_fixed(args, first)
-        if i >= args.warmup:
-            vals.append(s["gates_per_s"])
-            samples.append(s)
-    v = statistics.median(vals)
-    s = samples[-1]
+    s = ReferenceSampler(args)
+    ks = [s.k1, s.k2]
+    for i in range(args.warmup):
+        s.sample(ks[i % 2])
+    s.times = {s.k1: [], s.k2: []}
+    for i in range(max(args.steps, 2)):
+        s.sample(ks[i % 2])
+    est = s.estimate()
+    v = est["gates_per_s"]
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "gates/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * s["wall_seconds"], "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
-        "cpu_baseline": {"value": v, "unit": "gates/s", "cores": cores, "kind": "reference",
-                         "sample": sample_text(args, s, cores)},
+        "ms_per_step": 1e3 * est["full_circuit_s"], "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args),
+        "cpu_baseline": {"value": v, "unit": "gates/s", "cores": s.cores, "kind": "reference",
+                         "sample": s.text(est)},
+        "reference_samples_s": {str(k): v for k, v in s.times.items()},
         "e2e": {"value": v, "unit": "gates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
     return 0
 
 
-def workload_config(args) -> dict:
+def workload_config(args, circuit=None, n=None, m=None, eb=None) -> dict:
+    circuit = circuit or args.circuit
+    n = n or args.n
+    m = m or args.m
+    eb = eb or args.eb
     where = "HBM-resident store" if args.residency == "hbm" else "host-staged store (pinned host RAM)"
-    return {"workload": f"{args.circuit}-{args.n} compressed-chunk pipeline, {where}",
-            "circuit": args.circuit, "num_qubits": args.n, "chunk_qubits": args.c,
-            "batch_qubits": args.m, "error_bound": args.eb,
-            "l2": "inputs larger than L2 (2^n x 16 B dense state per stage sweep)"}
+    cfg = {"workload": f"{circuit}-{n} compressed-chunk pipeline, {where}",
+           "circuit": circuit, "num_qubits": n, "chunk_qubits": args.c,
+           "batch_qubits": m, "error_bound": eb,
+           "l2": "inputs larger than L2 (2^n x 16 B dense state per stage sweep)"}
+    if circuit == "supremacy":
+        cfg["depth"] = args.depth
+    return cfg
 
 
 # ----------------------------------------------------------------- engine --
+def peaks() -> tuple[float, str]:
+    if PEAKS.exists():
+        p = json.loads(PEAKS.read_text())
+        if p.get("hbm_gbs"):
+            return float(p["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy read+write, burst)"
+    return FALLBACK_HBM, "B200_PROFILING.md fallback"
+
+
+def family(name: str) -> str:
+    if name.startswith("tile_pass_reg") or name == "tile_swaps":
+        return "gate_pass"
+    if name in ("k_dec_lossy_coop", "k_dec_lossy", "k_dec_lossless"):
+        return "decode"
+    if name in ("k_enc_lossy", "k_enc_lossless"):
+        return "encode"
+    return name
+
+
+def roofline_from_kprof(recs, steps, stats, hbm_peak, peak_src) -> dict:
+    """Dominant launch (largest share of the step) + per-family rooflines.
+    Records of the timed region only; a launch is keyed by (stage, kernel,
+    pass index) so the same pass of every step averages together."""
+    run = [r for r in recs if r["stage"] != 0xFFFFFFFF]
+    per_key = {}
+    for r in run:
+        per_key.setdefault((r["stage"], r["name"], r["tag"]), []).append(r)
+    total = sum(r["seconds"] for r in run) / steps
+    best, best_t = None, -1.0
+    for key, rs in per_key.items():
+        if key[1] in ("replay_pass", "replay_decode"):
+            continue
+        t = sum(r["seconds"] for r in rs) / steps
+        if t > best_t:
+            best, best_t = key, t
+    rs = per_key[best]
+    avg = sum(r["seconds"] for r in rs) / len(rs)
+    nbytes = rs[0]["bytes"]
+    fam = {}
+    for r in recs:   # init_basis included in the families (its kernels run in the step)
+        f = fam.setdefault(family(r["name"]), {"seconds": 0.0, "bytes": 0.0, "launches": 0})
+        f["seconds"] += r["seconds"] / steps
+        f["bytes"] += r["bytes"] / steps
+        f["launches"] += 1
+    # codec families: compressed bytes read / written per step (stats are the last step's)
+    if "decode" in fam:
+        fam["decode"]["bytes"] += stats["payload_in_bytes"]
+    if "encode" in fam:
+        fam["encode"]["bytes"] += stats["payload_out_bytes"]
+    kernels = {}
+    for k, f in sorted(fam.items(), key=lambda kv: -kv[1]["seconds"]):
+        ach = f["bytes"] / f["seconds"] / 1e9 if f["seconds"] > 0 and f["bytes"] > 0 else None
+        kernels[k] = {"ms_per_step": 1e3 * f["seconds"], "share": f["seconds"] / total if total else None,
+                      "launches_per_step": f["launches"] / steps,
+                      "GBps": ach, "frac": ach / hbm_peak if ach else None}
+    ach = nbytes / avg / 1e9
+    return {"bound": "hbm", "kernel": f"{best[1]} (stage {best[0]}, pass {best[2]})",
+            "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
+            "traffic": None, "bytes_per_launch": nbytes, "avg_launch_s": avg,
+            "share_of_step": best_t / total if total else None,
+            "peak_source": peak_src,
+            "bytes_basis": "algorithmic: 32 B per window amplitude per gate pass (read + write), "
+                           "codec families 16 B per dense amplitude + compressed payload bytes",
+            "kernels": kernels}
+
+
+def committed_traffic(key: str, kernel: str):
+    tfile = ROOT / "profiles" / "traffic.json"
+    if tfile.exists():
+        t = json.loads(tfile.read_text()).get(key)
+        if t and t.get("kernel", kernel).split(" ")[0] == kernel.split(" ")[0]:
+            return t
+    return None
+
+
+def timed_steps(eng, sim, gates, steps, local, kprof=True):
+    """K steps of init + run on the device clock; returns (seconds, kprof
+    records, clocks, engine launches)."""
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(1.0)   # nvidia-smi's first samples arrive before the timed region
+    eng.timer_begin()
+    eng.timer_end()
+    launches0 = eng.kernel_launches
+    if kprof:
+        eng.kprof_enable(True)
+    clocks.mark_begin()
+    eng.timer_begin()
+    for _ in range(steps):
+        sim.init_basis()
+        sim.run(gates)
+    t_dev = eng.timer_end()
+    clocks.mark_end()
+    recs = eng.kprof_read() if kprof else []
+    eng.kprof_enable(False)
+    launches = eng.kernel_launches - launches0
+    return t_dev, recs, clocks.stop(), launches
+
+
+def fidelity_of(eng, sim, n, gates):
+    try:
+        dense = eng.dense_state(n, gates)
+        f = sim.fidelity(dense)
+        dense.free()
+        return {"fidelity": f, "infidelity": 1.0 - f}
+    except Exception as e:  # not enough HBM for the dense state next to the store
+        return {"fidelity": None, "infidelity": None, "note": f"unavailable: {e}"}
+
+
+def companion(eng, args, name, n, m, eb, depth, steps, warmup, hbm_peak, peak_src, cpu=True):
+    """A second workload timed the same way (extra key, not the headline)."""
+    from paper_2309_16979_b200 import circuits
+    gates = circuits.supremacy(n, depth=depth) if name == "supremacy" else circuits.make(name, n)
+    sim = eng.simulator(n, args.c, m, eb, init=False)
+    for _ in range(warmup):
+        sim.init_basis()
+        sim.run(gates)
+    t, recs, clk, launches = timed_steps(eng, sim, gates, steps, eng.device)
+    st = sim.stats()
+    out = {"workload": f"{name}-{n}" + (f" depth {depth}" if name == "supremacy" else "") +
+                       f" c={args.c} m={m} eb={eb}, HBM-resident",
+           "gates": len(gates), "value": len(gates) * steps / t, "unit": "gates/s",
+           "ms_per_step": 1e3 * t / steps, "steps": steps, "stages": st["stages"],
+           "gate_passes": st["gate_passes"], "replays": st["replays"],
+           "compression_ratio": st["ratio"], "digest": f"{sim.digest():016x}",
+           "phases_ms": {"decode": 1e3 * st["decode_seconds"], "gates": 1e3 * st["gate_seconds"],
+                         "encode": 1e3 * st["encode_seconds"]},
+           "payload_in_GB": st["payload_in_bytes"] / 1e9, "payload_out_GB": st["payload_out_bytes"] / 1e9,
+           "gpu_launches": launches, "clocks": clk}
+    out["roofline"] = roofline_from_kprof(recs, steps, st, hbm_peak, peak_src)
+    out.update(fidelity_of(eng, sim, n, gates))
+    sim.close()
+    if cpu:
+        try:
+            a = argparse.Namespace(**vars(args))
+            a.circuit, a.n, a.m, a.eb, a.depth = name, n, m, eb, depth
+            s = ReferenceSampler(a)
+            for k in (s.k1, s.k2):
+                s.sample(k)
+            est = s.estimate()
+            out["cpu_baseline"] = {"value": est["gates_per_s"], "unit": "gates/s", "cores": s.cores,
+                                   "kind": "reference", "sample": s.text(est)}
+        except Exception as e:
+            out["cpu_baseline"] = {"value": None, "sample": f"unavailable: {e}"}
+    return out
+
+
+def relaunch_under_torchrun(args) -> int:
+    import socket
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main() -> int:
     args = parse_args()
-    from paper_2309_16979_b200 import circuits
-    gates = circuits.make(args.circuit, args.n)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch_under_torchrun(args)
     if args.impl == "reference":
-        return run_reference_arm(args, gates)
+        return run_reference_arm(args)
+    gates = make_circuit(args.circuit, args.n, args.depth)
 
     from paper_2309_16979_b200.engine import Engine
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -241,7 +438,12 @@ def main() -> int:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    mode = args.mode or ("shard" if world > 1 else "replicas")
+    eng = Engine(device=local)
+    if world > 1 and mode == "shard":
+        return run_sharded(args, eng, gates, dist, rank, world, local)
 
     def barrier():
         if dist:
@@ -255,35 +457,18 @@ def main() -> int:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    eng = Engine(device=local)
     ngates = len(gates)
-    if args.shard and world > 1:
-        return run_sharded(args, eng, gates, dist, rank, world, local)
-    sim = eng.simulator(args.n, args.c, args.m, args.eb, init=False,
-                        fuse=False if args.no_fuse else ("strict" if args.strict_passes else True),
+    fuse = {"relaxed": True, "strict": "strict", "checked": "checked", "none": False}[args.fuse]
+    sim = eng.simulator(args.n, args.c, args.m, args.eb, init=False, fuse=fuse,
                         residency=args.residency)
-
     for _ in range(args.warmup):
         sim.init_basis()
         sim.run(gates)
 
     # ---- timed region: K steps, device time (CUDA events on the engine stream)
-    clocks = ClockSampler(local)
-    clocks.start()
-    time.sleep(1.0)   # nvidia-smi's first samples arrive before the timed region
     barrier()
-    eng.timer_begin()
-    eng.timer_end()
-    launches0 = eng.kernel_launches
-    clocks.mark_begin()
-    eng.timer_begin()
-    for _ in range(args.steps):
-        sim.init_basis()
-        sim.run(gates)
-    t_dev = eng.timer_end()
-    clocks.mark_end()
-    launches = eng.kernel_launches - launches0
-    clk = clocks.stop()
+    t_dev, recs, clk, launches = timed_steps(eng, sim, gates, args.steps, local,
+                                             kprof=not args.no_kprof)
     t_max = max_over_ranks(t_dev)
     barrier()
     st = sim.stats()          # last step's counters
@@ -310,56 +495,32 @@ def main() -> int:
     e2e_t = max_over_ranks(statistics.median(e2e_times))
 
     if rank != 0:
+        if dist:
+            dist.destroy_process_group()
         return 0
 
-    # ---- fidelity of the compressed run against an uncompressed fp64 run of
-    # the same circuit on the GPU (outside the timed region; BASELINE metric)
-    fidelity = None
-    if not args.no_fidelity:
-        try:
-            dense = eng.dense_state(args.n, gates)
-            fidelity = sim.fidelity(dense)
-            dense.free()
-        except Exception as e:  # not enough HBM for the dense state next to the store
-            fidelity = f"unavailable: {e}"
-
+    hbm_peak, peak_src = peaks()
     value = world * ngates * args.steps / t_max
-    # ---- roofline of the dominant kernel (from the engine's event timers)
-    peaks = json.loads(PEAKS.read_text()) if PEAKS.exists() else {}
-    hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    phases = {"decode": st["decode_seconds"], "gates": st["gate_seconds"],
-              "encode": st["encode_seconds"]}
-    win_amps = (1 << args.n) // max(1, st["windows"] // max(1, st["stages"]))
-    pass_bytes = 32 * win_amps
-    avg_pass = st["gate_seconds"] / max(1, st["gate_passes"])
-    gate_ach = pass_bytes / avg_pass / 1e9 if avg_pass > 0 else 0.0
-    payload = len(blob)
-    dec_bytes = st["stages"] * (16 * (1 << args.n) + payload)   # approx: final payload size
-    enc_bytes = dec_bytes
-    # measured DRAM bytes per launch of the dominant kernel from the committed
-    # `ncu --set full` capture (profiles/traffic.json, written by
-    # tools/profile_round.sh) for this workload, when present
-    traffic = None
-    tfile = ROOT / "profiles" / "traffic.json"
-    if tfile.exists():
-        t = json.loads(tfile.read_text()).get(f"{args.circuit}-{args.n}-m{args.m}")
-        traffic = t["dram_bytes_per_launch"] if t else None
-    roofline = {"bound": "hbm", "kernel": "tile_pass_reg + tile_swaps (fused gate passes)",
-                "achieved": gate_ach, "peak": hbm_peak, "unit": "GB/s",
-                "frac": gate_ach / hbm_peak, "traffic": traffic,
-                "bytes_per_launch": pass_bytes, "avg_launch_s": avg_pass,
-                "launches": st["gate_passes"],
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
-                "codec": {"decode_GBps": dec_bytes / st["decode_seconds"] / 1e9 if st["decode_seconds"] else None,
-                          "encode_GBps": enc_bytes / st["encode_seconds"] / 1e9 if st["encode_seconds"] else None,
-                          "note": "decode/encode phase = crc+index+decode / encode+size+scan+assemble+crc"}}
+    fid = {"fidelity": None, "infidelity": None} if args.no_fidelity else \
+        fidelity_of(eng, sim, args.n, gates)
+    if recs:
+        roofline = roofline_from_kprof(recs, args.steps, st, hbm_peak, peak_src)
+        tr = committed_traffic(f"{args.circuit}-{args.n}-m{args.m}", roofline["kernel"])
+        if tr:
+            roofline["traffic"] = tr["dram_bytes_per_launch"]
+            roofline["traffic_source"] = tr.get("source", "profiles/traffic.json")
+    else:
+        roofline = {"bound": "hbm", "note": "--no-kprof: no per-launch timing"}
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         try:
-            s = reference_sample(args.circuit, args.n, args.c, args.m, args.eb, args.cpu_budget)
-            cpu = {"value": s["gates_per_s"], "unit": "gates/s", "cores": os.cpu_count(),
-                   "kind": "reference", "sample": sample_text(args, s, os.cpu_count())}
+            s = ReferenceSampler(args)
+            for k in (s.k1, s.k2):
+                s.sample(k)
+            est = s.estimate()
+            cpu = {"value": est["gates_per_s"], "unit": "gates/s", "cores": s.cores,
+                   "kind": "reference", "sample": s.text(est)}
         except Exception as e:  # reference library absent on this box
             cpu = {"value": None, "unit": "gates/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {e}"}
@@ -375,6 +536,18 @@ def main() -> int:
                      "bytes_per_step": io,
                      "note": "compressed payload bytes moved host<->HBM per circuit / circuit "
                              "time, vs measured pinned cudaMemcpy bandwidth"}
+
+    companions = []
+    if world == 1 and not args.no_companions and args.circuit == "qft" and args.n == 30:
+        sim.close()
+        for (name, n, m, eb, depth, steps) in (("supremacy", 30, 30, 1e-7, 20, 2),
+                                               ("qft", 30, 20, 1e-5, 20, 2)):
+            try:
+                companions.append(companion(eng, args, name, n, m, eb, depth, steps, 1, hbm_peak,
+                                            peak_src, cpu=not args.no_cpu_baseline))
+            except Exception as e:
+                companions.append({"workload": f"{name}-{n} m={m}", "error": str(e)})
+
     line = {
         "metric": METRIC, "value": value, "unit": "gates/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps,
@@ -383,11 +556,12 @@ def main() -> int:
                                             gates=ngates),
         "circuit_seconds": t_max / args.steps,
         "compression_ratio": st["ratio"],
-        "fidelity": fidelity,
+        "fidelity": fid["fidelity"], "infidelity": fid["infidelity"],
         "peak_ratio": st["dense_bytes"] / st["peak_bytes"] if st["peak_bytes"] else None,
         "digest": f"{digest:016x}",
-        "phases_s": phases, "stages": st["stages"], "gate_passes": st["gate_passes"],
-        "replays": st["replays"],
+        "phases_s": {"decode": st["decode_seconds"], "gates": st["gate_seconds"],
+                     "encode": st["encode_seconds"]},
+        "stages": st["stages"], "gate_passes": st["gate_passes"], "replays": st["replays"],
         "gpu_launches": launches,
         "roofline": roofline,
         "host_link": host_link,
@@ -395,6 +569,7 @@ def main() -> int:
         "e2e": {"value": world * ngates / e2e_t, "unit": "gates/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h)},
         "clocks": clk,
+        "companions": companions,
     }
     print(json.dumps(line))
     if dist:
@@ -404,42 +579,59 @@ def main() -> int:
 
 def run_sharded(args, eng, gates, dist, rank, world, local):
     """One circuit over all ranks (sharding.py): each rank owns 2^(n-c-g)
-    chunks; compressed chunks move over NCCL at ownership changes."""
+    chunks; compressed chunks move device to device over NCCL at ownership
+    changes.  Strong scaling: the total work is fixed as N grows."""
     import torch
     from paper_2309_16979_b200 import sharding as S
     g = world.bit_length() - 1
     if 1 << g != world:
-        raise SystemExit("--shard needs a power-of-two number of ranks")
+        raise SystemExit("--mode shard needs a power-of-two number of ranks")
     grp = S.TorchGroup(dist, device=f"cuda:{local}")
     run = S.ShardedRun(eng, args.n, args.c, args.m, args.eb, g, [rank], grp)
     for _ in range(args.warmup):
-        run.owners = list(range(args.n - g, args.n))
         run.init_basis()
         run.run(gates)
     dist.barrier()
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    ex0 = run.exchanged_bytes
+    ex0, b0 = run.exchanges, run.exchanged_bytes
+    eng.timer_begin()
     for _ in range(args.steps):
-        run.owners = list(range(args.n - g, args.n))
         run.init_basis()
         run.run(gates)
-    torch.cuda.synchronize()
-    el = time.perf_counter() - t0
+    el = eng.timer_end()
     t = torch.tensor([el], dtype=torch.float64, device=f"cuda:{local}")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    tmax = float(t.item())
+    # e2e: the same through the public API with the sharded store gathered
+    # to host memory at the end of every step
+    e2e = []
+    d2h = 0
+    for _ in range(max(1, args.steps // 2)):
+        dist.barrier()
+        t0 = time.perf_counter()
+        run.init_basis()
+        run.run(gates)
+        recs = run.local_records()
+        d2h = sum(len(p) for _, _, p in recs)
+        dist.barrier()
+        e2e.append(time.perf_counter() - t0)
+    te = torch.tensor([statistics.median(e2e)], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
     digest = run.digest()
     if rank == 0:
-        tmax = float(t.item())
         print(json.dumps({
             "metric": METRIC, "value": len(gates) * args.steps / tmax, "unit": "gates/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * tmax / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": dict(workload_config(args), parallelism=f"shard{world}", gates=len(gates)),
-            "digest": f"{digest:016x}", "exchanges": run.exchanges,
-            "exchanged_bytes_per_step": (run.exchanged_bytes - ex0) // max(1, args.steps),
-            "timing": "device-synchronized interval, max over ranks"}))
+            "config": dict(workload_config(args), parallelism=f"shard{world}", gates=len(gates),
+                           transport="NCCL send/recv of compressed chunk records, device to device"),
+            "digest": f"{digest:016x}", "exchanges_per_step": (run.exchanges - ex0) / args.steps,
+            "exchanged_bytes_per_step": (run.exchanged_bytes - b0) // max(1, args.steps),
+            "gpu_launches": eng.kernel_launches,
+            "e2e": {"value": len(gates) / float(te.item()), "unit": "gates/s",
+                    "h2d_bytes_per_step": int(gates.nbytes), "d2h_bytes_per_step": int(d2h) * world},
+            "timing": "CUDA events on the engine stream, max over ranks"}))
     dist.destroy_process_group()
     return 0
 

@@ -85,6 +85,26 @@ uint64_t qzc_kernel_launches(const qzc_context *ctx);
 int qzc_timer_begin(qzc_context *ctx);
 int qzc_timer_end(qzc_context *ctx, double *seconds_out);
 
+/* Per-launch kernel timing (the reference's OpBegin/OpEnd brackets,
+ * device.cpp:308-321, 358-390, at kernel granularity).  When enabled, every
+ * fused gate pass and codec kernel the engine launches is bracketed by two
+ * CUDA events on its own stream.  Records: kernel name, tag (pass index
+ * within the stage plan; 0 for codec kernels), stage index, seconds and the
+ * launch's algorithmic bytes (32 B per window amplitude for a gate pass,
+ * 16 B per dense amplitude for codec kernels — payload bytes excluded).
+ * enable() clears the records; read() synchronizes the device, returns the
+ * count in *count and, when out != NULL, copies up to cap records and
+ * clears them.  Process-wide (one engine device per process). */
+typedef struct qzc_kprof_record {
+    char name[32];
+    uint32_t tag;
+    uint32_t stage;
+    double seconds;
+    double bytes;
+} qzc_kprof_record;
+int qzc_kprof_enable(qzc_context *ctx, int on);
+int qzc_kprof_read(qzc_context *ctx, qzc_kprof_record *out, uint64_t cap, uint64_t *count);
+
 /* ---- chunk codec (replaces codec.hpp:61-70) ----------------------------- */
 /* Worst-case payload bytes for one chunk of `elements` amplitudes. */
 uint64_t qzc_payload_bound(uint64_t elements, double error_bound);
@@ -230,6 +250,10 @@ typedef struct qzc_sim_stats {
                                     outside their tile and were re-applied by
                                     their strict sub-plan (device-side, same
                                     bytes)                                    */
+    uint64_t payload_in_bytes;   /* compressed bytes the stages decoded
+                                    (sum over stages of the store's payload
+                                    total at stage start)                    */
+    uint64_t payload_out_bytes;  /* compressed bytes the stages encoded      */
 } qzc_sim_stats;
 
 int qzc_sim_create(qzc_context *ctx, const qzc_sim_config *cfg,
@@ -237,6 +261,9 @@ int qzc_sim_create(qzc_context *ctx, const qzc_sim_config *cfg,
 void qzc_sim_destroy(qzc_sim *sim);
 /* |0...0> through the reference's init (store.cpp:26-81). */
 int qzc_sim_init_basis(qzc_sim *sim);
+/* The zero vector: every chunk is the reference's zero-chunk payload (the
+ * ranks that do not hold amplitude 0 of a sharded |0...0>). */
+int qzc_sim_init_zero(qzc_sim *sim);
 /* Execute a circuit through the staged, batched, compressed pipeline. */
 int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates);
 int qzc_sim_stats_get(const qzc_sim *sim, qzc_sim_stats *out);
@@ -266,6 +293,54 @@ int qzc_sim_write_chunk(qzc_sim *sim, uint64_t index, const double *amps);
  * amplitudes (oracle.cpp:95-113). */
 int qzc_sim_fidelity_dev(qzc_sim *sim, const double *dense_dev,
                          double *fidelity_out);
+
+/* ---- checkpoint / resume (ChunkStore::save / load, store.cpp:152-217) ---- */
+/* The reference's QZST file: "QZST", n:u32, c:u32, eb:f64, then per chunk in
+ * index order len:u32, crc:u32, payload.  save streams the payloads out of
+ * the device arenas through a page-locked buffer; load streams them back in,
+ * verifies every CRC on the device (QZC_ESTORE "checksum mismatch in chunk
+ * i", store.cpp:200-201) and needs the simulator's n, c and error bound.
+ * Saving between two qzc_sim_run calls that split a circuit at a stage
+ * boundary of its plan and resuming from the file reproduces the unsplit
+ * run's bytes (each stage is one codec round trip). */
+int qzc_sim_save(qzc_sim *sim, const char *path);
+int qzc_sim_load(qzc_sim *sim, const char *path);
+
+/* ---- sharded runs: ownership change by chunk exchange --- */
+/* No reference counterpart (the reference is one process).  A
+ * rank's simulator holds the 2^(n-g-c) chunks whose global chunk index has
+ * the rank's bits at the g owner positions (global qubit - c).  To move to
+ * new owner positions:
+ *   1. exchange_plan: per destination rank, the bytes (send_bytes[2^g]) and
+ *      chunk count of its record group (host metadata only);
+ *   2. exchange_pack: packs every group into a device buffer (engine-owned,
+ *      valid until the next engine call on this sim; *send_dev_out), group d
+ *      at the prefix sum of send_bytes — a group is a u64 record count, a
+ *      padded array of 24-byte records (new local index, payload offset,
+ *      len, crc) and the payloads, copied from the arena on the device;
+ *   3. the caller moves the groups GPU to GPU (all_to_all over NCCL) into
+ *      exchange_recv_buffer(total received bytes), source s at the prefix
+ *      sum of recv_bytes;
+ *   4. exchange_unpack: the received groups become the store in place (the
+ *      receive buffer is the other arena; every local chunk must arrive
+ *      exactly once, else QZC_ESTORE).
+ * Payload bytes and CRCs are never re-encoded, so digests are unchanged. */
+int qzc_sim_exchange_plan(qzc_sim *sim, uint32_t g, uint32_t rank, const uint32_t *old_pos,
+                          const uint32_t *new_pos, uint64_t *send_bytes, uint64_t *send_chunks);
+int qzc_sim_exchange_pack(qzc_sim *sim, void **send_dev_out, uint64_t *bytes_out);
+int qzc_sim_exchange_recv_buffer(qzc_sim *sim, uint64_t bytes, void **recv_dev_out);
+int qzc_sim_exchange_unpack(qzc_sim *sim, const uint64_t *recv_bytes);
+/* The same record layout built / parsed on the host from a store given as
+ * payloads in local chunk order (2^local_bits chunks) — the exchange's index
+ * and format logic without a GPU (CPU tests over gloo).  pack_host writes
+ * the groups into out (NULL: sizes only) and send_bytes[2^g]; unpack_host
+ * turns received groups back into payloads / sizes / crcs in local order. */
+int qzc_exchange_pack_host(uint32_t local_bits, uint32_t g, uint32_t rank, const uint32_t *old_pos,
+                           const uint32_t *new_pos, const uint8_t *payloads, const uint32_t *sizes,
+                           const uint32_t *crcs, uint8_t *out, uint64_t cap, uint64_t *send_bytes);
+int qzc_exchange_unpack_host(uint32_t world, const uint8_t *recv, const uint64_t *recv_bytes,
+                             uint32_t local_bits, uint8_t *payload_out, uint64_t cap, uint32_t *sizes,
+                             uint32_t *crcs);
 
 /* ---- dense fp64 reference run on the GPU (fidelity baseline) ------------ */
 /* Uncompressed double-precision state on the device, same gate kernels.

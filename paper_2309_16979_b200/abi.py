@@ -77,7 +77,15 @@ class SimStats(C.Structure):
                [(name, C.c_uint64) for name in
                 ("stages", "batches", "gate_passes", "chunk_decompress_count",
                  "chunk_recompress_count", "h2d_bytes", "d2h_bytes", "kernel_launches",
-                 "current_bytes", "peak_bytes", "dense_bytes", "windows", "replays")]
+                 "current_bytes", "peak_bytes", "dense_bytes", "windows", "replays",
+                 "payload_in_bytes", "payload_out_bytes")]
 
     def as_dict(self) -> dict:
         return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+class KProfRecord(C.Structure):
+    """qzc_kprof_record: one timed kernel launch."""
+    _fields_ = [("name", C.c_char * 32), ("tag", C.c_uint32), ("stage", C.c_uint32),
+                ("seconds", C.c_double), ("bytes", C.c_double)]
+

@@ -17,6 +17,7 @@
 #include <cmath>
 
 #include "qz_codec.cuh"
+#include "qz_kprof.cuh"
 
 namespace qz {
 
@@ -85,15 +86,21 @@ __host__ __device__ inline uint32_t x8nmodp(uint64_t n) {
 
 __device__ uint32_t crc_range(const uint32_t *T, const uint8_t *p, uint64_t n) {
     uint32_t c = 0xFFFFFFFFu;
-    while (n >= 8) {
-        uint32_t lo = c ^ ld_u32(p), hi = ld_u32(p + 4);
+    // bytes up to an 8-byte boundary, then aligned 8-byte words (slicing-by-8)
+    while (n && (reinterpret_cast<uintptr_t>(p) & 7)) {
+        c = T[(c ^ *p++) & 0xff] ^ (c >> 8);
+        --n;
+    }
+    const uint2 *w = reinterpret_cast<const uint2 *>(p);
+    for (; n >= 8; n -= 8, ++w) {
+        const uint2 x = __ldg(w);
+        const uint32_t lo = c ^ x.x, hi = x.y;
         c = T[7 * 256 + (lo & 0xff)] ^ T[6 * 256 + ((lo >> 8) & 0xff)] ^
             T[5 * 256 + ((lo >> 16) & 0xff)] ^ T[4 * 256 + (lo >> 24)] ^
             T[3 * 256 + (hi & 0xff)] ^ T[2 * 256 + ((hi >> 8) & 0xff)] ^
             T[1 * 256 + ((hi >> 16) & 0xff)] ^ T[0 * 256 + (hi >> 24)];
-        p += 8;
-        n -= 8;
     }
+    p = reinterpret_cast<const uint8_t *>(w);
     while (n--) c = T[(c ^ *p++) & 0xff] ^ (c >> 8);
     return c ^ 0xFFFFFFFFu;
 }
@@ -642,6 +649,136 @@ __global__ void __launch_bounds__(256) k_dec_lossy_warp(
     }
 }
 
+// Lossy decode, cooperative (codec.cpp:217-249): a CTA of 8 warps owns
+// kDecSlots chunks = 2 kDecSlots chains (slot, half) and walks them 32
+// elements per step.
+//  A (expand, all warps): warp w expands chains w, w+8, ... — for each, the
+//    32 codes of the step from its two byte planes (plane_block: warp scan of
+//    the runs + shuffle search), raw escapes ranked by ballot and fetched in
+//    parallel, and writes val = raw ? value : code * 2eb plus the raw mask
+//    to shared memory;
+//  B (chain, one thread per chain): pred = raw ? val : pred + val, the
+//    reference's sequence of roundings, 32 steps from shared memory — the
+//    only serial part, one lane per chain instead of one warp;
+//  C (store, all warps): the [kDecSlots x 32] amplitude tile as coalesced
+//    512 B rows.
+// The chain stays in a register across steps; plane cursors and raw counts
+// stay in the expanding warp's registers.
+constexpr uint32_t kDecSlots = 16;
+constexpr uint32_t kDecChains = 2 * kDecSlots;
+constexpr uint32_t kDecChainsPerWarp = kDecChains / 8;
+
+__global__ void __launch_bounds__(256) k_dec_lossy_coop(
+    const uint8_t *__restrict__ arena, const DecIdx *__restrict__ idx,
+    const uint64_t *__restrict__ slot_chunk, uint64_t nslots, CodecGeom g,
+    double2 *__restrict__ win, DevStatus *status, const uint32_t *cond) {
+    if (cond && *cond == 0) return;
+    __shared__ double V[kDecChains][33];
+    __shared__ uint32_t R[kDecChains];
+    __shared__ double2 O[kDecSlots][33];
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t slot0 = uint64_t(blockIdx.x) * kDecSlots;
+    const uint32_t rows = uint32_t(umin64(kDecSlots, nslots - slot0));
+    const uint64_t N = g.N;
+    // expansion state of this warp's chains
+    PlaneRd lo[kDecChainsPerWarp], hi[kDecChainsPerWarp];
+    uint32_t raw_i[kDecChainsPerWarp];
+    bool live[kDecChainsPerWarp];
+    double twoeb[kDecChainsPerWarp];
+    const uint8_t *pb[kDecChainsPerWarp];
+#pragma unroll
+    for (uint32_t k = 0; k < kDecChainsPerWarp; ++k) {
+        const uint32_t c = warp + 8 * k, r = c >> 1, h = c & 1;
+        live[k] = r < rows && idx[slot0 + r].len != 0;
+        lo[k] = PlaneRd{0, 0};
+        hi[k] = PlaneRd{0, 0};
+        raw_i[k] = 0;
+        twoeb[k] = 0.0;
+        pb[k] = arena;
+        if (live[k]) {
+            const DecIdx &d = idx[slot0 + r];
+            const uint8_t *p = arena + d.base;
+            pb[k] = p;
+            lo[k] = PlaneRd{d.pos[0][h], uint32_t(__ldg(p + d.pos[0][h] + 1)) - d.skip[0][h]};
+            hi[k] = PlaneRd{d.pos[1][h], uint32_t(__ldg(p + d.pos[1][h] + 1)) - d.skip[1][h]};
+            // a zero remainder: the half starts at the next pair
+            if (lo[k].rem == 0) { lo[k].pp += 2; lo[k].rem = __ldg(p + lo[k].pp + 1); }
+            if (hi[k].rem == 0) { hi[k].pp += 2; hi[k].rem = __ldg(p + hi[k].pp + 1); }
+            raw_i[k] = h ? d.raw_re : 0;
+            twoeb[k] = 2.0 * d.eb;
+        }
+    }
+    // chain state (warp 0: lane = chain)
+    double pred = 0.0;
+    for (uint64_t e0 = 0; e0 < N; e0 += 32) {
+        // A: expand
+#pragma unroll
+        for (uint32_t k = 0; k < kDecChainsPerWarp; ++k) {
+            const uint32_t c = warp + 8 * k;
+            double val = 0.0;
+            uint32_t rm = 0;
+            if (live[k]) {
+                const uint8_t *p = pb[k];
+                const uint32_t z = plane_block(lo[k], p, lane) | (plane_block(hi[k], p, lane) << 8);
+                const bool raw = z == 0xFFFFu;
+                rm = __ballot_sync(0xffffffffu, raw);
+                const DecIdx &d = idx[slot0 + (c >> 1)];
+                if (raw) {
+                    const uint32_t q = raw_i[k] + __popc(rm & ((1u << lane) - 1));
+                    val = q < d.raw_count ? __longlong_as_double((long long)ld_u64(p + d.raw_pos + 8ull * q)) : 0.0;
+                } else {
+                    // ((double)code * 2.0) * eb == (double)code * (2 eb) exactly
+                    val = __dmul_rn(double(unzigzag16(z)), twoeb[k]);
+                }
+                raw_i[k] += __popc(rm);
+            }
+            V[c][lane] = val;
+            if (lane == 0) R[c] = rm;
+        }
+        __syncthreads();
+        // B: the chains
+        if (warp == 0) {
+            const uint32_t c = lane, r = c >> 1, h = c & 1;
+            const uint32_t rm = R[c];
+            const double *vc = V[c];
+            double *oc = reinterpret_cast<double *>(O[r]) + h;
+            if (rm == 0) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    pred = __dadd_rn(pred, vc[i]);
+                    oc[2 * i] = pred;
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    const double x = vc[i];
+                    pred = ((rm >> i) & 1) ? x : __dadd_rn(pred, x);
+                    oc[2 * i] = pred;
+                }
+            }
+        }
+        __syncthreads();
+        // C: store the tile (row r: 32 amplitudes = 512 B)
+        for (uint32_t i = threadIdx.x; i < rows * 32; i += blockDim.x) {
+            const uint32_t r = i >> 5, e = i & 31;
+            const uint64_t s = slot0 + r;
+            // an invalid chunk (len == 0: its index walk failed) decodes to zeros
+            __stcs(win + s * N + e0 + e, O[r][e]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (uint32_t k = 0; k < kDecChainsPerWarp; ++k) {
+        const uint32_t c = warp + 8 * k, r = c >> 1, h = c & 1;
+        if (live[k] && lane == 0) {
+            const DecIdx &d = idx[slot0 + r];
+            const uint64_t chunk = slot_chunk ? slot_chunk[slot0 + r] : slot0 + r;
+            if (raw_i[k] > d.raw_count) dev_fail(status, QZS_RAW_UNDER, chunk);
+            else if (h == 1 && raw_i[k] != d.raw_count) dev_fail(status, QZS_RAW_UNUSED, chunk);
+        }
+    }
+}
+
 // Lossy decode (codec.cpp:217-249): thread = (slot, half).  WIDE: a launch
 // with fewer chunks than one CTA row set uses wide tiles (tile_width).
 template <bool WIDE>
@@ -752,102 +889,17 @@ __global__ void __launch_bounds__(2 * kSlotsPerCta) k_dec_lossless(
 
 // ----------------------------------------------------------------- encode --
 
-// One RLE sub-stream of one half, written to scratch 8 bytes at a time.
-struct Rle {
-    uint8_t *out;
-    uint32_t npairs;
-    uint32_t cur, cnt;   // open run
-    uint32_t hold;       // imaginary half: first run not emitted yet
-    uint32_t head_byte, head_len;
-};
-
-__device__ __forceinline__ void rle_init(Rle &s, uint8_t *out, uint32_t hold) {
-    s.out = out;
-    s.npairs = 0;
-    s.cur = 0x100;
-    s.cnt = 0;
-    s.hold = hold;
-    s.head_byte = 0;
-    s.head_len = 0;
-}
-
-__device__ __forceinline__ void rle_emit(Rle &s, uint32_t b, uint32_t run) {
-    // one 16-bit (byte, run) store per pair (fire-and-forget; L2 merges the
-    // consecutive pairs of a stream)
-    reinterpret_cast<uint16_t *>(s.out)[s.npairs] = uint16_t(b | (run << 8));
-    ++s.npairs;
-}
-
-// rle_encode (codec.cpp:52-63) restated as a streaming state machine.
-__device__ __forceinline__ void rle_push(Rle &s, uint32_t x) {
-    if (x == s.cur) {
-        ++s.cnt;
-        if (!s.hold && s.cnt == 255) {
-            rle_emit(s, s.cur, 255);
-            s.cnt = 0;
-        }
-    } else {
-        if (s.cur != 0x100) {
-            if (s.hold) {
-                s.head_byte = s.cur;
-                s.head_len = s.cnt;
-                s.hold = 0;
-            } else if (s.cnt > 0) {
-                rle_emit(s, s.cur, s.cnt);
-            }
-        }
-        s.cur = x;
-        s.cnt = 1;
-    }
-}
-
-// n pushes of byte x (the same run state as n calls of rle_push).
-__device__ __forceinline__ void rle_push_n(Rle &s, uint32_t x, uint32_t n) {
-    if (n == 0) return;
-    if (x != s.cur) {
-        rle_push(s, x);
-        --n;
-    }
-    if (s.hold) {
-        s.cnt += n;
-        return;
-    }
-    uint32_t tot = s.cnt + n;
-    while (tot >= 255) {
-        rle_emit(s, x, 255);
-        tot -= 255;
-    }
-    s.cnt = tot;
-}
-
-// Close a half: real half keeps (cur, cnt) as its open tail; imaginary half
-// emits its last run (or, if still holding, reports the whole half as head).
-__device__ __forceinline__ void rle_finish(Rle &s, uint32_t h, EncHalf &m, int k) {
-    if (h == 0) {
-        m.edge_byte[k] = uint8_t(s.cur);
-        m.edge_len[k] = s.cnt;
-    } else {
-        if (s.hold) {
-            s.head_byte = s.cur;
-            s.head_len = s.cnt;
-        } else if (s.cnt > 0) {
-            rle_emit(s, s.cur, s.cnt);
-        }
-        m.edge_byte[k] = uint8_t(s.head_byte);
-        m.edge_len[k] = s.head_len;
-    }
-    m.npairs[k] = s.npairs;
-}
-
-__device__ __forceinline__ uint8_t *scratch_half(uint8_t *scratch, const CodecGeom &g,
-                                                 uint64_t slot, uint32_t h) {
-    return scratch + (2 * slot + h) * g.half_stride;
-}
-
-// Double-buffered tile of kSlotsPerCta rows x kTileElems amplitudes.
-struct EncTiles {
-    double2 f[2][kSlotsPerCta * (kTileElems + 1)];   // row r at r * (te + 1)
-};
+// Tiles of kSlotsPerCta rows x kTileElems amplitudes (dynamic shared memory,
+// kEncStages deep: the next tile's loads are in flight while the chains walk
+// the current one).
+constexpr int kEncStages = 2;
+constexpr uint32_t kEncTileDoubles2 = kSlotsPerCta * (kTileElems + 1);
+// RLE pairs staged per tile: 4 streams (half x plane) per row, up to te + 2
+// pairs each (rows * (te + 2) <= kSlotsPerCta * (kTileElems + 2)), double
+// buffered, plus per-stream (global start, count) words
+constexpr uint32_t kEncPairWords = kSlotsPerCta * (kTileElems + 2) * 4;
+constexpr size_t kEncSmem = sizeof(double2) * kEncTileDoubles2 * kEncStages +
+                            2 * sizeof(uint16_t) * kEncPairWords + 2 * sizeof(uint32_t) * 2 * 4 * kSlotsPerCta;
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
     const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
@@ -858,131 +910,257 @@ template <int N> __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-// Quantiser step (codec.cpp:138): q = round((v - pred) / (2 eb)) with the
-// division replaced by a multiplication by the rounded reciprocal.  |t' - t|
-// <= |t'| 2^-52 (two roundings), so whenever t' is farther than |t'| 2^-49
-// from every half-integer, round(t') == round(t) exactly; otherwise (and for
-// non-finite values) the correctly rounded division decides.  With a
-// power-of-two 2eb the reciprocal is exact and no check is needed.
-__device__ __forceinline__ double quantise(double d, const CodecGeom &g) {
-    const double t = __dmul_rn(d, g.inv2eb);
-    double q = round(t);
-    if (!g.exact_inv) {
-        const double dist = fabs(__dsub_rn(fabs(__dsub_rn(t, trunc(t))), 0.5));
-        if (!(dist > __dmul_rn(fabs(t), 0x1p-49))) q = round(__ddiv_rn(d, g.twoeb));
-    }
-    return q;
+// One byte plane's RLE of one half (rle_encode, codec.cpp:52-63, restated as
+// a branch-free per-byte step).  The real half keeps its last run open (the
+// assembler continues it into the imaginary half); the imaginary half holds
+// back its first run (head), which may exceed 255 until the merge.  Pair k
+// (k = 0, 1, ... over the whole half) goes to dst[k - np0]: the scratch
+// stream itself (np0 = 0), or a shared-memory staging buffer that holds the
+// pairs emitted since pair np0.
+struct RleS {
+    uint16_t *dst;
+    uint32_t np0;         // pair index of dst[0]
+    uint32_t np;          // pairs emitted
+    uint32_t cur, cnt;    // open run (cur = 0x100: none yet)
+    uint32_t hold;        // imaginary half, first run not closed yet
+    uint32_t head_byte, head_len;
+};
+
+__device__ __forceinline__ void rle_start(RleS &s, uint16_t *dst, uint32_t hold) {
+    s.dst = dst;
+    s.np0 = 0;
+    s.np = 0;
+    s.cur = 0x100;
+    s.cnt = 0;
+    s.hold = hold;
+    s.head_byte = 0;
+    s.head_len = 0;
 }
 
-// Lossy encode (codec.cpp:121-168): thread = (slot, half).  The next tile is
-// prefetched with cp.async while the current one is walked.
-__global__ void __launch_bounds__(2 * kSlotsPerCta) k_enc_lossy(
+__device__ __forceinline__ void rle_emit(RleS &s, uint32_t v) { s.dst[s.np++ - s.np0] = uint16_t(v); }
+
+// Same pair stream as the reference's greedy split: a run is emitted when it
+// closes or reaches 255 (then restarts at 0), one (byte, run) u16 per pair.
+__device__ __forceinline__ void rle_step(RleS &s, uint32_t x) {
+    const bool diff = x != s.cur;
+    if (diff && s.hold && s.cnt) {
+        // the imaginary half's first run closes: it is the head
+        s.head_byte = s.cur;
+        s.head_len = s.cnt;
+        s.hold = 0;
+        s.cnt = 0;
+    }
+    const uint32_t c1 = s.cnt + 1;
+    const bool emit = diff ? s.cnt != 0 : (c1 == 255 && !s.hold);
+    const uint32_t val = s.cur | ((diff ? s.cnt : 255u) << 8);
+    if (emit) rle_emit(s, val);
+    s.cnt = diff ? 1u : (emit ? 0u : c1);
+    s.cur = x;
+}
+
+// n steps of byte x (fast-forward tiles).
+__device__ __forceinline__ void rle_step_n(RleS &s, uint32_t x, uint32_t n) {
+    if (n == 0) return;
+    if (x != s.cur) {
+        rle_step(s, x);
+        --n;
+    }
+    if (s.hold) {
+        s.cnt += n;
+        return;
+    }
+    uint32_t tot = s.cnt + n;
+    while (tot >= 255) {
+        rle_emit(s, x | (255u << 8));
+        tot -= 255;
+    }
+    s.cnt = tot;
+}
+
+// Close a half: the real half reports its open tail, the imaginary half
+// emits its last run (or, still holding, reports the whole half as head).
+__device__ __forceinline__ void rle_close(RleS &s, uint32_t h, EncHalf &m, int k) {
+    if (h == 0) {
+        m.edge_byte[k] = uint8_t(s.cur);
+        m.edge_len[k] = s.cnt;
+    } else {
+        if (s.hold) {
+            s.head_byte = s.cur;
+            s.head_len = s.cnt;
+        } else if (s.cnt > 0) {
+            rle_emit(s, s.cur | (s.cnt << 8));
+        }
+        m.edge_byte[k] = uint8_t(s.head_byte);
+        m.edge_len[k] = s.head_len;
+    }
+    m.npairs[k] = s.np;
+}
+
+__device__ __forceinline__ uint8_t *scratch_half(uint8_t *scratch, const CodecGeom &g,
+                                                 uint64_t slot, uint32_t h) {
+    return scratch + (2 * slot + h) * g.half_stride;
+}
+
+// Lossy encode (codec.cpp:121-168).  CTA = kSlotsPerCta chunks, 4 warps:
+//  * warps 0-1, thread = (slot, half): the sequential quantiser chain and the
+//    RLE state machines of the half's two byte planes, emitting pairs into a
+//    shared-memory staging buffer per stream;
+//  * warps 2-3: flush the previous tile's staged pairs to the scratch streams
+//    (each stream's new pairs as one contiguous, coalesced warp store);
+//  * all 4 warps: cp.async the next tile ([32 chunks x te] amplitudes,
+//    coalesced 512 B rows).
+// Quantiser (codec.cpp:138-149) on the critical path, division-free and
+// branch-free: t = d * fl(1/2eb), k = (t + 1.5*2^52) - 1.5*2^52 (t rounded
+// to the nearest integer, ties to even, exact for |t| < 2^51), f = t - k
+// (exact).  t differs from the reference's quotient fl(d / 2eb) by at most
+// two roundings (|t| 2^-52 < 2^-37 for |t| < 2^15), so whenever
+// |f| < 0.4999999 and |t| < 32767, round-half-away(fl(d/2eb)) == k exactly
+// and |q| < 32768.  Everything else — a quotient near a half-integer, a
+// code near the 16-bit limit, NaN / Inf, a forced raw — takes the exact
+// path (the reference's division and std::round).  rec = pred + k * 2eb
+// equals reconstruct(pred, code, eb) = pred + (code * 2.0) * eb exactly
+// (multiplying by 2 commutes with rounding); k is never -0.
+constexpr uint32_t kEncThreads = 4 * kSlotsPerCta;
+
+__global__ void __launch_bounds__(kEncThreads) k_enc_lossy(
     const double2 *__restrict__ win, uint64_t nslots, CodecGeom g,
     const uint64_t *__restrict__ forced, uint32_t nforced, uint8_t *__restrict__ scratch,
     EncHalf *__restrict__ meta) {
-    __shared__ __align__(16) EncTiles tiles;
-    const uint32_t r = threadIdx.x >> 1, h = threadIdx.x & 1;
+    extern __shared__ __align__(16) unsigned char enc_smem[];
+    double2 *tiles = reinterpret_cast<double2 *>(enc_smem);
+    uint16_t *pairs = reinterpret_cast<uint16_t *>(tiles + kEncTileDoubles2 * kEncStages);
+    uint32_t *sinfo = reinterpret_cast<uint32_t *>(pairs + 2 * kEncPairWords);   // [2][start, count][4 * 32]
+    const bool chain = threadIdx.x < 2 * kSlotsPerCta;
+    const uint32_t r = (threadIdx.x >> 1) & (kSlotsPerCta - 1), h = threadIdx.x & 1;
     const uint64_t slot0 = uint64_t(blockIdx.x) * kSlotsPerCta, s = slot0 + r;
-    const bool active = s < nslots;
+    const uint32_t rows = uint32_t(umin64(kSlotsPerCta, nslots - slot0));
+    const bool active = chain && r < rows;
     const uint64_t N = g.N;
+    const uint32_t te = tile_width(rows, N), lte = 31 - __clz(te);
+    const uint64_t ntiles = N / te;
+    const uint32_t pcap = te + 2;   // staged pairs per stream per tile
+    // stream q = 4 r + 2 h + plane; its staging slice in buffer b
+    auto stage = [&](int b, uint32_t q) { return pairs + b * kEncPairWords + q * pcap; };
     uint8_t *base = scratch_half(scratch, g, active ? s : 0, h);
-    Rle lo, hi;
-    rle_init(lo, base, h);
-    rle_init(hi, base + g.scap, h);
+    RleS lo, hi;
+    rle_start(lo, stage(0, 4 * r + 2 * h), h);
+    rle_start(hi, stage(0, 4 * r + 2 * h + 1), h);
     double *raws = reinterpret_cast<double *>(base + 2 * g.scap);
     uint32_t nraw = 0;
     // forced raw cursor (sorted flat indices, codec.cpp:124-129)
     uint32_t fc = 0;
-    while (fc < nforced && forced[fc] < h * N) ++fc;
+    while (active && fc < nforced && forced[fc] < h * N) ++fc;
     uint64_t next_forced = fc < nforced ? forced[fc] : ~uint64_t(0);
-    const double eb = g.eb, twoeb = g.twoeb;
+    const double eb = g.eb, twoeb = g.twoeb, inv = g.inv2eb;
+    const double kRne = 6755399441055744.0;   // 1.5 * 2^52
     const double thr = __dmul_rn(0.99, eb);
     double pred = 0.0;
-    const uint32_t rows = uint32_t(umin64(kSlotsPerCta, nslots - slot0));
-    const uint32_t te = tile_width(rows, N), lte = 31 - __clz(te);
-    auto at = [&](int buf, uint32_t rr, uint32_t e) -> double2 & { return tiles.f[buf][rr * (te + 1) + e]; };
-    auto issue = [&](int buf, uint64_t e0) {
-        for (uint32_t i = threadIdx.x; i < rows * te; i += blockDim.x) {
-            const uint32_t rr = i >> lte, e = i & (te - 1);
-            cp_async16(&at(buf, rr, e), win + (slot0 + rr) * N + e0 + e);
+    auto tile = [&](uint64_t i) -> double2 * { return tiles + (i % kEncStages) * kEncTileDoubles2; };
+    auto issue = [&](uint64_t i) {
+        if (i < ntiles) {
+            double2 *dst = tile(i);
+            const uint64_t e0 = i * te;
+            for (uint32_t j = threadIdx.x; j < rows * te; j += blockDim.x) {
+                const uint32_t rr = j >> lte, e = j & (te - 1);
+                cp_async16(dst + rr * (te + 1) + e, win + (slot0 + rr) * N + e0 + e);
+            }
         }
-        cp_async_commit();
+        cp_async_commit();   // (empty groups keep the wait count uniform)
     };
-    issue(0, 0);
-    int buf = 0;
-    for (uint64_t e0 = 0; e0 < N; e0 += te, buf ^= 1) {
-        if (e0 + te < N) {
-            issue(buf ^ 1, e0 + te);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
+    // flush warps: copy buffer b's staged pairs of every stream to scratch
+    auto flush = [&](int b) {
+        const uint32_t lane = threadIdx.x & 31, fw = (threadIdx.x >> 5) - 2;
+        const uint32_t *info = sinfo + b * 2 * 4 * kSlotsPerCta;
+        for (uint32_t q = fw; q < 4 * rows; q += 2) {
+            const uint32_t start = info[q], cnt = info[4 * kSlotsPerCta + q];
+            uint16_t *out = reinterpret_cast<uint16_t *>(scratch_half(scratch, g, slot0 + (q >> 2), (q >> 1) & 1) +
+                                                         (q & 1) * g.scap) + start;
+            const uint16_t *src = stage(b, q);
+            for (uint32_t i = lane; i < cnt; i += 32) out[i] = src[i];
         }
+    };
+    issue(0);
+    for (uint64_t ti = 0; ti < ntiles; ++ti) {
+        const int pb = int(ti & 1);
+        issue(ti + 1);
+        cp_async_wait<1>();
         __syncthreads();
-        // fast-forward: if every value of the tile is within 0.99 eb of the
-        // predictor, every element quantises to code 0 (|d / 2eb| < 0.495
-        // rounds to 0 in any rounding of the quotient), reconstructs to
-        // rec = pred + (+0) = pred (a -0 predictor becomes +0) and passes the
-        // error check — the predictor never moves, so the tile is two runs of
-        // byte 0 (zero runs of sparse states, slowly varying amplitudes)
-        bool ff = active && next_forced >= h * N + e0 + te;
-        if (ff) {
-            bool all = true;
-#pragma unroll 8
-            for (uint32_t e = 0; e < te; ++e)
-                all &= fabs(__dsub_rn(comp(at(buf, r, e), h), pred)) < thr;
-            ff = all;
+        if (!chain) {
+            if (ti) flush(pb ^ 1);
+        } else if (active) {
+            const double *rowc = reinterpret_cast<const double *>(tile(ti) + r * (te + 1)) + h;
+            const uint64_t tile0 = h * N + ti * te;
+            lo.dst = stage(pb, 4 * r + 2 * h);
+            hi.dst = stage(pb, 4 * r + 2 * h + 1);
+            lo.np0 = lo.np;
+            hi.np0 = hi.np;
+            // fast-forward: every value of the tile within 0.99 eb of the
+            // predictor quantises to code 0 with the predictor fixed (rec =
+            // pred + (+0), a -0 predictor becomes +0): two runs of byte 0
+            bool ff = next_forced >= tile0 + te && fabs(__dsub_rn(rowc[0], pred)) < thr;
             if (ff) {
-                rle_push_n(lo, 0, te);
-                rle_push_n(hi, 0, te);
-                pred = __dadd_rn(pred, 0.0);
+                bool all = true;
+#pragma unroll 8
+                for (uint32_t e = 1; e < te; ++e) all &= fabs(__dsub_rn(rowc[2 * e], pred)) < thr;
+                ff = all;
+                if (ff) {
+                    rle_step_n(lo, 0, te);
+                    rle_step_n(hi, 0, te);
+                    pred = __dadd_rn(pred, 0.0);
+                }
             }
-        }
-        if (active && !ff) {
-            // this half's component of the row, and the next forced index
-            // relative to the tile (~0 when beyond it)
-            const double *rowc = reinterpret_cast<const double *>(&at(buf, r, 0)) + h;
-            const uint64_t tile0 = h * N + e0;
-            uint32_t fr = next_forced - tile0 < te ? uint32_t(next_forced - tile0) : ~0u;
-            for (uint32_t e = 0; e < te; ++e) {
-                const double v = rowc[2 * e];
-                bool raw = false;
-                int32_t code = 0;
-                if (e == fr) {
-                    const uint64_t flat = tile0 + e;
-                    raw = true;
-                    do { ++fc; } while (fc < nforced && forced[fc] == flat);
-                    next_forced = fc < nforced ? forced[fc] : ~uint64_t(0);
-                    fr = next_forced - tile0 < te ? uint32_t(next_forced - tile0) : ~0u;
-                } else {
-                    const double q = quantise(__dsub_rn(v, pred), g);
-                    if (!(fabs(q) < 32768.0)) {
-                        raw = true;
-                    } else {
-                        code = int32_t(q);
-                        // (double)code * 2.0 * eb == q' * (2 eb) exactly (q' = q with -0 -> +0)
-                        const double rec = __dadd_rn(pred, __dmul_rn(__dadd_rn(q, 0.0), twoeb));
-                        if (!(fabs(__dsub_rn(rec, v)) <= eb)) raw = true;
-                        else pred = rec;
+            if (!ff) {
+                uint32_t fr = next_forced - tile0 < te ? uint32_t(next_forced - tile0) : ~0u;
+                for (uint32_t e = 0; e < te; ++e) {
+                    const double v = rowc[2 * e];
+                    const double d = __dsub_rn(v, pred);
+                    const double t = __dmul_rn(d, inv);
+                    double q = __dsub_rn(__dadd_rn(t, kRne), kRne);
+                    const double f = __dsub_rn(t, q);
+                    bool raw = false;
+                    if (!(fabs(f) < 0.4999999 && fabs(t) < 32767.0) || e == fr) {
+                        if (e == fr) {
+                            raw = true;
+                            const uint64_t flat = tile0 + e;
+                            do { ++fc; } while (fc < nforced && forced[fc] == flat);
+                            next_forced = fc < nforced ? forced[fc] : ~uint64_t(0);
+                            fr = next_forced - tile0 < te ? uint32_t(next_forced - tile0) : ~0u;
+                        } else {
+                            // the reference's quotient and std::round (half away)
+                            q = round(__ddiv_rn(d, twoeb));
+                            if (!(fabs(q) < 32768.0)) raw = true;
+                            else q = __dadd_rn(q, 0.0);   // code 0 from -0
+                        }
                     }
+                    const double rec = __dadd_rn(pred, __dmul_rn(q, twoeb));
+                    raw = raw || !(fabs(__dsub_rn(rec, v)) <= eb);
+                    pred = raw ? v : rec;
+                    const uint32_t z = raw ? 0xFFFFu : zigzag16(int32_t(q));
+                    if (raw) raws[nraw++] = v;
+                    rle_step(lo, z & 0xffu);
+                    rle_step(hi, z >> 8);
                 }
-                uint32_t z;
-                if (raw) {
-                    raws[nraw++] = v;
-                    pred = v;
-                    z = 0xFFFFu;
-                } else {
-                    z = zigzag16(code);
-                }
-                rle_push(lo, z & 0xff);
-                rle_push(hi, z >> 8);
             }
+            uint32_t *info = sinfo + pb * 2 * 4 * kSlotsPerCta;
+            info[4 * r + 2 * h] = lo.np0;
+            info[4 * r + 2 * h + 1] = hi.np0;
+            info[4 * kSlotsPerCta + 4 * r + 2 * h] = lo.np - lo.np0;
+            info[4 * kSlotsPerCta + 4 * r + 2 * h + 1] = hi.np - hi.np0;
         }
-        __syncthreads();  // the buffer is refilled two tiles later
+        __syncthreads();  // tile and staging buffers are reused next round
     }
+    cp_async_wait<0>();
+    if (!chain && ntiles) flush(int((ntiles - 1) & 1));
     if (active) {
+        // the closing pair goes straight to the scratch stream
+        uint16_t *slo = reinterpret_cast<uint16_t *>(base), *shi = reinterpret_cast<uint16_t *>(base + g.scap);
+        lo.dst = slo;
+        lo.np0 = 0;
+        hi.dst = shi;
+        hi.np0 = 0;
         EncHalf &m = meta[2 * s + h];
-        rle_finish(lo, h, m, 0);
-        rle_finish(hi, h, m, 1);
+        rle_close(lo, h, m, 0);
+        rle_close(hi, h, m, 1);
         m.nraw = nraw;
     }
 }
@@ -997,8 +1175,8 @@ __global__ void __launch_bounds__(16 * kLLSlots) k_enc_lossless(
     const uint64_t slot0 = uint64_t(blockIdx.x) * kLLSlots, s = slot0 + r;
     const bool active = s < nslots;
     const uint64_t N = g.N;
-    Rle st;
-    rle_init(st, scratch_half(scratch, g, active ? s : 0, h) + k * g.scap, h);
+    RleS st;
+    rle_start(st, reinterpret_cast<uint16_t *>(scratch_half(scratch, g, active ? s : 0, h) + k * g.scap), h);
     const uint32_t te = uint32_t(umin64(kTileElems, N));
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (uint64_t e0 = 0; e0 < N; e0 += te) {
@@ -1010,12 +1188,12 @@ __global__ void __launch_bounds__(16 * kLLSlots) k_enc_lossless(
         if (!active) continue;
         for (uint32_t e = 0; e < te; ++e) {
             const uint64_t bits = (uint64_t)__double_as_longlong(comp(tile[r][e], h));
-            rle_push(st, uint32_t(bits >> (8 * k)) & 0xff);
+            rle_step(st, uint32_t(bits >> (8 * k)) & 0xff);
         }
     }
     if (active) {
         EncHalf &m = meta[2 * s + h];
-        rle_finish(st, h, m, k);
+        rle_close(st, h, m, k);
         if (k == 0) m.nraw = 0;
     }
 }
@@ -1074,9 +1252,31 @@ __global__ void k_arena_alloc(const uint64_t *rel_off, const uint64_t *sizes, ui
     *base_out = base;
 }
 
+// Warp copy of n bytes, any alignment: head bytes up to an 8-byte boundary
+// of dst, then 8 bytes per lane (two aligned source words funnel-shifted into
+// place), tail bytes.  Reads up to 8 bytes past the source range (scratch
+// buffers keep >= 64 bytes of slack).
 __device__ __forceinline__ void warp_copy(uint8_t *dst, const uint8_t *src, uint64_t n,
                                           uint32_t lane) {
-    for (uint64_t i = lane; i < n; i += 32) dst[i] = src[i];
+    const uint64_t head = umin64((8 - (reinterpret_cast<uintptr_t>(dst) & 7)) & 7, n);
+    if (lane < head) dst[lane] = src[lane];
+    dst += head;
+    src += head;
+    n -= head;
+    const uint64_t words = n >> 3;
+    const uint32_t sh = uint32_t(reinterpret_cast<uintptr_t>(src) & 7);
+    const uint64_t *s8 = reinterpret_cast<const uint64_t *>(src - sh);
+    uint64_t *d8 = reinterpret_cast<uint64_t *>(dst);
+    if (sh == 0) {
+        for (uint64_t i = lane; i < words; i += 32) d8[i] = s8[i];
+    } else {
+        for (uint64_t i = lane; i < words; i += 32) {
+            const uint64_t w0 = s8[i], w1 = s8[i + 1];
+            d8[i] = (w0 >> (8 * sh)) | (w1 << (64 - 8 * sh));
+        }
+    }
+    const uint64_t t0 = words << 3;
+    if (t0 + lane < n) dst[t0 + lane] = src[t0 + lane];
 }
 
 // Warp per slot: header, merged planes, raws (codec.cpp:115-168).
@@ -1289,6 +1489,7 @@ void launch_crc(const CodecTables &tabs, const uint8_t *arena, ChunkTable table,
                 const uint64_t *slot_chunk, uint64_t nslots, bool verify, DevStatus *status,
                 cudaStream_t s) {
     const unsigned grid = (unsigned)std::min<uint64_t>(ceil_div(nslots, 8), kNumSMs * 64);
+    KProfScope prof(s, verify ? "k_crc(verify)" : "k_crc", 0, 0.0);
     k_crc<<<grid, 256, 0, s>>>(tabs.crc8, arena, table, slot_chunk, nslots, verify ? 1 : 0, status);
     QZ_CHECK_LAUNCH();
 }
@@ -1296,6 +1497,7 @@ void launch_crc(const CodecTables &tabs, const uint8_t *arena, ChunkTable table,
 void launch_dec_index(const uint8_t *arena, ChunkTable table, const uint64_t *slot_chunk,
                       uint64_t nslots, const CodecGeom &g, DecIdx *idx, DevStatus *status,
                       cudaStream_t s, uint32_t *nzslot) {
+    KProfScope prof(s, "k_dec_index", 0, 0.0);
     if (nzslot) QZ_CUDA(cudaMemsetAsync(nzslot + nslots, 0, 4, s));
     if (g.lossy && g.N >= 64 && 4 * g.N / 256 + 1 <= kIdxMaxSteps)
         k_dec_index_warp<<<grid_for(nslots, kIdxWarps), 32 * kIdxWarps, 0, s>>>(arena, table, slot_chunk,
@@ -1312,13 +1514,15 @@ void launch_decode(const uint8_t *arena, const DecIdx *idx, const uint64_t *slot
                    uint64_t nslots, const CodecGeom &g, double2 *win, DevStatus *status,
                    cudaStream_t s, const uint32_t *cond, bool sparse) {
     const unsigned grid = grid_for(nslots, kSlotsPerCta);
+    const double dense = 16.0 * double(g.N) * double(nslots);
+    KProfScope prof(s, cond ? "replay_decode" : (g.lossy && g.N >= 32 && !sparse) ? "k_dec_lossy_coop"
+                                            : g.lossy ? "k_dec_lossy" : "k_dec_lossless", 0, dense);
     // dense payloads: warp per chunk-half (parallel RLE expansion, serial
     // predictor chain only); a store known to be mostly zero runs (right
     // after init): thread per chunk-half with run fills
     if (g.lossy && g.N >= 32 && !sparse) {
-        // warp per (slot, half): 4 slots per 256-thread CTA
-        k_dec_lossy_warp<<<grid_for(nslots, 4), 256, 0, s>>>(arena, idx, slot_chunk, nslots, g, win,
-                                                              status, cond);
+        k_dec_lossy_coop<<<grid_for(nslots, kDecSlots), 256, 0, s>>>(arena, idx, slot_chunk, nslots, g, win,
+                                                                      status, cond);
     } else if (g.lossy && nslots < uint64_t(kSlotsPerCta))
         k_dec_lossy<true><<<grid, 2 * kSlotsPerCta, 0, s>>>(arena, idx, slot_chunk, nslots, g, win,
                                                              status, cond);
@@ -1333,8 +1537,14 @@ void launch_decode(const uint8_t *arena, const DecIdx *idx, const uint64_t *slot
 void launch_encode(const double2 *win, uint64_t nslots, const CodecGeom &g,
                    const uint64_t *forced, uint32_t nforced, uint8_t *scratch, EncHalf *meta,
                    cudaStream_t s) {
+    KProfScope prof(s, g.lossy ? "k_enc_lossy" : "k_enc_lossless", 0, 16.0 * double(g.N) * double(nslots));
+    static bool attr = false;
+    if (!attr) {
+        QZ_CUDA(cudaFuncSetAttribute(k_enc_lossy, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kEncSmem)));
+        attr = true;
+    }
     if (g.lossy)
-        k_enc_lossy<<<grid_for(nslots, kSlotsPerCta), 2 * kSlotsPerCta, 0, s>>>(
+        k_enc_lossy<<<grid_for(nslots, kSlotsPerCta), kEncThreads, kEncSmem, s>>>(
             win, nslots, g, forced, nforced, scratch, meta);
     else
         k_enc_lossless<<<grid_for(nslots, kLLSlots), 16 * kLLSlots, 0, s>>>(win, nslots, g,

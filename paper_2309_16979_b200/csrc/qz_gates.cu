@@ -19,6 +19,7 @@
 #include <cstring>
 
 #include "qz_gates.cuh"
+#include "qz_kprof.cuh"
 
 namespace qz {
 
@@ -1959,7 +1960,13 @@ void set_attrs() {
 }
 
 void launch_pass(const DevPlan &plan, const PassDesc &pd, const double2 *src, double2 *dst,
-                 uint32_t nbits, cudaStream_t s, uint32_t *flag, const uint32_t *cond, NzMap nz) {
+                 uint32_t nbits, cudaStream_t s, uint32_t *flag, const uint32_t *cond, NzMap nz,
+                 uint32_t tag) {
+    // replay launches (cond != nullptr) are device-side no-ops unless flagged:
+    // they are not timed as passes
+    static const char *const kName[3] = {"tile_pass_reg<All>", "tile_pass_reg<DiagH>", "tile_pass_reg<Gen>"};
+    KProfScope prof(s, cond ? "replay_pass" : pd.kind == PASS_SWAPS ? "tile_swaps" : kName[pd.variant % 3],
+                    tag, 32.0 * double(uint64_t(1) << nbits));
     if (pd.kind == PASS_SWAPS) {
         const uint64_t tiles = uint64_t(1) << (nbits > 2 * kSwapLow ? nbits - 2 * kSwapLow : 0);
         const uint64_t grid = std::min<uint64_t>(std::max<uint64_t>(tiles, 1), uint64_t(kNumSMs) * 8);
@@ -1999,7 +2006,8 @@ uint64_t run_passes(const DevPlan &plan, double2 *buf, uint32_t nbits, cudaStrea
                     const uint32_t *cond, NzMap nz) {
     if (plan.relaxed) throw Failure(QZC_EDEVICE, "relaxed plan run without its replay plan");
     set_attrs();
-    for (const PassDesc &pd : plan.host_passes) launch_pass(plan, pd, buf, buf, nbits, s, nullptr, cond, nz);
+    for (size_t p = 0; p < plan.host_passes.size(); ++p)
+        launch_pass(plan, plan.host_passes[p], buf, buf, nbits, s, nullptr, cond, nz, uint32_t(p));
     return plan.host_passes.size();
 }
 
@@ -2017,16 +2025,17 @@ double2 *run_relaxed(const DevPlan &plan, const DevPlan &replay, double2 *buf, d
         const PassDesc &pd = plan.host_passes[p];
         if (pd.relaxed != 2) {
             if (pd.relaxed && force_replay) QZ_CUDA(cudaMemsetAsync(win_flag, 1, 1, s));
-            launch_pass(plan, pd, cur, cur, nbits, s, pd.relaxed ? win_flag : nullptr, nullptr, nz);
+            launch_pass(plan, pd, cur, cur, nbits, s, pd.relaxed ? win_flag : nullptr, nullptr, nz, uint32_t(p));
             ++launches;
             continue;
         }
         if (force_replay) QZ_CUDA(cudaMemsetAsync(flag, 1, 1, s));
-        launch_pass(plan, pd, cur, oth, nbits, s, flag, nullptr, nz);
+        launch_pass(plan, pd, cur, oth, nbits, s, flag, nullptr, nz, uint32_t(p));
         // strict replay of this pass from its untouched input (no-ops unless flagged)
         const auto &rr = plan.replay_range.at(p);
         for (uint32_t q = rr.first; q < rr.second; ++q)
-            launch_pass(replay, replay.host_passes[q], q == rr.first ? cur : oth, oth, nbits, s, nullptr, flag, nz);
+            launch_pass(replay, replay.host_passes[q], q == rr.first ? cur : oth, oth, nbits, s, nullptr, flag, nz,
+                        uint32_t(q));
         k_flag_done<<<1, 1, 0, s>>>(flag, replays);
         QZ_CHECK_LAUNCH();
         launches += 2 + (rr.second - rr.first);

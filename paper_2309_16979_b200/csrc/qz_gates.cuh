@@ -97,10 +97,11 @@ struct GroupDesc {
 
 // A fused pass: gates whose buffer bits all lie in the tile bit set T.
 // Case sets of the fused pass kernel: a pass whose fast lists only hold
-// diagonal runs, 1q diagonals, real 1q matrices (H) and CP5 ops gets a kernel
-// (tile_pass_reg<kPassDiagH>)
-// whose jump table has only those cases (anything else would go to the
-// exact path, so the set only affects speed, never results).
+// PDIAG runs (case ids 0..11), the H-type real GEN1 cases (28, 31, 43, 46,
+// 58, 61) and CP5 ops (72..83) gets a kernel (tile_pass_reg<kPassDiagH>)
+// whose jump table has only those cases; passes with 1q diagonal gates
+// (OP_DIAG ids 12..26) take kPassGen or kPassAll.  Anything outside a set
+// would go to the exact path, so the set only affects speed, never results.
 // kPassGen: diagonal runs, every 1q case, CX and CX-diagonal ops (QAOA /
 // supremacy-style layers).
 constexpr int kPassAll = 0, kPassDiagH = 1, kPassGen = 2;

@@ -25,137 +25,20 @@
 
 #include "qz_codec.cuh"
 #include "qz_gates.cuh"
+#include "qz_kprof.cuh"
 #include "qz_plan.cuh"
+#include "qz_runtime.cuh"
 
 using namespace qz;
 
-namespace {
-
-thread_local std::string g_last_error;
-
-constexpr uint64_t kPerChunkOverhead = 48;   // ChunkStore::kPerChunkOverhead (store.hpp:48)
-
-// Grow-only device buffer.
-struct DevBuf {
-    void *p = nullptr;
-    size_t cap = 0;
-    void ensure(size_t bytes) {
-        if (bytes <= cap) return;
-        if (p) cudaFree(p);
-        p = nullptr;
-        cap = 0;
-        QZ_CUDA(cudaMalloc(&p, bytes ? bytes : 1));
-        cap = bytes;
-    }
-    void release() {
-        if (p) cudaFree(p);
-        p = nullptr;
-        cap = 0;
-    }
-    template <class T> T *as() const { return static_cast<T *>(p); }
-};
-
-const char *status_text(int code) {
-    switch (code) {
-    case QZS_CRC: return "checksum mismatch on chunk ";
-    case QZS_HEADER: return "malformed payload: bad header on chunk ";
-    case QZS_RLE_TRUNC: return "malformed payload: truncated RLE stream on chunk ";
-    case QZS_RLE_RUN: return "malformed payload: bad RLE run length on chunk ";
-    case QZS_RAW_MISSING: return "malformed payload: missing raw values on chunk ";
-    case QZS_RAW_UNDER: return "malformed payload: raw value underflow on chunk ";
-    case QZS_RAW_UNUSED: return "malformed payload: unused raw values on chunk ";
-    case QZS_ARENA: return "compressed arena capacity exhausted, needed bytes ";
-    default: return "device error ";
-    }
+namespace qz {
+std::string &last_error() {
+    thread_local std::string e;
+    return e;
 }
+} // namespace qz
 
-// Scratch set for one window of codec work.
-struct Window {
-    DevBuf amps, scratch, meta, idx, slot_chunk, sizes, reloff, base, cub, delta, maxd;
-    DevBuf replay;   // uint32 flag raised by a relaxed gate pass
-    DevBuf alt;      // second dense buffer: relaxed passes run out of place
-    DevBuf nzslot;   // per slot: may be nonzero (0 = known all-(+0) after decode)
-    // host-staged residency: HBM staging of the window's payloads
-    DevBuf stage_in, stage_out, lt_off, lt_len, lt_crc, padded, soff, lused, hbase;
-    uint64_t slots = 0, stage_in_cap = 0, stage_out_cap = 0;
-    ChunkTable local() {
-        return ChunkTable{lt_off.as<uint64_t>(), lt_len.as<uint32_t>(), lt_crc.as<uint32_t>()};
-    }
-    // host-staged pipeline: the second input set (slot map, staged
-    // payloads, slot-indexed table, decode cursors) of a single window
-    void reserve_input(const CodecGeom &g, uint64_t nslots) {
-        const uint64_t bound = payload_bound(g.N, g.lossy ? 1.0 : 0.0);
-        slots = nslots;
-        stage_in_cap = nslots * (bound + 48) + 64;
-        stage_in.ensure(stage_in_cap);
-        lt_off.ensure(8 * nslots);
-        lt_len.ensure(4 * nslots);
-        lt_crc.ensure(4 * nslots);
-        padded.ensure(8 * nslots);
-        soff.ensure(8 * nslots);
-        slot_chunk.ensure(sizeof(uint64_t) * nslots);
-        idx.ensure(sizeof(DecIdx) * nslots);
-        size_t t1 = 0;
-        cub::DeviceScan::ExclusiveSum(nullptr, t1, (uint64_t *)nullptr, (uint64_t *)nullptr,
-                                      (int)std::min<uint64_t>(nslots, INT32_MAX));
-        cub.ensure(t1 + 256);
-    }
-    DevBuf out_off, out_len, out_crc;   // encode output table (pipelined host-staged)
-    ChunkTable out_local() {
-        return ChunkTable{out_off.as<uint64_t>(), out_len.as<uint32_t>(), out_crc.as<uint32_t>()};
-    }
-    void reserve_staging(const CodecGeom &g, uint64_t nslots) {
-        const uint64_t bound = payload_bound(g.N, g.lossy ? 1.0 : 0.0);
-        stage_in_cap = nslots * (bound + 48) + 64;
-        stage_out_cap = nslots * bound + 64;
-        stage_in.ensure(stage_in_cap);
-        stage_out.ensure(stage_out_cap);
-        out_off.ensure(8 * nslots);
-        out_len.ensure(4 * nslots);
-        out_crc.ensure(4 * nslots);
-        lt_off.ensure(8 * nslots);
-        lt_len.ensure(4 * nslots);
-        lt_crc.ensure(4 * nslots);
-        padded.ensure(8 * nslots);
-        soff.ensure(8 * nslots);
-        lused.ensure(16);
-        hbase.ensure(16);
-    }
-    void reserve(const CodecGeom &g, uint64_t nslots) {
-        amps.ensure(sizeof(double2) * nslots * g.N);
-        nzslot.ensure(4 * (nslots + 1) + 16);
-        QZ_CUDA(cudaMemset(nzslot.p, 0, 4 * (nslots + 1)));   // count 0: map unused until a decode
-        scratch.ensure(2 * nslots * g.half_stride);
-        meta.ensure(sizeof(EncHalf) * 2 * nslots);
-        idx.ensure(sizeof(DecIdx) * nslots);
-        slot_chunk.ensure(sizeof(uint64_t) * nslots);
-        sizes.ensure(sizeof(uint64_t) * nslots);
-        reloff.ensure(sizeof(uint64_t) * nslots);
-        delta.ensure(sizeof(int64_t) * nslots);
-        base.ensure(sizeof(uint64_t) * 2);
-        maxd.ensure(sizeof(int64_t) * 2);
-        if (!replay.p) {
-            replay.ensure(16);
-            QZ_CUDA(cudaMemset(replay.p, 0, 16));
-        }
-        size_t t1 = 0, t2 = 0;
-        cub::DeviceScan::ExclusiveSum(nullptr, t1, (uint64_t *)nullptr, (uint64_t *)nullptr,
-                                      (int)std::min<uint64_t>(nslots, INT32_MAX));
-        cub::DeviceScan::InclusiveSum(nullptr, t2, (int64_t *)nullptr, (int64_t *)nullptr,
-                                      (int)std::min<uint64_t>(nslots, INT32_MAX));
-        size_t t3 = 0;
-        cub::DeviceReduce::Max(nullptr, t3, (int64_t *)nullptr, (int64_t *)nullptr,
-                               (int)std::min<uint64_t>(nslots, INT32_MAX));
-        cub.ensure(std::max({t1, t2, t3}) + 256);
-        slots = std::max(slots, nslots);
-    }
-    void release() {
-        for (DevBuf *b : {&amps, &scratch, &meta, &idx, &slot_chunk, &sizes, &reloff, &base, &cub,
-                          &delta, &maxd, &stage_in, &stage_out, &lt_off, &lt_len, &lt_crc, &padded,
-                          &soff, &lused, &hbase, &out_off, &out_len, &out_crc, &replay, &alt, &nzslot})
-            b->release();
-    }
-};
+namespace {
 
 // ---- accounting kernels ---------------------------------------------------
 // delta[s] = new_size[s] - old_len[chunk(s)]  (ChunkStore::account_store order)
@@ -256,81 +139,6 @@ double now_s() {
 
 } // namespace
 
-// ============================================================== context ====
-
-struct qzc_context {
-    int device = 0;
-    cudaStream_t stream = nullptr;
-    uint64_t budget = 0;
-    CodecTables tabs;
-    DevStatus *status = nullptr;      // device
-    DevStatus *status_host = nullptr; // pinned
-    uint64_t launches = 0;
-    Window win;                       // scratch for the host codec / gate entry points
-    DevBuf arena, table_off, table_len, table_crc, forced, used;
-    std::mutex mu;
-    cudaEvent_t t_begin = nullptr, t_end = nullptr;
-
-    void check_status(uint64_t index_base = 0) {
-        QZ_CUDA(cudaMemcpyAsync(status_host, status, sizeof(DevStatus), cudaMemcpyDeviceToHost, stream));
-        QZ_CUDA(cudaStreamSynchronize(stream));
-        if (status_host->code != 0) {
-            const int code = status_host->code;
-            const uint64_t idx = status_host->index;
-            QZ_CUDA(cudaMemsetAsync(status, 0, sizeof(DevStatus), stream));
-            QZ_CUDA(cudaStreamSynchronize(stream));
-            throw Failure(code == QZS_ARENA ? QZC_ENOMEM : QZC_ECODEC,
-                          std::string(status_text(code)) + std::to_string(idx + (code == QZS_ARENA ? 0 : index_base)));
-        }
-    }
-};
-
-// ============================================================ simulator ====
-
-struct qzc_sim {
-    qzc_context *ctx = nullptr;
-    qzc_sim_config cfg{};
-    uint32_t n = 0, c = 0, m = 0;
-    double eb = 0;
-    uint64_t N = 0, nchunks = 0;
-    CodecGeom geom{};
-    DevBuf arena[2], off[2], len[2], crc[2];
-    // host-staged residency: the arenas live in mapped page-locked host memory
-    bool host_res = false;
-    uint8_t *harena[2] = {nullptr, nullptr};      // host view
-    uint8_t *harena_dev[2] = {nullptr, nullptr};  // device view of the same bytes
-    DevBuf io_bytes;  // uint64[2]: host->HBM and HBM->host payload bytes
-    DevBuf replays;   // uint64: windows replayed with the strict plan
-    DevBuf small;     // uint64[4] scratch for init_basis (slot / forced lists)
-    DevPlan plans[3]; // stage plans (relaxed / per-pass replay / whole strict), device buffers reused
-    DevBuf used;   // uint64[2] bump pointers
-    DevBuf acct;   // int64[2] current / peak
-    uint64_t arena_cap = 0;
-    int cur = 0;
-    uint64_t win_amps = 0;   // amplitudes per pipeline window
-    Window win;              // window set 0 (also used by the host entry points)
-    Window win2;             // window set 1: second stream of the stage pipeline
-    bool two_windows = false;
-    int relax = 1;              // 1: +0-safe diagonal units relaxed; 2: checked units too
-    bool force_replay = false;  // debug_flags bit 0
-    cudaStream_t streams[3] = {nullptr, nullptr, nullptr};   // [2]: host-staged write-back
-    bool pipelined = false;   // host-staged, one window: gather / compute / write-back streams
-    bool sparse_store = false;   // store = the init state (zero-chunk aliases): decode with run fills
-    DevBuf gcub;              // scan scratch of the gather stream
-    std::vector<cudaEvent_t> pevents;
-    cudaEvent_t acct_ev[2] = {nullptr, nullptr};
-    qzc_sim_stats stats{};
-    bool initialized = false;
-    std::vector<cudaEvent_t> events;
-
-    ChunkTable table(int i) {
-        return ChunkTable{off[i].as<uint64_t>(), len[i].as<uint32_t>(), crc[i].as<uint32_t>()};
-    }
-    cudaStream_t st() const { return ctx->stream; }
-    uint8_t *arena_ptr(int i) { return host_res ? harena_dev[i] : arena[i].as<uint8_t>(); }
-    uint64_t *used_ptr(int i) { return used.as<uint64_t>() + i; }
-};
-
 namespace {
 
 // Encode win slots [0, nslots) into arena `a` / table `t` via slot_chunk map.
@@ -344,6 +152,7 @@ void encode_window(qzc_context *ctx, Window &w, const CodecGeom &g, uint64_t nsl
     if (!acct_map) acct_map = slot_chunk;
     launch_encode(w.amps.as<double2>(), nslots, g, forced, nforced, w.scratch.as<uint8_t>(),
                   w.meta.as<EncHalf>(), s);
+    const int tail = kprof_begin(s);
     launch_enc_sizes(w.meta.as<EncHalf>(), nslots, g, w.sizes.as<uint64_t>(), s);
     size_t tb = w.cub.cap;
     QZ_CUDA(cub::DeviceScan::ExclusiveSum(w.cub.p, tb, w.sizes.as<uint64_t>(), w.reloff.as<uint64_t>(),
@@ -368,9 +177,12 @@ void encode_window(qzc_context *ctx, Window &w, const CodecGeom &g, uint64_t nsl
         if (acct_done) QZ_CUDA(cudaEventRecord(acct_done, s));
         launches += 5;
     }
+    kprof_end(tail, s, "enc_sizes+scan+alloc", 0, 0.0);
+    const int asm_h = kprof_begin(s);
     launch_assemble(w.scratch.as<uint8_t>(), w.meta.as<EncHalf>(), w.reloff.as<uint64_t>(),
                     w.sizes.as<uint64_t>(), w.base.as<uint64_t>(), slot_chunk, nslots, g, arena, t,
                     ctx->status, s);
+    kprof_end(asm_h, s, "k_assemble", 0, 0.0);
     launch_crc(ctx->tabs, arena, t, slot_chunk, nslots, false, ctx->status, s);
     launches += 6;
 }
@@ -538,22 +350,9 @@ void run_window_passes(qzc_sim *sim, Window &W, const DevPlan &dp, const DevPlan
 
 // ================================================================== C ABI ==
 
-#define QZ_API_BEGIN try {
-#define QZ_API_END                                                                             \
-    }                                                                                          \
-    catch (const Failure &f) {                                                                 \
-        g_last_error = f.what();                                                               \
-        return f.code;                                                                         \
-    }                                                                                          \
-    catch (const std::exception &e) {                                                          \
-        g_last_error = e.what();                                                               \
-        return QZC_EINVAL;                                                                     \
-    }                                                                                          \
-    return QZC_OK;
-
 extern "C" {
 
-const char *qzc_last_error(void) { return g_last_error.c_str(); }
+const char *qzc_last_error(void) { return qz::last_error().c_str(); }
 const char *qzc_version(void) { return "qzcuda 0.1 sm_100a"; }
 
 int qzc_gate_matrix(const qzc_gate *gate, double *mat_out, uint32_t *dim_out) {
@@ -1002,8 +801,26 @@ void qzc_sim_destroy(qzc_sim *sim) {
     delete sim;
 }
 
+namespace {
+// |0...0> (basis = true, store.cpp:26-81) or the zero vector (every chunk the
+// zero-chunk payload: the non-zero ranks of a sharded |0...0>).
+void init_store(qzc_sim *sim, bool basis);
+} // namespace
+
 int qzc_sim_init_basis(qzc_sim *sim) {
     QZ_API_BEGIN
+    init_store(sim, true);
+    QZ_API_END
+}
+
+int qzc_sim_init_zero(qzc_sim *sim) {
+    QZ_API_BEGIN
+    init_store(sim, false);
+    QZ_API_END
+}
+
+namespace {
+void init_store(qzc_sim *sim, bool basis) {
     qzc_context *ctx = sim->ctx;
     QZ_CUDA(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
@@ -1012,6 +829,7 @@ int qzc_sim_init_basis(qzc_sim *sim) {
     const int a = sim->cur;
     static const bool trace = getenv("QZ_TRACE") && *getenv("QZ_TRACE") == '1';
     const double ti0 = now_s();
+    kprof_set_stage(0xFFFFFFFFu);   // init launches are tagged apart from the stages
     QZ_CUDA(cudaMemsetAsync(sim->used.p, 0, 16, s));
     // slot 0 = zero chunk, slot 1 = basis chunk (store.cpp:46-51)
     QZ_CUDA(cudaMemsetAsync(w.amps.p, 0, 32 * N, s));
@@ -1051,6 +869,11 @@ int qzc_sim_init_basis(qzc_sim *sim) {
     QZ_CUDA(cudaMemcpyAsync(len2, t.len, 8, cudaMemcpyDeviceToHost, s));
     QZ_CUDA(cudaMemcpyAsync(crc2, t.crc, 8, cudaMemcpyDeviceToHost, s));
     QZ_CUDA(cudaStreamSynchronize(s));
+    if (!basis) {
+        off2[1] = off2[0];
+        len2[1] = len2[0];
+        crc2[1] = crc2[0];
+    }
     k_fill_init<<<(unsigned)ceil_div(sim->nchunks, 256), 256, 0, s>>>(
         t, sim->nchunks, off2[0], len2[0], crc2[0], off2[1], len2[1], crc2[1]);
     QZ_CHECK_LAUNCH();
@@ -1062,13 +885,14 @@ int qzc_sim_init_basis(qzc_sim *sim) {
     sim->initialized = true;
     sim->sparse_store = true;
     sim->stats = qzc_sim_stats{};
+    sim->payload_now = uint64_t(bytes) - kPerChunkOverhead * sim->nchunks;
     if (sim->host_res) QZ_CUDA(cudaMemset(sim->io_bytes.p, 0, 16));
     QZ_CUDA(cudaMemset(sim->replays.p, 0, 8));
     if (trace)
         fprintf(stderr, "qz trace: init encode %.2f ms total %.2f ms\n", 1e3 * (ti1 - ti0),
                 1e3 * (now_s() - ti0));
-    QZ_API_END
 }
+} // namespace
 
 int qzc_pass_plan_stats(const qzc_gate *gates, uint64_t ngates, uint32_t nbits,
                         uint32_t fuse_mode, uint64_t *out) {
@@ -1141,6 +965,7 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
     };
     for (size_t si = 0; si < stages.size(); ++si) {
         const Stage &st = stages[si];
+        kprof_set_stage(uint32_t(sim->stats.stages));
         const uint32_t hs = (uint32_t)st.high.size();
         const uint32_t mb = c + hs;  // buffer bits of one batch
         uint64_t smask = 0;
@@ -1326,6 +1151,16 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
             sim->stats.gate_seconds += ms[1] * 1e-3;
             sim->stats.encode_seconds += ms[2] * 1e-3;
         }
+        {
+            // compressed bytes decoded / encoded by this stage (store payload
+            // totals before and after it; footprint minus per-chunk overhead)
+            int64_t acct[2];
+            QZ_CUDA(cudaMemcpy(acct, sim->acct.p, 16, cudaMemcpyDeviceToHost));
+            const uint64_t out_bytes = uint64_t(acct[0]) - kPerChunkOverhead * sim->nchunks;
+            sim->stats.payload_in_bytes += sim->payload_now;
+            sim->stats.payload_out_bytes += out_bytes;
+            sim->payload_now = out_bytes;
+        }
         sim->cur = b;
         sim->sparse_store = false;   // after a stage the payload density is unknown
         sim->stats.stages += 1;
@@ -1487,6 +1322,7 @@ int qzc_sim_import(qzc_sim *sim, const uint8_t *payloads, const uint32_t *sizes,
     QZ_CUDA(cudaMemcpyAsync(sim->acct.p, acct, 16, cudaMemcpyHostToDevice, s));
     QZ_CUDA(cudaStreamSynchronize(s));
     sim->stats.h2d_bytes += pos + 16 * sim->nchunks;
+    sim->payload_now = pos;
     sim->initialized = true;
     QZ_API_END
 }
@@ -1527,6 +1363,9 @@ int qzc_sim_write_chunk(qzc_sim *sim, uint64_t index, const double *amps) {
                   sim->arena_ptr(a), sim->used_ptr(a), sim->arena_cap, sim->table(a),
                   sim->len[a].as<uint32_t>(), sim->acct.as<int64_t>(), ctx->launches);
     ctx->check_status();
+    int64_t acct[2];
+    QZ_CUDA(cudaMemcpy(acct, sim->acct.p, 16, cudaMemcpyDeviceToHost));
+    sim->payload_now = uint64_t(acct[0]) - kPerChunkOverhead * sim->nchunks;
     QZ_API_END
 }
 

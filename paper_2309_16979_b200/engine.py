@@ -13,7 +13,7 @@ from pathlib import Path
 
 import numpy as np
 
-from .abi import GATE_DTYPE, Gate, SimConfig, SimStats, gate_ptr, to_array
+from .abi import GATE_DTYPE, Gate, KProfRecord, SimConfig, SimStats, gate_ptr, to_array
 
 # QZC_LIB: an alternative build of the same library (tuning experiments)
 LIB_PATH = Path(os.environ.get("QZC_LIB", Path(__file__).resolve().parent / "lib" / "libqzcuda.so"))
@@ -88,6 +88,11 @@ def load_library() -> C.CDLL:
         "qzc_sim_create": (C.c_int, [C.c_void_p, P(SimConfig), P(C.c_void_p)]),
         "qzc_sim_destroy": (None, [C.c_void_p]),
         "qzc_sim_init_basis": (C.c_int, [C.c_void_p]),
+        "qzc_sim_init_zero": (C.c_int, [C.c_void_p]),
+        "qzc_exchange_pack_host": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, u32p, u32p, u8p, u32p,
+                                             u32p, u8p, C.c_uint64, u64p]),
+        "qzc_exchange_unpack_host": (C.c_int, [C.c_uint32, u8p, u64p, C.c_uint32, u8p, C.c_uint64, u32p,
+                                               u32p]),
         "qzc_sim_run": (C.c_int, [C.c_void_p, P(Gate), C.c_uint64]),
         "qzc_sim_stats_get": (C.c_int, [C.c_void_p, P(SimStats)]),
         "qzc_sim_plan_stages": (C.c_int, [C.c_void_p, P(Gate), C.c_uint64, u64p]),
@@ -110,6 +115,14 @@ def load_library() -> C.CDLL:
         "qzc_host_alloc": (C.c_int, [C.c_void_p, C.c_uint64, P(C.c_void_p)]),
         "qzc_host_free": (None, [C.c_void_p, C.c_void_p]),
         "qzc_pass_plan_stats": (C.c_int, [P(Gate), C.c_uint64, C.c_uint32, C.c_uint32, u64p]),
+        "qzc_kprof_enable": (C.c_int, [C.c_void_p, C.c_int]),
+        "qzc_sim_save": (C.c_int, [C.c_void_p, C.c_char_p]),
+        "qzc_sim_load": (C.c_int, [C.c_void_p, C.c_char_p]),
+        "qzc_sim_exchange_plan": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, u32p, u32p, u64p, u64p]),
+        "qzc_sim_exchange_pack": (C.c_int, [C.c_void_p, P(C.c_void_p), u64p]),
+        "qzc_sim_exchange_recv_buffer": (C.c_int, [C.c_void_p, C.c_uint64, P(C.c_void_p)]),
+        "qzc_sim_exchange_unpack": (C.c_int, [C.c_void_p, u64p]),
+        "qzc_kprof_read": (C.c_int, [C.c_void_p, P(KProfRecord), C.c_uint64, u64p]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -181,6 +194,19 @@ class Engine:
         out = C.c_double()
         _check(self.lib.qzc_timer_end(self.h, C.byref(out)))
         return out.value
+
+    def kprof_enable(self, on: bool = True) -> None:
+        """Per-launch CUDA-event timing of the engine's kernels (clears records)."""
+        _check(self.lib.qzc_kprof_enable(self.h, 1 if on else 0))
+
+    def kprof_read(self) -> list[dict]:
+        """Timed launches since enable / the last read (synchronizes)."""
+        n = C.c_uint64()
+        _check(self.lib.qzc_kprof_read(self.h, None, 0, C.byref(n)))
+        recs = (KProfRecord * max(1, n.value))()
+        _check(self.lib.qzc_kprof_read(self.h, recs, n.value, C.byref(n)))
+        return [{"name": r.name.decode(), "tag": r.tag, "stage": r.stage, "seconds": r.seconds,
+                 "bytes": r.bytes} for r in recs[:n.value]]
 
     def pinned(self, nbytes: int, dtype=np.uint8) -> np.ndarray:
         """Page-locked host array (qzc_host_alloc), freed with the array."""
@@ -350,6 +376,10 @@ class Simulator:
     def init_basis(self) -> None:
         _check(self.lib.qzc_sim_init_basis(self.h))
 
+    def init_zero(self) -> None:
+        """Every chunk the zero-chunk payload (non-zero ranks of a sharded |0...0>)."""
+        _check(self.lib.qzc_sim_init_zero(self.h))
+
     def run(self, gates) -> None:
         arr = to_array(gates)
         _check(self.lib.qzc_sim_run(self.h, gate_ptr(arr), arr.size))
@@ -418,6 +448,44 @@ class Simulator:
         if a.size != 1 << self.c:
             raise StoreError(f"chunk size mismatch: expected {1 << self.c}, got {a.size}")
         _check(self.lib.qzc_sim_write_chunk(self.h, index, a.ctypes.data))
+
+    # ---- checkpoint / resume (ChunkStore::save / load, store.cpp:152-217) ----
+    def save(self, path) -> None:
+        """Write the store as a QZST file (the reference's format)."""
+        _check(self.lib.qzc_sim_save(self.h, os.fsencode(str(path))))
+
+    def load(self, path) -> None:
+        """Replace the store with a QZST file's chunks (CRCs verified on the GPU)."""
+        _check(self.lib.qzc_sim_load(self.h, os.fsencode(str(path))))
+
+    # ---- sharded exchange (device to device; sharding.py drives it) --------
+    def exchange_plan(self, g: int, rank: int, old_pos, new_pos):
+        """Per-destination record-group bytes and chunk counts of an ownership
+        change from owner positions old_pos to new_pos (chunk-index bits)."""
+        world = 1 << g
+        op = np.ascontiguousarray(old_pos, dtype=np.uint32)
+        np_ = np.ascontiguousarray(new_pos, dtype=np.uint32)
+        sb = np.zeros(world, np.uint64)
+        sc = np.zeros(world, np.uint64)
+        _check(self.lib.qzc_sim_exchange_plan(self.h, g, rank, op.ctypes.data_as(u32p),
+                                              np_.ctypes.data_as(u32p), sb.ctypes.data_as(u64p),
+                                              sc.ctypes.data_as(u64p)))
+        return sb, sc
+
+    def exchange_pack(self) -> tuple[int, int]:
+        """Pack the planned groups in HBM: (device pointer, bytes)."""
+        p, n = C.c_void_p(), C.c_uint64()
+        _check(self.lib.qzc_sim_exchange_pack(self.h, C.byref(p), C.byref(n)))
+        return int(p.value or 0), int(n.value)
+
+    def exchange_recv_buffer(self, nbytes: int) -> int:
+        p = C.c_void_p()
+        _check(self.lib.qzc_sim_exchange_recv_buffer(self.h, int(nbytes), C.byref(p)))
+        return int(p.value or 0)
+
+    def exchange_unpack(self, recv_bytes) -> None:
+        rb = np.ascontiguousarray(recv_bytes, dtype=np.uint64)
+        _check(self.lib.qzc_sim_exchange_unpack(self.h, rb.ctypes.data_as(u64p)))
 
     def fidelity(self, dense: DenseState) -> float:
         out = C.c_double()

@@ -17,19 +17,22 @@ the north star's item 4 / SURVEY §5 and §8e:
   global order — is identical to the reference's.
 * **Exchange.** When a stage touches an owner qubit, that owner position is
   re-assigned to a free qubit (the one whose next use is farthest away) and
-  whole *compressed* chunks move to their new owner: an all-to-all of
-  (new local index, size, crc, payload) records.  Over NVLink this is NCCL
-  all_to_all on the payload bytes; tests run it over gloo on CPU.
+  whole *compressed* chunks move to their new owner, device to device: the
+  engine packs per-destination record groups in HBM from the arena
+  (qzc_sim_exchange_plan / _pack), the transport moves them (NCCL
+  all_to_all over NVLink; gloo through host memory in the CPU-backed
+  tests), and the engine unpacks the received groups in place — the receive
+  buffer becomes the new arena (qzc_sim_exchange_unpack).  Only the group
+  sizes (2^g integers) cross the host.
 """
 from __future__ import annotations
 
 import ctypes as C
-import struct
 from dataclasses import dataclass
 
 import numpy as np
 
-from .abi import gate_ptr, to_array
+from .abi import to_array
 
 
 @dataclass
@@ -97,7 +100,8 @@ def plan_owners(n: int, c: int, g: int, stages: list[StageInfo]) -> list[list[in
     return plans
 
 
-def _positions(owners, c):
+def positions(owners, c) -> list[int]:
+    """Owner qubits -> chunk-index bit positions."""
     return [q - c for q in owners]
 
 
@@ -128,6 +132,22 @@ def expand(y: int, pos, rank: int) -> int:
     return out
 
 
+def expand_many(ys: np.ndarray, pos, rank: int, width: int) -> np.ndarray:
+    """Vectorised expand over local chunk indices (width = global index bits)."""
+    ys = np.asarray(ys, dtype=np.uint64)
+    x = np.zeros_like(ys)
+    taken = {p: i for i, p in enumerate(pos)}
+    j = 0
+    for b in range(width):
+        if b in taken:
+            if (rank >> taken[b]) & 1:
+                x |= np.uint64(1 << b)
+        else:
+            x |= ((ys >> np.uint64(j)) & np.uint64(1)) << np.uint64(b)
+            j += 1
+    return x
+
+
 def owner_of(x: int, pos) -> int:
     return sum(((x >> p) & 1) << i for i, p in enumerate(pos))
 
@@ -144,76 +164,147 @@ def local_gates(gates, owners, c):
     return arr
 
 
-def pack_records(records) -> bytes:
-    """(new_local_index, crc, payload) -> bytes"""
-    out = bytearray()
-    for idx, crc, payload in records:
-        out += struct.pack("<QII", idx, len(payload), crc) + payload
-    return bytes(out)
+# ------------------------------------------------------------------ host path
+def pack_groups_host(local_bits: int, g: int, rank: int, old_pos, new_pos, blob: bytes, sizes,
+                     crcs) -> tuple[bytes, np.ndarray]:
+    """The engine's record groups built on the host from a store given as
+    payloads in local chunk order (qzc_exchange_pack_host): (buffer, bytes per
+    destination).  Same layout the device pack writes."""
+    from .engine import _check, load_library
+    lib = load_library()
+    P = C.POINTER
+    op = np.ascontiguousarray(old_pos, np.uint32)
+    np_ = np.ascontiguousarray(new_pos, np.uint32)
+    sizes = np.ascontiguousarray(sizes, np.uint32)
+    crcs = np.ascontiguousarray(crcs, np.uint32)
+    payload = np.frombuffer(blob, np.uint8) if blob else np.zeros(1, np.uint8)
+    sb = np.zeros(1 << g, np.uint64)
+    args = (local_bits, g, rank, op.ctypes.data_as(P(C.c_uint32)), np_.ctypes.data_as(P(C.c_uint32)),
+            payload.ctypes.data_as(P(C.c_uint8)), sizes.ctypes.data_as(P(C.c_uint32)),
+            crcs.ctypes.data_as(P(C.c_uint32)))
+    _check(lib.qzc_exchange_pack_host(*args, None, 0, sb.ctypes.data_as(P(C.c_uint64))))
+    out = np.zeros(max(int(sb.sum()), 1), np.uint8)
+    _check(lib.qzc_exchange_pack_host(*args, out.ctypes.data_as(P(C.c_uint8)), out.size,
+                                      sb.ctypes.data_as(P(C.c_uint64))))
+    return out[: int(sb.sum())].tobytes(), sb
 
 
-def unpack_records(blob: bytes):
-    out, pos = [], 0
-    while pos < len(blob):
-        idx, size, crc = struct.unpack_from("<QII", blob, pos)
-        pos += 16
-        out.append((idx, crc, blob[pos:pos + size]))
-        pos += size
-    return out
+def unpack_groups_host(world: int, recv: bytes, recv_bytes, local_bits: int):
+    """Received groups -> (blob, sizes, crcs) in local chunk order
+    (qzc_exchange_unpack_host)."""
+    from .engine import _check, load_library
+    lib = load_library()
+    P = C.POINTER
+    buf = np.frombuffer(recv, np.uint8) if recv else np.zeros(1, np.uint8)
+    rb = np.ascontiguousarray(recv_bytes, np.uint64)
+    n = 1 << local_bits
+    sizes = np.zeros(n, np.uint32)
+    crcs = np.zeros(n, np.uint32)
+    out = np.zeros(max(len(recv), 1), np.uint8)
+    _check(lib.qzc_exchange_unpack_host(world, buf.ctypes.data_as(P(C.c_uint8)),
+                                        rb.ctypes.data_as(P(C.c_uint64)), local_bits,
+                                        out.ctypes.data_as(P(C.c_uint8)), out.size,
+                                        sizes.ctypes.data_as(P(C.c_uint32)),
+                                        crcs.ctypes.data_as(P(C.c_uint32))))
+    return out[: int(sizes.sum(dtype=np.uint64))].tobytes(), sizes, crcs
 
 
-def exchange_plan(store_blob: bytes, sizes, crcs, rank: int, old_owners, new_owners, c, world):
-    """Split this rank's exported store into per-destination record lists."""
-    old_pos, new_pos = _positions(old_owners, c), _positions(new_owners, c)
-    per_dest = [[] for _ in range(world)]
-    off = 0
-    for y, (sz, crc) in enumerate(zip(sizes, crcs)):
-        x = expand(y, old_pos, rank)
-        dst = owner_of(x, new_pos)
-        per_dest[dst].append((squeeze(x, new_pos), int(crc), store_blob[off:off + int(sz)]))
-        off += int(sz)
-    return per_dest
+# ---------------------------------------------------------------- transports
+class _DevBytes:
+    """Zero-copy __cuda_array_interface__ view of an engine device buffer."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (int(nbytes),), "typestr": "|u1",
+                                         "data": (int(ptr), False), "version": 3, "strides": None}
 
 
-def assemble_store(records, nlocal):
-    """Records (any order) -> (blob, sizes, crcs) in local chunk order."""
-    recs = sorted(records, key=lambda r: r[0])
-    assert [r[0] for r in recs] == list(range(nlocal)), "exchange lost or duplicated chunks"
-    blob = b"".join(r[2] for r in recs)
-    sizes = np.array([len(r[2]) for r in recs], np.uint32)
-    crcs = np.array([r[1] for r in recs], np.uint32)
-    return blob, sizes, crcs
+def device_view(ptr: int, nbytes: int, device):
+    import torch
+    if nbytes == 0:
+        return torch.empty(0, dtype=torch.uint8, device=device)
+    return torch.as_tensor(_DevBytes(ptr, nbytes), device=device)
 
 
 class LocalGroup:
-    """In-process transport: G ranks driven by one process (one GPU)."""
+    """In-process transport: G ranks driven by one process (one GPU); the
+    groups move with device-to-device copies."""
 
     def __init__(self, world: int):
         self.world = world
 
-    def all_to_all(self, sends):
-        # sends[r][d] -> recvs[d][r]
-        return [[sends[r][d] for r in range(self.world)] for d in range(self.world)]
+    def exchange(self, sims: dict, plans: dict, device) -> int:
+        import torch
+        sends = {r: sims[r].exchange_pack() for r in sims}
+        moved = 0
+        recv_bytes = {}
+        for d in range(self.world):
+            rb = np.array([int(plans[s][d]) for s in range(self.world)], np.uint64)
+            rptr = sims[d].exchange_recv_buffer(int(rb.sum()))
+            dst_off = 0
+            for s in range(self.world):
+                sptr, _ = sends[s]
+                src_off = int(plans[s][:d].sum())
+                n = int(plans[s][d])
+                if n:
+                    device_view(rptr + dst_off, n, device).copy_(device_view(sptr + src_off, n, device))
+                dst_off += n
+                moved += n if s != d else 0
+            recv_bytes[d] = rb
+        torch.cuda.synchronize(device)
+        for d in range(self.world):
+            sims[d].exchange_unpack(recv_bytes[d])
+        return moved
+
+    def allgather_bytes(self, payloads: dict) -> dict:
+        return payloads
 
 
 class TorchGroup:
-    """torch.distributed transport (gloo on CPU, NCCL over NVLink)."""
+    """torch.distributed transport: NCCL moves the groups GPU to GPU; gloo
+    (CPU-backed tests) stages them through host memory."""
 
     def __init__(self, dist, device=None):
         self.dist = dist
         self.world = dist.get_world_size()
         self.rank = dist.get_rank()
         self.device = device
+        self.nccl = dist.get_backend() == "nccl"
+
+    def exchange(self, sims: dict, plans: dict, device) -> int:
+        import torch
+        (r,) = sims
+        sim = sims[r]
+        sb = plans[r]
+        cdev = device if self.nccl else "cpu"
+        send_sizes = torch.tensor(sb.astype(np.int64), device=cdev)
+        recv_sizes = torch.empty_like(send_sizes)
+        self.dist.all_to_all_single(recv_sizes, send_sizes)
+        rb = recv_sizes.cpu().numpy().astype(np.uint64)
+        sptr, total = sim.exchange_pack()
+        rptr = sim.exchange_recv_buffer(int(rb.sum()))
+        send = device_view(sptr, total, device)
+        recv = device_view(rptr, int(rb.sum()), device)
+        if self.nccl:
+            self.dist.all_to_all_single(recv, send, [int(x) for x in rb], [int(x) for x in sb])
+            torch.cuda.synchronize(device)
+        else:
+            rcpu = torch.empty(int(rb.sum()), dtype=torch.uint8)
+            self.dist.all_to_all_single(rcpu, send.cpu(), [int(x) for x in rb], [int(x) for x in sb])
+            recv.copy_(rcpu.to(device))
+            torch.cuda.synchronize(device)
+        sim.exchange_unpack(rb)
+        return int(sb.sum() - sb[r])
 
     def all_to_all_bytes(self, send: list[bytes]) -> list[bytes]:
+        """Host byte strings to every rank (report path: digest gathering)."""
         import torch
-        dev = self.device or "cpu"
+        dev = self.device if self.nccl else "cpu"
         lens = torch.tensor([len(b) for b in send], dtype=torch.int64, device=dev)
         rlens = torch.empty_like(lens)
         self.dist.all_to_all_single(rlens, lens)
-        flat = torch.frombuffer(bytearray(b"".join(send)) or bytearray(1), dtype=torch.uint8)
-        if sum(len(b) for b in send) == 0:
-            flat = flat[:0]
+        joined = b"".join(send)
+        flat = torch.frombuffer(bytearray(joined), dtype=torch.uint8) if joined else \
+            torch.empty(0, dtype=torch.uint8)
         flat = flat.to(dev)
         out = torch.empty(int(rlens.sum()), dtype=torch.uint8, device=dev)
         self.dist.all_to_all_single(out, flat, output_split_sizes=rlens.tolist(),
@@ -245,39 +336,24 @@ class ShardedRun:
         self.sims = {r: e.simulator(self.nl, c, m, eb, init=False, **sim_kw)
                      for r, e in zip(self.ranks, engs)}
         self.engines = dict(zip(self.ranks, engs))
+        self.device = f"cuda:{engs[0].device}"
         self.owners = list(range(n - g, n))
         self.exchanges = 0
         self.exchanged_bytes = 0
 
     def init_basis(self):
         """|0...0>: rank 0 holds the basis chunk, all other ranks zeros."""
+        self.owners = list(range(self.n - self.g, self.n))
         for r, sim in self.sims.items():
-            sim.init_basis()
-            if r != 0:
-                blob, sizes, crcs = sim.export()
-                zero_payload, zcrc = self.engines[r].compress(
-                    np.zeros(1 << self.c, np.complex128), self.eb)
-                k = sim.chunk_count
-                sim.import_(zero_payload * k, np.full(k, len(zero_payload), np.uint32),
-                            np.full(k, zcrc, np.uint32))
+            if r == 0:
+                sim.init_basis()
+            else:
+                sim.init_zero()
 
     def _exchange(self, new_owners):
-        sends = {}
-        for r, sim in self.sims.items():
-            blob, sizes, crcs = sim.export()
-            per = exchange_plan(blob, sizes, crcs, r, self.owners, new_owners, self.c, self.world)
-            sends[r] = [pack_records(p) for p in per]
-        if isinstance(self.t, LocalGroup):
-            recv = self.t.all_to_all([sends[r] for r in range(self.world)])
-            recv = {r: recv[r] for r in self.ranks}
-        else:
-            (r,) = self.ranks
-            recv = {r: self.t.all_to_all_bytes(sends[r])}
-        nlocal = 1 << (self.nl - self.c)
-        for r, sim in self.sims.items():
-            self.exchanged_bytes += sum(len(b) for b in recv[r])
-            recs = [rec for b in recv[r] for rec in unpack_records(b)]
-            sim.import_(*assemble_store(recs, nlocal))
+        old_pos, new_pos = positions(self.owners, self.c), positions(new_owners, self.c)
+        plans = {r: sim.exchange_plan(self.g, r, old_pos, new_pos)[0] for r, sim in self.sims.items()}
+        self.exchanged_bytes += self.t.exchange(self.sims, plans, self.device)
         self.owners = list(new_owners)
         self.exchanges += 1
 
@@ -292,40 +368,62 @@ class ShardedRun:
             for sim in self.sims.values():
                 sim.run(lg)
 
-    def global_store(self):
-        """(blob, sizes, crcs) of the whole state in global chunk order
-        (ranks of this process only; LocalGroup holds all of them)."""
-        pos = _positions(self.owners, self.c)
-        recs = []
-        for r, sim in self.sims.items():
-            blob, sizes, crcs = sim.export()
-            off = 0
-            for y, (sz, crc) in enumerate(zip(sizes, crcs)):
-                recs.append((expand(y, pos, r), int(crc), blob[off:off + int(sz)]))
-                off += int(sz)
-        return recs
+    def local_export(self):
+        """This process's rank stores on the host: {rank: (blob, sizes, crcs)}."""
+        return {r: sim.export() for r, sim in self.sims.items()}
+
+    def global_chunk_indices(self, rank: int) -> np.ndarray:
+        nloc = 1 << (self.nl - self.c)
+        return expand_many(np.arange(nloc, dtype=np.uint64), positions(self.owners, self.c), rank,
+                           self.n - self.c)
 
     def gather_store(self):
-        """All ranks' chunks at rank 0 (global order); None elsewhere."""
-        recs = self.global_store()
-        if isinstance(self.t, LocalGroup):
-            return sorted(recs, key=lambda r: r[0])
-        send = [b""] * self.world
-        send[0] = pack_records(recs)
-        got = self.t.all_to_all_bytes(send)
-        if self.ranks[0] != 0:
-            return None
-        return sorted([r for b in got for r in unpack_records(b)], key=lambda r: r[0])
+        """All chunks at rank 0 in global chunk order: (blob, sizes, crcs);
+        None on the other ranks (report path, not timed)."""
+        import struct
+        parts = {}
+        for r, (blob, sizes, crcs) in self.local_export().items():
+            parts[r] = (self.global_chunk_indices(r), blob, sizes, crcs)
+        if not isinstance(self.t, LocalGroup):
+            (r,) = self.ranks
+            idx, blob, sizes, crcs = parts[r]
+            msg = struct.pack("<QQ", r, len(idx)) + idx.tobytes() + sizes.tobytes() + \
+                crcs.tobytes() + blob
+            send = [b""] * self.world
+            send[0] = msg
+            got = self.t.all_to_all_bytes(send)
+            if r != 0:
+                return None
+            parts = {}
+            for m_ in got:
+                src, k = struct.unpack_from("<QQ", m_, 0)
+                o = 16
+                idx = np.frombuffer(m_, np.uint64, k, o)
+                o += 8 * k
+                sizes = np.frombuffer(m_, np.uint32, k, o)
+                o += 4 * k
+                crcs = np.frombuffer(m_, np.uint32, k, o)
+                o += 4 * k
+                parts[src] = (idx, m_[o:], sizes, crcs)
+        total = 1 << (self.n - self.c)
+        sizes_g = np.zeros(total, np.uint32)
+        crcs_g = np.zeros(total, np.uint32)
+        chunks = [b""] * total
+        for idx, blob, sizes, crcs in parts.values():
+            offs = np.concatenate([[0], np.cumsum(sizes, dtype=np.uint64)]).astype(np.int64)
+            for j, x in enumerate(idx.tolist()):
+                chunks[x] = bytes(blob[offs[j]:offs[j + 1]])
+            sizes_g[idx.astype(np.int64)] = sizes
+            crcs_g[idx.astype(np.int64)] = crcs
+        return b"".join(chunks), sizes_g, crcs_g
 
     def digest(self):
         """FNV-1a over all payloads in global chunk order (rank 0; None elsewhere)."""
         from .engine import load_library
-        lib = load_library()
-        recs = self.gather_store()
-        if recs is None:
+        g = self.gather_store()
+        if g is None:
             return None
-        h = 0xcbf29ce484222325
-        for _, _, p in recs:
-            buf = np.frombuffer(p, np.uint8).copy() if p else np.zeros(1, np.uint8)
-            h = lib.qzc_fnv1a64(buf.ctypes.data_as(C.POINTER(C.c_uint8)), len(p), h)
-        return h
+        blob = g[0]
+        buf = np.frombuffer(blob, np.uint8) if blob else np.zeros(1, np.uint8)
+        return load_library().qzc_fnv1a64(buf.ctypes.data_as(C.POINTER(C.c_uint8)), len(blob),
+                                          0xcbf29ce484222325)

@@ -1,0 +1,164 @@
+"""Checkpoint / resume from the device arenas (QZST, store.cpp:152-217) and the
+device-to-device sharded exchange (sharding.py over qzc_sim_exchange_*):
+reference digests from tests/golden, two processes on one GPU exchanging
+compressed chunks through torch.distributed (gloo transport; the NCCL path
+is the same engine calls with device tensors)."""
+import json
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_2309_16979_b200 import circuits as CI
+from paper_2309_16979_b200 import engine as E
+from paper_2309_16979_b200 import sharding as S
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def _circ(golden, key):
+    from paper_2309_16979_b200.abi import to_array
+    if key.startswith("qft:"):
+        return CI.qft(int(key.split(":")[1]))
+    if key.startswith("ghz:"):
+        return CI.ghz(int(key.split(":")[1]))
+    return to_array([(g[0], tuple(g[1]), tuple(g[2])) for g in golden["circuits"][key]])
+
+
+def test_save_load_roundtrip_bytes(engine, tmp_path):
+    sim = engine.simulator(18, 10, 16, 1e-6)
+    sim.run(CI.qaoa(18))
+    blob, sizes, crcs = sim.export()
+    path = tmp_path / "s.qzst"
+    sim.save(path)
+    # the file is the reference's QZST layout: header + (len, crc, payload) per chunk
+    raw = path.read_bytes()
+    assert raw[:4] == b"QZST" and int.from_bytes(raw[4:8], "little") == 18
+    assert len(raw) == 20 + 8 * sim.chunk_count + len(blob)
+    other = engine.simulator(18, 10, 16, 1e-6, init=False)
+    other.load(path)
+    b2, s2, c2 = other.export()
+    assert b2 == blob and (s2 == sizes).all() and (c2 == crcs).all()
+    assert other.digest() == sim.digest()
+    assert other.stats()["current_bytes"] == sim.stats()["current_bytes"]
+
+
+def test_load_rejects_corruption_and_geometry(engine, tmp_path):
+    sim = engine.simulator(14, 8, 12, 1e-5)
+    sim.run(CI.qft(14))
+    path = tmp_path / "s.qzst"
+    sim.save(path)
+    raw = bytearray(path.read_bytes())
+    raw[40] ^= 0x5A   # inside the first chunk's payload
+    bad = tmp_path / "bad.qzst"
+    bad.write_bytes(bytes(raw))
+    with pytest.raises(E.StoreError, match="checksum mismatch in chunk 0"):
+        engine.simulator(14, 8, 12, 1e-5, init=False).load(bad)
+    with pytest.raises(E.StoreError):
+        engine.simulator(14, 7, 12, 1e-5, init=False).load(path)
+    (tmp_path / "trunc.qzst").write_bytes(path.read_bytes()[:-5])
+    with pytest.raises(E.StoreError, match="truncated"):
+        engine.simulator(14, 8, 12, 1e-5, init=False).load(tmp_path / "trunc.qzst")
+
+
+@pytest.mark.parametrize("key", [("qft:20", 12, 16, 1e-5), ("random:24:200:1", 16, 20, 1e-7)])
+def test_resume_at_stage_boundary_matches_reference(engine, golden, tmp_path, key):
+    """Checkpoint between two runs that split the circuit at a stage boundary
+    of its plan, resume in a fresh simulator from the file: the reference's
+    digest (each stage is one codec round trip, so the split is invisible)."""
+    circ_key, c, m, eb = key
+    rec = next(r for r in golden["runs"] if r["circuit"] == circ_key and r["c"] == c
+               and r["m"] == m and r["eb"] == eb)
+    g = _circ(golden, circ_key)
+    n = rec["n"]
+    stages = S.global_stages(n, c, m, g)
+    assert len(stages) >= 2
+    cut = stages[len(stages) // 2].first
+    a = engine.simulator(n, c, m, eb)
+    a.run(g[:cut])
+    a.save(tmp_path / "ck.qzst")
+    a.close()
+    b = engine.simulator(n, c, m, eb, init=False)
+    b.load(tmp_path / "ck.qzst")
+    b.run(g[cut:])
+    assert f"{b.digest():016x}" == rec["digest"]
+
+
+@pytest.mark.parametrize("g", [1, 2, 3])
+def test_device_exchange_roundtrip(engine, g):
+    """Ownership changes back and forth through the device exchange: every
+    chunk's payload lands at its new owner and returns unchanged."""
+    n, c, m, eb = 18, 8, 12, 1e-6
+    run = S.ShardedRun(engine, n, c, m, eb, g, range(1 << g), S.LocalGroup(1 << g))
+    run.init_basis()
+    run.run(CI.supremacy(n, depth=3))
+    before = run.gather_store()
+    owners0 = list(run.owners)
+    free = [q for q in range(c, n) if q not in owners0]
+    run._exchange([free[0]] + owners0[1:])
+    run._exchange([free[1]] + owners0[1:])
+    after_move = run.gather_store()
+    run._exchange(owners0)
+    after = run.gather_store()
+    for x in (after_move, after):
+        assert x[0] == before[0]
+        assert (x[1] == before[1]).all() and (x[2] == before[2]).all()
+
+
+_WORKER = r"""
+import json, os, sys
+import numpy as np
+import torch, torch.distributed as dist
+from paper_2309_16979_b200 import engine as E, sharding as S, circuits as CI
+from paper_2309_16979_b200.abi import to_array
+rank, world, port, cfg = int(sys.argv[1]), int(sys.argv[2]), sys.argv[3], json.loads(sys.argv[4])
+os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=port)
+dist.init_process_group("gloo", rank=rank, world_size=world)
+torch.cuda.set_device(0)
+eng = E.Engine(0)
+g = world.bit_length() - 1
+gates = to_array([tuple(x[:1]) + (tuple(x[1]), tuple(x[2])) for x in cfg["gates"]])
+run = S.ShardedRun(eng, cfg["n"], cfg["c"], cfg["m"], cfg["eb"], g, [rank],
+                   S.TorchGroup(dist, device="cuda:0"))
+run.init_basis()
+run.run(gates)
+d = run.digest()
+if rank == 0:
+    print(json.dumps({"digest": f"{d:016x}", "exchanges": run.exchanges,
+                      "bytes": run.exchanged_bytes}))
+dist.destroy_process_group()
+"""
+
+
+@pytest.mark.parametrize("key", [("random:24:200:1", 16, 20, 1e-7), ("qft:20", 12, 16, 1e-5)])
+def test_two_processes_torch_group_reference_digest(golden, tmp_path, key):
+    """Two processes, one engine each on cuda:0, one ShardedRun over
+    TorchGroup: compressed chunks packed / unpacked on the device, moved by
+    torch.distributed; the reference's digest."""
+    import socket
+    circ_key, c, m, eb = key
+    rec = next(r for r in golden["runs"] if r["circuit"] == circ_key and r["c"] == c
+               and r["m"] == m and r["eb"] == eb)
+    from paper_2309_16979_b200.abi import from_array
+    gates = [[nm, list(q), list(p)] for nm, q, p in from_array(_circ(golden, circ_key))]
+    cfg = json.dumps({"n": rec["n"], "c": c, "m": m, "eb": eb, "gates": gates})
+    script = tmp_path / "worker.py"
+    script.write_text(_WORKER)
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = str(sock.getsockname()[1])
+    sock.close()
+    env = dict(os.environ, PYTHONPATH=str(ROOT))
+    procs = [subprocess.Popen([sys.executable, str(script), str(r), "2", port, cfg], cwd=ROOT, env=env,
+                              stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)
+             for r in range(2)]
+    outs = [p.communicate(timeout=600) for p in procs]
+    for p, (o, e) in zip(procs, outs):
+        assert p.returncode == 0, e[-3000:]
+    res = json.loads(outs[0][0].strip().splitlines()[-1])
+    assert res["digest"] == rec["digest"]
+    assert res["exchanges"] >= 1 and res["bytes"] > 0

@@ -1,0 +1,32 @@
+"""Dense-state codec / pass timing probe: one circuit at n qubits, per-phase
+CUDA-event times and the store size (the codec's dense-workload numbers)."""
+import argparse
+import time
+
+from paper_2309_16979_b200 import circuits
+from paper_2309_16979_b200.engine import Engine
+
+ap = argparse.ArgumentParser()
+ap.add_argument("circuit")
+ap.add_argument("n", type=int)
+ap.add_argument("--c", type=int, default=16)
+ap.add_argument("--m", type=int, default=30)
+ap.add_argument("--eb", type=float, default=1e-7)
+ap.add_argument("--depth", type=int, default=20)
+ap.add_argument("--reps", type=int, default=2)
+a = ap.parse_args()
+eng = Engine()
+kw = {"depth": a.depth} if a.circuit == "supremacy" else {}
+gates = circuits.make(a.circuit, a.n, **kw)
+sim = eng.simulator(a.n, a.c, a.m, a.eb, init=False)
+for rep in range(a.reps):
+    t0 = time.perf_counter()
+    sim.init_basis()
+    sim.run(gates)
+    st = sim.stats()
+    el = time.perf_counter() - t0
+    print(f"{a.circuit}-{a.n} c={a.c} m={a.m} eb={a.eb}: {1e3*el:.1f} ms, stages {st['stages']} "
+          f"windows {st['windows']} passes {st['gate_passes']} replays {st['replays']} "
+          f"dec {1e3*st['decode_seconds']:.2f} gates {1e3*st['gate_seconds']:.2f} "
+          f"enc {1e3*st['encode_seconds']:.2f} ms payload {sim.payload_bytes()/1e9:.3f} GB "
+          f"ratio {st['ratio']:.3f} digest {sim.digest():016x}", flush=True)
