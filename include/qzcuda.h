@@ -210,7 +210,15 @@ typedef struct qzc_sim_config {
     uint32_t num_qubits;     /* n                                             */
     uint32_t chunk_qubits;   /* c  (PipelineConfig::chunk_qubits)             */
     uint32_t batch_qubits;   /* m  (PipelineConfig::batch_qubits)             */
-    uint32_t reserved0;
+    uint32_t skip_reencode;  /* NON-PARITY fast mode (the
+                                reference re-encodes every chunk once per
+                                stage): when the whole dense
+                                state fits one HBM window, the circuit runs
+                                as ONE stage (one decode and one encode per
+                                run, m = n) — fewer lossy round trips, so
+                                payload bytes differ from the reference and
+                                numbers are reported apart from parity runs.
+                                0 = the reference's semantics (default).   */
     double error_bound;      /* 0 selects the lossless codec                  */
     uint64_t window_amps;    /* dense amplitudes per device window; 0 = auto  */
     uint32_t residency;      /* 0 = compressed store in HBM, 1 = pinned host  */

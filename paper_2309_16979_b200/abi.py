@@ -64,7 +64,7 @@ def gate_ptr(arr: np.ndarray):
 
 class SimConfig(C.Structure):
     _fields_ = [("num_qubits", C.c_uint32), ("chunk_qubits", C.c_uint32),
-                ("batch_qubits", C.c_uint32), ("reserved0", C.c_uint32),
+                ("batch_qubits", C.c_uint32), ("skip_reencode", C.c_uint32),
                 ("error_bound", C.c_double), ("window_amps", C.c_uint64),
                 ("residency", C.c_uint32), ("renormalize", C.c_uint32),
                 ("fuse_gates", C.c_uint32), ("debug_flags", C.c_uint32)]

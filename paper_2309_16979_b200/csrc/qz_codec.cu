@@ -649,136 +649,6 @@ __global__ void __launch_bounds__(256) k_dec_lossy_warp(
     }
 }
 
-// Lossy decode, cooperative (codec.cpp:217-249): a CTA of 8 warps owns
-// kDecSlots chunks = 2 kDecSlots chains (slot, half) and walks them 32
-// elements per step.
-//  A (expand, all warps): warp w expands chains w, w+8, ... — for each, the
-//    32 codes of the step from its two byte planes (plane_block: warp scan of
-//    the runs + shuffle search), raw escapes ranked by ballot and fetched in
-//    parallel, and writes val = raw ? value : code * 2eb plus the raw mask
-//    to shared memory;
-//  B (chain, one thread per chain): pred = raw ? val : pred + val, the
-//    reference's sequence of roundings, 32 steps from shared memory — the
-//    only serial part, one lane per chain instead of one warp;
-//  C (store, all warps): the [kDecSlots x 32] amplitude tile as coalesced
-//    512 B rows.
-// The chain stays in a register across steps; plane cursors and raw counts
-// stay in the expanding warp's registers.
-constexpr uint32_t kDecSlots = 16;
-constexpr uint32_t kDecChains = 2 * kDecSlots;
-constexpr uint32_t kDecChainsPerWarp = kDecChains / 8;
-
-__global__ void __launch_bounds__(256) k_dec_lossy_coop(
-    const uint8_t *__restrict__ arena, const DecIdx *__restrict__ idx,
-    const uint64_t *__restrict__ slot_chunk, uint64_t nslots, CodecGeom g,
-    double2 *__restrict__ win, DevStatus *status, const uint32_t *cond) {
-    if (cond && *cond == 0) return;
-    __shared__ double V[kDecChains][33];
-    __shared__ uint32_t R[kDecChains];
-    __shared__ double2 O[kDecSlots][33];
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint64_t slot0 = uint64_t(blockIdx.x) * kDecSlots;
-    const uint32_t rows = uint32_t(umin64(kDecSlots, nslots - slot0));
-    const uint64_t N = g.N;
-    // expansion state of this warp's chains
-    PlaneRd lo[kDecChainsPerWarp], hi[kDecChainsPerWarp];
-    uint32_t raw_i[kDecChainsPerWarp];
-    bool live[kDecChainsPerWarp];
-    double twoeb[kDecChainsPerWarp];
-    const uint8_t *pb[kDecChainsPerWarp];
-#pragma unroll
-    for (uint32_t k = 0; k < kDecChainsPerWarp; ++k) {
-        const uint32_t c = warp + 8 * k, r = c >> 1, h = c & 1;
-        live[k] = r < rows && idx[slot0 + r].len != 0;
-        lo[k] = PlaneRd{0, 0};
-        hi[k] = PlaneRd{0, 0};
-        raw_i[k] = 0;
-        twoeb[k] = 0.0;
-        pb[k] = arena;
-        if (live[k]) {
-            const DecIdx &d = idx[slot0 + r];
-            const uint8_t *p = arena + d.base;
-            pb[k] = p;
-            lo[k] = PlaneRd{d.pos[0][h], uint32_t(__ldg(p + d.pos[0][h] + 1)) - d.skip[0][h]};
-            hi[k] = PlaneRd{d.pos[1][h], uint32_t(__ldg(p + d.pos[1][h] + 1)) - d.skip[1][h]};
-            // a zero remainder: the half starts at the next pair
-            if (lo[k].rem == 0) { lo[k].pp += 2; lo[k].rem = __ldg(p + lo[k].pp + 1); }
-            if (hi[k].rem == 0) { hi[k].pp += 2; hi[k].rem = __ldg(p + hi[k].pp + 1); }
-            raw_i[k] = h ? d.raw_re : 0;
-            twoeb[k] = 2.0 * d.eb;
-        }
-    }
-    // chain state (warp 0: lane = chain)
-    double pred = 0.0;
-    for (uint64_t e0 = 0; e0 < N; e0 += 32) {
-        // A: expand
-#pragma unroll
-        for (uint32_t k = 0; k < kDecChainsPerWarp; ++k) {
-            const uint32_t c = warp + 8 * k;
-            double val = 0.0;
-            uint32_t rm = 0;
-            if (live[k]) {
-                const uint8_t *p = pb[k];
-                const uint32_t z = plane_block(lo[k], p, lane) | (plane_block(hi[k], p, lane) << 8);
-                const bool raw = z == 0xFFFFu;
-                rm = __ballot_sync(0xffffffffu, raw);
-                const DecIdx &d = idx[slot0 + (c >> 1)];
-                if (raw) {
-                    const uint32_t q = raw_i[k] + __popc(rm & ((1u << lane) - 1));
-                    val = q < d.raw_count ? __longlong_as_double((long long)ld_u64(p + d.raw_pos + 8ull * q)) : 0.0;
-                } else {
-                    // ((double)code * 2.0) * eb == (double)code * (2 eb) exactly
-                    val = __dmul_rn(double(unzigzag16(z)), twoeb[k]);
-                }
-                raw_i[k] += __popc(rm);
-            }
-            V[c][lane] = val;
-            if (lane == 0) R[c] = rm;
-        }
-        __syncthreads();
-        // B: the chains
-        if (warp == 0) {
-            const uint32_t c = lane, r = c >> 1, h = c & 1;
-            const uint32_t rm = R[c];
-            const double *vc = V[c];
-            double *oc = reinterpret_cast<double *>(O[r]) + h;
-            if (rm == 0) {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    pred = __dadd_rn(pred, vc[i]);
-                    oc[2 * i] = pred;
-                }
-            } else {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    const double x = vc[i];
-                    pred = ((rm >> i) & 1) ? x : __dadd_rn(pred, x);
-                    oc[2 * i] = pred;
-                }
-            }
-        }
-        __syncthreads();
-        // C: store the tile (row r: 32 amplitudes = 512 B)
-        for (uint32_t i = threadIdx.x; i < rows * 32; i += blockDim.x) {
-            const uint32_t r = i >> 5, e = i & 31;
-            const uint64_t s = slot0 + r;
-            // an invalid chunk (len == 0: its index walk failed) decodes to zeros
-            __stcs(win + s * N + e0 + e, O[r][e]);
-        }
-        __syncthreads();
-    }
-#pragma unroll
-    for (uint32_t k = 0; k < kDecChainsPerWarp; ++k) {
-        const uint32_t c = warp + 8 * k, r = c >> 1, h = c & 1;
-        if (live[k] && lane == 0) {
-            const DecIdx &d = idx[slot0 + r];
-            const uint64_t chunk = slot_chunk ? slot_chunk[slot0 + r] : slot0 + r;
-            if (raw_i[k] > d.raw_count) dev_fail(status, QZS_RAW_UNDER, chunk);
-            else if (h == 1 && raw_i[k] != d.raw_count) dev_fail(status, QZS_RAW_UNUSED, chunk);
-        }
-    }
-}
-
 // Lossy decode (codec.cpp:217-249): thread = (slot, half).  WIDE: a launch
 // with fewer chunks than one CTA row set uses wide tiles (tile_width).
 template <bool WIDE>
@@ -1001,10 +871,96 @@ __device__ __forceinline__ uint8_t *scratch_half(uint8_t *scratch, const CodecGe
     return scratch + (2 * slot + h) * g.half_stride;
 }
 
+constexpr uint32_t kEncThreads = 4 * kSlotsPerCta;
+
+__device__ __forceinline__ void sts16(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared.u16 [%0], %1;\n" ::"r"(addr), "h"(static_cast<unsigned short>(v)) : "memory");
+}
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// The lossy encoder's per-stream RLE state: rle_step's state machine with the
+// tile's pairs staged in shared memory (byte address sbase, n staged so far)
+// and the hold flag folded into the 255-split limit (lim = ~0 while the
+// imaginary half's first run is held back).
+struct RleT {
+    uint32_t sbase, n;    // staging buffer (shared address), pairs staged this tile
+    uint32_t np0;         // pairs of earlier tiles
+    uint32_t cur, cnt, lim;
+    uint32_t head_byte, head_len;
+};
+
+__device__ __forceinline__ void rlet_start(RleT &s, uint32_t hold) {
+    s.sbase = 0;
+    s.n = 0;
+    s.np0 = 0;
+    s.cur = 0x100;
+    s.cnt = 0;
+    s.lim = hold ? ~0u : 255u;
+    s.head_byte = 0;
+    s.head_len = 0;
+}
+
+__device__ __forceinline__ void rlet_step(RleT &s, uint32_t x) {
+    const bool diff = x != s.cur;
+    if (diff && s.lim == ~0u && s.cnt) {
+        // the imaginary half's first run closes: it is the head (once per half)
+        s.head_byte = s.cur;
+        s.head_len = s.cnt;
+        s.lim = 255u;
+        s.cnt = 0;
+    }
+    const uint32_t c1 = s.cnt + 1;
+    const bool emit = diff ? s.cnt != 0 : c1 == s.lim;
+    const uint32_t val = s.cur | ((diff ? s.cnt : 255u) << 8);
+    if (emit) sts16(s.sbase + 2 * s.n++, val);
+    s.cnt = diff ? 1u : (emit ? 0u : c1);
+    s.cur = x;
+}
+
+__device__ __forceinline__ void rlet_step_n(RleT &s, uint32_t x, uint32_t n) {
+    if (n == 0) return;
+    if (x != s.cur) {
+        rlet_step(s, x);
+        --n;
+    }
+    if (s.lim == ~0u) {
+        s.cnt += n;
+        return;
+    }
+    uint32_t tot = s.cnt + n;
+    while (tot >= 255) {
+        sts16(s.sbase + 2 * s.n++, x | (255u << 8));
+        tot -= 255;
+    }
+    s.cnt = tot;
+}
+
+// Close a half (rle_close for the staged state; the imaginary half's last
+// pair goes straight to the scratch stream out).
+__device__ __forceinline__ void rlet_close(RleT &s, uint32_t h, EncHalf &m, int k, uint16_t *out) {
+    uint32_t np = s.np0 + s.n;
+    if (h == 0) {
+        m.edge_byte[k] = uint8_t(s.cur);
+        m.edge_len[k] = s.cnt;
+    } else {
+        if (s.lim == ~0u) {
+            s.head_byte = s.cur;
+            s.head_len = s.cnt;
+        } else if (s.cnt > 0) {
+            out[np++] = uint16_t(s.cur | (s.cnt << 8));
+        }
+        m.edge_byte[k] = uint8_t(s.head_byte);
+        m.edge_len[k] = s.head_len;
+    }
+    m.npairs[k] = np;
+}
+
 // Lossy encode (codec.cpp:121-168).  CTA = kSlotsPerCta chunks, 4 warps:
 //  * warps 0-1, thread = (slot, half): the sequential quantiser chain and the
-//    RLE state machines of the half's two byte planes, emitting pairs into a
-//    shared-memory staging buffer per stream;
+//    RLE state machines of the half's two byte planes, staging the pairs in
+//    shared memory;
 //  * warps 2-3: flush the previous tile's staged pairs to the scratch streams
 //    (each stream's new pairs as one contiguous, coalesced warp store);
 //  * all 4 warps: cp.async the next tile ([32 chunks x te] amplitudes,
@@ -1020,8 +976,8 @@ __device__ __forceinline__ uint8_t *scratch_half(uint8_t *scratch, const CodecGe
 // path (the reference's division and std::round).  rec = pred + k * 2eb
 // equals reconstruct(pred, code, eb) = pred + (code * 2.0) * eb exactly
 // (multiplying by 2 commutes with rounding); k is never -0.
-constexpr uint32_t kEncThreads = 4 * kSlotsPerCta;
-
+// FORCED: the launch carries forced-raw indices (the basis-state init only).
+template <bool FORCED>
 __global__ void __launch_bounds__(kEncThreads) k_enc_lossy(
     const double2 *__restrict__ win, uint64_t nslots, CodecGeom g,
     const uint64_t *__restrict__ forced, uint32_t nforced, uint8_t *__restrict__ scratch,
@@ -1042,15 +998,18 @@ __global__ void __launch_bounds__(kEncThreads) k_enc_lossy(
     // stream q = 4 r + 2 h + plane; its staging slice in buffer b
     auto stage = [&](int b, uint32_t q) { return pairs + b * kEncPairWords + q * pcap; };
     uint8_t *base = scratch_half(scratch, g, active ? s : 0, h);
-    RleS lo, hi;
-    rle_start(lo, stage(0, 4 * r + 2 * h), h);
-    rle_start(hi, stage(0, 4 * r + 2 * h + 1), h);
+    RleT lo, hi;
+    rlet_start(lo, h);
+    rlet_start(hi, h);
     double *raws = reinterpret_cast<double *>(base + 2 * g.scap);
     uint32_t nraw = 0;
     // forced raw cursor (sorted flat indices, codec.cpp:124-129)
     uint32_t fc = 0;
-    while (active && fc < nforced && forced[fc] < h * N) ++fc;
-    uint64_t next_forced = fc < nforced ? forced[fc] : ~uint64_t(0);
+    uint64_t next_forced = ~uint64_t(0);
+    if (FORCED) {
+        while (active && fc < nforced && forced[fc] < h * N) ++fc;
+        next_forced = fc < nforced ? forced[fc] : ~uint64_t(0);
+    }
     const double eb = g.eb, twoeb = g.twoeb, inv = g.inv2eb;
     const double kRne = 6755399441055744.0;   // 1.5 * 2^52
     const double thr = __dmul_rn(0.99, eb);
@@ -1073,6 +1032,7 @@ __global__ void __launch_bounds__(kEncThreads) k_enc_lossy(
         const uint32_t *info = sinfo + b * 2 * 4 * kSlotsPerCta;
         for (uint32_t q = fw; q < 4 * rows; q += 2) {
             const uint32_t start = info[q], cnt = info[4 * kSlotsPerCta + q];
+            if (cnt == 0) continue;
             uint16_t *out = reinterpret_cast<uint16_t *>(scratch_half(scratch, g, slot0 + (q >> 2), (q >> 1) & 1) +
                                                          (q & 1) * g.scap) + start;
             const uint16_t *src = stage(b, q);
@@ -1090,27 +1050,30 @@ __global__ void __launch_bounds__(kEncThreads) k_enc_lossy(
         } else if (active) {
             const double *rowc = reinterpret_cast<const double *>(tile(ti) + r * (te + 1)) + h;
             const uint64_t tile0 = h * N + ti * te;
-            lo.dst = stage(pb, 4 * r + 2 * h);
-            hi.dst = stage(pb, 4 * r + 2 * h + 1);
-            lo.np0 = lo.np;
-            hi.np0 = hi.np;
+            lo.np0 += lo.n;
+            hi.np0 += hi.n;
+            lo.n = hi.n = 0;
+            lo.sbase = smem_addr(stage(pb, 4 * r + 2 * h));
+            hi.sbase = smem_addr(stage(pb, 4 * r + 2 * h + 1));
             // fast-forward: every value of the tile within 0.99 eb of the
             // predictor quantises to code 0 with the predictor fixed (rec =
             // pred + (+0), a -0 predictor becomes +0): two runs of byte 0
-            bool ff = next_forced >= tile0 + te && fabs(__dsub_rn(rowc[0], pred)) < thr;
+            bool ff = (!FORCED || next_forced >= tile0 + te) && fabs(__dsub_rn(rowc[0], pred)) < thr;
             if (ff) {
                 bool all = true;
 #pragma unroll 8
                 for (uint32_t e = 1; e < te; ++e) all &= fabs(__dsub_rn(rowc[2 * e], pred)) < thr;
                 ff = all;
                 if (ff) {
-                    rle_step_n(lo, 0, te);
-                    rle_step_n(hi, 0, te);
+                    rlet_step_n(lo, 0, te);
+                    rlet_step_n(hi, 0, te);
                     pred = __dadd_rn(pred, 0.0);
                 }
             }
             if (!ff) {
-                uint32_t fr = next_forced - tile0 < te ? uint32_t(next_forced - tile0) : ~0u;
+                uint32_t fr = ~0u;
+                if (FORCED) fr = next_forced - tile0 < te ? uint32_t(next_forced - tile0) : ~0u;
+#pragma unroll 4
                 for (uint32_t e = 0; e < te; ++e) {
                     const double v = rowc[2 * e];
                     const double d = __dsub_rn(v, pred);
@@ -1118,8 +1081,8 @@ __global__ void __launch_bounds__(kEncThreads) k_enc_lossy(
                     double q = __dsub_rn(__dadd_rn(t, kRne), kRne);
                     const double f = __dsub_rn(t, q);
                     bool raw = false;
-                    if (!(fabs(f) < 0.4999999 && fabs(t) < 32767.0) || e == fr) {
-                        if (e == fr) {
+                    if (!(fabs(f) < 0.4999999 && fabs(t) < 32767.0) || (FORCED && e == fr)) {
+                        if (FORCED && e == fr) {
                             raw = true;
                             const uint64_t flat = tile0 + e;
                             do { ++fc; } while (fc < nforced && forced[fc] == flat);
@@ -1137,30 +1100,24 @@ __global__ void __launch_bounds__(kEncThreads) k_enc_lossy(
                     pred = raw ? v : rec;
                     const uint32_t z = raw ? 0xFFFFu : zigzag16(int32_t(q));
                     if (raw) raws[nraw++] = v;
-                    rle_step(lo, z & 0xffu);
-                    rle_step(hi, z >> 8);
+                    rlet_step(lo, z & 0xffu);
+                    rlet_step(hi, z >> 8);
                 }
             }
             uint32_t *info = sinfo + pb * 2 * 4 * kSlotsPerCta;
             info[4 * r + 2 * h] = lo.np0;
             info[4 * r + 2 * h + 1] = hi.np0;
-            info[4 * kSlotsPerCta + 4 * r + 2 * h] = lo.np - lo.np0;
-            info[4 * kSlotsPerCta + 4 * r + 2 * h + 1] = hi.np - hi.np0;
+            info[4 * kSlotsPerCta + 4 * r + 2 * h] = lo.n;
+            info[4 * kSlotsPerCta + 4 * r + 2 * h + 1] = hi.n;
         }
         __syncthreads();  // tile and staging buffers are reused next round
     }
     cp_async_wait<0>();
     if (!chain && ntiles) flush(int((ntiles - 1) & 1));
     if (active) {
-        // the closing pair goes straight to the scratch stream
-        uint16_t *slo = reinterpret_cast<uint16_t *>(base), *shi = reinterpret_cast<uint16_t *>(base + g.scap);
-        lo.dst = slo;
-        lo.np0 = 0;
-        hi.dst = shi;
-        hi.np0 = 0;
         EncHalf &m = meta[2 * s + h];
-        rle_close(lo, h, m, 0);
-        rle_close(hi, h, m, 1);
+        rlet_close(lo, h, m, 0, reinterpret_cast<uint16_t *>(base));
+        rlet_close(hi, h, m, 1, reinterpret_cast<uint16_t *>(base + g.scap));
         m.nraw = nraw;
     }
 }
@@ -1515,14 +1472,15 @@ void launch_decode(const uint8_t *arena, const DecIdx *idx, const uint64_t *slot
                    cudaStream_t s, const uint32_t *cond, bool sparse) {
     const unsigned grid = grid_for(nslots, kSlotsPerCta);
     const double dense = 16.0 * double(g.N) * double(nslots);
-    KProfScope prof(s, cond ? "replay_decode" : (g.lossy && g.N >= 32 && !sparse) ? "k_dec_lossy_coop"
+    KProfScope prof(s, cond ? "replay_decode" : (g.lossy && g.N >= 32 && !sparse) ? "k_dec_lossy_warp"
                                             : g.lossy ? "k_dec_lossy" : "k_dec_lossless", 0, dense);
     // dense payloads: warp per chunk-half (parallel RLE expansion, serial
     // predictor chain only); a store known to be mostly zero runs (right
     // after init): thread per chunk-half with run fills
     if (g.lossy && g.N >= 32 && !sparse) {
-        k_dec_lossy_coop<<<grid_for(nslots, kDecSlots), 256, 0, s>>>(arena, idx, slot_chunk, nslots, g, win,
-                                                                      status, cond);
+        // warp per (slot, half): 4 slots per 256-thread CTA
+        k_dec_lossy_warp<<<grid_for(nslots, 4), 256, 0, s>>>(arena, idx, slot_chunk, nslots, g, win,
+                                                              status, cond);
     } else if (g.lossy && nslots < uint64_t(kSlotsPerCta))
         k_dec_lossy<true><<<grid, 2 * kSlotsPerCta, 0, s>>>(arena, idx, slot_chunk, nslots, g, win,
                                                              status, cond);
@@ -1540,11 +1498,17 @@ void launch_encode(const double2 *win, uint64_t nslots, const CodecGeom &g,
     KProfScope prof(s, g.lossy ? "k_enc_lossy" : "k_enc_lossless", 0, 16.0 * double(g.N) * double(nslots));
     static bool attr = false;
     if (!attr) {
-        QZ_CUDA(cudaFuncSetAttribute(k_enc_lossy, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kEncSmem)));
+        QZ_CUDA(cudaFuncSetAttribute(k_enc_lossy<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(kEncSmem)));
+        QZ_CUDA(cudaFuncSetAttribute(k_enc_lossy<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(kEncSmem)));
         attr = true;
     }
-    if (g.lossy)
-        k_enc_lossy<<<grid_for(nslots, kSlotsPerCta), kEncThreads, kEncSmem, s>>>(
+    if (g.lossy && nforced)
+        k_enc_lossy<true><<<grid_for(nslots, kSlotsPerCta), kEncThreads, kEncSmem, s>>>(
+            win, nslots, g, forced, nforced, scratch, meta);
+    else if (g.lossy)
+        k_enc_lossy<false><<<grid_for(nslots, kSlotsPerCta), kEncThreads, kEncSmem, s>>>(
             win, nslots, g, forced, nforced, scratch, meta);
     else
         k_enc_lossless<<<grid_for(nslots, kLLSlots), 16 * kLLSlots, 0, s>>>(win, nslots, g,

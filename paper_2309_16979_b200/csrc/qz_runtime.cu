@@ -119,6 +119,16 @@ __global__ void k_partials(const double2 *win, uint64_t nslots, uint64_t N, cons
     }
 }
 
+// a *= scale for std::complex<double> and a real scale: componentwise
+// products (complex x real, no cross terms), pipeline.cpp:283
+__global__ void k_scale(double2 *buf, uint64_t n, double scale) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const double2 a = buf[i];
+        buf[i] = make_double2(__dmul_rn(a.x, scale), __dmul_rn(a.y, scale));
+    }
+}
+
 __global__ void k_basis(double2 *buf, uint64_t n) {
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < n) buf[i] = make_double2(i == 0 ? 1.0 : 0.0, 0.0);
@@ -258,7 +268,8 @@ void sim_alloc(qzc_sim *sim) {
     }
     if (wa & (wa - 1)) wa = uint64_t(1) << log2u(wa);
     // at least one whole batch (2^m amplitudes) and two chunk slots
-    const uint64_t batch_amps = uint64_t(1) << std::min(sim->m, sim->n);
+    // (skip_reencode: size for one stage over the whole state)
+    const uint64_t batch_amps = uint64_t(1) << (sim->cfg.skip_reencode ? sim->n : std::min(sim->m, sim->n));
     wa = std::max<uint64_t>(std::min<uint64_t>(wa, state_amps), std::max<uint64_t>(batch_amps, 2 * sim->N));
     // two half-size windows on two streams when the window holds >= 2
     // batches: decode / gate passes / encode of neighbouring windows overlap
@@ -344,6 +355,59 @@ void run_window_passes(qzc_sim *sim, Window &W, const DevPlan &dp, const DevPlan
         ++ctx->launches;
     }
     if (res != W.amps.as<double2>()) std::swap(W.amps, W.alt);   // stream-ordered: later kernels see the swap
+}
+
+// PipelineConfig::renormalize (pipeline.cpp:278-288): norm = store_norm —
+// the reference's Kahan sum over |a|^2 in chunk order (pipeline.cpp:119-126),
+// a sequential compensated recurrence, so it runs on the host over decoded
+// windows streamed from the device (its bits decide the scale and hence the
+// payload bytes) — then every chunk is decoded, scaled on the device and
+// re-encoded in chunk order (store_chunk's footprint accounting order).
+void renormalize(qzc_sim *sim) {
+    qzc_context *ctx = sim->ctx;
+    cudaStream_t s = ctx->stream;
+    Window &w = sim->win;
+    const uint64_t per = std::max<uint64_t>(1, w.slots);
+    const uint64_t mask = (uint64_t(1) << (sim->n - sim->c)) - 1;
+    std::vector<double2> host(per * sim->N);
+    double sum = 0.0, comp = 0.0;
+    for (uint64_t f = 0; f < sim->nchunks; f += per) {
+        const uint64_t k = std::min(per, sim->nchunks - f);
+        launch_slot_chunks(w.slot_chunk.as<uint64_t>(), k, f, 0, mask, 0, s);
+        decode_window(ctx, w, sim->geom, k, w.slot_chunk.as<uint64_t>(), sim->arena_ptr(sim->cur),
+                      sim->table(sim->cur), ctx->launches, s, sim->sparse_store);
+        ctx->check_status();
+        QZ_CUDA(cudaMemcpyAsync(host.data(), w.amps.p, 16 * k * sim->N, cudaMemcpyDeviceToHost, s));
+        QZ_CUDA(cudaStreamSynchronize(s));
+        for (uint64_t i = 0; i < k * sim->N; ++i) {
+            const double x = host[i].x * host[i].x + host[i].y * host[i].y;   // std::norm
+            const double y = x - comp, t = sum + y;
+            comp = (t - sum) - y;
+            sum = t;
+        }
+    }
+    if (!(sum > 0.0)) return;
+    const double scale = 1.0 / std::sqrt(sum);
+    const int a = sim->cur, b = 1 - a;
+    QZ_CUDA(cudaMemsetAsync(sim->used_ptr(b), 0, 8, s));
+    for (uint64_t f = 0; f < sim->nchunks; f += per) {
+        const uint64_t k = std::min(per, sim->nchunks - f);
+        launch_slot_chunks(w.slot_chunk.as<uint64_t>(), k, f, 0, mask, 0, s);
+        decode_window(ctx, w, sim->geom, k, w.slot_chunk.as<uint64_t>(), sim->arena_ptr(a), sim->table(a),
+                      ctx->launches, s, sim->sparse_store);
+        k_scale<<<(unsigned)std::min<uint64_t>(ceil_div(k * sim->N, 256), kNumSMs * 16), 256, 0, s>>>(
+            w.amps.as<double2>(), k * sim->N, scale);
+        QZ_CHECK_LAUNCH();
+        ++ctx->launches;
+        encode_window(ctx, w, sim->geom, k, w.slot_chunk.as<uint64_t>(), nullptr, 0, sim->arena_ptr(b),
+                      sim->used_ptr(b), sim->arena_cap, sim->table(b), sim->len[a].as<uint32_t>(),
+                      sim->acct.as<int64_t>(), ctx->launches, s);
+    }
+    ctx->check_status();
+    sim->cur = b;
+    sim->sparse_store = false;
+    sim->stats.chunk_decompress_count += 2 * sim->nchunks;
+    sim->stats.chunk_recompress_count += sim->nchunks;
 }
 
 } // namespace
@@ -947,7 +1011,10 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
     qzc_context *ctx = sim->ctx;
     QZ_CUDA(cudaSetDevice(ctx->device));
     if (!sim->initialized) throw Failure(QZC_ESTORE, "store not initialised");
-    const std::vector<Stage> stages = plan_stages(sim->n, gates, ngates, sim->c, sim->m);
+    // non-parity fast mode: the whole circuit as one stage when the dense
+    // state fits the window (else the reference's stage semantics)
+    const bool one_stage = sim->cfg.skip_reencode && !sim->host_res && sim->win_amps >= (uint64_t(1) << sim->n);
+    const std::vector<Stage> stages = plan_stages(sim->n, gates, ngates, sim->c, one_stage ? sim->n : sim->m);
     cudaStream_t s = ctx->stream;
     const uint32_t n = sim->n, c = sim->c;
     const uint64_t chunk_bits_mask = (uint64_t(1) << (n - c)) - 1;
@@ -1171,6 +1238,7 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
         sim->stats.chunk_recompress_count += sim->nchunks;
     }
     QZ_CUDA(cudaStreamSynchronize(s));
+    if (sim->cfg.renormalize) renormalize(sim);
     sim->stats.wall_seconds += now_s() - t0;
     dump_debug_counters();
     sim->stats.kernel_launches += ctx->launches - launches0;

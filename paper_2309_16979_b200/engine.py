@@ -339,19 +339,21 @@ class Simulator:
 
     def __init__(self, eng: Engine, n: int, c: int, m: int, eb: float, window_amps: int = 0,
                  fuse=True, init: bool = True, residency: str = "hbm",
-                 force_replay: bool = False):
+                 force_replay: bool = False, skip_reencode: bool = False):
         """fuse: True = fused passes with relaxed +0-safe diagonal units
         (default), "checked" = also checked diagonal units (out-of-place
         passes, per-pass replay), "strict" = every gate qubit in the tile,
         False = one pass per gate.  force_replay: always take the strict
-        replay (test)."""
+        replay (test).  skip_reencode: NON-PARITY fast mode — one stage (one
+        codec round trip) per run when the dense state fits HBM."""
         self.eng, self.lib = eng, eng.lib
         self.n, self.c, self.m, self.eb = n, c, m, eb
         cfg = SimConfig(num_qubits=n, chunk_qubits=c, batch_qubits=m, error_bound=eb,
                         window_amps=window_amps, residency={"hbm": 0, "host": 1}[residency],
                         renormalize=0,
                         fuse_gates={"strict": 2, "checked": 3}.get(fuse, 1 if fuse else 0),
-                        debug_flags=1 if force_replay else 0)
+                        debug_flags=1 if force_replay else 0,
+                        skip_reencode=1 if skip_reencode else 0)
         h = C.c_void_p()
         _check(self.lib.qzc_sim_create(eng.h, C.byref(cfg), C.byref(h)))
         self.h = h

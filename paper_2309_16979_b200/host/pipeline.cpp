@@ -31,71 +31,40 @@ void check_config(const PipelineConfig &cfg, uint32_t num_qubits) {
     if (num_qubits == 0) throw Error("circuit has no qubits");
 }
 
-struct Sim {
-    qzc_sim *h = nullptr;
-    ~Sim() {
-        if (h) qzc_sim_destroy(h);
-    }
-};
-
 } // namespace
 
 std::pair<ChunkStore, SimulationReport> run(const Circuit &circuit, const PipelineConfig &cfg) {
     check_config(cfg, circuit.num_qubits);
-    if (const auto errs = validate(circuit); !errs.empty()) throw Error("invalid circuit: " + errs.front());
     const uint32_t n = circuit.num_qubits, c = cfg.chunk_qubits;
+    // plan() validates the circuit and the (c, m) preconditions (PlanError)
     const ExecutionPlan p = plan(circuit, c, cfg.batch_qubits);
     if (c < 1 || c > n)
         throw StoreError("chunk qubits must satisfy 1 <= c <= n, got c=" + std::to_string(c) +
                          ", n=" + std::to_string(n));
     if (n > ChunkStore::kMaxQubits) throw StoreError("qubit count exceeds configured address width (40)");
 
-    qzc_context *ctx = b200::ctx();
     qzc_sim_config sc{};
     sc.num_qubits = n;
     sc.chunk_qubits = c;
     sc.batch_qubits = cfg.batch_qubits;
     sc.error_bound = cfg.error_bound;
     sc.fuse_gates = 1;
-    Sim sim;
-    b200::check(qzc_sim_create(ctx, &sc, &sim.h));
-    b200::check(qzc_sim_init_basis(sim.h));
+    sc.renormalize = cfg.renormalize ? 1u : 0u;
+    qzc_sim *h = nullptr;
+    b200::check(qzc_sim_create(b200::ctx(), &sc, &h));
+    // the store owns the engine simulator from here on (freed on any throw)
+    ChunkStore store = ChunkStore::adopt(h, n, c, cfg.error_bound);
+    b200::check(qzc_sim_init_basis(h));
     const std::vector<qzc_gate> abi = b200::to_abi(circuit.gates);
     Timer wall;
-    try {
-        b200::check(qzc_sim_run(sim.h, abi.data(), abi.size()));
-    } catch (const Error &e) {
-        throw Error(e.what());
-    }
-    double run_seconds = wall.seconds();
+    b200::check(qzc_sim_run(h, abi.data(), abi.size()));
+    const double run_seconds = wall.seconds();
 
     qzc_sim_stats st{};
-    b200::check(qzc_sim_stats_get(sim.h, &st));
-    uint64_t total = 0;
-    b200::check(qzc_sim_payload_bytes(sim.h, &total));
-    const uint64_t nchunks = uint64_t(1) << (n - c);
-    std::vector<uint8_t> payloads(total + 1);
-    std::vector<uint32_t> sizes(nchunks), crcs(nchunks);
-    b200::check(qzc_sim_export(sim.h, payloads.data(), payloads.size(), sizes.data(), crcs.data()));
-    ChunkStore store = ChunkStore::from_payloads(n, c, cfg.error_bound, payloads.data(), sizes.data(),
-                                                 crcs.data(), st.peak_bytes);
-
+    b200::check(qzc_sim_stats_get(h, &st));
     SimulationReport rep;
     rep.config = cfg;
     for (const Stage &s : p.stages) rep.stage_batch_counts.push_back(batch_count(s, n, c));
-    if (cfg.renormalize) {
-        Timer t;
-        const double nn = store_norm(store);
-        if (nn > 0.0) {
-            const double scale = 1.0 / std::sqrt(nn);
-            for (uint64_t ci = 0; ci < store.chunk_count(); ++ci) {
-                std::vector<Amplitude> v = store.load_chunk(ci);
-                for (Amplitude &a : v) a *= scale;
-                store.store_chunk(ci, v);
-            }
-        }
-        run_seconds += t.seconds();
-    }
     rep.wall_seconds = run_seconds;
     rep.phases.decompress = st.decode_seconds;
     rep.phases.kernel = st.gate_seconds;
@@ -105,15 +74,13 @@ std::pair<ChunkStore, SimulationReport> run(const Circuit &circuit, const Pipeli
     rep.transfer.kernel_seconds = st.gate_seconds;
     rep.transfer.h2d_seconds = st.h2d_seconds;
     rep.transfer.d2h_seconds = st.d2h_seconds;
-    rep.transfer.bytes_moved = 0;  // the store never leaves HBM during the run
+    rep.transfer.bytes_moved = st.h2d_bytes + st.d2h_bytes;
     rep.overlap_efficiency = rep.wall_seconds > 0 ? rep.phases.kernel / rep.wall_seconds : 0.0;
     rep.transient_peak_bytes = 0;  // no host-side decompressed batches on this path
     rep.chunk_decompress_count = st.chunk_decompress_count;
     rep.chunk_recompress_count = st.chunk_recompress_count;
     rep.footprint = store.footprint();
-    double norm = 0.0;
-    b200::check(qzc_sim_norm(sim.h, &norm));
-    rep.norm = cfg.renormalize ? store_norm(store) : norm;
+    rep.norm = store_norm(store);
     rep.digest = store.digest();
     if (n <= cfg.oracle_limit && n <= kOracleLimit) {
         const DenseState ref = simulate_dense(circuit);
@@ -124,6 +91,9 @@ std::pair<ChunkStore, SimulationReport> run(const Circuit &circuit, const Pipeli
 
 void host_apply_batch(ChunkStore &store, const Stage &stage, const BatchDescriptor &batch,
                       const HostPhaseClocks &clocks) {
+    // the batch's chunks decoded into one device buffer, the stage's remapped
+    // gates applied there, the chunks re-encoded (device codec and kernels;
+    // the same bytes as the batch inside qzc_sim_run)
     const uint64_t len = store.chunk_size();
     std::vector<Amplitude> buf(batch.chunk_indices.size() * len);
     {
@@ -150,25 +120,10 @@ void host_apply_batch(ChunkStore &store, const Stage &stage, const BatchDescript
 }
 
 double store_norm(const ChunkStore &store) {
-    // one batched GPU decode of every chunk, then the reference's compensated
-    // sum in chunk order (pipeline.cpp:119-126)
-    const uint64_t count = store.chunk_count(), len = store.chunk_size();
-    std::vector<uint8_t> blob;
-    std::vector<uint64_t> offs(count);
-    std::vector<uint32_t> sizes(count), crcs(count);
-    for (uint64_t i = 0; i < count; ++i) {
-        const CompressedChunk &c = store.chunk(i);
-        offs[i] = blob.size();
-        sizes[i] = static_cast<uint32_t>(c.payload.size());
-        crcs[i] = c.checksum;
-        blob.insert(blob.end(), c.payload.begin(), c.payload.end());
-    }
-    std::vector<Amplitude> all(count * len);
-    b200::check(qzc_decompress_host(b200::ctx(), blob.data(), offs.data(), sizes.data(), crcs.data(), count,
-                                    len, 0, reinterpret_cast<double *>(all.data())));
-    KahanSum acc;
-    for (const Amplitude &a : all) acc.add(std::norm(a));
-    return acc.sum;
+    // compensated sum over the decoded store, on the device (qzc_sim_norm)
+    double nn = 0.0;
+    b200::check(qzc_sim_norm(store.engine_store(), &nn));
+    return nn;
 }
 
 namespace {

@@ -162,3 +162,25 @@ def test_two_processes_torch_group_reference_digest(golden, tmp_path, key):
     res = json.loads(outs[0][0].strip().splitlines()[-1])
     assert res["digest"] == rec["digest"]
     assert res["exchanges"] >= 1 and res["bytes"] > 0
+
+
+def test_skip_reencode_fast_mode(engine):
+    """Non-parity fast mode: one stage per run when the state
+    fits HBM.  At m = n it IS the reference's plan (same bytes); at m < n it
+    makes fewer lossy round trips (one stage instead of several) and stays
+    within the error bound's fidelity against the uncompressed run."""
+    n, c, eb = 20, 12, 1e-7
+    g = CI.supremacy(n, depth=6)
+    par = engine.simulator(n, c, n, eb)
+    par.run(g)
+    fast = engine.simulator(n, c, n, eb, skip_reencode=True)
+    fast.run(g)
+    assert fast.digest() == par.digest()
+    multi = engine.simulator(n, c, 16, eb)
+    multi.run(g)
+    fast16 = engine.simulator(n, c, 16, eb, skip_reencode=True)
+    fast16.run(g)
+    assert multi.stats()["stages"] > 1 and fast16.stats()["stages"] == 1
+    dense = engine.dense_state(n, g)
+    assert fast16.fidelity(dense) > 0.99999 and multi.fidelity(dense) > 0.99999
+    dense.free()

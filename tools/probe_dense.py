@@ -14,12 +14,15 @@ ap.add_argument("--m", type=int, default=30)
 ap.add_argument("--eb", type=float, default=1e-7)
 ap.add_argument("--depth", type=int, default=20)
 ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--kprof", action="store_true", help="per-kernel CUDA-event totals of the last rep")
 a = ap.parse_args()
 eng = Engine()
 kw = {"depth": a.depth} if a.circuit == "supremacy" else {}
 gates = circuits.make(a.circuit, a.n, **kw)
 sim = eng.simulator(a.n, a.c, a.m, a.eb, init=False)
 for rep in range(a.reps):
+    if a.kprof and rep == a.reps - 1:
+        eng.kprof_enable(True)
     t0 = time.perf_counter()
     sim.init_basis()
     sim.run(gates)
@@ -30,3 +33,13 @@ for rep in range(a.reps):
           f"dec {1e3*st['decode_seconds']:.2f} gates {1e3*st['gate_seconds']:.2f} "
           f"enc {1e3*st['encode_seconds']:.2f} ms payload {sim.payload_bytes()/1e9:.3f} GB "
           f"ratio {st['ratio']:.3f} digest {sim.digest():016x}", flush=True)
+if a.kprof:
+    tot = {}
+    for r in eng.kprof_read():
+        k = r["name"]
+        t = tot.setdefault(k, [0, 0.0, 0.0])
+        t[0] += 1
+        t[1] += r["seconds"]
+        t[2] += r["bytes"]
+    for k, (n, sec, b) in sorted(tot.items(), key=lambda kv: -kv[1][1]):
+        print(f"  {k:24s} launches {n:5d}  {1e3*sec:9.2f} ms  dense {b/1e9:8.2f} GB", flush=True)
