@@ -16,11 +16,12 @@ HDRS := $(wildcard $(SRC)/*.cuh) include/qzcuda.h
 OBJS := $(patsubst $(SRC)/%.cu,$(OBJ)/%.o,$(CU_SRCS)) $(patsubst $(SRC)/%.cpp,$(OBJ)/%.o,$(CPP_SRCS))
 
 HOSTLIB := $(PKG)/lib/libqzsim_b200.so
+TOOLS := build/tools/bench_transfer
 HOST_SRCS := $(wildcard $(PKG)/host/*.cpp)
 HOST_OBJS := $(patsubst $(PKG)/host/%.cpp,$(OBJ)/host_%.o,$(HOST_SRCS))
 QZSIM_HDRS := $(wildcard include/qzsim/*.hpp) $(wildcard $(PKG)/host/*.hpp)
 
-all: $(LIB) $(HOSTLIB) oracle
+all: $(LIB) $(HOSTLIB) oracle $(TOOLS)
 
 $(OBJ)/host_%.o: $(PKG)/host/%.cpp $(QZSIM_HDRS) include/qzcuda.h
 	@mkdir -p $(OBJ)
@@ -43,6 +44,13 @@ $(LIB): $(OBJS)
 	@mkdir -p $(dir $@)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart
 
+# tools over the drop-in (paper Table 1: tools/cpp/bench_transfer.cpp)
+build/tools/bench_transfer: tools/cpp/bench_transfer.cpp $(HOSTLIB) $(QZSIM_HDRS)
+	@mkdir -p build/tools
+	g++ -std=gnu++20 -O2 -Iinclude $< -o $@ -L$(PKG)/lib -lqzsim_b200 -lqzcuda -Wl,-rpath,'$$ORIGIN/../../$(PKG)/lib'
+
+tools: $(TOOLS)
+
 oracle:
 	$(MAKE) -C oracle all
 
@@ -52,4 +60,4 @@ ref:
 clean:
 	rm -rf build $(PKG)/lib oracle/liboracle.so
 
-.PHONY: all oracle ref clean
+.PHONY: all oracle ref clean tools

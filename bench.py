@@ -609,7 +609,9 @@ def run_sharded(args, eng, gates, dist, rank, world, local):
     if 1 << g != world:
         raise SystemExit("--mode shard needs a power-of-two number of ranks")
     grp = S.TorchGroup(dist, device=f"cuda:{local}")
-    run = S.ShardedRun(eng, args.n, args.c, args.m, args.eb, g, [rank], grp)
+    # each rank's local register has n - g qubits: the batch window shrinks to fit
+    m = min(args.m, args.n - g)
+    run = S.ShardedRun(eng, args.n, args.c, m, args.eb, g, [rank], grp)
     for _ in range(args.warmup):
         run.init_basis()
         run.run(gates)
@@ -633,8 +635,7 @@ def run_sharded(args, eng, gates, dist, rank, world, local):
         t0 = time.perf_counter()
         run.init_basis()
         run.run(gates)
-        recs = run.local_records()
-        d2h = sum(len(p) for _, _, p in recs)
+        d2h = sum(len(blob) + sizes.nbytes + crcs.nbytes for blob, sizes, crcs in run.local_export().values())
         dist.barrier()
         e2e.append(time.perf_counter() - t0)
     te = torch.tensor([statistics.median(e2e)], dtype=torch.float64, device=f"cuda:{local}")
@@ -646,7 +647,7 @@ def run_sharded(args, eng, gates, dist, rank, world, local):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * tmax / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": dict(workload_config(args), parallelism=f"shard{world}", gates=len(gates),
+            "config": dict(workload_config(args, m=m), parallelism=f"shard{world}", gates=len(gates),
                            transport="NCCL send/recv of compressed chunk records, device to device"),
             "digest": f"{digest:016x}", "exchanges_per_step": (run.exchanges - ex0) / args.steps,
             "exchanged_bytes_per_step": (run.exchanged_bytes - b0) // max(1, args.steps),

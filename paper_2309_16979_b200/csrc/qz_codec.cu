@@ -769,7 +769,8 @@ constexpr uint32_t kEncTileDoubles2 = kSlotsPerCta * (kTileElems + 1);
 // buffered, plus per-stream (global start, count) words
 constexpr uint32_t kEncPairWords = kSlotsPerCta * (kTileElems + 2) * 4;
 constexpr size_t kEncSmem = sizeof(double2) * kEncTileDoubles2 * kEncStages +
-                            2 * sizeof(uint16_t) * kEncPairWords + 2 * sizeof(uint32_t) * 2 * 4 * kSlotsPerCta;
+                            2 * sizeof(uint16_t) * kEncPairWords + 2 * sizeof(uint32_t) * 2 * 4 * kSlotsPerCta +
+                            sizeof(uint16_t *) * 4 * kSlotsPerCta;
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
     const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
@@ -871,7 +872,8 @@ __device__ __forceinline__ uint8_t *scratch_half(uint8_t *scratch, const CodecGe
     return scratch + (2 * slot + h) * g.half_stride;
 }
 
-constexpr uint32_t kEncThreads = 4 * kSlotsPerCta;
+constexpr uint32_t kEncFlushWarps = 4;
+constexpr uint32_t kEncThreads = 2 * kSlotsPerCta + 32 * kEncFlushWarps;
 
 __device__ __forceinline__ void sts16(uint32_t addr, uint32_t v) {
     asm volatile("st.shared.u16 [%0], %1;\n" ::"r"(addr), "h"(static_cast<unsigned short>(v)) : "memory");
@@ -986,10 +988,14 @@ __global__ void __launch_bounds__(kEncThreads) k_enc_lossy(
     double2 *tiles = reinterpret_cast<double2 *>(enc_smem);
     uint16_t *pairs = reinterpret_cast<uint16_t *>(tiles + kEncTileDoubles2 * kEncStages);
     uint32_t *sinfo = reinterpret_cast<uint32_t *>(pairs + 2 * kEncPairWords);   // [2][start, count][4 * 32]
+    uint16_t **sout = reinterpret_cast<uint16_t **>(sinfo + 2 * 2 * 4 * kSlotsPerCta);   // stream q's scratch
     const bool chain = threadIdx.x < 2 * kSlotsPerCta;
     const uint32_t r = (threadIdx.x >> 1) & (kSlotsPerCta - 1), h = threadIdx.x & 1;
     const uint64_t slot0 = uint64_t(blockIdx.x) * kSlotsPerCta, s = slot0 + r;
     const uint32_t rows = uint32_t(umin64(kSlotsPerCta, nslots - slot0));
+    for (uint32_t q = threadIdx.x; q < 4 * rows; q += blockDim.x)
+        sout[q] = reinterpret_cast<uint16_t *>(scratch_half(scratch, g, slot0 + (q >> 2), (q >> 1) & 1) +
+                                               (q & 1) * g.scap);
     const bool active = chain && r < rows;
     const uint64_t N = g.N;
     const uint32_t te = tile_width(rows, N), lte = 31 - __clz(te);
@@ -1030,11 +1036,10 @@ __global__ void __launch_bounds__(kEncThreads) k_enc_lossy(
     auto flush = [&](int b) {
         const uint32_t lane = threadIdx.x & 31, fw = (threadIdx.x >> 5) - 2;
         const uint32_t *info = sinfo + b * 2 * 4 * kSlotsPerCta;
-        for (uint32_t q = fw; q < 4 * rows; q += 2) {
-            const uint32_t start = info[q], cnt = info[4 * kSlotsPerCta + q];
+        for (uint32_t q = fw; q < 4 * rows; q += kEncFlushWarps) {
+            const uint32_t cnt = info[4 * kSlotsPerCta + q];
             if (cnt == 0) continue;
-            uint16_t *out = reinterpret_cast<uint16_t *>(scratch_half(scratch, g, slot0 + (q >> 2), (q >> 1) & 1) +
-                                                         (q & 1) * g.scap) + start;
+            uint16_t *out = sout[q] + info[q];
             const uint16_t *src = stage(b, q);
             for (uint32_t i = lane; i < cnt; i += 32) out[i] = src[i];
         }

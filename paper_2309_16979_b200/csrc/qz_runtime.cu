@@ -232,6 +232,35 @@ uint32_t log2u(uint64_t x) {
     return r;
 }
 
+uint64_t host_ram() {
+    return uint64_t(sysconf(_SC_PHYS_PAGES)) * uint64_t(sysconf(_SC_PAGE_SIZE));
+}
+
+void alloc_host_arena(qzc_sim *sim, int i, uint64_t cap) {
+    if (sim->harena[i]) QZ_CUDA(cudaFreeHost(sim->harena[i]));
+    sim->harena[i] = sim->harena_dev[i] = nullptr;
+    void *h = nullptr, *d = nullptr;
+    QZ_CUDA(cudaHostAlloc(&h, cap + 64, cudaHostAllocMapped | cudaHostAllocPortable));
+    QZ_CUDA(cudaHostGetDevicePointer(&d, h, 0));
+    sim->harena[i] = static_cast<uint8_t *>(h);
+    sim->harena_dev[i] = static_cast<uint8_t *>(d);
+    sim->hcap[i] = cap;
+}
+
+// Output arena b overflowed (needed >= the failing allocation's end): give it
+// at least twice the room (bounded by the worst case and 40% of host RAM).
+// Returns false when it cannot grow.
+bool grow_host_arena(qzc_sim *sim, int b, uint64_t needed) {
+    const uint64_t worst = std::max<uint64_t>(sim->nchunks, 2) * payload_bound(sim->N, sim->eb) + 4096;
+    const uint64_t limit = std::min<uint64_t>(worst, host_ram() * 2 / 5);
+    const uint64_t want = std::min<uint64_t>(limit, std::max<uint64_t>(2 * sim->hcap[b], needed + needed / 2));
+    if (want <= sim->hcap[b]) return false;
+    QZ_CUDA(cudaDeviceSynchronize());
+    alloc_host_arena(sim, b, want);
+    sim->arena_cap = std::max(sim->hcap[0], sim->hcap[1]);
+    return true;
+}
+
 void sim_alloc(qzc_sim *sim) {
     qzc_context *ctx = sim->ctx;
     const uint64_t tbl_entries = std::max<uint64_t>(sim->nchunks, 2);
@@ -303,16 +332,16 @@ void sim_alloc(qzc_sim *sim) {
         throw Failure(QZC_ENOMEM, "not enough HBM for the compressed store");
     if (sim->host_res) {
         // page-locked, mapped host arenas (the store leaves HBM; windows
-        // stream their payloads through it).  Cap by 40% of host RAM each.
-        const uint64_t ram = uint64_t(sysconf(_SC_PHYS_PAGES)) * uint64_t(sysconf(_SC_PAGE_SIZE));
-        sim->arena_cap = std::min<uint64_t>(worst, ram * 2 / 5);
-        for (int i = 0; i < 2; ++i) {
-            void *h = nullptr, *d = nullptr;
-            QZ_CUDA(cudaHostAlloc(&h, sim->arena_cap + 64, cudaHostAllocMapped | cudaHostAllocPortable));
-            QZ_CUDA(cudaHostGetDevicePointer(&d, h, 0));
-            sim->harena[i] = static_cast<uint8_t *>(h);
-            sim->harena_dev[i] = static_cast<uint8_t *>(d);
-        }
+        // stream their payloads through it).  Sized for a compression ratio
+        // of 4 to start (at least 1 GiB, at most the worst case and 40% of
+        // host RAM each) and grown when a stage's output overflows
+        // (grow_host_arena) — pinning worst-case arenas up front cost
+        // minutes at 34 qubits.
+        const uint64_t dense = (uint64_t(1) << sim->n) * 16;
+        sim->arena_cap = std::min<uint64_t>({worst, host_ram() * 2 / 5, std::max<uint64_t>(dense / 4, uint64_t(1) << 30)});
+        if (const char *e = getenv("QZ_HOST_ARENA_START"))   // test hook: force the growth path
+            sim->arena_cap = std::max<uint64_t>(4096, std::strtoull(e, nullptr, 10));
+        for (int i = 0; i < 2; ++i) alloc_host_arena(sim, i, sim->arena_cap);
         sim->win.reserve_staging(sim->geom, sim->win.slots);
         if (sim->two_windows) {
             sim->win2.reserve_staging(sim->geom, sim->win2.slots);
@@ -400,7 +429,7 @@ void renormalize(qzc_sim *sim) {
         QZ_CHECK_LAUNCH();
         ++ctx->launches;
         encode_window(ctx, w, sim->geom, k, w.slot_chunk.as<uint64_t>(), nullptr, 0, sim->arena_ptr(b),
-                      sim->used_ptr(b), sim->arena_cap, sim->table(b), sim->len[a].as<uint32_t>(),
+                      sim->used_ptr(b), sim->cap(b), sim->table(b), sim->len[a].as<uint32_t>(),
                       sim->acct.as<int64_t>(), ctx->launches, s);
     }
     ctx->check_status();
@@ -901,7 +930,7 @@ void init_store(qzc_sim *sim, bool basis) {
     QZ_CUDA(cudaMemcpyAsync(w.amps.as<double2>() + N, one, 16, cudaMemcpyHostToDevice, s));
     ChunkTable t = sim->table(a);
     encode_window(ctx, w, sim->geom, 2, nullptr, nullptr, 0, sim->arena_ptr(a),
-                  sim->used_ptr(a), sim->arena_cap, t, nullptr, nullptr, ctx->launches);
+                  sim->used_ptr(a), sim->cap(a), t, nullptr, nullptr, ctx->launches);
     ctx->check_status();
     const double ti1 = now_s();
     if (sim->eb > 0.0) {
@@ -922,7 +951,7 @@ void init_store(qzc_sim *sim, bool basis) {
             QZ_CUDA(cudaMemsetAsync(w.amps.p, 0, 16 * N, s));
             QZ_CUDA(cudaMemcpyAsync(w.amps.p, one, 16, cudaMemcpyHostToDevice, s));
             encode_window(ctx, w, sim->geom, 1, sc, sc + 1, N > 1 ? 2u : 1u,
-                          sim->arena_ptr(a), sim->used_ptr(a), sim->arena_cap, t, nullptr,
+                          sim->arena_ptr(a), sim->used_ptr(a), sim->cap(a), t, nullptr,
                           nullptr, ctx->launches);
             ctx->check_status();
         }
@@ -1069,13 +1098,19 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
             if (any_inplace) upload_plan(build_passes(dg, wbits, kTileBits, true, false), dfull, s);
         }
         const int a = sim->cur, b = 1 - sim->cur;
+        // host-staged stores start with arenas sized for a typical ratio and
+        // grow on demand: a stage whose output overflows its arena is re-run
+        // from its (untouched) input arena after the output arena grew
+        int64_t acct_before[2] = {0, 0};
+        if (sim->host_res) QZ_CUDA(cudaMemcpy(acct_before, sim->acct.p, 16, cudaMemcpyDeviceToHost));
+        const uint64_t nwin = nbatches / bpw;
+        const uint64_t nslots = bpw << hs;
+        for (int attempt = 0;; ++attempt) {
         QZ_CUDA(cudaMemsetAsync(sim->used_ptr(b), 0, 8, s));
         // the stage's plan upload and arena reset happen on the context
         // stream; both window streams start after them
-        const uint64_t nwin = nbatches / bpw;
         cudaEvent_t ready = ev(4 * nwin);
         QZ_CUDA(cudaEventRecord(ready, s));
-        const uint64_t nslots = bpw << hs;
         const double tp1 = now_s();
         // pipeline events: 3 per window (gathered, encoded, written back)
         auto pev = [&](uint64_t i) {
@@ -1133,7 +1168,7 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
             QZ_CUDA(cudaEventRecord(pev(3 * w + 1), S));
             // write-back (D2H) of window w on SO
             QZ_CUDA(cudaStreamWaitEvent(SO, pev(3 * w + 1), 0));
-            launch_copy_out(W.stage_out.as<uint8_t>(), W.lused.as<uint64_t>(), sim->used_ptr(b), sim->arena_cap,
+            launch_copy_out(W.stage_out.as<uint8_t>(), W.lused.as<uint64_t>(), sim->used_ptr(b), sim->cap(b),
                             W.hbase.as<uint64_t>(), sim->arena_ptr(b), W.out_local(), In.slot_chunk.as<uint64_t>(),
                             nslots, sim->table(b), ctx->status, SO);
             k_io_count_out<<<1, 1, 0, SO>>>(W.lused.as<uint64_t>(), sim->io_bytes.as<uint64_t>());
@@ -1187,14 +1222,14 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
                               W.slot_chunk.as<uint64_t>());
                 // HBM -> host arena (zero-copy 16 B writes) + chunk table
                 launch_copy_out(W.stage_out.as<uint8_t>(), W.lused.as<uint64_t>(), sim->used_ptr(b),
-                                sim->arena_cap, W.hbase.as<uint64_t>(), sim->arena_ptr(b), W.local(),
+                                sim->cap(b), W.hbase.as<uint64_t>(), sim->arena_ptr(b), W.local(),
                                 W.slot_chunk.as<uint64_t>(), nslots, sim->table(b), ctx->status, S);
                 k_io_count_out<<<1, 1, 0, S>>>(W.lused.as<uint64_t>(), sim->io_bytes.as<uint64_t>());
                 QZ_CHECK_LAUNCH();
                 ctx->launches += 4;
             } else {
                 encode_window(ctx, W, sim->geom, nslots, W.slot_chunk.as<uint64_t>(), nullptr, 0,
-                              sim->arena_ptr(b), sim->used_ptr(b), sim->arena_cap,
+                              sim->arena_ptr(b), sim->used_ptr(b), sim->cap(b),
                               sim->table(b), sim->len[a].as<uint32_t>(), sim->acct.as<int64_t>(),
                               ctx->launches, S, w ? sim->acct_ev[(w - 1) & 1] : nullptr,
                               sim->acct_ev[w & 1]);
@@ -1209,7 +1244,13 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
         try {
             ctx->check_status();
         } catch (const Failure &f) {
+            if (f.code == QZC_ENOMEM && sim->host_res && attempt < 4 && grow_host_arena(sim, b, ctx->last_needed)) {
+                QZ_CUDA(cudaMemcpy(sim->acct.p, acct_before, 16, cudaMemcpyHostToDevice));
+                continue;
+            }
             throw Failure(f.code, "stage " + std::to_string(si) + ": " + f.what());
+        }
+        break;
         }
         for (uint64_t w = 0; w < nwin; ++w) {
             float ms[3];
@@ -1376,8 +1417,8 @@ int qzc_sim_import(qzc_sim *sim, const uint8_t *payloads, const uint32_t *sizes,
         pos += sizes[i];
         acct_bytes += sizes[i] + kPerChunkOverhead;
     }
-    if (pos > sim->arena_cap) throw Failure(QZC_ENOMEM, "store does not fit the HBM arena");
     const int a = sim->cur;
+    if (pos > sim->cap(a)) throw Failure(QZC_ENOMEM, "store does not fit the arena");
     if (sim->host_res)
         std::memcpy(sim->harena[a], payloads, pos);
     else
@@ -1428,7 +1469,7 @@ int qzc_sim_write_chunk(qzc_sim *sim, uint64_t index, const double *amps) {
     QZ_CUDA(cudaMemcpyAsync(sim->win.slot_chunk.p, &index, 8, cudaMemcpyHostToDevice, s));
     // the table of the live arena is updated in place; old bytes become garbage
     encode_window(ctx, sim->win, sim->geom, 1, sim->win.slot_chunk.as<uint64_t>(), nullptr, 0,
-                  sim->arena_ptr(a), sim->used_ptr(a), sim->arena_cap, sim->table(a),
+                  sim->arena_ptr(a), sim->used_ptr(a), sim->cap(a), sim->table(a),
                   sim->len[a].as<uint32_t>(), sim->acct.as<int64_t>(), ctx->launches);
     ctx->check_status();
     int64_t acct[2];

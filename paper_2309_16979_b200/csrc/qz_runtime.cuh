@@ -164,6 +164,7 @@ struct qzc_context {
     DevBuf arena, table_off, table_len, table_crc, forced, used;
     std::mutex mu;
     cudaEvent_t t_begin = nullptr, t_end = nullptr;
+    uint64_t last_needed = 0;   // arena bytes a QZS_ARENA failure asked for
 
     void check_status(uint64_t index_base = 0) {
         QZ_CUDA(cudaMemcpyAsync(status_host, status, sizeof(DevStatus), cudaMemcpyDeviceToHost, stream));
@@ -171,6 +172,7 @@ struct qzc_context {
         if (status_host->code != 0) {
             const int code = status_host->code;
             const uint64_t idx = status_host->index;
+            if (code == QZS_ARENA) last_needed = idx;
             QZ_CUDA(cudaMemsetAsync(status, 0, sizeof(DevStatus), stream));
             QZ_CUDA(cudaStreamSynchronize(stream));
             throw Failure(code == QZS_ARENA ? QZC_ENOMEM : QZC_ECODEC,
@@ -199,7 +201,8 @@ struct qzc_sim {
     DevPlan plans[3]; // stage plans (relaxed / per-pass replay / whole strict), device buffers reused
     DevBuf used;   // uint64[2] bump pointers
     DevBuf acct;   // int64[2] current / peak
-    uint64_t arena_cap = 0;
+    uint64_t arena_cap = 0;   // bytes per arena (host-staged: the larger of hcap)
+    uint64_t hcap[2] = {0, 0}; // host-staged arena capacities (grown on overflow)
     int cur = 0;
     uint64_t win_amps = 0;   // amplitudes per pipeline window
     Window win;              // window set 0 (also used by the host entry points)
@@ -225,6 +228,7 @@ struct qzc_sim {
     cudaStream_t st() const { return ctx->stream; }
     uint8_t *arena_ptr(int i) { return host_res ? harena_dev[i] : arena[i].as<uint8_t>(); }
     uint64_t *used_ptr(int i) { return used.as<uint64_t>() + i; }
+    uint64_t cap(int i) const { return host_res ? hcap[i] : arena_cap; }
 };
 
 #define QZ_API_BEGIN try {

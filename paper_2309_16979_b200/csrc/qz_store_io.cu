@@ -324,7 +324,7 @@ int qzc_sim_load(qzc_sim *sim, const char *path) {
     uint64_t used = 0, fill = 0, flushed = 0;
     auto flush = [&] {
         if (!fill) return;
-        if (used + fill > sim->arena_cap) throw Failure(QZC_ENOMEM, "store does not fit the arena");
+        if (used + fill > sim->cap(a)) throw Failure(QZC_ENOMEM, "store does not fit the arena");
         if (sim->host_res) std::memcpy(sim->harena[a] + flushed, host.bytes(), fill);
         else QZ_CUDA(cudaMemcpy(sim->arena[a].as<uint8_t>() + flushed, host.bytes(), fill, cudaMemcpyHostToDevice));
         sim->stats.h2d_bytes += fill;
@@ -494,7 +494,7 @@ int qzc_sim_exchange_pack(qzc_sim *sim, void **send_dev_out, uint64_t *bytes_out
 int qzc_sim_exchange_recv_buffer(qzc_sim *sim, uint64_t bytes, void **recv_dev_out) {
     QZ_API_BEGIN
     if (!sim || !recv_dev_out) throw Failure(QZC_EINVAL, "null argument");
-    if (bytes > sim->arena_cap) throw Failure(QZC_ENOMEM, "exchange does not fit the arena");
+    if (bytes > sim->cap(1 - sim->cur)) throw Failure(QZC_ENOMEM, "exchange does not fit the arena");
     QZ_CUDA(cudaSetDevice(sim->ctx->device));
     *recv_dev_out = sim->arena_ptr(1 - sim->cur);
     QZ_API_END

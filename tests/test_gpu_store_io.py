@@ -184,3 +184,33 @@ def test_skip_reencode_fast_mode(engine):
     dense = engine.dense_state(n, g)
     assert fast16.fidelity(dense) > 0.99999 and multi.fidelity(dense) > 0.99999
     dense.free()
+
+
+def test_host_arena_growth_keeps_reference_bytes(golden, tmp_path):
+    """Host-staged arenas start small and grow when a stage's output
+    overflows (the stage is re-run from its untouched input): forced here
+    with a 64 KiB starting arena; the reference digests hold."""
+    recs = [r for r in golden["runs"] if r["n"] >= 14][:3]
+    script = (
+        "import json, sys\n"
+        "from paper_2309_16979_b200 import engine as E, circuits as CI\n"
+        "from paper_2309_16979_b200.abi import to_array\n"
+        "recs, golden = json.loads(sys.argv[1]), json.load(open(sys.argv[2]))\n"
+        "eng = E.Engine()\n"
+        "out = []\n"
+        "for rec in recs:\n"
+        "    k = rec['circuit']\n"
+        "    if k.startswith('qft:'): g = CI.qft(int(k.split(':')[1]))\n"
+        "    elif k.startswith('ghz:'): g = CI.ghz(int(k.split(':')[1]))\n"
+        "    else: g = to_array([(x[0], tuple(x[1]), tuple(x[2])) for x in golden['circuits'][k]])\n"
+        "    sim = eng.simulator(rec['n'], rec['c'], rec['m'], rec['eb'], residency='host')\n"
+        "    sim.run(g)\n"
+        "    out.append(f'{sim.digest():016x}')\n"
+        "    sim.close()\n"
+        "print(json.dumps(out))\n")
+    env = dict(os.environ, QZ_HOST_ARENA_START="65536", PYTHONPATH=str(ROOT))
+    res = subprocess.run([sys.executable, "-c", script, json.dumps(recs),
+                          str(ROOT / "tests" / "golden" / "golden.json")],
+                         cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    assert json.loads(res.stdout.strip().splitlines()[-1]) == [r["digest"] for r in recs]
