@@ -771,7 +771,9 @@ void upload_plan(const GatePlan &plan, DevPlan &out, cudaStream_t s) {
     // kernel case set per pass: the narrow one when every fast-list entry of
     // every group is in it (and no group needs the shared-memory generic path)
     static const bool narrow_off = getenv("QZ_NO_NARROW") != nullptr;
+    static const bool wmap_off = getenv("QZ_NO_WMAP") != nullptr;
     for (PassDesc &pd : out.host_passes) {
+        pd.wmap = wmap_off ? 0u : 1u;
         pd.variant = kPassAll;
         for (int S : {kPassDiagH, kPassGen}) {
             bool narrow = !narrow_off && pd.kind != PASS_SWAPS;
@@ -1521,7 +1523,11 @@ __device__ __forceinline__ void mask_apply(uint32_t &SR, uint32_t &SI, const Til
 }
 
 // Bank-conflict swizzle of the 16 B shared-memory slots inside each 128 B row.
-__device__ __forceinline__ uint32_t swz(uint32_t l) { return l ^ ((l >> 3) & 7u); }
+// Shared-memory slot of tile element l: its low 3 bits XOR bits 3-5 and 6-8
+// (a bijection), so 16-byte accesses whose lanes differ in bits 3-8 — the
+// contiguous tile fill, a register group's block under either thread map —
+// spread over all 8 bank groups.
+__device__ __forceinline__ uint32_t swz(uint32_t l) { return l ^ ((l >> 3) & 7u) ^ ((l >> 6) & 7u); }
 
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
@@ -1587,6 +1593,8 @@ __global__ void __launch_bounds__(1 << (kTileBits - kRegBits), (kTileBits >= 12 
     const uint64_t himask = pd.tmask & ~((uint64_t(1) << L) - 1);
     const uint32_t lowmask = (1u << L) - 1;
     const uint32_t tid = threadIdx.x, nth = blockDim.x;   // nth == tile / NB
+    // register-group position of this thread (PassDesc::wmap)
+    const uint32_t tmap = (pd.wmap && nth >= 64) ? (tid >> 5) | ((tid & 31u) << (31 - __clz(nth >> 5))) : tid;
     for (uint32_t h = tid; h < nhi; h += nth) offhi[h] = deposit_bits(h, himask);
     // the zero-slot count, read once per CTA (other CTAs update it)
     __shared__ uint32_t s_zc;
@@ -1661,9 +1669,10 @@ __global__ void __launch_bounds__(1 << (kTileBits - kRegBits), (kTileBits >= 12 
                 bm[i] = 1u << G.gbits[i];
                 gm |= bm[i];
             }
-            // tid with zeros inserted at the (ascending) register bits ==
-            // deposit of tid into the tile bits outside gm
-            uint32_t mybase = tid;
+            // thread id with zeros inserted at the (ascending) register bits
+            // == deposit into the tile bits outside gm; under pd.wmap the
+            // warp index takes the lowest of those bits
+            uint32_t mybase = tmap;
 #pragma unroll
             for (int i = 0; i < kRegBits; ++i) {
                 const uint32_t b = G.gbits[i];

@@ -129,6 +129,10 @@ struct PassDesc {
                            // a flag replays the whole window; 2 relaxed with checked
                            // units: out of place, replayed pass by pass
     uint32_t variant;      // kernel case set (host side: kPassAll / kPassDiagH / kPassGen)
+    uint32_t wmap;         // register-group thread map: the warp index spells the LOWEST
+                           // non-register tile bits (lanes the higher ones), so blocks that
+                           // differ only in low bits — the all-(+0) blocks of sparse states —
+                           // fall on whole warps, which then skip the group uniformly
     uint8_t perm[48];
 };
 

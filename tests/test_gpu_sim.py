@@ -454,13 +454,16 @@ def test_full_case_set_same_digest(engine, golden, oracle, tmp_path):
     assert json.loads(res.stdout.strip().splitlines()[-1]) == [r["digest"] for r in recs]
 
 
-@pytest.mark.parametrize("kw", [{}, {"fuse": "checked"}, {"force_replay": True},
-                                {"residency": "host"}])
-def test_zero_slot_map_off_same_digest(engine, golden, oracle, tmp_path, kw):
-    """The zero-slot map only skips work: with QZ_NO_NZMAP=1 (no tile is
-    skipped on the map's say-so) the reference digests hold for the relaxed,
-    checked, forced-replay and host-staged variants.  Fresh process: the
-    switch is read once per process."""
+@pytest.mark.parametrize("switch,kw", [("QZ_NO_NZMAP", {}), ("QZ_NO_NZMAP", {"fuse": "checked"}),
+                                    ("QZ_NO_NZMAP", {"force_replay": True}),
+                                    ("QZ_NO_NZMAP", {"residency": "host"}),
+                                    ("QZ_NO_WMAP", {}), ("QZ_NO_WMAP", {"fuse": "checked"})])
+def test_skip_switches_off_same_digest(engine, golden, oracle, tmp_path, switch, kw):
+    """Work-skipping devices only skip work: with QZ_NO_NZMAP=1 (no tile
+    skipped on the zero-slot map's say-so) or QZ_NO_WMAP=1 (register groups
+    on the plain thread map, no warp-uniform block skips) the reference
+    digests hold for the relaxed, checked, forced-replay and host-staged
+    variants.  Fresh process: the switches are read once per process."""
     import json
     import os
     import subprocess
@@ -485,7 +488,8 @@ def test_zero_slot_map_off_same_digest(engine, golden, oracle, tmp_path, kw):
         "    out.append(f'{sim.digest():016x}')\n"
         "    sim.close()\n"
         "print(json.dumps(out))\n")
-    env = dict(os.environ, QZ_NO_NZMAP="1", PYTHONPATH=str(root))
+    env = dict(os.environ, PYTHONPATH=str(root))
+    env[switch] = "1"
     res = subprocess.run([sys.executable, "-c", script, json.dumps(recs), str(tmp_path),
                           json.dumps(kw)], cwd=root, env=env, capture_output=True, text=True,
                          timeout=600)
