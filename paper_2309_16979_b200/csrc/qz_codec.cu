@@ -1049,9 +1049,12 @@ __global__ void __launch_bounds__(kEncThreads) k_enc_lossy(
         const int pb = int(ti & 1);
         issue(ti + 1);
         cp_async_wait<1>();
-        __syncthreads();
+        // (the barrier also tells whether the previous tile staged any pair:
+        // fast-forwarded tiles of sparse states stage none, so the flush
+        // warps skip their stream loop)
+        const int staged = __syncthreads_or(active && (lo.n | hi.n) != 0);
         if (!chain) {
-            if (ti) flush(pb ^ 1);
+            if (ti && staged) flush(pb ^ 1);
         } else if (active) {
             const double *rowc = reinterpret_cast<const double *>(tile(ti) + r * (te + 1)) + h;
             const uint64_t tile0 = h * N + ti * te;
@@ -1118,7 +1121,7 @@ __global__ void __launch_bounds__(kEncThreads) k_enc_lossy(
         __syncthreads();  // tile and staging buffers are reused next round
     }
     cp_async_wait<0>();
-    if (!chain && ntiles) flush(int((ntiles - 1) & 1));
+    if (__syncthreads_or(active && (lo.n | hi.n) != 0) && !chain && ntiles) flush(int((ntiles - 1) & 1));
     if (active) {
         EncHalf &m = meta[2 * s + h];
         rlet_close(lo, h, m, 0, reinterpret_cast<uint16_t *>(base));

@@ -333,12 +333,11 @@ void sim_alloc(qzc_sim *sim) {
     if (sim->host_res) {
         // page-locked, mapped host arenas (the store leaves HBM; windows
         // stream their payloads through it).  Sized for a compression ratio
-        // of 4 to start (at least 1 GiB, at most the worst case and 40% of
+        // of 2.5 to start (at least 1 GiB, at most the worst case and 40% of
         // host RAM each) and grown when a stage's output overflows
-        // (grow_host_arena) — pinning worst-case arenas up front cost
-        // minutes at 34 qubits.
+        // (grow_host_arena) instead of pinning worst-case arenas up front.
         const uint64_t dense = (uint64_t(1) << sim->n) * 16;
-        sim->arena_cap = std::min<uint64_t>({worst, host_ram() * 2 / 5, std::max<uint64_t>(dense / 4, uint64_t(1) << 30)});
+        sim->arena_cap = std::min<uint64_t>({worst, host_ram() * 2 / 5, std::max<uint64_t>(dense / 5 * 2, uint64_t(1) << 30)});
         if (const char *e = getenv("QZ_HOST_ARENA_START"))   // test hook: force the growth path
             sim->arena_cap = std::max<uint64_t>(4096, std::strtoull(e, nullptr, 10));
         for (int i = 0; i < 2; ++i) alloc_host_arena(sim, i, sim->arena_cap);

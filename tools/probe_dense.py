@@ -36,7 +36,7 @@ for rep in range(a.reps):
 if a.kprof:
     tot = {}
     for r in eng.kprof_read():
-        k = r["name"]
+        k = r["name"] + (f" #{r['tag']}" if r["name"].startswith("tile") and r["stage"] == 0 else "")
         t = tot.setdefault(k, [0, 0.0, 0.0])
         t[0] += 1
         t[1] += r["seconds"]
