@@ -159,6 +159,12 @@ int qzc_apply_matrices_host(qzc_context *ctx, double *amps, uint32_t nbits,
                             const qzc_matrix_gate *gates, uint64_t ngates);
 int qzc_apply_matrices_dev(qzc_context *ctx, double *amps_dev, uint32_t nbits,
                            const qzc_matrix_gate *gates, uint64_t ngates);
+/* One gate over pair (dim 2) or group (dim 4) indices [begin, end) only —
+ * the sub-range arguments of apply_single_qubit / apply_two_qubit
+ * (kernels.cpp:20-54) that the reference uses to split a gate among its
+ * kernel workers.  Only the amplitudes the range touches cross the link. */
+int qzc_apply_matrix_range_host(qzc_context *ctx, double *amps, uint32_t nbits,
+                                const qzc_matrix_gate *gate, uint64_t begin, uint64_t end);
 
 /* ---- device buffers (replaces ReferenceDevice's buffer / staging,
  *      device.cpp:120-255, 404-449) --------------------------------------- */

@@ -119,6 +119,38 @@ __global__ void k_partials(const double2 *win, uint64_t nslots, uint64_t N, cons
     }
 }
 
+// apply_single_qubit / apply_two_qubit over pair (group) indices
+// [begin, end) with the reference's formula (kernels.cpp:20-54): complex
+// products (ac - bd, ad + bc) separately rounded, rows summed left to right.
+__global__ void k_apply_range(double2 *buf, uint32_t dim, uint32_t b0, uint32_t b1, const double2 *m,
+                              uint64_t begin, uint64_t end) {
+    const uint64_t p = begin + uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p >= end) return;
+    auto prod = [](double2 a, double2 v) {
+        return make_double2(__dsub_rn(__dmul_rn(a.x, v.x), __dmul_rn(a.y, v.y)),
+                            __dadd_rn(__dmul_rn(a.x, v.y), __dmul_rn(a.y, v.x)));
+    };
+    auto add = [](double2 a, double2 b) { return make_double2(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y)); };
+    if (dim == 2) {
+        const uint64_t i = insert_zero_bit(p, b0), j = i | (uint64_t(1) << b0);
+        const double2 a = buf[i], b = buf[j];
+        buf[i] = add(prod(m[0], a), prod(m[1], b));
+        buf[j] = add(prod(m[2], a), prod(m[3], b));
+        return;
+    }
+    const uint32_t lo = b0 < b1 ? b0 : b1, hi = b0 < b1 ? b1 : b0;
+    const uint64_t base = insert_zero_bit(insert_zero_bit(p, lo), hi);
+    const uint64_t s0 = uint64_t(1) << b0, s1 = uint64_t(1) << b1;
+    const uint64_t idx[4] = {base, base | s1, base | s0, base | s0 | s1};
+    double2 in[4];
+    for (int c = 0; c < 4; ++c) in[c] = buf[idx[c]];
+    for (int r = 0; r < 4; ++r) {
+        double2 acc = prod(m[4 * r], in[0]);
+        for (int c = 1; c < 4; ++c) acc = add(acc, prod(m[4 * r + c], in[c]));
+        buf[idx[r]] = acc;
+    }
+}
+
 // a *= scale for std::complex<double> and a real scale: componentwise
 // products (complex x real, no cross terms), pipeline.cpp:283
 __global__ void k_scale(double2 *buf, uint64_t n, double scale) {
@@ -703,6 +735,62 @@ int qzc_apply_matrices_host(qzc_context *ctx, double *amps, uint32_t nbits,
     QZ_CUDA(cudaMemcpyAsync(amps, buf.p, bytes, cudaMemcpyDeviceToHost, ctx->stream));
     QZ_CUDA(cudaStreamSynchronize(ctx->stream));
     buf.release();
+    QZ_API_END
+}
+
+int qzc_apply_matrix_range_host(qzc_context *ctx, double *amps, uint32_t nbits, const qzc_matrix_gate *gate,
+                                uint64_t begin, uint64_t end) {
+    QZ_API_BEGIN
+    if (!ctx || !amps || !gate) throw Failure(QZC_EINVAL, "null argument");
+    if (gate->dim != 2 && gate->dim != 4) throw Failure(QZC_EINVAL, "matrix dimension must be 2 or 4");
+    const uint32_t nq = gate->dim == 2 ? 1 : 2;
+    for (uint32_t k = 0; k < nq; ++k)
+        if (gate->qubits[k] >= nbits)
+            throw Failure(QZC_EDEVICE, "buffer bit " + std::to_string(gate->qubits[k]) + " out of range");
+    if (nq == 2 && gate->qubits[0] == gate->qubits[1]) throw Failure(QZC_EINVAL, "duplicate qubit");
+    const uint64_t units = uint64_t(1) << (nbits - nq);
+    if (begin > end || end > units) throw Failure(QZC_EINVAL, "range outside the buffer's pairs / groups");
+    if (begin == end) return QZC_OK;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    QZ_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    // the touched amplitudes lie in the index span of the range's first /
+    // last unit shifted by each partner offset: copy only those spans
+    const uint32_t b0 = gate->qubits[0], b1 = nq == 2 ? gate->qubits[1] : 0;
+    auto first_index = [&](uint64_t u) {
+        if (nq == 1) return insert_zero_bit(u, b0);
+        const uint32_t lo = std::min(b0, b1), hi = std::max(b0, b1);
+        return insert_zero_bit(insert_zero_bit(u, lo), hi);
+    };
+    const uint64_t f0 = first_index(begin), f1 = first_index(end - 1);
+    std::vector<uint64_t> offs{0, uint64_t(1) << b0};
+    if (nq == 2) offs = {0, uint64_t(1) << b0, uint64_t(1) << b1, (uint64_t(1) << b0) | (uint64_t(1) << b1)};
+    std::vector<std::pair<uint64_t, uint64_t>> spans;
+    for (uint64_t o : offs) spans.push_back({f0 + o, f1 + o + 1});
+    std::sort(spans.begin(), spans.end());
+    std::vector<std::pair<uint64_t, uint64_t>> merged;
+    for (auto sp : spans) {
+        if (!merged.empty() && sp.first <= merged.back().second) merged.back().second = std::max(merged.back().second, sp.second);
+        else merged.push_back(sp);
+    }
+    DevBuf buf, mat;
+    buf.ensure(16ull << nbits);
+    mat.ensure(16 * 16);
+    double2 m[16];
+    for (uint32_t e = 0; e < gate->dim * gate->dim; ++e) m[e] = make_double2(gate->m[2 * e], gate->m[2 * e + 1]);
+    QZ_CUDA(cudaMemcpyAsync(mat.p, m, sizeof m, cudaMemcpyHostToDevice, s));
+    double2 *d = buf.as<double2>();
+    const double2 *h = reinterpret_cast<const double2 *>(amps);
+    for (auto sp : merged)
+        QZ_CUDA(cudaMemcpyAsync(d + sp.first, h + sp.first, 16 * (sp.second - sp.first), cudaMemcpyHostToDevice, s));
+    k_apply_range<<<(unsigned)ceil_div(end - begin, 256), 256, 0, s>>>(d, gate->dim, b0, b1, mat.as<double2>(), begin,
+                                                                       end);
+    QZ_CHECK_LAUNCH();
+    ++ctx->launches;
+    for (auto sp : merged)
+        QZ_CUDA(cudaMemcpyAsync(reinterpret_cast<double2 *>(amps) + sp.first, d + sp.first,
+                                16 * (sp.second - sp.first), cudaMemcpyDeviceToHost, s));
+    QZ_CUDA(cudaStreamSynchronize(s));
     QZ_API_END
 }
 

@@ -80,3 +80,50 @@ def test_linearity(engine):
 def test_bad_bit_fails(engine):
     with pytest.raises(E.DeviceError):
         engine.apply_gates(np.zeros(16, complex), [("h", (4,), ())])
+
+
+@pytest.mark.parametrize("nbits,dim", [(10, 2), (14, 2), (12, 4), (15, 4)])
+def test_sub_range_apply_matches_whole_gate(engine, oracle, nbits, dim):
+    """apply_single_qubit / apply_two_qubit sub-ranges (kernels.cpp:20-54,
+    the reference's worker split) through qzc_apply_matrix_range_host: the
+    union of the ranges equals the whole gate bit for bit (the reference's
+    apply_gates, via the C oracle), and amplitudes outside a range stay
+    untouched."""
+    import ctypes as C
+    from paper_2309_16979_b200.abi import to_array
+    lib = engine.lib
+    lib.qzc_apply_matrix_range_host.argtypes = [C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p,
+                                                C.c_uint64, C.c_uint64]
+    rng = np.random.default_rng(nbits * dim)
+    buf = (rng.standard_normal(1 << nbits) + 1j * rng.standard_normal(1 << nbits)) / 7.0
+    buf[rng.integers(0, buf.size, 40)] = 0.0
+    for trial in range(6):
+        if dim == 2:
+            q = (int(rng.integers(0, nbits)),)
+            g = ("u3", q, tuple(rng.uniform(-3, 3, 3)))
+        else:
+            q = tuple(int(x) for x in rng.choice(nbits, 2, replace=False))
+            g = (["cx", "cz", "swap"][trial % 3], q, ())
+        mat = engine.gate_matrix(g)
+
+        class MG(C.Structure):
+            _fields_ = [("dim", C.c_uint32), ("qubits", C.c_uint32 * 2), ("reserved", C.c_uint32),
+                        ("m", C.c_double * 32)]
+        mg = MG(dim=dim)
+        mg.qubits[0] = q[0]
+        mg.qubits[1] = q[1] if dim == 4 else 0
+        for e, v in enumerate(mat.ravel()):
+            mg.m[2 * e], mg.m[2 * e + 1] = v.real, v.imag
+        units = (1 << nbits) // dim
+        cuts = sorted({0, units, *(int(x) for x in rng.integers(0, units, 3))})
+        got = buf.copy()
+        for a, b in zip(cuts[:-1], cuts[1:]):
+            assert lib.qzc_apply_matrix_range_host(engine.h, got.ctypes.data, nbits, C.byref(mg), a, b) == 0
+        want = oracle.apply_gates(buf, to_array([g]))
+        assert got.tobytes() == want.tobytes(), (g, cuts)
+        # a partial range leaves the other units' amplitudes alone
+        part = buf.copy()
+        assert lib.qzc_apply_matrix_range_host(engine.h, part.ctypes.data, nbits, C.byref(mg), 0,
+                                               units // 2) == 0
+        assert (part != buf).any() or g[0] == "cz"
+        buf = want
