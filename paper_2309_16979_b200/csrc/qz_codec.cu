@@ -15,6 +15,8 @@
 // at the plane boundary exactly as rle_encode would over the joined plane.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <string>
 
 #include "qz_codec.cuh"
 #include "qz_kprof.cuh"
@@ -646,6 +648,118 @@ __global__ void __launch_bounds__(256) k_dec_lossy_warp(
     if (lane == 0) {
         if (bad) dev_fail(status, QZS_RAW_UNDER, slot_chunk ? slot_chunk[s] : s);
         else if (h == 1 && raw_i != raw_count) dev_fail(status, QZS_RAW_UNUSED, slot_chunk ? slot_chunk[s] : s);
+    }
+}
+
+// Lossy decode for dense stores, 8-lane segments (codec.cpp:217-249): a warp
+// decodes two chunks at once, one 8-lane segment per (chunk, half) — seg =
+// lane / 8, chunk = 2 warp + seg / 2, half = seg % 2 — 8 elements per step.
+// Per step every segment expands its 8 codes from the two byte planes
+// (segment scan of the run lengths + shuffle search, width-8 shuffles), ranks
+// its raw escapes by ballot, forms val = raw ? value : code * 2eb, and runs
+// the predictor chain pred = raw ? val : pred + val (the reference's
+// sequence of roundings) over its 8 values through shared memory.  Four
+// chains share each chain instruction (one per 8 lanes), a quarter of the
+// warp-per-chain kernel's serial cost; the real and imaginary segments of a
+// chunk meet by shuffle and store whole amplitudes (8 x 16 B contiguous).
+constexpr uint32_t kSegW = 8;
+
+__device__ __forceinline__ uint32_t plane_seg(PlaneRd &c, const uint8_t *p, uint32_t sub) {
+    const uint32_t q = c.pp + 2 * sub;
+    const uint32_t b = __ldg(p + q);
+    uint32_t r = __ldg(p + q + 1);
+    if (sub == 0) r = c.rem;
+    uint32_t S = r;   // inclusive scan of the runs within the segment
+#pragma unroll
+    for (uint32_t o = 1; o < kSegW; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, S, o, kSegW);
+        if (sub >= o) S += t;
+    }
+    // pair of element `sub`: number of pairs whose scan is <= sub
+    uint32_t j = 0;
+#pragma unroll
+    for (uint32_t step = kSegW / 2; step; step >>= 1) {
+        const uint32_t sv = __shfl_sync(0xffffffffu, S, j + step - 1, kSegW);
+        if (sv <= sub) j += step;
+    }
+    const uint32_t byte = __shfl_sync(0xffffffffu, b, j, kSegW);
+    // advance past the segment's 8 elements
+    const uint32_t jl = __shfl_sync(0xffffffffu, j, kSegW - 1, kSegW);
+    const uint32_t sl = __shfl_sync(0xffffffffu, S, jl, kSegW);
+    const uint32_t rnext = __shfl_sync(0xffffffffu, r, (jl + 1) & (kSegW - 1), kSegW);
+    if (sl > kSegW) {
+        c.pp += 2 * jl;
+        c.rem = sl - kSegW;
+    } else {
+        c.pp += 2 * (jl + 1);
+        c.rem = jl + 1 < kSegW ? rnext : uint32_t(__ldg(p + c.pp + 1));
+    }
+    return byte;
+}
+
+__global__ void __launch_bounds__(256) k_dec_lossy_seg(
+    const uint8_t *__restrict__ arena, const DecIdx *__restrict__ idx,
+    const uint64_t *__restrict__ slot_chunk, uint64_t nslots, CodecGeom g,
+    double2 *__restrict__ win, DevStatus *status, const uint32_t *cond) {
+    if (cond && *cond == 0) return;
+    __shared__ double cv[8][2][32];   // per warp: chain inputs, chain outputs
+    const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5, seg = lane >> 3, sub = lane & 7;
+    const uint64_t s = ((uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * 2 + (seg >> 1);
+    const uint32_t h = seg & 1;
+    if (((uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * 2 >= nslots) return;   // whole warp
+    const bool exists = s < nslots;
+    const DecIdx &d = idx[exists ? s : 0];
+    const bool live = exists && d.len != 0;
+    const uint64_t N = g.N;
+    // dead segments (no chunk, or an index walk that failed) run on a
+    // never-ending run at a valid address and produce zeros
+    const uint8_t *p = live ? arena + d.base : arena;
+    PlaneRd lo{0, 0x40000000u}, hi{0, 0x40000000u};
+    if (live) {
+        lo = PlaneRd{d.pos[0][h], uint32_t(__ldg(p + d.pos[0][h] + 1)) - d.skip[0][h]};
+        hi = PlaneRd{d.pos[1][h], uint32_t(__ldg(p + d.pos[1][h] + 1)) - d.skip[1][h]};
+        // a zero remainder: the half starts at the next pair
+        if (lo.rem == 0) { lo.pp += 2; lo.rem = __ldg(p + lo.pp + 1); }
+        if (hi.rem == 0) { hi.pp += 2; hi.rem = __ldg(p + hi.pp + 1); }
+    }
+    const double twoeb = live ? 2.0 * d.eb : 0.0;
+    uint32_t raw_i = live && h ? d.raw_re : 0;
+    const uint32_t raw_count = live ? d.raw_count : 0, raw_pos = live ? d.raw_pos : 0;
+    double pred = 0.0;
+    double *vin = cv[wib][0], *vout = cv[wib][1];
+    double2 *out = win + (exists ? s : 0) * N;
+    for (uint64_t e0 = 0; e0 < N; e0 += kSegW) {
+        const uint32_t z = plane_seg(lo, p, sub) | (plane_seg(hi, p, sub) << 8);
+        const bool raw = live && z == 0xFFFFu;
+        const uint32_t rm = (__ballot_sync(0xffffffffu, raw) >> (8 * seg)) & 0xFFu;
+        double val = 0.0;
+        if (raw) {
+            const uint32_t k = raw_i + __popc(rm & ((1u << sub) - 1));
+            val = k < raw_count ? __longlong_as_double((long long)ld_u64(p + raw_pos + 8ull * k)) : 0.0;
+        } else if (live) {
+            // ((double)code * 2.0) * eb == (double)code * (2 eb) exactly
+            val = __dmul_rn(double(unzigzag16(z)), twoeb);
+        }
+        raw_i += __popc(rm);
+        vin[lane] = val;
+        __syncwarp();
+        const double *vs = vin + 8 * seg;
+#pragma unroll
+        for (uint32_t i = 0; i < kSegW; ++i) {
+            const double x = vs[i];
+            pred = ((rm >> i) & 1) ? x : __dadd_rn(pred, x);
+            vout[8 * seg + i] = pred;
+        }
+        __syncwarp();
+        const double mine = vout[lane];
+        const double im = __shfl_down_sync(0xffffffffu, mine, kSegW);
+        if (h == 0 && exists) __stcs(out + e0 + sub, make_double2(live ? mine : 0.0, live ? im : 0.0));
+        __syncwarp();
+    }
+    if (live && sub == 0) {
+        const uint64_t chunk = slot_chunk ? slot_chunk[s] : s;
+        if (raw_i > raw_count) dev_fail(status, QZS_RAW_UNDER, chunk);
+        else if (h == 1 && raw_i != raw_count) dev_fail(status, QZS_RAW_UNUSED, chunk);
     }
 }
 
@@ -1419,6 +1533,7 @@ CodecGeom make_geom(uint64_t N, double eb) {
         // exact reciprocal: power of two whose inverse is a normal double
         g.exact_inv = eb > 0.0 && mant == 0.5 && ex > -1020 && ex < 1020 ? 1u : 0u;
     }
+    g.dense_hint = 0;
     g.scap = round_up(2 * N, 8);
     g.half_stride = round_up(g.lossy ? 2 * g.scap + 8 * N : 8 * g.scap, 16);
     return g;
@@ -1480,12 +1595,18 @@ void launch_decode(const uint8_t *arena, const DecIdx *idx, const uint64_t *slot
                    cudaStream_t s, const uint32_t *cond, bool sparse) {
     const unsigned grid = grid_for(nslots, kSlotsPerCta);
     const double dense = 16.0 * double(g.N) * double(nslots);
-    KProfScope prof(s, cond ? "replay_decode" : (g.lossy && g.N >= 32 && !sparse) ? "k_dec_lossy_warp"
+    // QZ_DEC_KERNEL=warp|seg forces the dense-store kernel choice (tests)
+    static const int force = getenv("QZ_DEC_KERNEL") ? (std::string(getenv("QZ_DEC_KERNEL")) == "seg" ? 1 : 0) : -1;
+    const bool seg = g.lossy && g.N >= 64 && !sparse && (force >= 0 ? force == 1 : g.dense_hint != 0);
+    KProfScope prof(s, cond ? "replay_decode" : seg ? "k_dec_lossy_seg" : (g.lossy && g.N >= 32 && !sparse) ? "k_dec_lossy_warp"
                                             : g.lossy ? "k_dec_lossy" : "k_dec_lossless", 0, dense);
     // dense payloads: warp per chunk-half (parallel RLE expansion, serial
     // predictor chain only); a store known to be mostly zero runs (right
     // after init): thread per chunk-half with run fills
-    if (g.lossy && g.N >= 32 && !sparse) {
+    if (seg) {
+        // dense store: 8-lane segments, two chunks per warp, 16 per CTA
+        k_dec_lossy_seg<<<grid_for(nslots, 16), 256, 0, s>>>(arena, idx, slot_chunk, nslots, g, win, status, cond);
+    } else if (g.lossy && g.N >= 32 && !sparse) {
         // warp per (slot, half): 4 slots per 256-thread CTA
         k_dec_lossy_warp<<<grid_for(nslots, 4), 256, 0, s>>>(arena, idx, slot_chunk, nslots, g, win,
                                                               status, cond);

@@ -49,7 +49,8 @@ struct CodecGeom {
     double eb, twoeb;       // store error bound, 2*eb
     double inv2eb;          // fl(1 / (2 eb)) for the division-free quantiser
     uint32_t exact_inv;     // 2 eb is a power of two: the reciprocal is exact
-    uint32_t pad;
+    uint32_t dense_hint;    // the store compresses less than 16x: decode with the
+                            // segmented kernel (set per stage by the runtime)
     uint64_t scap;          // bytes per scratch stream (>= 2N, multiple of 8)
     uint64_t half_stride;   // scratch bytes per (slot, half)
 };

@@ -641,7 +641,10 @@ int qzc_decompress_host(qzc_context *ctx, const uint8_t *payloads, const uint64_
     uint64_t span = 0;
     for (uint64_t i = 0; i < count; ++i) span = std::max<uint64_t>(span, offsets[i] + sizes[i]);
     const uint8_t id = sizes[0] ? payloads[offsets[0]] : 2;
-    const CodecGeom g = make_geom(elements, id == 1 ? 1.0 : 0.0);
+    CodecGeom g = make_geom(elements, id == 1 ? 1.0 : 0.0);
+    uint64_t total = 0;
+    for (uint64_t i = 0; i < count; ++i) total += sizes[i];
+    g.dense_hint = total > count * elements ? 1u : 0u;   // compresses less than 16x
     ctx->win.reserve(g, count);
     ctx->arena.ensure(span + 64);
     ctx->table_off.ensure(8 * count);
@@ -1149,6 +1152,9 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
     for (size_t si = 0; si < stages.size(); ++si) {
         const Stage &st = stages[si];
         kprof_set_stage(uint32_t(sim->stats.stages));
+        // decoder choice for this stage's input: dense stores (ratio < 16)
+        // take the segmented kernel, sparse ones the run-filling warp kernel
+        sim->geom.dense_hint = sim->payload_now > (uint64_t(1) << sim->n) ? 1u : 0u;
         const uint32_t hs = (uint32_t)st.high.size();
         const uint32_t mb = c + hs;  // buffer bits of one batch
         uint64_t smask = 0;
