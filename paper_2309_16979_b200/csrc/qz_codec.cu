@@ -898,13 +898,12 @@ template <int N> __device__ __forceinline__ void cp_async_wait() {
 // One byte plane's RLE of one half (rle_encode, codec.cpp:52-63, restated as
 // a branch-free per-byte step).  The real half keeps its last run open (the
 // assembler continues it into the imaginary half); the imaginary half holds
-// back its first run (head), which may exceed 255 until the merge.  Pair k
-// (k = 0, 1, ... over the whole half) goes to dst[k - np0]: the scratch
-// stream itself (np0 = 0), or a shared-memory staging buffer that holds the
-// pairs emitted since pair np0.
+// back its first run (head), which may exceed 255 until the merge.  Pairs
+// go straight to the scratch stream (the lossless encoder; the lossy one
+// stages its pairs in shared memory, RleT below).
 struct RleS {
     uint16_t *dst;
-    uint32_t np0;         // pair index of dst[0]
+    uint32_t np0;         // pair index of dst[0] (0: dst is the stream)
     uint32_t np;          // pairs emitted
     uint32_t cur, cnt;    // open run (cur = 0x100: none yet)
     uint32_t hold;        // imaginary half, first run not closed yet
@@ -941,25 +940,6 @@ __device__ __forceinline__ void rle_step(RleS &s, uint32_t x) {
     if (emit) rle_emit(s, val);
     s.cnt = diff ? 1u : (emit ? 0u : c1);
     s.cur = x;
-}
-
-// n steps of byte x (fast-forward tiles).
-__device__ __forceinline__ void rle_step_n(RleS &s, uint32_t x, uint32_t n) {
-    if (n == 0) return;
-    if (x != s.cur) {
-        rle_step(s, x);
-        --n;
-    }
-    if (s.hold) {
-        s.cnt += n;
-        return;
-    }
-    uint32_t tot = s.cnt + n;
-    while (tot >= 255) {
-        rle_emit(s, x | (255u << 8));
-        tot -= 255;
-    }
-    s.cnt = tot;
 }
 
 // Close a half: the real half reports its open tail, the imaginary half

@@ -110,7 +110,6 @@ void gate_matrix_host(const qzc_gate &g, double2 *m, uint32_t *dim) {
     }
 }
 
-static bool is_zero_h(double2 v) { return v.x == 0.0 && v.y == 0.0; }
 
 static uint32_t coef_kind(double2 v) {
     if (v.x == 0.0 && v.y == 0.0) return CK_ZERO;
