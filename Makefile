@@ -36,13 +36,28 @@ $(OBJ)/%.o: $(SRC)/%.cu $(HDRS)
 	@mkdir -p $(OBJ)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $@.ptxas.log || (cat $@.ptxas.log; false)
 
+# the device headers the runtime-specialised passes compile against (NVRTC),
+# embedded as raw strings
+JIT_HDRS := $(SRC)/qz_rtc_types.cuh $(SRC)/qz_bits.cuh $(SRC)/qz_gate_types.cuh $(SRC)/qz_gates_dev.cuh
+$(OBJ)/jit_headers.inc: $(JIT_HDRS)
+	@mkdir -p $(OBJ)
+	@{ echo "static const int kJitHeaderCount = 4;"; \
+	   echo "static const char *const kJitHeaderNames[] = {"; \
+	   for f in $(JIT_HDRS); do echo "\"$$(basename $$f)\","; done; echo "};"; \
+	   echo "static const char *const kJitHeaderSrc[] = {"; \
+	   for f in $(JIT_HDRS); do echo 'R"QZSRC('; cat $$f; echo ')QZSRC",'; done; echo "};"; } > $@
+
+$(OBJ)/qz_jit.o: $(SRC)/qz_jit.cu $(HDRS) $(OBJ)/jit_headers.inc
+	@mkdir -p $(OBJ)
+	$(NVCC) $(NVFLAGS) -I$(OBJ) -c $< -o $@ 2> $@.ptxas.log || (cat $@.ptxas.log; false)
+
 $(OBJ)/%.o: $(SRC)/%.cpp $(HDRS)
 	@mkdir -p $(OBJ)
 	g++ -std=c++17 -O2 -fPIC -Wall -I$(CUDA)/include -c $< -o $@
 
 $(LIB): $(OBJS)
 	@mkdir -p $(dir $@)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart -ldl
 
 # tools over the drop-in (paper Table 1: tools/cpp/bench_transfer.cpp)
 build/tools/bench_transfer: tools/cpp/bench_transfer.cpp $(HOSTLIB) $(QZSIM_HDRS)

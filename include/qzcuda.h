@@ -105,6 +105,16 @@ typedef struct qzc_kprof_record {
 int qzc_kprof_enable(qzc_context *ctx, int on);
 int qzc_kprof_read(qzc_context *ctx, qzc_kprof_record *out, uint64_t cap, uint64_t *count);
 
+/* Runtime-specialised gate passes (NVRTC; QZ_JIT=0 disables).  Full-tile
+ * passes over windows of >= 2^QZ_JIT_MIN_BITS amplitudes are also compiled
+ * as straight-line kernels on host threads and used once built; results are
+ * identical to the AOT kernels.  qzc_jit_wait blocks until every queued
+ * compile finished (returns how many built); qzc_jit_selftest compiles the
+ * widest pass of `gates` (on buffer bits of a 2^nbits window) with NVRTC,
+ * no GPU needed: QZC_OK or an error carrying NVRTC's log. */
+uint64_t qzc_jit_wait(void);
+int qzc_jit_selftest(const qzc_gate *gates, uint64_t ngates, uint32_t nbits);
+
 /* ---- chunk codec (replaces codec.hpp:61-70) ----------------------------- */
 /* Worst-case payload bytes for one chunk of `elements` amplitudes. */
 uint64_t qzc_payload_bound(uint64_t elements, double error_bound);

@@ -14,6 +14,7 @@
 #include <string>
 
 #include "../../include/qzcuda.h"
+#include "qz_bits.cuh"
 
 namespace qz {
 
@@ -66,28 +67,6 @@ __device__ __forceinline__ cplx cmul(double mr, double mi, double2 a) {
     r.re = __dsub_rn(__dmul_rn(mr, a.x), __dmul_rn(mi, a.y));
     r.im = __dadd_rn(__dmul_rn(mr, a.y), __dmul_rn(mi, a.x));
     return r;
-}
-
-__host__ __device__ __forceinline__ uint64_t insert_zero_bit(uint64_t x, uint32_t bit) {
-    uint64_t low = x & ((uint64_t(1) << bit) - 1);
-    return ((x >> bit) << (bit + 1)) | low;
-}
-
-__host__ __device__ __forceinline__ uint32_t insert_zero_bit32(uint32_t x, uint32_t bit) {
-    uint32_t low = x & ((1u << bit) - 1);
-    return ((x >> bit) << (bit + 1)) | low;
-}
-
-// Scatter the low bits of v into the set bits of mask (ascending), i.e. pdep.
-__host__ __device__ __forceinline__ uint64_t deposit_bits(uint64_t v, uint64_t mask) {
-    uint64_t out = 0;
-    while (mask) {
-        uint64_t low = mask & (~mask + 1);
-        if (v & 1) out |= low;
-        v >>= 1;
-        mask &= mask - 1;
-    }
-    return out;
 }
 
 inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }

@@ -1181,7 +1181,7 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
         const double tp0 = now_s();
         GatePlan gp = build_passes(dg, wbits, kTileBits, sim->cfg.fuse_gates != 0, sim->relax);
         DevPlan &dp = sim->plans[0], &dsub = sim->plans[1], &dfull = sim->plans[2];
-        upload_plan(gp, dp, s);
+        upload_plan(gp, dp, s, wbits);
         dsub.host_passes.clear();
         dfull.host_passes.clear();
         if (dp.relaxed) {

@@ -123,6 +123,8 @@ def load_library() -> C.CDLL:
         "qzc_sim_exchange_recv_buffer": (C.c_int, [C.c_void_p, C.c_uint64, P(C.c_void_p)]),
         "qzc_sim_exchange_unpack": (C.c_int, [C.c_void_p, u64p]),
         "qzc_kprof_read": (C.c_int, [C.c_void_p, P(KProfRecord), C.c_uint64, u64p]),
+        "qzc_jit_wait": (C.c_uint64, []),
+        "qzc_jit_selftest": (C.c_int, [P(Gate), C.c_uint64, C.c_uint32]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -142,6 +144,21 @@ def pass_plan_stats(gates, nbits: int, fuse="relaxed") -> dict:
     _check(lib.qzc_pass_plan_stats(arr.ctypes.data_as(P(Gate)), arr.size, nbits, mode, out))
     keys = ("passes", "groups", "relaxed_groups", "gates", "fast_ops", "pdiag_ops")
     return dict(zip(keys, (int(x) for x in out)))
+
+
+def jit_selftest(gates, nbits: int) -> None:
+    """Compile the widest fused pass of `gates` (on buffer bits of a 2^nbits
+    window) as a runtime-specialised kernel with NVRTC (host only, no GPU);
+    raises with NVRTC's log when the toolchain cannot build it."""
+    lib = load_library()
+    arr = to_array(gates)
+    _check(lib.qzc_jit_selftest(arr.ctypes.data_as(P(Gate)), arr.size, nbits))
+
+
+def jit_wait() -> int:
+    """Block until every queued specialised-pass compile has finished
+    (e.g. after a warm-up run); returns how many were built."""
+    return int(load_library().qzc_jit_wait())
 
 
 def exported_symbols() -> list[str]:

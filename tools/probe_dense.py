@@ -4,7 +4,7 @@ import argparse
 import time
 
 from paper_2309_16979_b200 import circuits
-from paper_2309_16979_b200.engine import Engine
+from paper_2309_16979_b200.engine import Engine, jit_wait
 
 ap = argparse.ArgumentParser()
 ap.add_argument("circuit")
@@ -33,6 +33,10 @@ for rep in range(a.reps):
           f"dec {1e3*st['decode_seconds']:.2f} gates {1e3*st['gate_seconds']:.2f} "
           f"enc {1e3*st['encode_seconds']:.2f} ms payload {sim.payload_bytes()/1e9:.3f} GB "
           f"ratio {st['ratio']:.3f} digest {sim.digest():016x}", flush=True)
+    if rep == 0:
+        t0 = time.perf_counter()
+        built = jit_wait()
+        print(f"  specialised passes built: {built} (waited {time.perf_counter() - t0:.1f} s)", flush=True)
 if a.kprof:
     tot = {}
     for r in eng.kprof_read():
