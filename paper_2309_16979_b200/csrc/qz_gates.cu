@@ -764,15 +764,13 @@ GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_
     return plan;
 }
 
-void upload_plan(const GatePlan &plan, DevPlan &out, cudaStream_t s, uint32_t jit_bits) {
-    out.ngates = plan.gates.size();
-    out.ngroups = plan.groups.size();
-    out.host_passes = plan.passes;
+std::vector<PassDesc> launch_passes(const GatePlan &plan) {
+    std::vector<PassDesc> out = plan.passes;
     // kernel case set per pass: the narrow one when every fast-list entry of
     // every group is in it (and no group needs the shared-memory generic path)
     static const bool narrow_off = getenv("QZ_NO_NARROW") != nullptr;
     static const bool wmap_off = getenv("QZ_NO_WMAP") != nullptr;
-    for (PassDesc &pd : out.host_passes) {
+    for (PassDesc &pd : out) {
         pd.wmap = wmap_off ? 0u : 1u;
         pd.variant = kPassAll;
         for (int S : {kPassDiagH, kPassGen}) {
@@ -801,6 +799,13 @@ void upload_plan(const GatePlan &plan, DevPlan &out, cudaStream_t s, uint32_t ji
             fprintf(stderr, "\n");
         }
     }
+    return out;
+}
+
+void upload_plan(const GatePlan &plan, DevPlan &out, cudaStream_t s, uint32_t jit_bits) {
+    out.ngates = plan.gates.size();
+    out.ngroups = plan.groups.size();
+    out.host_passes = launch_passes(plan);
     out.jit.assign(out.host_passes.size(), nullptr);
     if (jit_bits)
         for (size_t p = 0; p < out.host_passes.size(); ++p) out.jit[p] = jit_request(plan, out.host_passes[p], jit_bits);

@@ -58,6 +58,8 @@ struct DevPlan {
 };
 // Stream-ordered upload into `out`, reusing its device buffers when they are
 // large enough (no allocator calls on the steady-state stage loop).
+// The plan's passes with their launch fields set (kernel variant, thread map).
+std::vector<PassDesc> launch_passes(const GatePlan &plan);
 // jit_bits > 0: also queue runtime-specialised kernels for the plan's
 // full-tile passes over 2^jit_bits windows (used once built).
 void upload_plan(const GatePlan &plan, DevPlan &out, cudaStream_t s, uint32_t jit_bits = 0);

@@ -7,6 +7,7 @@
 #include <dlfcn.h>
 #include <nvrtc.h>
 
+#include <atomic>
 #include <condition_variable>
 #include <cstdio>
 #include <cstdlib>
@@ -187,6 +188,14 @@ std::unordered_map<std::string, std::shared_ptr<JitPass>> g_cache;
 
 void compile_job(const std::shared_ptr<JitPass> &j) {
     const Nvrtc &n = nvrtc();
+    if (const char *dir = getenv("QZ_JIT_DUMP")) {   // inspection: write the source
+        static std::atomic<int> seq{0};
+        const std::string path = std::string(dir) + "/qz_jit_" + std::to_string(seq++) + ".cu";
+        if (FILE *f = std::fopen(path.c_str(), "w")) {
+            std::fputs(j->source.c_str(), f);
+            std::fclose(f);
+        }
+    }
     std::string cubin, log;
     bool ok = n.ok;
     if (ok) {
@@ -194,9 +203,11 @@ void compile_job(const std::shared_ptr<JitPass> &j) {
         ok = n.create(&prog, j->source.c_str(), "qz_jit_pass.cu", kJitHeaderCount, kJitHeaderSrc, kJitHeaderNames) ==
              NVRTC_SUCCESS;
         if (ok) {
+            static const std::string ctas =
+                std::string("-DQZ_MIN_CTAS=") + (getenv("QZ_JIT_MIN_CTAS") ? getenv("QZ_JIT_MIN_CTAS") : "3");
             const char *opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "--fmad=false", "-lineinfo",
-                                  "-DQZ_JIT_SOURCE=1"};
-            const nvrtcResult rc = n.compile(prog, 5, opts);
+                                  "-DQZ_JIT_SOURCE=1", ctas.c_str()};
+            const nvrtcResult rc = n.compile(prog, 6, opts);
             size_t ls = 0;
             n.log_size(prog, &ls);
             log.resize(ls);
@@ -372,19 +383,26 @@ int qzc_jit_selftest(const qzc_gate *gates, uint64_t ngates, uint32_t nbits) {
         std::vector<DevGate> dg;
         for (uint64_t i = 0; i < ngates; ++i) dg.push_back(make_dev_gate(gates[i]));
         const GatePlan gp = build_passes(dg, nbits, kTileBits, true, 1);
-        for (const PassDesc &pd : gp.passes) {
+        static const bool all = getenv("QZ_JIT_SELFTEST_ALL") != nullptr;   // every pass (inspection)
+        std::vector<std::shared_ptr<JitPass>> jobs;
+        for (const PassDesc &pd : launch_passes(gp)) {
             if (pd.kind != PASS_TILE || pd.k != kTileBits) continue;
-            auto j = request(gp, pd);
+            jobs.push_back(request(gp, pd));
+            if (!all) break;
+        }
+        if (jobs.empty()) {
+            qz::last_error() = "jit: no full-tile pass in the plan";
+            return QZC_EINVAL;
+        }
+        for (auto &j : jobs) {
             std::unique_lock<std::mutex> lk(j->mu);
             j->cv.wait(lk, [&] { return j->compiled; });
             if (j->failed) {
                 qz::last_error() = "jit: " + j->log;
                 return QZC_EDEVICE;
             }
-            return QZC_OK;
         }
-        qz::last_error() = "jit: no full-tile pass in the plan";
-        return QZC_EINVAL;
+        return QZC_OK;
     } catch (const std::exception &e) {
         qz::last_error() = e.what();
         return QZC_EINVAL;
