@@ -288,9 +288,11 @@ def peaks() -> tuple[float, str]:
 
 
 def family(name: str) -> str:
-    if name.startswith("tile_pass_reg") or name == "tile_swaps":
+    if name.startswith(("tile_pass_reg", "tile_pass_jit")):
         return "gate_pass"
-    if name in ("k_dec_lossy_warp", "k_dec_lossy", "k_dec_lossless"):
+    if name == "tile_swaps":
+        return "swap_pass"
+    if name in ("k_dec_lossy_seg", "k_dec_lossy_warp", "k_dec_lossy", "k_dec_lossless"):
         return "decode"
     if name in ("k_enc_lossy", "k_enc_lossless"):
         return "encode"

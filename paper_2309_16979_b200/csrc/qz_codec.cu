@@ -1579,7 +1579,7 @@ void launch_decode(const uint8_t *arena, const DecIdx *idx, const uint64_t *slot
     static const int force = getenv("QZ_DEC_KERNEL") ? (std::string(getenv("QZ_DEC_KERNEL")) == "seg" ? 1 : 0) : -1;
     const bool seg = g.lossy && g.N >= 64 && !sparse && (force >= 0 ? force == 1 : g.dense_hint != 0);
     KProfScope prof(s, cond ? "replay_decode" : seg ? "k_dec_lossy_seg" : (g.lossy && g.N >= 32 && !sparse) ? "k_dec_lossy_warp"
-                                            : g.lossy ? "k_dec_lossy" : "k_dec_lossless", 0, dense);
+                                            : g.lossy ? "k_dec_lossy" : "k_dec_lossless", 0, cond ? 0.0 : dense);
     // dense payloads: warp per chunk-half (parallel RLE expansion, serial
     // predictor chain only); a store known to be mostly zero runs (right
     // after init): thread per chunk-half with run fills

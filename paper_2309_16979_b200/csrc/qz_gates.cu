@@ -904,7 +904,7 @@ void launch_pass(const DevPlan &plan, const PassDesc &pd, const double2 *src, do
     // `tag` is the pass's index in `plan`
     JitPass *jit = tag < plan.jit.size() && plan.jit[tag] && jit_ready(*plan.jit[tag]) ? plan.jit[tag].get() : nullptr;
     KProfScope prof(s, cond ? "replay_pass" : pd.kind == PASS_SWAPS ? "tile_swaps" : (jit ? kJitName : kName)[pd.variant % 3],
-                    tag, 32.0 * double(uint64_t(1) << nbits));
+                    tag, cond ? 0.0 : 32.0 * double(uint64_t(1) << nbits));   // replays: no-ops unless flagged
     if (pd.kind == PASS_SWAPS) {
         const uint64_t tiles = uint64_t(1) << (nbits > 2 * kSwapLow ? nbits - 2 * kSwapLow : 0);
         const uint64_t grid = std::min<uint64_t>(std::max<uint64_t>(tiles, 1), uint64_t(kNumSMs) * 8);
