@@ -802,13 +802,58 @@ std::vector<PassDesc> launch_passes(const GatePlan &plan) {
     return out;
 }
 
-void upload_plan(const GatePlan &plan, DevPlan &out, cudaStream_t s, uint32_t jit_bits) {
+bool gate_diagonal(const DevGate &g) {
+    for (uint32_t r = 0; r < g.dim; ++r)
+        for (uint32_t c = 0; c < g.dim; ++c)
+            if (r != c && ((g.kinds >> (4 * (r * g.dim + c))) & 15u) != CK_ZERO) return false;
+    return true;
+}
+
+bool gate_keeps_pos_zero(const DevGate &g) { return maps_pos_zero(g); }
+
+Fresh fresh_gate(Fresh f, uint32_t op, uint32_t nq, uint32_t b0, uint32_t b1, uint64_t kinds, bool diagonal) {
+    auto bit = [](uint64_t x, uint32_t b) { return (x >> b) & 1; };
+    const uint64_t m0 = uint64_t(1) << b0, m1 = nq == 2 ? uint64_t(1) << b1 : 0;
+    if (diagonal) return f;
+    if (nq == 2 && op == OP_CX) {
+        // basis states to basis states: a fresh control keeps the target's
+        // freshness (and flips its value when 1); a superposed one ends it
+        if (bit(f.mask, b0)) {
+            if (bit(f.val, b0)) f.val ^= m1;
+        } else {
+            f.mask &= ~m1;
+        }
+    } else if (nq == 2 && op == OP_SWAP) {
+        const uint64_t a = bit(f.mask, b0), b = bit(f.mask, b1), va = bit(f.val, b0), vb = bit(f.val, b1);
+        f.mask = (f.mask & ~(m0 | m1)) | (b << b0) | (a << b1);
+        f.val = (f.val & ~(m0 | m1)) | (vb << b0) | (va << b1);
+    } else if (nq == 1 && op == OP_GEN1 && (kinds & 0xFFFF) == ((uint64_t(CK_ONE) << 4) | (uint64_t(CK_ONE) << 8))) {
+        f.val ^= m0;   // X
+    } else {
+        f.mask &= ~(m0 | m1);
+    }
+    f.val &= f.mask;
+    return f;
+}
+
+Fresh fresh_after(const std::vector<DevGate> &dg, size_t g0, size_t g1, Fresh f) {
+    for (size_t i = g0; i < g1 && f.mask; ++i) {
+        const DevGate &g = dg[i];
+        if (!maps_pos_zero(g)) return Fresh{};
+        f = fresh_gate(f, g.op, g.nq, g.b0, g.b1, g.kinds, gate_diagonal(g));
+    }
+    return f;
+}
+
+void upload_plan(const GatePlan &plan, DevPlan &out, cudaStream_t s, uint32_t jit_bits,
+                 const std::vector<Fresh> &fresh) {
     out.ngates = plan.gates.size();
     out.ngroups = plan.groups.size();
     out.host_passes = launch_passes(plan);
     out.jit.assign(out.host_passes.size(), nullptr);
     if (jit_bits)
-        for (size_t p = 0; p < out.host_passes.size(); ++p) out.jit[p] = jit_request(plan, out.host_passes[p], jit_bits);
+        for (size_t p = 0; p < out.host_passes.size(); ++p)
+            out.jit[p] = jit_request(plan, out.host_passes[p], jit_bits, p < fresh.size() ? fresh[p] : Fresh{});
     out.relaxed = false;
     for (const PassDesc &pd : plan.passes) out.relaxed |= pd.relaxed != 0;
     out.replay_range.clear();
@@ -855,8 +900,8 @@ unsigned long long *debug_counters() {
         init = true;
         const char *e = getenv("QZ_DEBUG_COUNTERS");
         if (e && *e == '1') {
-            QZ_CUDA(cudaMalloc(&ptr, 8 * 8));
-            QZ_CUDA(cudaMemset(ptr, 0, 8 * 8));
+            QZ_CUDA(cudaMalloc(&ptr, 8 * 16));
+            QZ_CUDA(cudaMemset(ptr, 0, 8 * 16));
         }
     }
     return ptr;
@@ -865,8 +910,11 @@ unsigned long long *debug_counters() {
 void dump_debug_counters() {
     unsigned long long *p = debug_counters();
     if (!p) return;
-    unsigned long long h[8];
+    unsigned long long h[16];
     QZ_CUDA(cudaMemcpy(h, p, sizeof h, cudaMemcpyDeviceToHost));
+    if (h[8] | h[9] | h[15])
+        fprintf(stderr, "qz group clocks (CTA-thread-0 cycles): load+census=%llu g0=%llu g1=%llu g2=%llu g3=%llu "
+                        "g4=%llu g5+=%llu store=%llu\n", h[8], h[9], h[10], h[11], h[12], h[13], h[14], h[15]);
     fprintf(stderr, "qz counters: tiles_skipped=%llu grp_pz_skip=%llu grp_mask=%llu grp_fast=%llu "
                     "grp_exact=%llu grp_fast_then_exact=%llu\n",
             h[0], h[1], h[2], h[3], h[4], h[5]);
@@ -892,6 +940,15 @@ void set_attrs() {
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
         attr_set = true;
     }
+}
+
+// QZ_DEBUG_COUNTERS=1 QZ_COUNTERS_PER_PASS=1: counters after every pass (synchronous)
+void dump_pass_counters(const PassDesc &pd, uint32_t tag, const uint32_t *cond, cudaStream_t s) {
+    static const bool per_pass = getenv("QZ_COUNTERS_PER_PASS") != nullptr;
+    if (!per_pass || !debug_counters()) return;
+    QZ_CUDA(cudaStreamSynchronize(s));
+    fprintf(stderr, "qz pass %u (k=%u groups=%u%s):\n", tag, pd.k, pd.ngroups, cond ? ", replay" : "");
+    dump_debug_counters();
 }
 
 void launch_pass(const DevPlan &plan, const PassDesc &pd, const double2 *src, double2 *dst,
@@ -944,6 +1001,7 @@ void launch_pass(const DevPlan &plan, const PassDesc &pd, const double2 *src, do
                             &a_ctr, &a_flag, &a_cond, &a_nz, &a_cbits};
             if (jit_launch(*jit, (unsigned)grid, threads, smem, s, args)) {
                 QZ_CHECK_LAUNCH();
+                dump_pass_counters(pd, tag, cond, s);
                 return;
             }
         }
@@ -955,6 +1013,7 @@ void launch_pass(const DevPlan &plan, const PassDesc &pd, const double2 *src, do
                                                    usable ? nz.slot : nullptr, nz.cbits);
     }
     QZ_CHECK_LAUNCH();
+    dump_pass_counters(pd, tag, cond, s);
 }
 
 } // namespace

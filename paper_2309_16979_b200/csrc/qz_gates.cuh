@@ -60,9 +60,28 @@ struct DevPlan {
 // large enough (no allocator calls on the steady-state stage loop).
 // The plan's passes with their launch fields set (kernel variant, thread map).
 std::vector<PassDesc> launch_passes(const GatePlan &plan);
+
+// Buffer bits statically in a basis value ("fresh": no non-diagonal gate has
+// touched them since |0...0>): every amplitude whose bit b (in mask) differs
+// from val's bit b is +0.  The runtime-specialised passes skip products on
+// registers that are +0 this way (qz_jit.cu).
+struct Fresh {
+    uint64_t mask = 0, val = 0;
+};
+bool gate_diagonal(const DevGate &g);
+// every row maps an all-(+0) input to +0 (zeros keep their sign)
+bool gate_keeps_pos_zero(const DevGate &g);
+// Fresh state after gates [g0, g1): a non-diagonal gate ends its qubits'
+// freshness, a gate that may turn +0 into -0 ends all of it.
+Fresh fresh_after(const std::vector<DevGate> &dg, size_t g0, size_t g1, Fresh f);
+// one gate (buffer bits b0, b1): X / CX / SWAP permute basis states and keep
+// fresh bits fresh (values updated); other non-diagonal gates end them
+Fresh fresh_gate(Fresh f, uint32_t op, uint32_t nq, uint32_t b0, uint32_t b1, uint64_t kinds, bool diagonal);
 // jit_bits > 0: also queue runtime-specialised kernels for the plan's
 // full-tile passes over 2^jit_bits windows (used once built).
-void upload_plan(const GatePlan &plan, DevPlan &out, cudaStream_t s, uint32_t jit_bits = 0);
+// (fresh: per pass, the fresh state at its start; empty = none)
+void upload_plan(const GatePlan &plan, DevPlan &out, cudaStream_t s, uint32_t jit_bits = 0,
+                 const std::vector<Fresh> &fresh = {});
 void free_plan(DevPlan &p);   // releases the device buffers
 
 // Per-chunk-slot "may be nonzero" words of a window (slot = amplitude >> cbits):

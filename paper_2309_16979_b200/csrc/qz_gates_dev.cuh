@@ -227,8 +227,11 @@ __device__ __forceinline__ void reg_apply2(double2 (&v)[NB], const TileGate &g) 
 // `bad`; the caller then redoes the whole group on the exact path.
 // SPEC = 1: every row +0-safe and the kinds are the template's (no checks,
 // no kind branches); SPEC = 0: run-time kinds and safety.
+// zm (every op below): registers statically +0 at op entry (runtime-specialised
+// passes over fresh qubits, qz_jit.cu; the op maps all-(+0) inputs to +0):
+// their products are skipped.  A compile-time constant where it is nonzero.
 template <int R, int K0 = -1, int K1 = -1, int SPEC = 0>
-__device__ __forceinline__ void fast_diag(double2 (&v)[NB], const TileGate &g, bool &bad) {
+__device__ __forceinline__ void fast_diag(double2 (&v)[NB], const TileGate &g, bool &bad, uint32_t zm = 0) {
     constexpr int sh = 1 << R;
     const uint32_t k00 = uint32_t(g.kinds) & 15u, k11 = uint32_t(g.kinds >> 12) & 15u;
     const double2 m00 = g.m[0], m11 = g.m[3];
@@ -238,7 +241,7 @@ __device__ __forceinline__ void fast_diag(double2 (&v)[NB], const TileGate &g, b
         const int i = izb(p, R), j = i | sh;
         const double2 a = v[i], b = v[j];
         // a zero in a row that is not +0-safe: that row's exact value
-        if (K0 == CK_ONE || (K0 < 0 && k00 == CK_ONE)) {
+        if (K0 == CK_ONE || (K0 < 0 && k00 == CK_ONE) || ((zm >> i) & 1)) {
         } else {
             double2 o = termk<K0>(k00, m00, a);
             if (u0 && zc(o)) {
@@ -247,7 +250,7 @@ __device__ __forceinline__ void fast_diag(double2 (&v)[NB], const TileGate &g, b
             }
             v[i] = o;
         }
-        if (K1 == CK_ONE || (K1 < 0 && k11 == CK_ONE)) {
+        if (K1 == CK_ONE || (K1 < 0 && k11 == CK_ONE) || ((zm >> j) & 1)) {
         } else {
             double2 o = termk<K1>(k11, m11, b);
             if (u1 && zc(o)) {
@@ -260,7 +263,7 @@ __device__ __forceinline__ void fast_diag(double2 (&v)[NB], const TileGate &g, b
 }
 
 template <int R, int K00 = -1, int K01 = -1, int K10 = -1, int K11 = -1, int SPEC = 0>
-__device__ __forceinline__ void fast_gen1(double2 (&v)[NB], const TileGate &g, bool &bad) {
+__device__ __forceinline__ void fast_gen1(double2 (&v)[NB], const TileGate &g, bool &bad, uint32_t zm = 0) {
     constexpr int sh = 1 << R;
     const uint32_t kd = uint32_t(g.kinds);
     const uint32_t k00 = kd & 15u, k01 = (kd >> 4) & 15u, k10 = (kd >> 8) & 15u, k11 = (kd >> 12) & 15u;
@@ -268,6 +271,7 @@ __device__ __forceinline__ void fast_gen1(double2 (&v)[NB], const TileGate &g, b
 #pragma unroll
     for (int p = 0; p < NB / 2; ++p) {
         const int i = izb(p, R), j = i | sh;
+        if ((zm >> i) & (zm >> j) & 1) continue;
         const double2 a = v[i], b = v[j];
         double2 oi, oj;
         if constexpr (SPEC) {
@@ -318,10 +322,10 @@ __device__ __forceinline__ void fast_cx(double2 (&v)[NB]) {
 }
 
 template <int A, int B>
-__device__ __forceinline__ void fast_cz(double2 (&v)[NB], const TileGate &g, bool &bad) {
+__device__ __forceinline__ void fast_cz(double2 (&v)[NB], const TileGate &g, bool &bad, uint32_t zm = 0) {
 #pragma unroll
     for (int i = 0; i < NB; ++i)
-        if (((i >> A) & 1) && ((i >> B) & 1)) {
+        if (((i >> A) & 1) && ((i >> B) & 1) && !((zm >> i) & 1)) {
             const double2 o = make_double2(dneg(v[i].x), dneg(v[i].y));
             if (zc(o)) {
                 // the -1 row is not +0-safe: its exact value (the other three
@@ -350,7 +354,7 @@ __device__ __forceinline__ void fast_swap(double2 (&v)[NB]) {
 // CP5 on (A, B): p01 <- m3(m2 v01), p10 <- m2(m1 v10), p11 <- m3(m1 v11)
 // (the CX swaps folded into the indexing; same products, same order).
 template <int A, int B, int SPEC = 0>
-__device__ __forceinline__ void fast_cp5(double2 (&v)[NB], const TileGate &g, bool &bad) {
+__device__ __forceinline__ void fast_cp5(double2 (&v)[NB], const TileGate &g, bool &bad, uint32_t zm = 0) {
     const uint32_t k1 = uint32_t(g.kinds) & 15u, k2 = uint32_t(g.kinds >> 4) & 15u,
                    k3 = uint32_t(g.kinds >> 8) & 15u;
     const double2 m1 = g.m[0], m2 = g.m[1], m3 = g.m[2];
@@ -360,28 +364,34 @@ __device__ __forceinline__ void fast_cp5(double2 (&v)[NB], const TileGate &g, bo
     for (int i = 0; i < NB; ++i) {
         if (((i >> A) & 1) || ((i >> B) & 1)) continue;
         const int i01 = i | (1 << B), i10 = i | (1 << A), i11 = i | (1 << A) | (1 << B);
-        double2 x01 = termk<KC>(k2, m2, v[i01]);
-        if (u2) bad |= zc(x01);
-        x01 = termk<KC>(k3, m3, x01);
-        if (u3) bad |= zc(x01);
-        double2 x10 = termk<KC>(k1, m1, v[i10]);
-        if (u1) bad |= zc(x10);
-        x10 = termk<KC>(k2, m2, x10);
-        if (u2) bad |= zc(x10);
-        double2 x11 = termk<KC>(k1, m1, v[i11]);
-        if (u1) bad |= zc(x11);
-        x11 = termk<KC>(k3, m3, x11);
-        if (u3) bad |= zc(x11);
-        v[i01] = x01;
-        v[i10] = x10;
-        v[i11] = x11;
+        if (!((zm >> i01) & 1)) {
+            double2 x01 = termk<KC>(k2, m2, v[i01]);
+            if (u2) bad |= zc(x01);
+            x01 = termk<KC>(k3, m3, x01);
+            if (u3) bad |= zc(x01);
+            v[i01] = x01;
+        }
+        if (!((zm >> i10) & 1)) {
+            double2 x10 = termk<KC>(k1, m1, v[i10]);
+            if (u1) bad |= zc(x10);
+            x10 = termk<KC>(k2, m2, x10);
+            if (u2) bad |= zc(x10);
+            v[i10] = x10;
+        }
+        if (!((zm >> i11) & 1)) {
+            double2 x11 = termk<KC>(k1, m1, v[i11]);
+            if (u1) bad |= zc(x11);
+            x11 = termk<KC>(k3, m3, x11);
+            if (u3) bad |= zc(x11);
+            v[i11] = x11;
+        }
     }
 }
 
 // CXD on (A, B), D = diag(d0, d1) on B: p00 <- d0 v00, p01 <- d1 v01,
 // p10 <- d1 v10, p11 <- d0 v11.
 template <int A, int B, int SPEC = 0>
-__device__ __forceinline__ void fast_cxd(double2 (&v)[NB], const TileGate &g, bool &bad) {
+__device__ __forceinline__ void fast_cxd(double2 (&v)[NB], const TileGate &g, bool &bad, uint32_t zm = 0) {
     const uint32_t k0 = uint32_t(g.kinds) & 15u, k1 = uint32_t(g.kinds >> 4) & 15u;
     const double2 d0 = g.m[0], d1 = g.m[1];
     const bool u0 = !SPEC && !(g.srow & 1), u1 = !SPEC && !(g.srow & 2);
@@ -390,14 +400,26 @@ __device__ __forceinline__ void fast_cxd(double2 (&v)[NB], const TileGate &g, bo
     for (int i = 0; i < NB; ++i) {
         if (((i >> A) & 1) || ((i >> B) & 1)) continue;
         const int i01 = i | (1 << B), i10 = i | (1 << A), i11 = i | (1 << A) | (1 << B);
-        const double2 x00 = termk<KC>(k0, d0, v[i]), x01 = termk<KC>(k1, d1, v[i01]);
-        const double2 x10 = termk<KC>(k1, d1, v[i10]), x11 = termk<KC>(k0, d0, v[i11]);
-        if (u0) bad |= zc(x00) | zc(x11);
-        if (u1) bad |= zc(x01) | zc(x10);
-        v[i] = x00;
-        v[i01] = x01;
-        v[i10] = x10;
-        v[i11] = x11;
+        if (!((zm >> i) & 1)) {
+            const double2 x00 = termk<KC>(k0, d0, v[i]);
+            if (u0) bad |= zc(x00);
+            v[i] = x00;
+        }
+        if (!((zm >> i01) & 1)) {
+            const double2 x01 = termk<KC>(k1, d1, v[i01]);
+            if (u1) bad |= zc(x01);
+            v[i01] = x01;
+        }
+        if (!((zm >> i10) & 1)) {
+            const double2 x10 = termk<KC>(k1, d1, v[i10]);
+            if (u1) bad |= zc(x10);
+            v[i10] = x10;
+        }
+        if (!((zm >> i11) & 1)) {
+            const double2 x11 = termk<KC>(k0, d0, v[i11]);
+            if (u0) bad |= zc(x11);
+            v[i11] = x11;
+        }
     }
 }
 
@@ -406,7 +428,7 @@ __device__ __forceinline__ void fast_cxd(double2 (&v)[NB], const TileGate &g, bo
 // SPEC = 1: every step CPLX and +0-safe (no kind branches, no checks).
 template <int R, int SPEC = 0>
 __device__ __forceinline__ void fast_pdiag(double2 (&v)[NB], const TileGate &g, uint32_t var,
-                                           bool &bad) {
+                                           bool &bad, uint32_t zm = 0) {
     const uint32_t kd = uint32_t(g.kinds >> (16 * var));
     const uint32_t sf = g.srow >> (4 * var);
     constexpr int KC = SPEC ? int(CK_CPLX) : -1;
@@ -422,6 +444,7 @@ __device__ __forceinline__ void fast_pdiag(double2 (&v)[NB], const TileGate &g, 
 #pragma unroll
             for (int i = 0; i < NB; ++i) {
                 if (R < kRegBits && ((i >> R) & 1) != st) continue;
+                if ((zm >> i) & 1) continue;
                 v[i] = termk<KC>(kind, m, v[i]);
                 if (chk) bad |= zc(v[i]);
             }
@@ -433,7 +456,7 @@ __device__ __forceinline__ void fast_pdiag(double2 (&v)[NB], const TileGate &g, 
 // checks; per op only the thread's variant and register bit are resolved.
 template <int R>
 __device__ __forceinline__ void pdiag_spec(double2 (&v)[NB], const double2 *__restrict__ mm,
-                                           uint32_t act) {
+                                           uint32_t act, uint32_t zm = 0) {
 #pragma unroll
     for (int st = 0; st < (R < kRegBits ? 2 : 1); ++st) {
 #pragma unroll
@@ -444,6 +467,7 @@ __device__ __forceinline__ void pdiag_spec(double2 (&v)[NB], const double2 *__re
 #pragma unroll
             for (int i = 0; i < NB; ++i) {
                 if (R < kRegBits && ((i >> R) & 1) != st) continue;
+                if ((zm >> i) & 1) continue;
                 v[i] = termk<CK_CPLX>(CK_CPLX, m, v[i]);
             }
         }
@@ -466,13 +490,13 @@ __device__ __forceinline__ uint32_t pdiag_var(const TileGate &g, uint64_t gidx) 
 // A run mixes uniform ops (no register bit) with ops on register bit R.
 template <int R>
 __device__ __forceinline__ void run_pdiag_r(double2 (&v)[NB], const TileGate *__restrict__ gp,
-                                            uint32_t n, uint64_t gidx) {
+                                            uint32_t n, uint64_t gidx, uint32_t zm = 0) {
     for (uint32_t q = 0; q < n; ++q) {
         const TileGate &g = gp[q];
         const uint32_t var = pdiag_var(g, gidx);
         const uint32_t act = (g.steps >> (4 * var)) & 15u;
-        if (R == kRegBits || g.nq == 0) pdiag_spec<kRegBits>(v, g.m + 4 * var, act);
-        else pdiag_spec<R>(v, g.m + 4 * var, act);
+        if (R == kRegBits || g.nq == 0) pdiag_spec<kRegBits>(v, g.m + 4 * var, act, zm);
+        else pdiag_spec<R>(v, g.m + 4 * var, act, zm);
     }
 }
 
@@ -481,330 +505,330 @@ __device__ __forceinline__ void run_pdiag_r(double2 (&v)[NB], const TileGate *__
 // them directly in the plan's order.
 template <int C>
 __device__ __forceinline__ uint32_t fast_cid(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q,
-                                             uint64_t gidx, bool &bad);
-template <> __device__ __forceinline__ uint32_t fast_cid<0>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; run_pdiag_r<0>(v, fp + q, g.run, gidx); return g.run;
+                                             uint64_t gidx, bool &bad, uint32_t zm = 0);
+template <> __device__ __forceinline__ uint32_t fast_cid<0>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; run_pdiag_r<0>(v, fp + q, g.run, gidx, zm); return g.run;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<1>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; run_pdiag_r<1>(v, fp + q, g.run, gidx); return g.run;
+template <> __device__ __forceinline__ uint32_t fast_cid<1>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; run_pdiag_r<1>(v, fp + q, g.run, gidx, zm); return g.run;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<2>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; run_pdiag_r<2>(v, fp + q, g.run, gidx); return g.run;
+template <> __device__ __forceinline__ uint32_t fast_cid<2>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; run_pdiag_r<2>(v, fp + q, g.run, gidx, zm); return g.run;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<3>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; run_pdiag_r<3>(v, fp + q, g.run, gidx); return g.run;
+template <> __device__ __forceinline__ uint32_t fast_cid<3>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; run_pdiag_r<3>(v, fp + q, g.run, gidx, zm); return g.run;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<4>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_pdiag<0, 0>(v, g, pdiag_var(g, gidx), bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<4>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_pdiag<0, 0>(v, g, pdiag_var(g, gidx), bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<5>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_pdiag<0, 1>(v, g, pdiag_var(g, gidx), bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<5>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_pdiag<0, 1>(v, g, pdiag_var(g, gidx), bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<6>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_pdiag<1, 0>(v, g, pdiag_var(g, gidx), bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<6>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_pdiag<1, 0>(v, g, pdiag_var(g, gidx), bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<7>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_pdiag<1, 1>(v, g, pdiag_var(g, gidx), bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<7>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_pdiag<1, 1>(v, g, pdiag_var(g, gidx), bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<8>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_pdiag<2, 0>(v, g, pdiag_var(g, gidx), bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<8>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_pdiag<2, 0>(v, g, pdiag_var(g, gidx), bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<9>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_pdiag<2, 1>(v, g, pdiag_var(g, gidx), bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<9>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_pdiag<2, 1>(v, g, pdiag_var(g, gidx), bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<10>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_pdiag<3, 0>(v, g, pdiag_var(g, gidx), bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<10>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_pdiag<3, 0>(v, g, pdiag_var(g, gidx), bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<11>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_pdiag<3, 1>(v, g, pdiag_var(g, gidx), bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<11>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_pdiag<3, 1>(v, g, pdiag_var(g, gidx), bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<12>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_diag<0, CK_ONE, CK_CPLX, 1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<12>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_diag<0, CK_ONE, CK_CPLX, 1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<13>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_diag<0, CK_CPLX, CK_CPLX, 1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<13>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_diag<0, CK_CPLX, CK_CPLX, 1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<14>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_diag<0, CK_ONE, CK_CPLX, 2>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<14>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_diag<0, CK_ONE, CK_CPLX, 2>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<15>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_diag<0, CK_CPLX, CK_CPLX, 2>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<15>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_diag<0, CK_CPLX, CK_CPLX, 2>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<16>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_diag<0>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<16>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_diag<0>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<17>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_diag<1, CK_ONE, CK_CPLX, 1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<17>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_diag<1, CK_ONE, CK_CPLX, 1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<18>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_diag<1, CK_CPLX, CK_CPLX, 1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<18>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_diag<1, CK_CPLX, CK_CPLX, 1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<19>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_diag<1, CK_ONE, CK_CPLX, 2>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<19>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_diag<1, CK_ONE, CK_CPLX, 2>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<20>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_diag<1, CK_CPLX, CK_CPLX, 2>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<20>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_diag<1, CK_CPLX, CK_CPLX, 2>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<21>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_diag<1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<21>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_diag<1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<22>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_diag<2, CK_ONE, CK_CPLX, 1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<22>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_diag<2, CK_ONE, CK_CPLX, 1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<23>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_diag<2, CK_CPLX, CK_CPLX, 1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<23>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_diag<2, CK_CPLX, CK_CPLX, 1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<24>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_diag<2, CK_ONE, CK_CPLX, 2>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<24>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_diag<2, CK_ONE, CK_CPLX, 2>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<25>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_diag<2, CK_CPLX, CK_CPLX, 2>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<25>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_diag<2, CK_CPLX, CK_CPLX, 2>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<26>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_diag<2>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<26>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_diag<2>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<27>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<0, CK_REAL, CK_IMAG, CK_IMAG, CK_REAL, 1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<27>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<0, CK_REAL, CK_IMAG, CK_IMAG, CK_REAL, 1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<28>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<0, CK_REAL, CK_REAL, CK_REAL, CK_REAL, 1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<28>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<0, CK_REAL, CK_REAL, CK_REAL, CK_REAL, 1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<29>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<0, CK_CPLX, CK_CPLX, CK_CPLX, CK_CPLX, 1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<29>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<0, CK_CPLX, CK_CPLX, CK_CPLX, CK_CPLX, 1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<30>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<0, CK_REAL, CK_IMAG, CK_IMAG, CK_REAL, 2>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<30>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<0, CK_REAL, CK_IMAG, CK_IMAG, CK_REAL, 2>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<31>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<0, CK_REAL, CK_REAL, CK_REAL, CK_REAL, 2>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<31>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<0, CK_REAL, CK_REAL, CK_REAL, CK_REAL, 2>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<32>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<0, CK_CPLX, CK_CPLX, CK_CPLX, CK_CPLX, 2>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<32>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<0, CK_CPLX, CK_CPLX, CK_CPLX, CK_CPLX, 2>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<33>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<0, CK_ZERO, CK_ONE, CK_ONE, CK_ZERO, 1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<33>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<0, CK_ZERO, CK_ONE, CK_ONE, CK_ZERO, 1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<34>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<0, CK_ZERO, CK_IMAG, CK_IMAG, CK_ZERO, 1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<34>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<0, CK_ZERO, CK_IMAG, CK_IMAG, CK_ZERO, 1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<35>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<0, CK_REAL, CK_CPLX, CK_CPLX, CK_CPLX, 1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<35>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<0, CK_REAL, CK_CPLX, CK_CPLX, CK_CPLX, 1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<36>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<0, CK_REAL, CK_CPLX, CK_REAL, CK_CPLX, 1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<36>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<0, CK_REAL, CK_CPLX, CK_REAL, CK_CPLX, 1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<37>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<0, CK_ZERO, CK_ONE, CK_ONE, CK_ZERO, 2>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<37>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<0, CK_ZERO, CK_ONE, CK_ONE, CK_ZERO, 2>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<38>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<0, CK_ZERO, CK_IMAG, CK_IMAG, CK_ZERO, 2>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<38>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<0, CK_ZERO, CK_IMAG, CK_IMAG, CK_ZERO, 2>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<39>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<0, CK_REAL, CK_CPLX, CK_CPLX, CK_CPLX, 2>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<39>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<0, CK_REAL, CK_CPLX, CK_CPLX, CK_CPLX, 2>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<40>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<0, CK_REAL, CK_CPLX, CK_REAL, CK_CPLX, 2>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<40>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<0, CK_REAL, CK_CPLX, CK_REAL, CK_CPLX, 2>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<41>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<0>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<41>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<0>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<42>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<1, CK_REAL, CK_IMAG, CK_IMAG, CK_REAL, 1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<42>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<1, CK_REAL, CK_IMAG, CK_IMAG, CK_REAL, 1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<43>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<1, CK_REAL, CK_REAL, CK_REAL, CK_REAL, 1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<43>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<1, CK_REAL, CK_REAL, CK_REAL, CK_REAL, 1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<44>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<1, CK_CPLX, CK_CPLX, CK_CPLX, CK_CPLX, 1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<44>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<1, CK_CPLX, CK_CPLX, CK_CPLX, CK_CPLX, 1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<45>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<1, CK_REAL, CK_IMAG, CK_IMAG, CK_REAL, 2>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<45>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<1, CK_REAL, CK_IMAG, CK_IMAG, CK_REAL, 2>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<46>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<1, CK_REAL, CK_REAL, CK_REAL, CK_REAL, 2>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<46>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<1, CK_REAL, CK_REAL, CK_REAL, CK_REAL, 2>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<47>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<1, CK_CPLX, CK_CPLX, CK_CPLX, CK_CPLX, 2>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<47>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<1, CK_CPLX, CK_CPLX, CK_CPLX, CK_CPLX, 2>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<48>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<1, CK_ZERO, CK_ONE, CK_ONE, CK_ZERO, 1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<48>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<1, CK_ZERO, CK_ONE, CK_ONE, CK_ZERO, 1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<49>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<1, CK_ZERO, CK_IMAG, CK_IMAG, CK_ZERO, 1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<49>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<1, CK_ZERO, CK_IMAG, CK_IMAG, CK_ZERO, 1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<50>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<1, CK_REAL, CK_CPLX, CK_CPLX, CK_CPLX, 1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<50>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<1, CK_REAL, CK_CPLX, CK_CPLX, CK_CPLX, 1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<51>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<1, CK_REAL, CK_CPLX, CK_REAL, CK_CPLX, 1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<51>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<1, CK_REAL, CK_CPLX, CK_REAL, CK_CPLX, 1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<52>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<1, CK_ZERO, CK_ONE, CK_ONE, CK_ZERO, 2>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<52>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<1, CK_ZERO, CK_ONE, CK_ONE, CK_ZERO, 2>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<53>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<1, CK_ZERO, CK_IMAG, CK_IMAG, CK_ZERO, 2>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<53>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<1, CK_ZERO, CK_IMAG, CK_IMAG, CK_ZERO, 2>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<54>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<1, CK_REAL, CK_CPLX, CK_CPLX, CK_CPLX, 2>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<54>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<1, CK_REAL, CK_CPLX, CK_CPLX, CK_CPLX, 2>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<55>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<1, CK_REAL, CK_CPLX, CK_REAL, CK_CPLX, 2>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<55>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<1, CK_REAL, CK_CPLX, CK_REAL, CK_CPLX, 2>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<56>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<56>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<57>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<2, CK_REAL, CK_IMAG, CK_IMAG, CK_REAL, 1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<57>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<2, CK_REAL, CK_IMAG, CK_IMAG, CK_REAL, 1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<58>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<2, CK_REAL, CK_REAL, CK_REAL, CK_REAL, 1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<58>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<2, CK_REAL, CK_REAL, CK_REAL, CK_REAL, 1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<59>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<2, CK_CPLX, CK_CPLX, CK_CPLX, CK_CPLX, 1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<59>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<2, CK_CPLX, CK_CPLX, CK_CPLX, CK_CPLX, 1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<60>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<2, CK_REAL, CK_IMAG, CK_IMAG, CK_REAL, 2>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<60>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<2, CK_REAL, CK_IMAG, CK_IMAG, CK_REAL, 2>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<61>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<2, CK_REAL, CK_REAL, CK_REAL, CK_REAL, 2>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<61>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<2, CK_REAL, CK_REAL, CK_REAL, CK_REAL, 2>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<62>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<2, CK_CPLX, CK_CPLX, CK_CPLX, CK_CPLX, 2>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<62>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<2, CK_CPLX, CK_CPLX, CK_CPLX, CK_CPLX, 2>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<63>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<2, CK_ZERO, CK_ONE, CK_ONE, CK_ZERO, 1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<63>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<2, CK_ZERO, CK_ONE, CK_ONE, CK_ZERO, 1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<64>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<2, CK_ZERO, CK_IMAG, CK_IMAG, CK_ZERO, 1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<64>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<2, CK_ZERO, CK_IMAG, CK_IMAG, CK_ZERO, 1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<65>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<2, CK_REAL, CK_CPLX, CK_CPLX, CK_CPLX, 1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<65>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<2, CK_REAL, CK_CPLX, CK_CPLX, CK_CPLX, 1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<66>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<2, CK_REAL, CK_CPLX, CK_REAL, CK_CPLX, 1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<66>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<2, CK_REAL, CK_CPLX, CK_REAL, CK_CPLX, 1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<67>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<2, CK_ZERO, CK_ONE, CK_ONE, CK_ZERO, 2>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<67>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<2, CK_ZERO, CK_ONE, CK_ONE, CK_ZERO, 2>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<68>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<2, CK_ZERO, CK_IMAG, CK_IMAG, CK_ZERO, 2>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<68>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<2, CK_ZERO, CK_IMAG, CK_IMAG, CK_ZERO, 2>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<69>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<2, CK_REAL, CK_CPLX, CK_CPLX, CK_CPLX, 2>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<69>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<2, CK_REAL, CK_CPLX, CK_CPLX, CK_CPLX, 2>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<70>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<2, CK_REAL, CK_CPLX, CK_REAL, CK_CPLX, 2>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<70>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<2, CK_REAL, CK_CPLX, CK_REAL, CK_CPLX, 2>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<71>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<2>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<71>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_gen1<2>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<72>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cp5<0, 1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<72>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cp5<0, 1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<73>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cp5<0, 1, 1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<73>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cp5<0, 1, 1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<74>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cp5<0, 2>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<74>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cp5<0, 2>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<75>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cp5<0, 2, 1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<75>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cp5<0, 2, 1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<76>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cp5<1, 0>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<76>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cp5<1, 0>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<77>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cp5<1, 0, 1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<77>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cp5<1, 0, 1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<78>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cp5<1, 2>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<78>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cp5<1, 2>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<79>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cp5<1, 2, 1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<79>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cp5<1, 2, 1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<80>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cp5<2, 0>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<80>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cp5<2, 0>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<81>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cp5<2, 0, 1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<81>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cp5<2, 0, 1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<82>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cp5<2, 1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<82>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cp5<2, 1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<83>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cp5<2, 1, 1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<83>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cp5<2, 1, 1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<84>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cxd<0, 1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<84>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cxd<0, 1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<85>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cxd<0, 1, 1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<85>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cxd<0, 1, 1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<86>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cxd<0, 2>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<86>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cxd<0, 2>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<87>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cxd<0, 2, 1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<87>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cxd<0, 2, 1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<88>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cxd<1, 0>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<88>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cxd<1, 0>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<89>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cxd<1, 0, 1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<89>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cxd<1, 0, 1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<90>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cxd<1, 2>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<90>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cxd<1, 2>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<91>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cxd<1, 2, 1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<91>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cxd<1, 2, 1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<92>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cxd<2, 0>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<92>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cxd<2, 0>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<93>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cxd<2, 0, 1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<93>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cxd<2, 0, 1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<94>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cxd<2, 1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<94>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cxd<2, 1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<95>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cxd<2, 1, 1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<95>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cxd<2, 1, 1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<96>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cx<0, 1>(v); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<96>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; (void)zm; fast_cx<0, 1>(v); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<97>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cx<0, 2>(v); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<97>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; (void)zm; fast_cx<0, 2>(v); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<98>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cx<1, 0>(v); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<98>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; (void)zm; fast_cx<1, 0>(v); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<99>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cx<1, 2>(v); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<99>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; (void)zm; fast_cx<1, 2>(v); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<100>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cx<2, 0>(v); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<100>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; (void)zm; fast_cx<2, 0>(v); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<101>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cx<2, 1>(v); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<101>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; (void)zm; fast_cx<2, 1>(v); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<102>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cz<0, 1>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<102>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cz<0, 1>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<103>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cz<0, 2>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<103>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cz<0, 2>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<104>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cz<1, 2>(v, g, bad); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<104>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_cz<1, 2>(v, g, bad, zm); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<105>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_swap<0, 1>(v); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<105>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; (void)zm; fast_swap<0, 1>(v); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<106>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_swap<0, 2>(v); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<106>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; (void)zm; fast_swap<0, 2>(v); return 1;
 }
-template <> __device__ __forceinline__ uint32_t fast_cid<107>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad) {
-    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; fast_swap<1, 2>(v); return 1;
+template <> __device__ __forceinline__ uint32_t fast_cid<107>(double2 (&v)[NB], const TileGate *__restrict__ fp, uint32_t q, uint64_t gidx, bool &bad, uint32_t zm) {
+    const TileGate &g = fp[q]; (void)g; (void)gidx; (void)bad; (void)zm; fast_swap<1, 2>(v); return 1;
 }
 
 template <int S>
@@ -1130,6 +1154,9 @@ __device__ __forceinline__ void tile_pass_body(const double2 *__restrict__ src, 
                 continue;
             }
         }
+#ifdef QZ_GROUP_CLOCKS
+        const long long ck_t0 = clock64();
+#endif
 #pragma unroll
         for (int i = 0; i < NB; ++i) {
             const uint32_t l = tid + i * nth;
@@ -1163,6 +1190,12 @@ __device__ __forceinline__ void tile_pass_body(const double2 *__restrict__ src, 
             continue;
         }
         bool clean = __syncthreads_and(okv) != 0;
+#ifdef QZ_GROUP_CLOCKS
+        // inspection: CTA time per phase (thread 0's view, barrier to barrier)
+        // counters[8] load+census, [9 + gi] group gi, [15] store
+        long long ck = clock64();
+        if (counters && tid == 0) atomicAdd(&counters[8], (unsigned long long)(ck - ck_t0));
+#endif
         for (uint32_t gi = 0; gi < pd.ngroups; ++gi) {
             const GroupDesc &G = groups[pd.first_group + gi];
             const TileGate *gp = gates + G.first_gate;
@@ -1256,9 +1289,18 @@ __device__ __forceinline__ void tile_pass_body(const double2 *__restrict__ src, 
 #pragma unroll
                 for (int r = 0; r < NB; ++r) s[addr[r]] = v[r];
             }
+#ifndef QZ_GROUP_CLOCKS
             if (counters) atomicAdd(&counters[path], 1ull);
+#endif
             // the sign-mask and exact paths may leave -0 behind
             clean = __syncthreads_and(path == 1 || path == 3) != 0;
+#ifdef QZ_GROUP_CLOCKS
+            {
+                const long long c2 = clock64();
+                if (counters && tid == 0) atomicAdd(&counters[9 + (gi < 6 ? gi : 5)], (unsigned long long)(c2 - ck));
+                ck = c2;
+            }
+#endif
         }
         double2 out[NB];
 #pragma unroll
@@ -1279,11 +1321,14 @@ __device__ __forceinline__ void tile_pass_body(const double2 *__restrict__ src, 
             }
         }
         __syncthreads();
+#ifdef QZ_GROUP_CLOCKS
+        if (counters && tid == 0) atomicAdd(&counters[15], (unsigned long long)(clock64() - ck));
+#endif
     }
 }
 
 template <int S>
-__global__ void __launch_bounds__(1 << (kTileBits - kRegBits), (kTileBits >= 12 ? 1 : (kTileBits == 11 ? QZ_MIN_CTAS : 4)))
+__global__ void __launch_bounds__(1 << (kTileBits - kRegBits), (kTileBits >= 12 ? 1 : QZ_MIN_CTAS))
 tile_pass_reg(const double2 *__restrict__ src, double2 *__restrict__ dst, uint32_t nbits, PassDesc pd,
               const GroupDesc *__restrict__ groups, const TileGate *__restrict__ gates, uint64_t ntiles,
               unsigned long long *__restrict__ counters, uint32_t *__restrict__ flag,

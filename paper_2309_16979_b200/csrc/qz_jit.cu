@@ -22,7 +22,13 @@
 
 #include "qz_jit.cuh"
 
+#ifndef QZ_MIN_CTAS
+#define QZ_MIN_CTAS 3   // as in qz_gates_dev.cuh
+#endif
+
 namespace qz {
+
+constexpr int NB_HOST = 1 << kRegBits;
 
 namespace {
 
@@ -203,11 +209,17 @@ void compile_job(const std::shared_ptr<JitPass> &j) {
         ok = n.create(&prog, j->source.c_str(), "qz_jit_pass.cu", kJitHeaderCount, kJitHeaderSrc, kJitHeaderNames) ==
              NVRTC_SUCCESS;
         if (ok) {
+            // the build's tile geometry (the device headers' macros)
             static const std::string ctas =
-                std::string("-DQZ_MIN_CTAS=") + (getenv("QZ_JIT_MIN_CTAS") ? getenv("QZ_JIT_MIN_CTAS") : "3");
+                std::string("-DQZ_MIN_CTAS=") +
+                (getenv("QZ_JIT_MIN_CTAS") ? std::string(getenv("QZ_JIT_MIN_CTAS")) : std::to_string(QZ_MIN_CTAS));
+            static const std::string tbits = "-DQZ_TILE_BITS=" + std::to_string(kTileBits);
+            // inspection builds: QZ_JIT_DEFINE=<macro> (e.g. QZ_GROUP_CLOCKS)
+            static const std::string extra =
+                std::string("-D") + (getenv("QZ_JIT_DEFINE") ? getenv("QZ_JIT_DEFINE") : "QZ_JIT_NODEF");
             const char *opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "--fmad=false", "-lineinfo",
-                                  "-DQZ_JIT_SOURCE=1", ctas.c_str()};
-            const nvrtcResult rc = n.compile(prog, 6, opts);
+                                  "-DQZ_JIT_SOURCE=1", ctas.c_str(), tbits.c_str(), extra.c_str()};
+            const nvrtcResult rc = n.compile(prog, 8, opts);
             size_t ls = 0;
             n.log_size(prog, &ls);
             log.resize(ls);
@@ -237,7 +249,18 @@ void compile_job(const std::shared_ptr<JitPass> &j) {
 }
 } // namespace
 
-std::string jit_source(const GatePlan &plan, const PassDesc &pd) {
+// Registers statically +0 under `f` for a group whose register bits sit on
+// buffer bits bb[]: some fresh register bit holds the value whose amplitudes
+// are all +0.
+static uint32_t static_zero_regs(const Fresh &f, const uint32_t (&bb)[kRegBits]) {
+    uint32_t zm = 0;
+    for (uint32_t r = 0; r < uint32_t(NB_HOST); ++r)
+        for (int i = 0; i < kRegBits; ++i)
+            if (((f.mask >> bb[i]) & 1) && ((r >> i) & 1) != ((f.val >> bb[i]) & 1)) zm |= 1u << r;
+    return zm;
+}
+
+std::string jit_source(const GatePlan &plan, const PassDesc &pd, Fresh fresh) {
     std::string o;
     o.reserve(1 << 16);
     o += "#include \"qz_rtc_types.cuh\"\n#include \"qz_gate_types.cuh\"\n#include \"qz_bits.cuh\"\n";
@@ -264,16 +287,37 @@ std::string jit_source(const GatePlan &plan, const PassDesc &pd) {
     o += "};\n";
     o += "struct Prog {\n  static __device__ __forceinline__ void run(uint32_t gi, const TileGate *__restrict__, "
          "uint32_t, double2 (&v)[NB], uint64_t gidx, bool &bad) {\n    switch (gi) {\n";
+    // tile bit t of this pass is buffer bit tb[t]
+    std::vector<uint32_t> tb;
+    for (uint32_t b = 0; b < 64; ++b)
+        if ((pd.tmask >> b) & 1) tb.push_back(b);
     for (uint32_t gi = 0; gi < pd.ngroups; ++gi) {
         const GroupDesc &G = plan.groups[pd.first_group + gi];
-        if (G.generic || G.nfast == 0) continue;
+        if (G.generic || G.nfast == 0) {
+            fresh = Fresh{};   // (conservative)
+            continue;
+        }
+        uint32_t bb[kRegBits];
+        for (int i = 0; i < kRegBits; ++i) bb[i] = G.gbits[i] < tb.size() ? tb[G.gbits[i]] : 63u;
+        // statically +0 registers are skipped only where every gate keeps
+        // all-(+0) blocks all-(+0) (then they stay +0, sign included)
+        const bool use = G.pz_stable && fresh.mask;
         o += "    case " + std::to_string(gi) + ": {\n      const TileGate *f = kG + " + std::to_string(goff[gi]) + ";\n";
         for (uint32_t q = 0; q < G.nfast;) {
             const TileGate &t = plan.gates[G.first_fast + q];
-            o += "      if (!bad) fast_cid<" + std::to_string(t.cid) + ">(v, f, " + std::to_string(q) + "u, gidx, bad);\n";
+            const uint32_t zm = use ? static_zero_regs(fresh, bb) : 0u;
+            o += "      if (!bad) fast_cid<" + std::to_string(t.cid) + ">(v, f, " + std::to_string(q) + "u, gidx, bad, " +
+                 std::to_string(zm) + "u);\n";
+            // freshness after the op (PDIAG / DIAG / CZ and the fused CP5 /
+            // CXD are diagonal)
+            if (t.op == OP_GEN1 || t.op == OP_CX || t.op == OP_SWAP)
+                fresh = fresh_gate(fresh, t.op, t.nq, bb[t.r0], t.nq == 2 ? bb[t.r1] : 0u, t.kinds, false);
+            else if (t.op != OP_PDIAG && t.op != OP_DIAG && t.op != OP_CZ && t.op != OP_CP5 && t.op != OP_CXD)
+                fresh = Fresh{};
             // PDIAG runs (case ids 0..3) cover `run` ops, everything else one
             q += (t.cid <= 3 && t.run) ? t.run : 1;
         }
+        if (!G.pz_stable) fresh = Fresh{};   // zeros may have turned -0
         o += "      break;\n    }\n";
     }
     o += "    default: break;\n    }\n  }\n};\n} }\n";
@@ -290,34 +334,38 @@ std::string jit_source(const GatePlan &plan, const PassDesc &pd) {
 namespace {
 // Cache key: the bytes the source is generated from (cheaper than the
 // source itself on the per-stage upload path).
-std::string cache_key(const GatePlan &plan, const PassDesc &pd) {
+std::string cache_key(const GatePlan &plan, const PassDesc &pd, const Fresh &fresh) {
     std::string k;
     k.push_back(char(pd.variant));
+    const uint64_t hdr0[3] = {pd.tmask, fresh.mask, fresh.val};
+    k.append(reinterpret_cast<const char *>(hdr0), sizeof hdr0);
     for (uint32_t gi = 0; gi < pd.ngroups; ++gi) {
         const GroupDesc &G = plan.groups[pd.first_group + gi];
-        const uint32_t hdr[2] = {G.generic ? 0xFFFFFFFFu : G.nfast, gi};
+        const uint32_t hdr[6] = {G.generic ? 0xFFFFFFFFu : G.nfast, gi, G.pz_stable, G.gbits[0], G.gbits[1],
+                                 G.gbits[2]};
         k.append(reinterpret_cast<const char *>(hdr), sizeof hdr);
         k.append(reinterpret_cast<const char *>(&plan.gates[G.first_fast]), sizeof(TileGate) * G.nfast);
     }
     return k;
 }
 
-std::shared_ptr<JitPass> request(const GatePlan &plan, const PassDesc &pd) {
-    std::string key = cache_key(plan, pd);
+std::shared_ptr<JitPass> request(const GatePlan &plan, const PassDesc &pd, const Fresh &fresh) {
+    std::string key = cache_key(plan, pd, fresh);
     std::lock_guard<std::mutex> lk(g_cache_mu);
     auto it = g_cache.find(key);
     if (it != g_cache.end()) return it->second;
     auto j = std::make_shared<JitPass>();
-    j->source = jit_source(plan, pd);
+    j->source = jit_source(plan, pd, fresh);
     g_cache.emplace(std::move(key), j);
     pool().submit([j] { compile_job(j); });
     return j;
 }
 } // namespace
 
-std::shared_ptr<JitPass> jit_request(const GatePlan &plan, const PassDesc &pd, uint32_t nbits) {
+std::shared_ptr<JitPass> jit_request(const GatePlan &plan, const PassDesc &pd, uint32_t nbits, Fresh fresh) {
     if (!jit_enabled() || nbits < min_bits() || pd.kind != PASS_TILE || pd.k != kTileBits) return nullptr;
-    return request(plan, pd);
+    static const bool no_fresh = getenv("QZ_NO_FRESH") != nullptr;   // control: no static skipping
+    return request(plan, pd, no_fresh ? Fresh{} : fresh);
 }
 
 std::string &last_error();   // qz_runtime.cu
@@ -329,7 +377,31 @@ bool jit_ready(JitPass &j) {
     return j.compiled && !j.failed;
 }
 
-size_t jit_wait_all() {
+namespace {
+// Load a compiled pass into the current context (caller holds j.mu).
+bool load_locked(JitPass &j) {
+    if (j.failed) return false;
+    if (j.loaded) return true;
+    const Driver &d = driver();
+    CUmodule mod = nullptr;
+    if (!d.ok || d.load(&mod, j.cubin.data()) != CUDA_SUCCESS ||
+        d.get_fn(&j.fn, mod, "qz_jit_pass") != CUDA_SUCCESS ||
+        d.set_attr(j.fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, 110 * 1024) != CUDA_SUCCESS) {
+        j.failed = true;
+        static bool warned = false;
+        if (!warned) {
+            warned = true;
+            std::fprintf(stderr, "qz: specialised pass could not be loaded; using the AOT kernel\n");
+        }
+        return false;
+    }
+    j.loaded = true;
+    j.cubin.clear();
+    return true;
+}
+} // namespace
+
+size_t jit_wait_all(bool load) {
     std::vector<std::shared_ptr<JitPass>> all;
     {
         std::lock_guard<std::mutex> lk(g_cache_mu);
@@ -339,6 +411,7 @@ size_t jit_wait_all() {
     for (auto &j : all) {
         std::unique_lock<std::mutex> lk(j->mu);
         j->cv.wait(lk, [&] { return j->compiled; });
+        if (load) load_locked(*j);
         built += !j->failed;
     }
     return built;
@@ -347,24 +420,7 @@ size_t jit_wait_all() {
 bool jit_launch(JitPass &j, unsigned grid, unsigned threads, size_t smem, cudaStream_t s, void **args) {
     std::unique_lock<std::mutex> lk(j.mu);
     j.cv.wait(lk, [&] { return j.compiled; });
-    if (j.failed) return false;
-    if (!j.loaded) {
-        const Driver &d = driver();
-        CUmodule mod = nullptr;
-        if (!d.ok || d.load(&mod, j.cubin.data()) != CUDA_SUCCESS ||
-            d.get_fn(&j.fn, mod, "qz_jit_pass") != CUDA_SUCCESS ||
-            d.set_attr(j.fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, 110 * 1024) != CUDA_SUCCESS) {
-            j.failed = true;
-            static bool warned = false;
-            if (!warned) {
-                warned = true;
-                std::fprintf(stderr, "qz: specialised pass could not be loaded; using the AOT kernel\n");
-            }
-            return false;
-        }
-        j.loaded = true;
-        j.cubin.clear();
-    }
+    if (!load_locked(j)) return false;
     return driver().launch(j.fn, grid, 1, 1, threads, 1, 1, unsigned(smem), reinterpret_cast<CUstream>(s), args,
                            nullptr) == CUDA_SUCCESS;
 }
@@ -385,9 +441,15 @@ int qzc_jit_selftest(const qzc_gate *gates, uint64_t ngates, uint32_t nbits) {
         const GatePlan gp = build_passes(dg, nbits, kTileBits, true, 1);
         static const bool all = getenv("QZ_JIT_SELFTEST_ALL") != nullptr;   // every pass (inspection)
         std::vector<std::shared_ptr<JitPass>> jobs;
+        // QZ_JIT_SELFTEST_FRESH=1: as after init_basis (every bit fresh at the start)
+        Fresh f;
+        if (getenv("QZ_JIT_SELFTEST_FRESH")) f.mask = nbits >= 64 ? ~uint64_t(0) : (uint64_t(1) << nbits) - 1;
+        size_t at = 0;
         for (const PassDesc &pd : launch_passes(gp)) {
+            f = fresh_after(dg, at, pd.dg0, f);
+            at = pd.dg0;
             if (pd.kind != PASS_TILE || pd.k != kTileBits) continue;
-            jobs.push_back(request(gp, pd));
+            jobs.push_back(request(gp, pd, f));
             if (!all) break;
         }
         if (jobs.empty()) {
@@ -411,6 +473,20 @@ int qzc_jit_selftest(const qzc_gate *gates, uint64_t ngates, uint32_t nbits) {
 
 // Wait for the specialised passes queued so far (e.g. after a warm-up run);
 // returns how many were built.
-uint64_t qzc_jit_wait(void) { return jit_wait_all(); }
+uint64_t qzc_jit_wait(void) {
+    // loads the built kernels into the calling thread's current context when
+    // it has one (the engine's device), so no later launch pays for it
+    CUcontext cur = nullptr;
+    static auto get_cur = [] {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult st;
+        return cudaGetDriverEntryPoint("cuCtxGetCurrent", &fn, cudaEnableDefault, &st) == cudaSuccess &&
+                       st == cudaDriverEntryPointSuccess
+                   ? reinterpret_cast<CUresult (*)(CUcontext *)>(fn)
+                   : nullptr;
+    }();
+    const bool has_ctx = get_cur && get_cur(&cur) == CUDA_SUCCESS && cur != nullptr;
+    return jit_wait_all(has_ctx);
+}
 
 } // extern "C"

@@ -23,20 +23,24 @@ struct JitPass;
 
 // Queue the specialised kernel for pass `pd` of `plan` over 2^nbits windows;
 // nullptr when the JIT is off or the pass does not qualify.
-std::shared_ptr<JitPass> jit_request(const GatePlan &plan, const PassDesc &pd, uint32_t nbits);
+// fresh: the pass's fresh buffer bits at its start (registers statically +0
+// skip their products).
+std::shared_ptr<JitPass> jit_request(const GatePlan &plan, const PassDesc &pd, uint32_t nbits,
+                                     Fresh fresh = {});
 
 // The kernel is built (or failed: then false).  Never waits unless
 // QZ_JIT_SYNC=1 — until a compile finishes its pass runs the AOT kernel.
 bool jit_ready(JitPass &j);
 
-// Block until every queued compile has finished; returns how many built.
-size_t jit_wait_all();
+// Block until every queued compile has finished (and, with load, load the
+// kernels into the current context); returns how many built.
+size_t jit_wait_all(bool load = false);
 
 // Launch it with tile_pass_reg's arguments; false when it could not be built
 // (the caller then launches the AOT kernel — same results).
 bool jit_launch(JitPass &j, unsigned grid, unsigned threads, size_t smem, cudaStream_t s, void **args);
 
 // The generated source of a pass (tests / inspection).
-std::string jit_source(const GatePlan &plan, const PassDesc &pd);
+std::string jit_source(const GatePlan &plan, const PassDesc &pd, Fresh fresh = {});
 
 } // namespace qz

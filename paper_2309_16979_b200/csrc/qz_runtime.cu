@@ -1005,6 +1005,7 @@ int qzc_sim_init_zero(qzc_sim *sim) {
 namespace {
 void init_store(qzc_sim *sim, bool basis) {
     qzc_context *ctx = sim->ctx;
+    sim->fresh_q = basis ? ((sim->n >= 64 ? ~uint64_t(0) : (uint64_t(1) << sim->n) - 1)) : 0;
     QZ_CUDA(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
     Window &w = sim->win;
@@ -1181,7 +1182,24 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
         const double tp0 = now_s();
         GatePlan gp = build_passes(dg, wbits, kTileBits, sim->cfg.fuse_gates != 0, sim->relax);
         DevPlan &dp = sim->plans[0], &dsub = sim->plans[1], &dfull = sim->plans[2];
-        upload_plan(gp, dp, s, wbits);
+        // fresh buffer bits at each pass's start (statically +0 registers)
+        Fresh stage_fresh;
+        for (uint32_t q = 0; q < n; ++q)
+            if ((sim->fresh_q >> q) & 1) {
+                const int bq = buffer_bit(st, q, c);
+                if (bq >= 0) stage_fresh.mask |= uint64_t(1) << bq;
+            }
+        std::vector<Fresh> pass_fresh;
+        {
+            Fresh f = stage_fresh;
+            size_t at = 0;
+            for (const PassDesc &pd : gp.passes) {
+                f = fresh_after(dg, at, pd.dg0, f);
+                at = pd.dg0;
+                pass_fresh.push_back(f);
+            }
+        }
+        upload_plan(gp, dp, s, wbits, pass_fresh);
         dsub.host_passes.clear();
         dfull.host_passes.clear();
         if (dp.relaxed) {
@@ -1364,6 +1382,19 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
         }
         sim->cur = b;
         sim->sparse_store = false;   // after a stage the payload density is unknown
+        {
+            // qubits the stage's gates leave fresh
+            bool keeps_zero = true;
+            for (const DevGate &g : dg) keeps_zero &= gate_keeps_pos_zero(g);
+            const Fresh f = fresh_after(dg, 0, dg.size(), stage_fresh);
+            uint64_t keep = 0;
+            for (uint32_t q = 0; q < n; ++q) {
+                const int bq = buffer_bit(st, q, c);
+                // a stage's gates act only on its buffer bits
+                if (bq < 0 || ((f.mask >> bq) & 1)) keep |= uint64_t(1) << q;
+            }
+            sim->fresh_q = keeps_zero ? (sim->fresh_q & keep) : 0;
+        }
         sim->stats.stages += 1;
         sim->stats.batches += nbatches;
         sim->stats.windows += nwin;
@@ -1499,6 +1530,7 @@ int qzc_sim_export(qzc_sim *sim, uint8_t *payload_out, uint64_t cap, uint32_t *s
 
 int qzc_sim_import(qzc_sim *sim, const uint8_t *payloads, const uint32_t *sizes, const uint32_t *crcs) {
     QZ_API_BEGIN
+    sim->fresh_q = 0;
     sim->sparse_store = false;
     qzc_context *ctx = sim->ctx;
     QZ_CUDA(cudaSetDevice(ctx->device));
@@ -1552,6 +1584,7 @@ int qzc_sim_read_chunks(qzc_sim *sim, uint64_t first, uint64_t count, double *am
 
 int qzc_sim_write_chunk(qzc_sim *sim, uint64_t index, const double *amps) {
     QZ_API_BEGIN
+    sim->fresh_q = 0;
     sim->sparse_store = false;
     qzc_context *ctx = sim->ctx;
     QZ_CUDA(cudaSetDevice(ctx->device));

@@ -218,6 +218,9 @@ struct qzc_sim {
     cudaEvent_t acct_ev[2] = {nullptr, nullptr};
     qzc_sim_stats stats{};
     bool initialized = false;
+    // qubits statically |0> (untouched by any non-diagonal gate since
+    // init_basis, every gate keeping +0 zeros +0): Fresh for the stage plans
+    uint64_t fresh_q = 0;
     uint64_t payload_now = 0;   // store payload bytes (host copy, refreshed per stage)
     std::shared_ptr<XPlan> xplan;   // last sharded-exchange plan (qz_store_io.cu)
     std::vector<cudaEvent_t> events;

@@ -299,6 +299,7 @@ int qzc_sim_save(qzc_sim *sim, const char *path) {
 
 int qzc_sim_load(qzc_sim *sim, const char *path) {
     QZ_API_BEGIN
+    sim->fresh_q = 0;
     if (!sim || !path) throw Failure(QZC_EINVAL, "null argument");
     qzc_context *ctx = sim->ctx;
     QZ_CUDA(cudaSetDevice(ctx->device));
@@ -502,6 +503,7 @@ int qzc_sim_exchange_recv_buffer(qzc_sim *sim, uint64_t bytes, void **recv_dev_o
 
 int qzc_sim_exchange_unpack(qzc_sim *sim, const uint64_t *recv_bytes) {
     QZ_API_BEGIN
+    sim->fresh_q = 0;
     if (!sim || !recv_bytes) throw Failure(QZC_EINVAL, "null argument");
     XPlan &xp = xplan(sim);
     if (!xp.world) throw Failure(QZC_EINVAL, "no exchange planned");
