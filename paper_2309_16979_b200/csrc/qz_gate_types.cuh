@@ -124,6 +124,10 @@ struct PassDesc {
                            // differ only in low bits — the all-(+0) blocks of sparse states —
                            // fall on whole warps, which then skip the group uniformly
     uint8_t perm[48];
+    // buffer bits outside T that are fresh (in a basis value) at the pass's
+    // start, and their values: a tile whose fixed bits differ from zval on
+    // zmask is all +0 and — pz_stable, in place — is never visited
+    uint64_t zmask, zval;
 };
 
 enum PassKind : uint32_t { PASS_TILE = 0, PASS_SWAPS = 1 };

@@ -379,7 +379,7 @@ static uint32_t case_id(const TileGate &t) {
 }
 
 GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_t kmax, bool fuse,
-                      int relax_level) {
+                      int relax_level, const Fresh *fresh) {
     bool relax = relax_level > 0;
     GatePlan plan;
     const uint32_t k = std::min(kmax, nbits);
@@ -396,13 +396,17 @@ GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_
         for (Unit &u : units)
             if (u.diag && !unit_safe(gates, u)) u.diag = false;
     std::vector<size_t> members;   // unit indices of the open pass
-    uint64_t tmask = low_mask;
+    // fresh state at the open pass's start / after its members so far: fresh
+    // low bits are not forced into T (a tile over them would be mostly +0)
+    Fresh fpass = fresh ? *fresh : Fresh{}, fcur = fpass;
+    uint64_t tmask = low_mask & ~fpass.mask;
     auto close = [&]() {
         if (members.empty()) return;
         // pad T to exactly k bits with the lowest free bits (longer contiguous
-        // global segments)
-        for (uint32_t b = 0; b < nbits && (uint32_t)__builtin_popcountll(tmask) < k; ++b)
-            tmask |= uint64_t(1) << b;
+        // global segments), bits fresh at the pass's start last
+        for (int round = 0; round < 2; ++round)
+            for (uint32_t b = 0; b < nbits && (uint32_t)__builtin_popcountll(tmask) < k; ++b)
+                if (round || !((fpass.mask >> b) & 1)) tmask |= uint64_t(1) << b;
         PassDesc pd;
         std::memset(&pd, 0, sizeof pd);
         pd.k = k;
@@ -410,6 +414,8 @@ GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_
         while (lowbits < 64 && ((tmask >> lowbits) & 1)) ++lowbits;
         pd.lowbits = std::min(lowbits, k);
         pd.tmask = tmask;
+        pd.zmask = fpass.mask & ~tmask;
+        pd.zval = fpass.val & pd.zmask;
         pd.first_gate = (uint32_t)plan.gates.size();
         pd.ngates = (uint32_t)members.size();
         pd.dg0 = (uint32_t)units[members.front()].first;
@@ -716,7 +722,11 @@ GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_
         }
         plan.passes.push_back(pd);
         members.clear();
-        tmask = low_mask;
+        fpass = fcur;
+        tmask = low_mask & ~fpass.mask;
+    };
+    auto advance = [&](const Unit &u) {   // fcur through the unit's gates
+        for (size_t i = u.first; i < u.first + u.count && fcur.mask; ++i) fcur = fresh_after_gate(fcur, gates[i]);
     };
     for (size_t ui = 0; ui < units.size(); ++ui) {
         const Unit &u = units[ui];
@@ -739,6 +749,9 @@ GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_
             }
             pd.pz_stable = 1;
             plan.passes.push_back(pd);
+            advance(u);
+            fpass = fcur;
+            tmask = low_mask & ~fpass.mask;
             continue;
         }
         const uint64_t need = u.diag ? 0 : u.bits;
@@ -746,19 +759,23 @@ GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_
         if (!fuse || (uint32_t)__builtin_popcountll(merged) > k) close();
         tmask |= need;
         members.push_back(ui);
+        advance(u);
     }
     close();
     if (getenv("QZ_TRACE") && getenv("QZ_TRACE")[0] == '2') {
         for (const PassDesc &pd : plan.passes) {
-            uint32_t nf = 0, npd = 0, nrel = 0;
+            uint32_t nf = 0, npd = 0, nrel = 0, nuns = 0;
             for (uint32_t gi = pd.first_group; gi < pd.first_group + pd.ngroups; ++gi) {
                 nf += plan.groups[gi].nfast;
                 nrel += plan.groups[gi].relaxed;
+                nuns += plan.groups[gi].unsafe;
                 for (uint32_t q = 0; q < plan.groups[gi].nfast; ++q)
                     npd += plan.gates[plan.groups[gi].first_fast + q].op == OP_PDIAG;
             }
-            fprintf(stderr, "qz plan: kind %u tmask %#llx groups %u (relaxed %u) fast ops %u pdiag %u gates %u\n",
-                    pd.kind, (unsigned long long)pd.tmask, pd.ngroups, nrel, nf, npd, pd.ngates);
+            fprintf(stderr, "qz plan: kind %u tmask %#llx groups %u (relaxed %u, unsafe %u) fast ops %u pdiag %u "
+                            "gates %u pass relaxed %u zmask %#llx\n",
+                    pd.kind, (unsigned long long)pd.tmask, pd.ngroups, nrel, nuns, nf, npd, pd.ngates, pd.relaxed,
+                    (unsigned long long)pd.zmask);
         }
     }
     return plan;
@@ -836,12 +853,36 @@ Fresh fresh_gate(Fresh f, uint32_t op, uint32_t nq, uint32_t b0, uint32_t b1, ui
     return f;
 }
 
-Fresh fresh_after(const std::vector<DevGate> &dg, size_t g0, size_t g1, Fresh f) {
-    for (size_t i = g0; i < g1 && f.mask; ++i) {
-        const DevGate &g = dg[i];
-        if (!maps_pos_zero(g)) return Fresh{};
-        f = fresh_gate(f, g.op, g.nq, g.b0, g.b1, g.kinds, gate_diagonal(g));
+Fresh fresh_after_gate(Fresh f, const DevGate &g) {
+    if (!f.mask) return f;
+    // amplitudes on the +0 side of a fresh qubit the gate does not touch
+    // form all-(+0) orbits: they stay +0 iff the gate maps all-(+0) to +0
+    if (!maps_pos_zero(g)) return Fresh{};
+    const uint64_t gm = (uint64_t(1) << g.b0) | (g.nq == 2 ? uint64_t(1) << g.b1 : 0);
+    if (!(f.mask & gm)) return f;
+    if (gate_diagonal(g)) {
+        // a +0-side row (a touched fresh bit on its +0 side) sums m_rr * (+0)
+        // with structural-zero products of live amplitudes (zeros of any
+        // sign): +0 only when m_rr is sign-safe; else those bits are lost
+        for (uint32_t r = 0; r < g.dim; ++r) {
+            const uint32_t v0 = g.nq == 2 ? (r >> 1) & 1 : r & 1, v1 = r & 1;
+            const bool zside = (((f.mask >> g.b0) & 1) && v0 != ((f.val >> g.b0) & 1)) ||
+                               (g.nq == 2 && ((f.mask >> g.b1) & 1) && v1 != ((f.val >> g.b1) & 1));
+            const uint32_t e = r * g.dim + r;
+            if (zside && !safe_coef(uint32_t(g.kinds >> (4 * e)) & 15u, g.m[e])) {
+                f.mask &= ~gm;
+                break;
+            }
+        }
+        f.val &= f.mask;
+        return f;
     }
+    // X / CX / SWAP: the +0 side maps through a 1 * (+0) term (stays +0)
+    return fresh_gate(f, g.op, g.nq, g.b0, g.b1, g.kinds, false);
+}
+
+Fresh fresh_after(const std::vector<DevGate> &dg, size_t g0, size_t g1, Fresh f) {
+    for (size_t i = g0; i < g1 && f.mask; ++i) f = fresh_after_gate(f, dg[i]);
     return f;
 }
 
@@ -981,7 +1022,10 @@ void launch_pass(const DevPlan &plan, const PassDesc &pd, const double2 *src, do
         const uint64_t ntiles = uint64_t(1) << (nbits - pd.k);
         const uint32_t threads = tile >> kRegBits;
         const size_t smem = sizeof(double2) * tile + sizeof(uint64_t) * (tile >> pd.lowbits);
-        const uint64_t grid = std::min<uint64_t>(ntiles, uint64_t(kNumSMs) * 2 * 8);
+        // live tiles (tile_pass_body's fresh-bit skip)
+        const uint64_t live = (pd.zmask && pd.pz_stable && src == dst) ? ntiles >> __builtin_popcountll(pd.zmask)
+                                                                       : ntiles;
+        const uint64_t grid = std::min<uint64_t>(std::max<uint64_t>(live, 1), uint64_t(kNumSMs) * 2 * 8);
         // the map is only used for passes inside one window of whole slots
         static const bool off = getenv("QZ_NO_NZMAP") != nullptr;
         const bool usable = nz.slot && nbits > nz.cbits && !off;

@@ -36,8 +36,11 @@ uint32_t gate_nparams(uint32_t kind);
 // relax: diagonal units do not need their qubits in the tile set (OP_PDIAG);
 // such a plan can raise the replay flag and must then be replayed strictly
 // from the same input (see run_passes).
+// fresh: buffer bits in a basis value at the start (see Fresh): tiles leave
+// them out where no gate needs them, and tiles on their +0 side are skipped.
+struct Fresh;
 GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_t kmax,
-                      bool fuse, int relax_level = 0);
+                      bool fuse, int relax_level = 0, const Fresh *fresh = nullptr);
 
 DevGate make_dev_gate(const qzc_gate &g);
 DevGate make_dev_gate_matrix(const double2 *m, uint32_t dim, uint32_t b0, uint32_t b1);
@@ -74,6 +77,7 @@ bool gate_keeps_pos_zero(const DevGate &g);
 // Fresh state after gates [g0, g1): a non-diagonal gate ends its qubits'
 // freshness, a gate that may turn +0 into -0 ends all of it.
 Fresh fresh_after(const std::vector<DevGate> &dg, size_t g0, size_t g1, Fresh f);
+Fresh fresh_after_gate(Fresh f, const DevGate &g);
 // one gate (buffer bits b0, b1): X / CX / SWAP permute basis states and keep
 // fresh bits fresh (values updated); other non-diagonal gates end them
 Fresh fresh_gate(Fresh f, uint32_t op, uint32_t nq, uint32_t b0, uint32_t b1, uint64_t kinds, bool diagonal);

@@ -1135,17 +1135,23 @@ __device__ __forceinline__ void tile_pass_body(const double2 *__restrict__ src, 
     __shared__ uint32_t s_zc;
     if (tid == 0) s_zc = nzslot ? nzslot[uint64_t(1) << (nbits - cbits)] : 0u;
     __syncthreads();
+    // live tiles only: those on the nonzero side of the pass's fresh outside
+    // bits (the others are all +0 and stay so: pz_stable, in place)
+    const bool zskip = pd.zmask && pd.pz_stable && src == dst;
+    const uint64_t ltmask = zskip ? ntmask & ~pd.zmask : ntmask;
+    const uint64_t zv = zskip ? pd.zval : 0;
+    if (zskip) ntiles >>= __popcll(pd.zmask);
     // tile bases: deposit(t) advanced by deposit(gridDim.x) with the carry
     // running through the tile-bit positions
-    const uint64_t dstep = deposit_bits(gridDim.x, ntmask);
-    uint64_t base = deposit_bits(blockIdx.x, ntmask);
+    const uint64_t dstep = deposit_bits(gridDim.x, ltmask);
+    uint64_t base = deposit_bits(blockIdx.x, ltmask) | zv;
     // known all-(+0) chunk slots: tiles made only of them are fixed points of
     // a pz_stable in-place pass (no load, no store)
     // the map is consulted / maintained only while it still holds zero slots
     if (s_zc == 0) nzslot = nullptr;
     const bool use_nz = nzslot && pd.pz_stable && src == dst && L <= cbits;
     for (uint64_t t = blockIdx.x; t < ntiles;
-         t += gridDim.x, base = ((base | ~ntmask) + dstep) & ntmask) {
+         t += gridDim.x, base = ((((base & ~zv) | ~ltmask) + dstep) & ltmask) | zv) {
         if (use_nz) {
             uint32_t nzt = 0;
             for (uint32_t h = tid; h < nhi; h += nth) nzt |= nzslot[(base + offhi[h]) >> cbits];

@@ -104,8 +104,10 @@ class Pool {
     }
     ~Pool() {
         {
+            // at exit: queued compiles are dropped, running ones finish
             std::lock_guard<std::mutex> lk(mu_);
             stop_ = true;
+            q_.clear();
         }
         cv_.notify_all();
         for (auto &t : threads_) t.join();
@@ -305,14 +307,37 @@ std::string jit_source(const GatePlan &plan, const PassDesc &pd, Fresh fresh) {
         o += "    case " + std::to_string(gi) + ": {\n      const TileGate *f = kG + " + std::to_string(goff[gi]) + ";\n";
         for (uint32_t q = 0; q < G.nfast;) {
             const TileGate &t = plan.gates[G.first_fast + q];
-            const uint32_t zm = use ? static_zero_regs(fresh, bb) : 0u;
+            uint32_t zm = use ? static_zero_regs(fresh, bb) : 0u;
+            // PDIAG / DIAG / CZ and the fused CP5 / CXD are diagonal: a +0
+            // register they touch through a fresh bit sums m_rr * (+0) with
+            // structural zeros of live amplitudes, +0 only for sign-safe rows
+            const bool diag = t.op == OP_PDIAG || t.op == OP_DIAG || t.op == OP_CZ || t.op == OP_CP5 ||
+                              t.op == OP_CXD;
+            if (diag) {
+                uint64_t touched = 0;
+                if (t.op == OP_PDIAG) {
+                    if (t.nq) touched |= uint64_t(1) << bb[t.r0];
+                } else {
+                    touched |= uint64_t(1) << bb[t.r0];
+                    if (t.nq == 2) touched |= uint64_t(1) << bb[t.r1];
+                }
+                const bool safe = t.op == OP_DIAG  ? (t.srow & 3u) == 3u
+                                  : t.op == OP_CP5 ? (t.srow & 7u) == 7u
+                                  : t.op == OP_CXD ? (t.srow & 3u) == 3u
+                                  : t.op == OP_PDIAG ? (t.srow & t.steps) == t.steps
+                                                     : false;
+                if ((fresh.mask & touched) && !safe) {
+                    zm = 0;
+                    fresh.mask &= ~touched;
+                    fresh.val &= fresh.mask;
+                }
+            }
             o += "      if (!bad) fast_cid<" + std::to_string(t.cid) + ">(v, f, " + std::to_string(q) + "u, gidx, bad, " +
                  std::to_string(zm) + "u);\n";
-            // freshness after the op (PDIAG / DIAG / CZ and the fused CP5 /
-            // CXD are diagonal)
+            // freshness after a non-diagonal op
             if (t.op == OP_GEN1 || t.op == OP_CX || t.op == OP_SWAP)
                 fresh = fresh_gate(fresh, t.op, t.nq, bb[t.r0], t.nq == 2 ? bb[t.r1] : 0u, t.kinds, false);
-            else if (t.op != OP_PDIAG && t.op != OP_DIAG && t.op != OP_CZ && t.op != OP_CP5 && t.op != OP_CXD)
+            else if (!diag)
                 fresh = Fresh{};
             // PDIAG runs (case ids 0..3) cover `run` ops, everything else one
             q += (t.cid <= 3 && t.run) ? t.run : 1;

@@ -1086,8 +1086,11 @@ int qzc_pass_plan_stats(const qzc_gate *gates, uint64_t ngates, uint32_t nbits,
     if (!err.empty()) throw Failure(QZC_EINVAL, err);
     std::vector<DevGate> dg;
     for (uint64_t i = 0; i < ngates; ++i) dg.push_back(make_dev_gate(gates[i]));
+    // QZ_PLAN_FRESH=1 (inspection): plan as for a store fresh from init_basis
+    Fresh fr;
+    if (getenv("QZ_PLAN_FRESH")) fr.mask = (uint64_t(1) << nbits) - 1;
     const GatePlan p = build_passes(dg, nbits, kTileBits, fuse_mode != 0,
-                                    fuse_mode == 1 ? 1 : (fuse_mode == 3 ? 2 : 0));
+                                    fuse_mode == 1 ? 1 : (fuse_mode == 3 ? 2 : 0), &fr);
     uint64_t relaxed = 0, fast = 0, pdiag = 0;
     for (const GroupDesc &g : p.groups) {
         relaxed += g.relaxed;
@@ -1180,15 +1183,16 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
         // relaxed plan (diagonal units need no tile bits) + the strict plan
         // it is replayed with, device-side, when a window raises the flag
         const double tp0 = now_s();
-        GatePlan gp = build_passes(dg, wbits, kTileBits, sim->cfg.fuse_gates != 0, sim->relax);
-        DevPlan &dp = sim->plans[0], &dsub = sim->plans[1], &dfull = sim->plans[2];
-        // fresh buffer bits at each pass's start (statically +0 registers)
+        // fresh buffer bits at the stage's start (qubits still |0>)
         Fresh stage_fresh;
-        for (uint32_t q = 0; q < n; ++q)
+        static const bool no_fresh = getenv("QZ_NO_FRESH") != nullptr;   // control
+        for (uint32_t q = 0; q < n && !no_fresh; ++q)
             if ((sim->fresh_q >> q) & 1) {
                 const int bq = buffer_bit(st, q, c);
                 if (bq >= 0) stage_fresh.mask |= uint64_t(1) << bq;
             }
+        GatePlan gp = build_passes(dg, wbits, kTileBits, sim->cfg.fuse_gates != 0, sim->relax, &stage_fresh);
+        DevPlan &dp = sim->plans[0], &dsub = sim->plans[1], &dfull = sim->plans[2];
         std::vector<Fresh> pass_fresh;
         {
             Fresh f = stage_fresh;
@@ -1393,6 +1397,10 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
                 // a stage's gates act only on its buffer bits
                 if (bq < 0 || ((f.mask >> bq) & 1)) keep |= uint64_t(1) << q;
             }
+            // the lossy codec reconstructs a zero that shares a chunk with
+            // nonzero amplitudes only within the error bound (all-zero chunks
+            // stay exact): chunk-local qubits are no longer fresh
+            if (sim->geom.lossy) keep &= ~((uint64_t(1) << c) - 1);
             sim->fresh_q = keeps_zero ? (sim->fresh_q & keep) : 0;
         }
         sim->stats.stages += 1;
@@ -1403,7 +1411,10 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
         sim->stats.chunk_recompress_count += sim->nchunks;
     }
     QZ_CUDA(cudaStreamSynchronize(s));
-    if (sim->cfg.renormalize) renormalize(sim);
+    if (sim->cfg.renormalize) {
+        renormalize(sim);   // re-encodes every chunk (see the stage loop)
+        if (sim->geom.lossy) sim->fresh_q &= ~((uint64_t(1) << c) - 1);
+    }
     sim->stats.wall_seconds += now_s() - t0;
     dump_debug_counters();
     sim->stats.kernel_launches += ctx->launches - launches0;
