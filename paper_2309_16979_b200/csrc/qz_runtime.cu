@@ -1006,6 +1006,7 @@ namespace {
 void init_store(qzc_sim *sim, bool basis) {
     qzc_context *ctx = sim->ctx;
     sim->fresh_q = basis ? ((sim->n >= 64 ? ~uint64_t(0) : (uint64_t(1) << sim->n) - 1)) : 0;
+    sim->fresh_v = 0;
     QZ_CUDA(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
     Window &w = sim->win;
@@ -1189,7 +1190,10 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
         for (uint32_t q = 0; q < n && !no_fresh; ++q)
             if ((sim->fresh_q >> q) & 1) {
                 const int bq = buffer_bit(st, q, c);
-                if (bq >= 0) stage_fresh.mask |= uint64_t(1) << bq;
+                if (bq >= 0) {
+                    stage_fresh.mask |= uint64_t(1) << bq;
+                    stage_fresh.val |= ((sim->fresh_v >> q) & 1) << bq;
+                }
             }
         GatePlan gp = build_passes(dg, wbits, kTileBits, sim->cfg.fuse_gates != 0, sim->relax, &stage_fresh);
         DevPlan &dp = sim->plans[0], &dsub = sim->plans[1], &dfull = sim->plans[2];
@@ -1394,14 +1398,21 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
             uint64_t keep = 0;
             for (uint32_t q = 0; q < n; ++q) {
                 const int bq = buffer_bit(st, q, c);
-                // a stage's gates act only on its buffer bits
-                if (bq < 0 || ((f.mask >> bq) & 1)) keep |= uint64_t(1) << q;
+                // a stage's gates act only on its buffer bits (X / CX / SWAP
+                // may have changed a fresh qubit's value)
+                if (bq < 0) {
+                    keep |= uint64_t(1) << q;
+                } else if ((f.mask >> bq) & 1) {
+                    keep |= uint64_t(1) << q;
+                    sim->fresh_v = (sim->fresh_v & ~(uint64_t(1) << q)) | (((f.val >> bq) & 1) << q);
+                }
             }
             // the lossy codec reconstructs a zero that shares a chunk with
             // nonzero amplitudes only within the error bound (all-zero chunks
             // stay exact): chunk-local qubits are no longer fresh
             if (sim->geom.lossy) keep &= ~((uint64_t(1) << c) - 1);
             sim->fresh_q = keeps_zero ? (sim->fresh_q & keep) : 0;
+            sim->fresh_v &= sim->fresh_q;
         }
         sim->stats.stages += 1;
         sim->stats.batches += nbatches;

@@ -220,7 +220,7 @@ struct qzc_sim {
     bool initialized = false;
     // qubits statically |0> (untouched by any non-diagonal gate since
     // init_basis, every gate keeping +0 zeros +0): Fresh for the stage plans
-    uint64_t fresh_q = 0;
+    uint64_t fresh_q = 0, fresh_v = 0;   // ... and their basis values
     uint64_t payload_now = 0;   // store payload bytes (host copy, refreshed per stage)
     std::shared_ptr<XPlan> xplan;   // last sharded-exchange plan (qz_store_io.cu)
     std::vector<cudaEvent_t> events;
