@@ -400,6 +400,12 @@ GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_
     // low bits are not forced into T (a tile over them would be mostly +0)
     Fresh fpass = fresh ? *fresh : Fresh{}, fcur = fpass;
     uint64_t tmask = low_mask & ~fpass.mask;
+    // a pass "opens" at most kOpen of its start's fresh bits (non-diagonal
+    // gates on them): the ops before an opening run on a mostly-(+0) tile
+    // where few warps have work, so a long run of openings is split into
+    // passes whose live tiles are dense
+    static const uint32_t kOpen = getenv("QZ_FRESH_OPEN") ? uint32_t(atoi(getenv("QZ_FRESH_OPEN"))) : 6u;
+    uint64_t opened = 0;
     auto close = [&]() {
         if (members.empty()) return;
         // pad T to exactly k bits with the lowest free bits (longer contiguous
@@ -724,6 +730,7 @@ GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_
         members.clear();
         fpass = fcur;
         tmask = low_mask & ~fpass.mask;
+        opened = 0;
     };
     auto advance = [&](const Unit &u) {   // fcur through the unit's gates
         for (size_t i = u.first; i < u.first + u.count && fcur.mask; ++i) fcur = fresh_after_gate(fcur, gates[i]);
@@ -752,12 +759,16 @@ GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_
             advance(u);
             fpass = fcur;
             tmask = low_mask & ~fpass.mask;
+            opened = 0;
             continue;
         }
         const uint64_t need = u.diag ? 0 : u.bits;
         const uint64_t merged = tmask | need;
-        if (!fuse || (uint32_t)__builtin_popcountll(merged) > k) close();
+        if (!fuse || (uint32_t)__builtin_popcountll(merged) > k ||
+            (opened && (uint32_t)__builtin_popcountll(opened | (need & fpass.mask)) > kOpen))
+            close();
         tmask |= need;
+        opened |= need & fpass.mask;
         members.push_back(ui);
         advance(u);
     }
