@@ -559,6 +559,12 @@ __device__ __forceinline__ uint32_t plane_block(PlaneRd &c, const uint8_t *p, ui
     return byte;
 }
 
+__device__ __forceinline__ bool chunk_dead(const CodecGeom &g, const uint64_t *slot_chunk, uint64_t s) {
+    if (!g.dead_mask) return false;
+    const uint64_t chunk = slot_chunk ? slot_chunk[s] : s;
+    return (chunk & g.dead_mask) != g.dead_val;
+}
+
 __global__ void __launch_bounds__(256) k_dec_lossy_warp(
     const uint8_t *__restrict__ arena, const DecIdx *__restrict__ idx,
     const uint64_t *__restrict__ slot_chunk, uint64_t nslots, CodecGeom g,
@@ -569,7 +575,7 @@ __global__ void __launch_bounds__(256) k_dec_lossy_warp(
     const uint64_t wg = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const uint64_t s = wg >> 1;
     const uint32_t h = uint32_t(wg & 1);
-    if (s >= nslots) return;
+    if (s >= nslots || chunk_dead(g, slot_chunk, s)) return;
     const DecIdx &d = idx[s];
     const uint64_t N = g.N;
     double *out = reinterpret_cast<double *>(win) + 2 * s * N + h;
@@ -707,6 +713,11 @@ __global__ void __launch_bounds__(256) k_dec_lossy_seg(
     const uint64_t s = ((uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * 2 + (seg >> 1);
     const uint32_t h = seg & 1;
     if (((uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * 2 >= nslots) return;   // whole warp
+    {
+        // both chunks of the warp statically +0: nothing to write
+        const uint64_t s0 = ((uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * 2;
+        if (chunk_dead(g, slot_chunk, s0) && (s0 + 1 >= nslots || chunk_dead(g, slot_chunk, s0 + 1))) return;
+    }
     const bool exists = s < nslots;
     const DecIdx &d = idx[exists ? s : 0];
     const bool live = exists && d.len != 0;
@@ -774,6 +785,8 @@ __global__ void __launch_bounds__(2 * kSlotsPerCta) k_dec_lossy(
     __shared__ TileSmem tile;
     const uint32_t r = threadIdx.x >> 1, h = threadIdx.x & 1;
     const uint64_t slot0 = uint64_t(blockIdx.x) * kSlotsPerCta, s = slot0 + r;
+    // every chunk of the CTA statically +0: nothing to write
+    if (!__syncthreads_or(s < nslots && !chunk_dead(g, slot_chunk, s))) return;
     const bool active = s < nslots && idx[min(s, nslots - 1)].len != 0;
     const DecIdx *d = &idx[min(s, nslots - 1)];
     const uint8_t *p = arena + d->base;
@@ -1516,6 +1529,7 @@ CodecGeom make_geom(uint64_t N, double eb) {
     g.dense_hint = 0;
     g.scap = round_up(2 * N, 8);
     g.half_stride = round_up(g.lossy ? 2 * g.scap + 8 * N : 8 * g.scap, 16);
+    g.dead_mask = g.dead_val = 0;
     return g;
 }
 
@@ -1574,7 +1588,13 @@ void launch_decode(const uint8_t *arena, const DecIdx *idx, const uint64_t *slot
                    uint64_t nslots, const CodecGeom &g, double2 *win, DevStatus *status,
                    cudaStream_t s, const uint32_t *cond, bool sparse) {
     const unsigned grid = grid_for(nslots, kSlotsPerCta);
-    const double dense = 16.0 * double(g.N) * double(nslots);
+    // bytes written: the live chunks only (a window's chunks cover every
+    // value of the stage's dead-mask bits equally)
+    const double dense = 16.0 * double(g.N) * double(nslots) / double(uint64_t(1) << __builtin_popcountll(g.dead_mask));
+    // with statically-(+0) chunks skipped, the few live ones of a sparse
+    // store decode warp-parallel (the run-filling kernel's per-CTA tail
+    // would dominate)
+    if (g.dead_mask) sparse = false;
     // QZ_DEC_KERNEL=warp|seg forces the dense-store kernel choice (tests)
     static const int force = getenv("QZ_DEC_KERNEL") ? (std::string(getenv("QZ_DEC_KERNEL")) == "seg" ? 1 : 0) : -1;
     const bool seg = g.lossy && g.N >= 64 && !sparse && (force >= 0 ? force == 1 : g.dense_hint != 0);

@@ -53,6 +53,11 @@ struct CodecGeom {
                             // segmented kernel (set per stage by the runtime)
     uint64_t scap;          // bytes per scratch stream (>= 2N, multiple of 8)
     uint64_t half_stride;   // scratch bytes per (slot, half)
+    // decode only: chunks whose index differs from dead_val on dead_mask are
+    // statically all +0 (fresh high qubits) and are not written — every
+    // later reader zero-fills them (qz_gates PassDesc::fmask, the runtime's
+    // dead fill before the encode)
+    uint64_t dead_mask, dead_val;
 };
 
 CodecGeom make_geom(uint64_t N, double eb);

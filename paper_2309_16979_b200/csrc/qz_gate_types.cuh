@@ -128,6 +128,10 @@ struct PassDesc {
     // start, and their values: a tile whose fixed bits differ from zval on
     // zmask is all +0 and — pz_stable, in place — is never visited
     uint64_t zmask, zval;
+    // every buffer bit fresh at the pass's start and its value: an element
+    // off zval on fmask is +0 and is zero-filled instead of loaded (the
+    // window may not hold it: the decode skips statically-(+0) chunks)
+    uint64_t fmask, fval;
 };
 
 enum PassKind : uint32_t { PASS_TILE = 0, PASS_SWAPS = 1 };

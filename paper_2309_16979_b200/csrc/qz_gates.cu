@@ -422,6 +422,8 @@ GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_
         pd.tmask = tmask;
         pd.zmask = fpass.mask & ~tmask;
         pd.zval = fpass.val & pd.zmask;
+        pd.fmask = fpass.mask;
+        pd.fval = fpass.val & fpass.mask;
         pd.first_gate = (uint32_t)plan.gates.size();
         pd.ngates = (uint32_t)members.size();
         pd.dg0 = (uint32_t)units[members.front()].first;

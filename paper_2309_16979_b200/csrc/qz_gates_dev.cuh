@@ -1149,7 +1149,10 @@ __device__ __forceinline__ void tile_pass_body(const double2 *__restrict__ src, 
     // a pz_stable in-place pass (no load, no store)
     // the map is consulted / maintained only while it still holds zero slots
     if (s_zc == 0) nzslot = nullptr;
-    const bool use_nz = nzslot && pd.pz_stable && src == dst && L <= cbits;
+    // fresh bits inside the tile: elements this pass may open are not yet in
+    // the window, so every visited tile is stored (no skip without a store)
+    const bool opens = (pd.fmask & pd.tmask) != 0;
+    const bool use_nz = nzslot && pd.pz_stable && src == dst && L <= cbits && !opens;
     for (uint64_t t = blockIdx.x; t < ntiles;
          t += gridDim.x, base = ((((base & ~zv) | ~ltmask) + dstep) & ltmask) | zv) {
         if (use_nz) {
@@ -1166,7 +1169,9 @@ __device__ __forceinline__ void tile_pass_body(const double2 *__restrict__ src, 
 #pragma unroll
         for (int i = 0; i < NB; ++i) {
             const uint32_t l = tid + i * nth;
-            cp_async16(s + swz(l), src + base + offhi[l >> L] + (l & lowmask));
+            const uint64_t e = base + offhi[l >> L] + (l & lowmask);
+            if ((e & pd.fmask) != pd.fval) s[swz(l)] = make_double2(0.0, 0.0);   // statically +0
+            else cp_async16(s + swz(l), src + e);
         }
         cp_async_wait_all();
         __syncthreads();
@@ -1186,7 +1191,7 @@ __device__ __forceinline__ void tile_pass_body(const double2 *__restrict__ src, 
             // an all-(+0) tile is a fixed point of the whole pass: skip it
             // (out of place: the output still needs the zeros)
             if (counters && tid == 0) atomicAdd(&counters[0], 1ull);
-            if (src != dst) {
+            if (src != dst || opens) {
 #pragma unroll
                 for (int i = 0; i < NB; ++i) {
                     const uint32_t l = tid + i * nth;

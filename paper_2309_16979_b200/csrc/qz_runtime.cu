@@ -394,6 +394,12 @@ void sim_alloc(qzc_sim *sim) {
     }
 }
 
+// Elements off `val` on `mask` (window bits still fresh at a stage's end) <- +0.
+__global__ void k_fill_dead(double2 *win, uint64_t n, uint64_t mask, uint64_t val) {
+    for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += uint64_t(gridDim.x) * blockDim.x)
+        if ((e & mask) != val) win[e] = make_double2(0.0, 0.0);
+}
+
 void run_window_passes(qzc_sim *sim, Window &W, const DevPlan &dp, const DevPlan &dsub, const DevPlan &dfull,
                        uint32_t wbits, cudaStream_t S,
                        const std::function<void(double2 *, const uint32_t *)> &redecode) {
@@ -1223,6 +1229,34 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
         int64_t acct_before[2] = {0, 0};
         if (sim->host_res) QZ_CUDA(cudaMemcpy(acct_before, sim->acct.p, 16, cudaMemcpyDeviceToHost));
         const uint64_t nwin = nbatches / bpw;
+        // statically-(+0) chunks (fresh high qubits) are not decoded: every
+        // pass zero-fills what it reads of them (PassDesc::fmask) and the
+        // elements still +0 at the stage's end are zero-filled before the
+        // encode.  Not with out-of-place passes (their replays read the
+        // window as decoded) or the host-staged store.
+        CodecGeom dgeom = sim->geom;
+        Fresh end_fresh;
+        {
+            bool out_of_place = false;
+            for (const PassDesc &pd : gp.passes) out_of_place |= pd.relaxed == 2;
+            // chunk-index bits of the stage's fresh high qubits (only those:
+            // the passes know the stage's buffer bits alone)
+            uint64_t fq = 0, fv = 0;
+            for (uint32_t q : st.high)
+                if ((sim->fresh_q >> q) & 1) {
+                    fq |= uint64_t(1) << (q - c);
+                    fv |= ((sim->fresh_v >> q) & 1) << (q - c);
+                }
+            if (!no_fresh && !sim->host_res && !out_of_place && fq && wbits >= 5) {
+                dgeom.dead_mask = fq;
+                dgeom.dead_val = fv;
+                end_fresh = fresh_after(dg, 0, dg.size(), stage_fresh);
+            }
+            if (trace)
+                fprintf(stderr, "qz trace: stage %zu dead-chunk mask %#llx val %#llx end-fresh %#llx pipelined %d\n",
+                        si, (unsigned long long)dgeom.dead_mask, (unsigned long long)dgeom.dead_val,
+                        (unsigned long long)end_fresh.mask, int(sim->pipelined));
+        }
         const uint64_t nslots = bpw << hs;
         for (int attempt = 0;; ++attempt) {
         QZ_CUDA(cudaMemsetAsync(sim->used_ptr(b), 0, 8, s));
@@ -1319,7 +1353,7 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
                 decode_window(ctx, W, sim->geom, nslots, nullptr, W.stage_in.as<uint8_t>(), W.local(),
                               ctx->launches, S, sim->sparse_store);
             } else {
-                decode_window(ctx, W, sim->geom, nslots, W.slot_chunk.as<uint64_t>(),
+                decode_window(ctx, W, dgeom, nslots, W.slot_chunk.as<uint64_t>(),
                               sim->arena_ptr(a), sim->table(a), ctx->launches, S, sim->sparse_store);
             }
             QZ_CUDA(cudaEventRecord(ev(4 * w + 1), S));
@@ -1347,6 +1381,12 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
                 QZ_CHECK_LAUNCH();
                 ctx->launches += 4;
             } else {
+                if (end_fresh.mask) {
+                    k_fill_dead<<<kNumSMs * 8, 256, 0, S>>>(W.amps.as<double2>(), uint64_t(1) << wbits,
+                                                             end_fresh.mask, end_fresh.val);
+                    QZ_CHECK_LAUNCH();
+                    ++ctx->launches;
+                }
                 encode_window(ctx, W, sim->geom, nslots, W.slot_chunk.as<uint64_t>(), nullptr, 0,
                               sim->arena_ptr(b), sim->used_ptr(b), sim->cap(b),
                               sim->table(b), sim->len[a].as<uint32_t>(), sim->acct.as<int64_t>(),
