@@ -132,6 +132,9 @@ struct PassDesc {
     // off zval on fmask is +0 and is zero-filled instead of loaded (the
     // window may not hold it: the decode skips statically-(+0) chunks)
     uint64_t fmask, fval;
+    // PASS_TILE: the swap network that followed is fused into the store —
+    // out of place, element e written to perm(e) (perm[] as for PASS_SWAPS)
+    uint32_t permute;
 };
 
 enum PassKind : uint32_t { PASS_TILE = 0, PASS_SWAPS = 1 };

@@ -379,7 +379,7 @@ static uint32_t case_id(const TileGate &t) {
 }
 
 GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_t kmax, bool fuse,
-                      int relax_level, const Fresh *fresh) {
+                      int relax_level, const Fresh *fresh, bool fuse_perm) {
     bool relax = relax_level > 0;
     GatePlan plan;
     const uint32_t k = std::min(kmax, nbits);
@@ -406,8 +406,31 @@ GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_
     // passes whose live tiles are dense
     static const uint32_t kOpen = getenv("QZ_FRESH_OPEN") ? uint32_t(atoi(getenv("QZ_FRESH_OPEN"))) : 6u;
     uint64_t opened = 0;
-    auto close = [&]() {
-        if (members.empty()) return;
+    // the bit permutation of a swap network unit (an involution)
+    auto unit_perm = [&](const Unit &u, uint8_t *perm) {
+        for (uint32_t b = 0; b < 48; ++b) perm[b] = uint8_t(b);
+        for (size_t i = u.first; i < u.first + u.count; ++i) {
+            perm[gates[i].b0] = uint8_t(gates[i].b1);
+            perm[gates[i].b1] = uint8_t(gates[i].b0);
+        }
+    };
+    // close the open pass; with `perm_unit`, try to fuse that swap network
+    // into its store (returns whether it did)
+    auto close = [&](const Unit *perm_unit = nullptr) -> bool {
+        if (members.empty()) return false;
+        uint8_t perm[48];
+        bool fusing = false;
+        if (perm_unit && nbits <= 48) {
+            // the stored tile needs the images of the low bits (coalesced
+            // output runs) among its bits
+            unit_perm(*perm_unit, perm);
+            uint64_t need_o = 0;
+            for (uint32_t b = 0; b < low; ++b) need_o |= uint64_t(1) << perm[b];
+            if ((uint32_t)__builtin_popcountll(tmask | need_o) <= k && low > 0) {
+                tmask |= need_o;
+                fusing = true;
+            }
+        }
         // pad T to exactly k bits with the lowest free bits (longer contiguous
         // global segments), bits fresh at the pass's start last
         for (int round = 0; round < 2; ++round)
@@ -728,11 +751,19 @@ GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_
             pd.pz_stable &= plan.groups[gi].pz_stable;
             if (plan.groups[gi].relaxed) pd.relaxed = std::max<uint32_t>(pd.relaxed, plan.groups[gi].unsafe ? 2u : 1u);
         }
+        // (out-of-place checked passes keep their own replay scheme)
+        const bool fused = fusing && pd.relaxed != 2;
+        if (fused) {
+            pd.permute = 1;
+            std::memcpy(pd.perm, perm, sizeof perm);
+            pd.dg1 = (uint32_t)(perm_unit->first + perm_unit->count);
+        }
         plan.passes.push_back(pd);
         members.clear();
         fpass = fcur;
         tmask = low_mask & ~fpass.mask;
         opened = 0;
+        return fused;
     };
     auto advance = [&](const Unit &u) {   // fcur through the unit's gates
         for (size_t i = u.first; i < u.first + u.count && fcur.mask; ++i) fcur = fresh_after_gate(fcur, gates[i]);
@@ -741,8 +772,14 @@ GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_
         const Unit &u = units[ui];
         if (u.bits >> nbits) throw Failure(QZC_EDEVICE, "gate bit outside buffer");
         if (u.swaps) {
-            // the whole swap network is one in-place bit-permutation pass
-            close();
+            // fused into the open pass's store, or one in-place
+            // bit-permutation pass of its own
+            if (close(fuse_perm ? &u : nullptr)) {
+                advance(u);
+                fpass = fcur;
+                tmask = low_mask & ~fpass.mask;
+                continue;
+            }
             PassDesc pd;
             std::memset(&pd, 0, sizeof pd);
             pd.kind = PASS_SWAPS;
@@ -909,7 +946,7 @@ void upload_plan(const GatePlan &plan, DevPlan &out, cudaStream_t s, uint32_t ji
         for (size_t p = 0; p < out.host_passes.size(); ++p)
             out.jit[p] = jit_request(plan, out.host_passes[p], jit_bits, p < fresh.size() ? fresh[p] : Fresh{});
     out.relaxed = false;
-    for (const PassDesc &pd : plan.passes) out.relaxed |= pd.relaxed != 0;
+    for (const PassDesc &pd : plan.passes) out.relaxed |= pd.relaxed != 0 || pd.permute != 0;   // (run_relaxed)
     out.replay_range.clear();
     if (out.ngates > out.cap_gates) {
         if (out.gates) QZ_CUDA(cudaFree(out.gates));
@@ -996,6 +1033,16 @@ void set_attrs() {
     }
 }
 
+// Chunks moved (swap network, permuted store): the zero map no longer
+// describes the slots.
+void reset_nz(NzMap nz, uint32_t nbits, cudaStream_t s) {
+    if (nz.slot && nbits > nz.cbits) {
+        const size_t ns = size_t(1) << (nbits - nz.cbits);
+        QZ_CUDA(cudaMemsetAsync(nz.slot, 1, 4 * ns, s));
+        QZ_CUDA(cudaMemsetAsync(nz.slot + ns, 0, 4, s));
+    }
+}
+
 // QZ_DEBUG_COUNTERS=1 QZ_COUNTERS_PER_PASS=1: counters after every pass (synchronous)
 void dump_pass_counters(const PassDesc &pd, uint32_t tag, const uint32_t *cond, cudaStream_t s) {
     static const bool per_pass = getenv("QZ_COUNTERS_PER_PASS") != nullptr;
@@ -1020,12 +1067,7 @@ void launch_pass(const DevPlan &plan, const PassDesc &pd, const double2 *src, do
         const uint64_t tiles = uint64_t(1) << (nbits > 2 * kSwapLow ? nbits - 2 * kSwapLow : 0);
         const uint64_t grid = std::min<uint64_t>(std::max<uint64_t>(tiles, 1), uint64_t(kNumSMs) * 8);
         tile_swaps<<<(unsigned)grid, 256, 0, s>>>(src, dst, nbits, pd, flag, cond);
-        // chunks moved: the zero map no longer describes the slots
-        if (nz.slot && nbits > nz.cbits) {
-            const size_t ns = size_t(1) << (nbits - nz.cbits);
-            QZ_CUDA(cudaMemsetAsync(nz.slot, 1, 4 * ns, s));
-            QZ_CUDA(cudaMemsetAsync(nz.slot + ns, 0, 4, s));
-        }
+        reset_nz(nz, nbits, s);
     } else if (pd.k < (uint32_t)kRegBits + 1) {
         // tile == whole buffer (nbits < 4): never relaxed, in place
         if (src != dst) throw Failure(QZC_EDEVICE, "tiny pass out of place");
@@ -1034,14 +1076,24 @@ void launch_pass(const DevPlan &plan, const PassDesc &pd, const double2 *src, do
         const uint32_t tile = 1u << pd.k;
         const uint64_t ntiles = uint64_t(1) << (nbits - pd.k);
         const uint32_t threads = tile >> kRegBits;
-        const size_t smem = sizeof(double2) * tile + sizeof(uint64_t) * (tile >> pd.lowbits);
+        size_t smem = sizeof(double2) * tile + sizeof(uint64_t) * (tile >> pd.lowbits);
+        if (pd.permute) {
+            // output offsets + the output-order slot map (tile_pass_body)
+            uint64_t ot = 0;
+            for (uint32_t b = 0; b < 48; ++b)
+                if ((pd.tmask >> b) & 1) ot |= uint64_t(1) << pd.perm[b];
+            uint32_t lo = 0;
+            while (lo < pd.k && ((ot >> lo) & 1)) ++lo;
+            smem += sizeof(uint64_t) * (tile >> lo) + sizeof(uint16_t) * tile;
+            if (src == dst) throw Failure(QZC_EDEVICE, "permuted pass in place");
+        }
         // live tiles (tile_pass_body's fresh-bit skip)
         const uint64_t live = (pd.zmask && pd.pz_stable && src == dst) ? ntiles >> __builtin_popcountll(pd.zmask)
                                                                        : ntiles;
         const uint64_t grid = std::min<uint64_t>(std::max<uint64_t>(live, 1), uint64_t(kNumSMs) * 2 * 8);
         // the map is only used for passes inside one window of whole slots
         static const bool off = getenv("QZ_NO_NZMAP") != nullptr;
-        const bool usable = nz.slot && nbits > nz.cbits && !off;
+        const bool usable = nz.slot && nbits > nz.cbits && !off && !pd.permute;
         if (jit) {
             const double2 *a_src = src;
             double2 *a_dst = dst;
@@ -1058,6 +1110,7 @@ void launch_pass(const DevPlan &plan, const PassDesc &pd, const double2 *src, do
                             &a_ctr, &a_flag, &a_cond, &a_nz, &a_cbits};
             if (jit_launch(*jit, (unsigned)grid, threads, smem, s, args)) {
                 QZ_CHECK_LAUNCH();
+                if (pd.permute) reset_nz(nz, nbits, s);
                 dump_pass_counters(pd, tag, cond, s);
                 return;
             }
@@ -1068,6 +1121,7 @@ void launch_pass(const DevPlan &plan, const PassDesc &pd, const double2 *src, do
         kern<<<(unsigned)grid, threads, smem, s>>>(src, dst, nbits, pd, plan.groups, plan.gates, ntiles,
                                                    debug_counters(), flag, cond,
                                                    usable ? nz.slot : nullptr, nz.cbits);
+        if (pd.permute) reset_nz(nz, nbits, s);
     }
     QZ_CHECK_LAUNCH();
     dump_pass_counters(pd, tag, cond, s);
@@ -1078,6 +1132,8 @@ void launch_pass(const DevPlan &plan, const PassDesc &pd, const double2 *src, do
 uint64_t run_passes(const DevPlan &plan, double2 *buf, uint32_t nbits, cudaStream_t s,
                     const uint32_t *cond, NzMap nz) {
     if (plan.relaxed) throw Failure(QZC_EDEVICE, "relaxed plan run without its replay plan");
+    for (const PassDesc &pd : plan.host_passes)
+        if (pd.permute) throw Failure(QZC_EDEVICE, "permuted pass in an in-place plan");
     set_attrs();
     for (size_t p = 0; p < plan.host_passes.size(); ++p)
         launch_pass(plan, plan.host_passes[p], buf, buf, nbits, s, nullptr, cond, nz, uint32_t(p));
@@ -1096,6 +1152,14 @@ double2 *run_relaxed(const DevPlan &plan, const DevPlan &replay, double2 *buf, d
     double2 *cur = buf, *oth = alt;
     for (size_t p = 0; p < plan.host_passes.size(); ++p) {
         const PassDesc &pd = plan.host_passes[p];
+        if (pd.permute) {
+            // fused swap network: out of place into the other buffer
+            if (pd.relaxed && force_replay) QZ_CUDA(cudaMemsetAsync(win_flag, 1, 1, s));
+            launch_pass(plan, pd, cur, oth, nbits, s, pd.relaxed ? win_flag : nullptr, nullptr, nz, uint32_t(p));
+            ++launches;
+            std::swap(cur, oth);
+            continue;
+        }
         if (pd.relaxed != 2) {
             if (pd.relaxed && force_replay) QZ_CUDA(cudaMemsetAsync(win_flag, 1, 1, s));
             launch_pass(plan, pd, cur, cur, nbits, s, pd.relaxed ? win_flag : nullptr, nullptr, nz, uint32_t(p));

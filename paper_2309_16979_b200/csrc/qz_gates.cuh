@@ -39,8 +39,11 @@ uint32_t gate_nparams(uint32_t kind);
 // fresh: buffer bits in a basis value at the start (see Fresh): tiles leave
 // them out where no gate needs them, and tiles on their +0 side are skipped.
 struct Fresh;
+// fuse_perm: a swap network right after a tile pass becomes that pass's
+// permuted out-of-place store (PassDesc::permute) when its tile can hold the
+// network's images of the low bits.
 GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_t kmax,
-                      bool fuse, int relax_level = 0, const Fresh *fresh = nullptr);
+                      bool fuse, int relax_level = 0, const Fresh *fresh = nullptr, bool fuse_perm = false);
 
 DevGate make_dev_gate(const qzc_gate &g);
 DevGate make_dev_gate_matrix(const double2 *m, uint32_t dim, uint32_t b0, uint32_t b1);

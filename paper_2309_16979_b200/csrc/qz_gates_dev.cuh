@@ -1064,6 +1064,17 @@ __device__ __forceinline__ void mask_apply(uint32_t &SR, uint32_t &SI, const Til
 // spread over all 8 bank groups.
 __device__ __forceinline__ uint32_t swz(uint32_t l) { return l ^ ((l >> 3) & 7u) ^ ((l >> 6) & 7u); }
 
+// Image of the bit set x under a bit permutation (PassDesc::perm).
+__device__ __forceinline__ uint64_t permute_bits(uint64_t x, const uint8_t (&perm)[48]) {
+    uint64_t r = 0;
+    while (x) {
+        const uint32_t b = __ffsll((long long)x) - 1;
+        x &= x - 1;
+        r |= uint64_t(1) << perm[b];
+    }
+    return r;
+}
+
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
     const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
@@ -1131,6 +1142,36 @@ __device__ __forceinline__ void tile_pass_body(const double2 *__restrict__ src, 
     // register-group position of this thread (PassDesc::wmap)
     const uint32_t tmap = (pd.wmap && nth >= 64) ? (tid >> 5) | ((tid & 31u) << (31 - __clz(nth >> 5))) : tid;
     for (uint32_t h = tid; h < nhi; h += nth) offhi[h] = deposit_bits(h, himask);
+    // permuted store (PassDesc::permute): the output tile spans perm(T); it
+    // is written in output order (runs of 2^Lo contiguous elements), element
+    // l_out taken from tile slot lmap[l_out]
+    uint64_t *offo = offhi + nhi;
+    uint16_t *lmap = nullptr;
+    uint32_t Lo = 0;
+    if (pd.permute) {
+        const uint64_t otmask = permute_bits(pd.tmask, pd.perm);
+        while (Lo < k && ((otmask >> Lo) & 1)) ++Lo;
+        const uint64_t ohimask = otmask & ~((uint64_t(1) << Lo) - 1);
+        lmap = reinterpret_cast<uint16_t *>(offo + (1u << (k - Lo)));
+        for (uint32_t h = tid; h < (1u << (k - Lo)); h += nth) offo[h] = deposit_bits(h, ohimask);
+        // output tile bit j (ascending in perm(T)) is input tile bit rank[j]
+        uint32_t rank[16];
+        {
+            uint64_t om = otmask;
+            for (uint32_t j = 0; j < k; ++j) {
+                const uint32_t ob = __ffsll((long long)om) - 1;
+                om &= om - 1;
+                const uint32_t ib = pd.perm[ob];
+                rank[j] = __popcll(pd.tmask & ((uint64_t(1) << ib) - 1));
+            }
+        }
+        for (uint32_t l = tid; l < tile; l += nth) {
+            uint32_t li = 0;
+            for (uint32_t j = 0; j < k; ++j) li |= ((l >> j) & 1u) << rank[j];
+            lmap[l] = uint16_t(li);
+        }
+    }
+    const uint32_t lomask = (1u << Lo) - 1;
     // the zero-slot count, read once per CTA (other CTAs update it)
     __shared__ uint32_t s_zc;
     if (tid == 0) s_zc = nzslot ? nzslot[uint64_t(1) << (nbits - cbits)] : 0u;
@@ -1192,10 +1233,13 @@ __device__ __forceinline__ void tile_pass_body(const double2 *__restrict__ src, 
             // (out of place: the output still needs the zeros)
             if (counters && tid == 0) atomicAdd(&counters[0], 1ull);
             if (src != dst || opens) {
+                const uint64_t pbase = pd.permute ? permute_bits(base, pd.perm) : 0;
 #pragma unroll
                 for (int i = 0; i < NB; ++i) {
                     const uint32_t l = tid + i * nth;
-                    __stcs(dst + base + offhi[l >> L] + (l & lowmask), make_double2(0.0, 0.0));
+                    __stcs(pd.permute ? dst + pbase + offo[l >> Lo] + (l & lomask)
+                                      : dst + base + offhi[l >> L] + (l & lowmask),
+                           make_double2(0.0, 0.0));
                 }
             }
             continue;
@@ -1314,12 +1358,23 @@ __device__ __forceinline__ void tile_pass_body(const double2 *__restrict__ src, 
 #endif
         }
         double2 out[NB];
+        if (pd.permute) {
+            const uint64_t pbase = permute_bits(base, pd.perm);
 #pragma unroll
-        for (int i = 0; i < NB; ++i) out[i] = s[swz(tid + i * nth)];
+            for (int i = 0; i < NB; ++i) out[i] = s[swz(lmap[tid + i * nth])];
 #pragma unroll
-        for (int i = 0; i < NB; ++i) {
-            const uint32_t l = tid + i * nth;
-            __stcs(dst + base + offhi[l >> L] + (l & lowmask), out[i]);
+            for (int i = 0; i < NB; ++i) {
+                const uint32_t l = tid + i * nth;
+                __stcs(dst + pbase + offo[l >> Lo] + (l & lomask), out[i]);
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < NB; ++i) out[i] = s[swz(tid + i * nth)];
+#pragma unroll
+            for (int i = 0; i < NB; ++i) {
+                const uint32_t l = tid + i * nth;
+                __stcs(dst + base + offhi[l >> L] + (l & lowmask), out[i]);
+            }
         }
         if (nzslot) {
             // every slot the tile covers (the low tile bits span 2^(L - cbits)

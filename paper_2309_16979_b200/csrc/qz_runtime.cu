@@ -1201,7 +1201,25 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
                     stage_fresh.val |= ((sim->fresh_v >> q) & 1) << bq;
                 }
             }
-        GatePlan gp = build_passes(dg, wbits, kTileBits, sim->cfg.fuse_gates != 0, sim->relax, &stage_fresh);
+        // a swap network after a tile pass is fused into its store (out of
+        // place: needs the second window buffer; QZ_NO_PERM_FUSE=1 keeps the
+        // separate swap pass)
+        static const bool no_perm = getenv("QZ_NO_PERM_FUSE") != nullptr;
+        GatePlan gp = build_passes(dg, wbits, kTileBits, sim->cfg.fuse_gates != 0, sim->relax, &stage_fresh,
+                                   !no_perm);
+        {
+            bool perm = false;
+            for (const PassDesc &pd : gp.passes) perm |= pd.permute != 0;
+            if (perm) {
+                try {
+                    sim->win.alt.ensure(sim->win.amps.cap);
+                    if (sim->two_windows) sim->win2.alt.ensure(sim->win2.amps.cap);
+                } catch (const Failure &) {
+                    (void)cudaGetLastError();   // out of memory: the unfused plan
+                    gp = build_passes(dg, wbits, kTileBits, sim->cfg.fuse_gates != 0, sim->relax, &stage_fresh, false);
+                }
+            }
+        }
         DevPlan &dp = sim->plans[0], &dsub = sim->plans[1], &dfull = sim->plans[2];
         std::vector<Fresh> pass_fresh;
         {
