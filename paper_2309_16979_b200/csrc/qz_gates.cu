@@ -431,6 +431,12 @@ GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_
                 fusing = true;
             }
         }
+        // a fused store: first the images of the next output bits (longer
+        // contiguous output runs), while not fresh
+        for (uint32_t b = low; fusing && b < nbits && (uint32_t)__builtin_popcountll(tmask) < k; ++b) {
+            if ((fpass.mask >> perm[b]) & 1) break;
+            tmask |= uint64_t(1) << perm[b];
+        }
         // pad T to exactly k bits with the lowest free bits (longer contiguous
         // global segments), bits fresh at the pass's start last
         for (int round = 0; round < 2; ++round)

@@ -46,6 +46,8 @@ struct Nvrtc {
     decltype(&nvrtcDestroyProgram) destroy = nullptr;
 };
 
+void drain_pool_at_exit();
+
 const Nvrtc &nvrtc() {
     static Nvrtc n = [] {
         Nvrtc r;
@@ -53,6 +55,9 @@ const Nvrtc &nvrtc() {
         for (const char *name : {"libnvrtc.so.12", "/usr/local/cuda/lib64/libnvrtc.so.12", "libnvrtc.so"})
             if (!h) h = dlopen(name, RTLD_NOW | RTLD_LOCAL);
         if (!h) return r;
+        // registered after libnvrtc's own exit handlers: runs before them, so
+        // no compile is still inside NVRTC while it is torn down
+        std::atexit(drain_pool_at_exit);
         r.create = reinterpret_cast<decltype(r.create)>(dlsym(h, "nvrtcCreateProgram"));
         r.compile = reinterpret_cast<decltype(r.compile)>(dlsym(h, "nvrtcCompileProgram"));
         r.log_size = reinterpret_cast<decltype(r.log_size)>(dlsym(h, "nvrtcGetProgramLogSize"));
@@ -102,15 +107,18 @@ class Pool {
         const unsigned n = std::max(2u, std::min(16u, std::thread::hardware_concurrency()));
         for (unsigned i = 0; i < n; ++i) threads_.emplace_back([this] { loop(); });
     }
-    ~Pool() {
+    ~Pool() { shutdown(); }
+    // queued compiles are dropped, running ones finish (idempotent)
+    void shutdown() {
         {
-            // at exit: queued compiles are dropped, running ones finish
             std::lock_guard<std::mutex> lk(mu_);
             stop_ = true;
             q_.clear();
         }
         cv_.notify_all();
-        for (auto &t : threads_) t.join();
+        std::lock_guard<std::mutex> lk(join_mu_);
+        for (auto &t : threads_)
+            if (t.joinable()) t.join();
     }
     void submit(std::function<void()> f) {
         {
@@ -134,7 +142,7 @@ class Pool {
             f();
         }
     }
-    std::mutex mu_;
+    std::mutex mu_, join_mu_;
     std::condition_variable cv_;
     std::deque<std::function<void()>> q_;
     std::vector<std::thread> threads_;
@@ -145,6 +153,8 @@ Pool &pool() {
     static Pool p;
     return p;
 }
+
+void drain_pool_at_exit() { pool().shutdown(); }
 
 void put_double(std::string &o, double x) {
     char b[40];

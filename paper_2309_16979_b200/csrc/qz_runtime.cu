@@ -1097,7 +1097,8 @@ int qzc_pass_plan_stats(const qzc_gate *gates, uint64_t ngates, uint32_t nbits,
     Fresh fr;
     if (getenv("QZ_PLAN_FRESH")) fr.mask = (uint64_t(1) << nbits) - 1;
     const GatePlan p = build_passes(dg, nbits, kTileBits, fuse_mode != 0,
-                                    fuse_mode == 1 ? 1 : (fuse_mode == 3 ? 2 : 0), &fr);
+                                    fuse_mode == 1 ? 1 : (fuse_mode == 3 ? 2 : 0), &fr,
+                                    getenv("QZ_PLAN_PERM") != nullptr);
     uint64_t relaxed = 0, fast = 0, pdiag = 0;
     for (const GroupDesc &g : p.groups) {
         relaxed += g.relaxed;

@@ -131,6 +131,10 @@ def load_library() -> C.CDLL:
         f.restype = res
         f.argtypes = args
     _lib = lib
+    # specialised-pass compiles still running at interpreter exit would race
+    # NVRTC's own teardown: let them finish first
+    import atexit
+    atexit.register(lib.qzc_jit_wait)
     return lib
 
 

@@ -1,0 +1,6 @@
+#!/bin/bash
+export PYTHONPATH=$PWD
+O=gpurun_out/pm2; mkdir -p $O
+python tools/probe_dense.py qft 30 --c 16 --m 30 --eb 1e-5 --reps 5 --kprof > $O/qft.log 2>&1
+python -m pytest tests -m gpu -q > $O/tests.log 2>&1; echo "rc=$?" >> $O/tests.log
+python -m pytest tests/test_gpu_sim.py -q -x -k "qft or large or relax or random" > $O/tests2.log 2>&1; echo "rc=$?" >> $O/tests2.log
