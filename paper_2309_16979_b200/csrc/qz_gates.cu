@@ -1067,8 +1067,17 @@ void launch_pass(const DevPlan &plan, const PassDesc &pd, const double2 *src, do
     static const char *const kJitName[3] = {"tile_pass_jit<All>", "tile_pass_jit<DiagH>", "tile_pass_jit<Gen>"};
     // `tag` is the pass's index in `plan`
     JitPass *jit = tag < plan.jit.size() && plan.jit[tag] && jit_ready(*plan.jit[tag]) ? plan.jit[tag].get() : nullptr;
+    // algorithmic bytes: 16 B per element loaded (live tiles, minus the
+    // statically-(+0) elements a pass zero-fills) + 16 B per element stored;
+    // replays are no-ops unless flagged
+    double pbytes = 32.0 * double(uint64_t(1) << nbits);
+    if (pd.kind == PASS_TILE && pd.k >= (uint32_t)kRegBits + 1) {
+        const double live = double(uint64_t(1) << nbits) /
+                            ((pd.zmask && pd.pz_stable && src == dst) ? double(uint64_t(1) << __builtin_popcountll(pd.zmask)) : 1.0);
+        pbytes = 16.0 * live * (1.0 + 1.0 / double(uint64_t(1) << __builtin_popcountll(pd.fmask & pd.tmask)));
+    }
     KProfScope prof(s, cond ? "replay_pass" : pd.kind == PASS_SWAPS ? "tile_swaps" : (jit ? kJitName : kName)[pd.variant % 3],
-                    tag, cond ? 0.0 : 32.0 * double(uint64_t(1) << nbits));   // replays: no-ops unless flagged
+                    tag, cond ? 0.0 : pbytes);
     if (pd.kind == PASS_SWAPS) {
         const uint64_t tiles = uint64_t(1) << (nbits > 2 * kSwapLow ? nbits - 2 * kSwapLow : 0);
         const uint64_t grid = std::min<uint64_t>(std::max<uint64_t>(tiles, 1), uint64_t(kNumSMs) * 8);
