@@ -404,7 +404,7 @@ GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_
     // gates on them): the ops before an opening run on a mostly-(+0) tile
     // where few warps have work, so a long run of openings is split into
     // passes whose live tiles are dense
-    static const uint32_t kOpen = getenv("QZ_FRESH_OPEN") ? uint32_t(atoi(getenv("QZ_FRESH_OPEN"))) : 6u;
+    static const uint32_t kOpen = getenv("QZ_FRESH_OPEN") ? uint32_t(atoi(getenv("QZ_FRESH_OPEN"))) : 3u;
     uint64_t opened = 0;
     // the bit permutation of a swap network unit (an involution)
     auto unit_perm = [&](const Unit &u, uint8_t *perm) {
@@ -431,11 +431,25 @@ GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_
                 fusing = true;
             }
         }
-        // a fused store: first the images of the next output bits (longer
-        // contiguous output runs), while not fresh
-        for (uint32_t b = low; fusing && b < nbits && (uint32_t)__builtin_popcountll(tmask) < k; ++b) {
-            if ((fpass.mask >> perm[b]) & 1) break;
-            tmask |= uint64_t(1) << perm[b];
+        // a fused store: alternately the lowest non-fresh input bit (the live
+        // elements' input runs) and the image of the next output bit (output
+        // runs), while they are not fresh
+        if (fusing) {
+            uint32_t ib = 0, ob = low;
+            for (bool more = true; more && (uint32_t)__builtin_popcountll(tmask) < k;) {
+                more = false;
+                while (ib < nbits && (((tmask >> ib) & 1) || ((fpass.mask >> ib) & 1))) ++ib;
+                if (ib < nbits) {
+                    tmask |= uint64_t(1) << ib;
+                    more = true;
+                }
+                if ((uint32_t)__builtin_popcountll(tmask) >= k) break;
+                while (ob < nbits && ((tmask >> perm[ob]) & 1)) ++ob;
+                if (ob < nbits && !((fpass.mask >> perm[ob]) & 1)) {
+                    tmask |= uint64_t(1) << perm[ob];
+                    more = true;
+                }
+            }
         }
         // pad T to exactly k bits with the lowest free bits (longer contiguous
         // global segments), bits fresh at the pass's start last

@@ -518,6 +518,44 @@ int qzc_context_create(int device, uint64_t hbm_budget_bytes, qzc_context **out)
     QZ_CUDA(cudaMalloc(&ctx->status, sizeof(DevStatus)));
     QZ_CUDA(cudaMemset(ctx->status, 0, sizeof(DevStatus)));
     QZ_CUDA(cudaMallocHost(&ctx->status_host, sizeof(DevStatus)));
+    // load the stage loop's kernels now (CUDA loads a kernel's module at its
+    // first launch): two tiny runs, lossy and lossless, multi-stage, so no
+    // timed run pays for module loading (QZ_NO_WARMUP=1 skips)
+    if (!getenv("QZ_NO_WARMUP")) {
+        auto g = [](uint32_t kind, uint32_t a, int b = -1, double p = 0.0) {
+            qzc_gate x{};
+            x.kind = kind;
+            x.nqubits = b < 0 ? 1 : 2;
+            x.qubits[0] = a;
+            x.qubits[1] = b < 0 ? 0 : uint32_t(b);
+            x.params[0] = p;
+            return x;
+        };
+        std::vector<qzc_gate> circ;
+        for (uint32_t q = 0; q < 8; ++q) circ.push_back(g(QZC_H, q));
+        for (const qzc_gate &x : {g(QZC_CX, 0, 1), g(QZC_CZ, 2, 3), g(QZC_U1, 4, -1, 0.3), g(QZC_X, 1),
+                                  g(QZC_RY, 2, -1, 0.4), g(QZC_T, 3), g(QZC_CX, 6, 2), g(QZC_SWAP, 5, 6),
+                                  g(QZC_SWAP, 0, 7), g(QZC_H, 7), g(QZC_U1, 7, -1, 2.5), g(QZC_CX, 7, 0)})
+            circ.push_back(x);
+        for (double eb : {1e-5, 0.0})
+            for (uint32_t m : {8u, 6u}) {
+                qzc_sim_config sc{};
+                sc.num_qubits = 8;
+                sc.chunk_qubits = 4;
+                sc.batch_qubits = m;
+                sc.error_bound = eb;
+                sc.fuse_gates = 1;
+                qzc_sim *sim = nullptr;
+                if (qzc_sim_create(ctx, &sc, &sim) == QZC_OK) {
+                    qzc_sim_init_basis(sim);
+                    qzc_sim_run(sim, circ.data(), circ.size());
+                    qzc_sim_destroy(sim);
+                }
+            }
+        QZ_CUDA(cudaDeviceSynchronize());
+        ctx->launches = 0;
+        last_error().clear();
+    }
     *out = ctx;
     QZ_API_END
 }
