@@ -1240,6 +1240,44 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
                     stage_fresh.val |= ((sim->fresh_v >> q) & 1) << bq;
                 }
             }
+        const uint64_t nwin = nbatches / bpw;
+        const uint64_t nslots = bpw << hs;
+        CodecGeom dgeom = sim->geom;
+        Fresh end_fresh;
+        {
+            // out-of-place checked passes exist only with relax level 2
+            const bool out_of_place = sim->relax == 2;
+            // chunk-index bits of the stage's fresh high qubits (only those:
+            // the passes know the stage's buffer bits alone)
+            uint64_t fq = 0, fv = 0;
+            for (uint32_t q : st.high)
+                if ((sim->fresh_q >> q) & 1) {
+                    fq |= uint64_t(1) << (q - c);
+                    fv |= ((sim->fresh_v >> q) & 1) << (q - c);
+                }
+            if (!no_fresh && !sim->host_res && !out_of_place && fq && wbits >= 5) {
+                dgeom.dead_mask = fq;
+                dgeom.dead_val = fv;
+                end_fresh = fresh_after(dg, 0, dg.size(), stage_fresh);
+            }
+            if (trace)
+                fprintf(stderr, "qz trace: stage %zu dead-chunk mask %#llx val %#llx end-fresh %#llx pipelined %d\n",
+                        si, (unsigned long long)dgeom.dead_mask, (unsigned long long)dgeom.dead_val,
+                        (unsigned long long)end_fresh.mask, int(sim->pipelined));
+        }
+        // HBM store, one stream per window: the first window's decode does
+        // not depend on the plan, so it is issued before planning and runs
+        // while the host plans
+        const bool pre_decode = !sim->host_res && !sim->pipelined;
+        if (pre_decode) {
+            Window &W0 = sim->win;
+            cudaStream_t S0 = sim->streams[0];
+            QZ_CUDA(cudaEventRecord(ev(0), S0));
+            launch_slot_chunks(W0.slot_chunk.as<uint64_t>(), nslots, 0, hs, fmask, smask, S0);
+            decode_window(ctx, W0, dgeom, nslots, W0.slot_chunk.as<uint64_t>(), sim->arena_ptr(sim->cur),
+                          sim->table(sim->cur), ctx->launches, S0, sim->sparse_store);
+            QZ_CUDA(cudaEventRecord(ev(1), S0));
+        }
         // a swap network after a tile pass is fused into its store (out of
         // place: needs the second window buffer; QZ_NO_PERM_FUSE=1 keeps the
         // separate swap pass)
@@ -1285,36 +1323,11 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
         // from its (untouched) input arena after the output arena grew
         int64_t acct_before[2] = {0, 0};
         if (sim->host_res) QZ_CUDA(cudaMemcpy(acct_before, sim->acct.p, 16, cudaMemcpyDeviceToHost));
-        const uint64_t nwin = nbatches / bpw;
         // statically-(+0) chunks (fresh high qubits) are not decoded: every
         // pass zero-fills what it reads of them (PassDesc::fmask) and the
         // elements still +0 at the stage's end are zero-filled before the
         // encode.  Not with out-of-place passes (their replays read the
         // window as decoded) or the host-staged store.
-        CodecGeom dgeom = sim->geom;
-        Fresh end_fresh;
-        {
-            bool out_of_place = false;
-            for (const PassDesc &pd : gp.passes) out_of_place |= pd.relaxed == 2;
-            // chunk-index bits of the stage's fresh high qubits (only those:
-            // the passes know the stage's buffer bits alone)
-            uint64_t fq = 0, fv = 0;
-            for (uint32_t q : st.high)
-                if ((sim->fresh_q >> q) & 1) {
-                    fq |= uint64_t(1) << (q - c);
-                    fv |= ((sim->fresh_v >> q) & 1) << (q - c);
-                }
-            if (!no_fresh && !sim->host_res && !out_of_place && fq && wbits >= 5) {
-                dgeom.dead_mask = fq;
-                dgeom.dead_val = fv;
-                end_fresh = fresh_after(dg, 0, dg.size(), stage_fresh);
-            }
-            if (trace)
-                fprintf(stderr, "qz trace: stage %zu dead-chunk mask %#llx val %#llx end-fresh %#llx pipelined %d\n",
-                        si, (unsigned long long)dgeom.dead_mask, (unsigned long long)dgeom.dead_val,
-                        (unsigned long long)end_fresh.mask, int(sim->pipelined));
-        }
-        const uint64_t nslots = bpw << hs;
         for (int attempt = 0;; ++attempt) {
         QZ_CUDA(cudaMemsetAsync(sim->used_ptr(b), 0, 8, s));
         // the stage's plan upload and arena reset happen on the context
@@ -1391,6 +1404,7 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
             Window &W = ws ? sim->win2 : sim->win;
             cudaStream_t S = sim->streams[ws];
             if (w < 2) QZ_CUDA(cudaStreamWaitEvent(S, ready, 0));
+            if (!(w == 0 && pre_decode)) {   // (window 0's decode was issued before planning)
             QZ_CUDA(cudaEventRecord(ev(4 * w), S));
             launch_slot_chunks(W.slot_chunk.as<uint64_t>(), nslots, w * bpw, hs, fmask, smask, S);
             if (sim->host_res) {
@@ -1414,6 +1428,7 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
                               sim->arena_ptr(a), sim->table(a), ctx->launches, S, sim->sparse_store);
             }
             QZ_CUDA(cudaEventRecord(ev(4 * w + 1), S));
+            }
             run_window_passes(sim, W, dp, dsub, dfull, wbits, S, [&](double2 *dst, const uint32_t *cond) {
                 if (sim->host_res)
                     launch_decode(W.stage_in.as<uint8_t>(), W.idx.as<DecIdx>(), nullptr, nslots, sim->geom, dst,
