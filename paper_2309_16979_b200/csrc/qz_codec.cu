@@ -114,7 +114,15 @@ __global__ void __launch_bounds__(256) k_crc(const uint32_t *__restrict__ tabs,
                                              const uint64_t *__restrict__ slot_chunk,
                                              uint64_t nslots, int verify, DevStatus *status) {
     __shared__ uint32_t T[8 * 256];
+    __shared__ uint32_t X2[32];   // x^(8 * 2^k) mod P
     for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) T[i] = tabs[i];
+    if (threadIdx.x == 0) {
+        uint32_t x = x8nmodp(1);
+        for (int k = 0; k < 32; ++k) {
+            X2[k] = x;
+            x = multmodp(x, x);
+        }
+    }
     __syncthreads();
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -125,16 +133,19 @@ __global__ void __launch_bounds__(256) k_crc(const uint32_t *__restrict__ tabs,
         const uint8_t *p = arena + table.off[chunk];
         const uint64_t seg = round_up((len + 31) / 32, 8);
         const uint64_t b = umin64(len, lane * seg), e = umin64(len, b + seg);
-        uint32_t c = crc_range(T, p + b, e - b);
-        uint32_t mylen = uint32_t(e - b);
-        // fold lane CRCs left to right: acc = acc * x^(8 len_i) ^ crc_i
-        uint32_t acc = c;
-        const uint32_t sh_full = lane == 0 ? x8nmodp(seg) : 0;
-        for (int i = 1; i < 32; ++i) {
-            const uint32_t ci = __shfl_sync(0xffffffffu, c, i);
-            const uint32_t li = __shfl_sync(0xffffffffu, mylen, i);
-            if (lane == 0 && li) acc = multmodp(li == seg ? sh_full : x8nmodp(li), acc) ^ ci;
+        const uint32_t c = crc_range(T, p + b, e - b);
+        // crc(A||B) = crc(A) * x^(8|B|) ^ crc(B) folds to
+        // XOR_i crc_i * x^(8 S_i), S_i = bytes after lane i's segment: every
+        // lane shifts its own CRC (powers from X2), then one XOR reduction
+        const uint32_t after = uint32_t(len - e);
+        uint32_t acc = 0;
+        if (e > b) {
+            uint32_t f = 0x80000000u;   // x^0
+            for (uint32_t r = after; r; r &= r - 1) f = multmodp(X2[__ffs(r) - 1], f);
+            acc = multmodp(f, c);
         }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc ^= __shfl_xor_sync(0xffffffffu, acc, o);
         if (lane == 0) {
             if (verify) {
                 if (acc != table.crc[chunk]) dev_fail(status, QZS_CRC, chunk);
