@@ -719,8 +719,7 @@ __global__ void __launch_bounds__(256) k_dec_lossy_seg(
     const uint64_t *__restrict__ slot_chunk, uint64_t nslots, CodecGeom g,
     double2 *__restrict__ win, DevStatus *status, const uint32_t *cond) {
     if (cond && *cond == 0) return;
-    __shared__ double cv[8][2][32];   // per warp: chain inputs, chain outputs
-    const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5, seg = lane >> 3, sub = lane & 7;
+    const uint32_t lane = threadIdx.x & 31, seg = lane >> 3, sub = lane & 7;
     const uint64_t s = ((uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * 2 + (seg >> 1);
     const uint32_t h = seg & 1;
     if (((uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * 2 >= nslots) return;   // whole warp
@@ -748,7 +747,6 @@ __global__ void __launch_bounds__(256) k_dec_lossy_seg(
     uint32_t raw_i = live && h ? d.raw_re : 0;
     const uint32_t raw_count = live ? d.raw_count : 0, raw_pos = live ? d.raw_pos : 0;
     double pred = 0.0;
-    double *vin = cv[wib][0], *vout = cv[wib][1];
     double2 *out = win + (exists ? s : 0) * N;
     for (uint64_t e0 = 0; e0 < N; e0 += kSegW) {
         const uint32_t z = plane_seg(lo, p, sub) | (plane_seg(hi, p, sub) << 8);
@@ -763,20 +761,17 @@ __global__ void __launch_bounds__(256) k_dec_lossy_seg(
             val = __dmul_rn(double(unzigzag16(z)), twoeb);
         }
         raw_i += __popc(rm);
-        vin[lane] = val;
-        __syncwarp();
-        const double *vs = vin + 8 * seg;
+        // the segment's chain in order, its values broadcast by shuffles
+        // (every lane of the segment runs it; lane `sub` keeps step sub)
+        double mine = 0.0;
 #pragma unroll
         for (uint32_t i = 0; i < kSegW; ++i) {
-            const double x = vs[i];
+            const double x = __shfl_sync(0xffffffffu, val, i, kSegW);
             pred = ((rm >> i) & 1) ? x : __dadd_rn(pred, x);
-            vout[8 * seg + i] = pred;
+            if (i == sub) mine = pred;
         }
-        __syncwarp();
-        const double mine = vout[lane];
         const double im = __shfl_down_sync(0xffffffffu, mine, kSegW);
         if (h == 0 && exists) __stcs(out + e0 + sub, make_double2(live ? mine : 0.0, live ? im : 0.0));
-        __syncwarp();
     }
     if (live && sub == 0) {
         const uint64_t chunk = slot_chunk ? slot_chunk[s] : s;
@@ -1607,7 +1602,10 @@ void launch_decode(const uint8_t *arena, const DecIdx *idx, const uint64_t *slot
     // would dominate)
     if (g.dead_mask) sparse = false;
     // QZ_DEC_KERNEL=warp|seg forces the dense-store kernel choice (tests)
-    static const int force = getenv("QZ_DEC_KERNEL") ? (std::string(getenv("QZ_DEC_KERNEL")) == "seg" ? 1 : 0) : -1;
+    static const int force = getenv("QZ_DEC_KERNEL") ? (std::string(getenv("QZ_DEC_KERNEL")) == "seg" ? 1
+                                                         : std::string(getenv("QZ_DEC_KERNEL")) == "thread" ? 2 : 0)
+                                                      : -1;
+    if (force == 2) sparse = true;   // (the thread-per-chain kernel on any store)
     const bool seg = g.lossy && g.N >= 64 && !sparse && (force >= 0 ? force == 1 : g.dense_hint != 0);
     KProfScope prof(s, cond ? "replay_decode" : seg ? "k_dec_lossy_seg" : (g.lossy && g.N >= 32 && !sparse) ? "k_dec_lossy_warp"
                                             : g.lossy ? "k_dec_lossy" : "k_dec_lossless", 0, cond ? 0.0 : dense);

@@ -435,13 +435,18 @@ GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_
         // elements' input runs) and the image of the next output bit (output
         // runs), while they are not fresh
         if (fusing) {
+            // QZ_FUSE_PAD (tuning): 0 alternate (default), 1 input runs first, 2 output runs first
+            static const int mode = getenv("QZ_FUSE_PAD") ? atoi(getenv("QZ_FUSE_PAD")) : 0;
             uint32_t ib = 0, ob = low;
             for (bool more = true; more && (uint32_t)__builtin_popcountll(tmask) < k;) {
                 more = false;
-                while (ib < nbits && (((tmask >> ib) & 1) || ((fpass.mask >> ib) & 1))) ++ib;
-                if (ib < nbits) {
-                    tmask |= uint64_t(1) << ib;
-                    more = true;
+                if (mode != 2) {
+                    while (ib < nbits && (((tmask >> ib) & 1) || ((fpass.mask >> ib) & 1))) ++ib;
+                    if (ib < nbits) {
+                        tmask |= uint64_t(1) << ib;
+                        more = true;
+                        if (mode == 1) continue;
+                    }
                 }
                 if ((uint32_t)__builtin_popcountll(tmask) >= k) break;
                 while (ob < nbits && ((tmask >> perm[ob]) & 1)) ++ob;
