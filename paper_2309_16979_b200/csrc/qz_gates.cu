@@ -848,9 +848,9 @@ GatePlan build_passes(const std::vector<DevGate> &gates, uint32_t nbits, uint32_
                     npd += plan.gates[plan.groups[gi].first_fast + q].op == OP_PDIAG;
             }
             fprintf(stderr, "qz plan: kind %u tmask %#llx groups %u (relaxed %u, unsafe %u) fast ops %u pdiag %u "
-                            "gates %u pass relaxed %u zmask %#llx\n",
+                            "gates %u pass relaxed %u zmask %#llx fmask %#llx permute %u\n",
                     pd.kind, (unsigned long long)pd.tmask, pd.ngroups, nrel, nuns, nf, npd, pd.ngates, pd.relaxed,
-                    (unsigned long long)pd.zmask);
+                    (unsigned long long)pd.zmask, (unsigned long long)pd.fmask, pd.permute);
         }
     }
     return plan;
@@ -1032,8 +1032,8 @@ void dump_debug_counters() {
         fprintf(stderr, "qz group clocks (CTA-thread-0 cycles): load+census=%llu g0=%llu g1=%llu g2=%llu g3=%llu "
                         "g4=%llu g5+=%llu store=%llu\n", h[8], h[9], h[10], h[11], h[12], h[13], h[14], h[15]);
     fprintf(stderr, "qz counters: tiles_skipped=%llu grp_pz_skip=%llu grp_mask=%llu grp_fast=%llu "
-                    "grp_exact=%llu grp_fast_then_exact=%llu\n",
-            h[0], h[1], h[2], h[3], h[4], h[5]);
+                    "grp_exact=%llu grp_fast_then_exact=%llu zero_filled=%llu loaded=%llu\n",
+            h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7]);
     QZ_CUDA(cudaMemset(p, 0, sizeof h));
 }
 

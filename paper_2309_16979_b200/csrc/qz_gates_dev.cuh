@@ -1213,6 +1213,9 @@ __device__ __forceinline__ void tile_pass_body(const double2 *__restrict__ src, 
             const uint64_t e = base + offhi[l >> L] + (l & lowmask);
             if ((e & pd.fmask) != pd.fval) s[swz(l)] = make_double2(0.0, 0.0);   // statically +0
             else cp_async16(s + swz(l), src + e);
+#ifdef QZ_COUNT_FILL
+            if (counters) atomicAdd(&counters[((e & pd.fmask) != pd.fval) ? 6 : 7], 1ull);
+#endif
         }
         cp_async_wait_all();
         __syncthreads();

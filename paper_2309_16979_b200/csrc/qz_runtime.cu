@@ -518,6 +518,9 @@ int qzc_context_create(int device, uint64_t hbm_budget_bytes, qzc_context **out)
     QZ_CUDA(cudaMalloc(&ctx->status, sizeof(DevStatus)));
     QZ_CUDA(cudaMemset(ctx->status, 0, sizeof(DevStatus)));
     QZ_CUDA(cudaMallocHost(&ctx->status_host, sizeof(DevStatus)));
+    // L2 fetch granularity hint (QZ_L2_FETCH bytes, tuning): the sparse
+    // opening passes read one 16 B element per 128 B line
+    if (const char *e = getenv("QZ_L2_FETCH")) QZ_CUDA(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, size_t(atoi(e))));
     // load the stage loop's kernels now (CUDA loads a kernel's module at its
     // first launch): two tiny runs, lossy and lossless, multi-stage, so no
     // timed run pays for module loading (QZ_NO_WARMUP=1 skips)
