@@ -294,7 +294,7 @@ def family(name: str) -> str:
         return "swap_pass"
     if name in ("k_dec_lossy_seg", "k_dec_lossy_warp", "k_dec_lossy", "k_dec_lossless"):
         return "decode"
-    if name in ("k_enc_lossy", "k_enc_lossless"):
+    if name in ("k_enc_lossy", "k_enc_lossy_direct", "k_enc_lossless"):
         return "encode"
     return name
 

@@ -1243,6 +1243,205 @@ __global__ void __launch_bounds__(kEncThreads) k_enc_lossy(
     }
 }
 
+// RLE state machine writing its pairs straight to the scratch stream, four
+// pairs per aligned 8-byte store (the stream starts 8-byte aligned).  Same
+// pair stream as RleT / rle_step.
+struct RleD {
+    uint16_t *out;
+    uint32_t np;          // pairs emitted
+    uint64_t acc;         // pairs np & ~3 .. np - 1, not yet stored
+    uint32_t cur, cnt, lim;
+    uint32_t head_byte, head_len;
+};
+
+__device__ __forceinline__ void rled_start(RleD &s, uint16_t *out, uint32_t hold) {
+    s.out = out;
+    s.np = 0;
+    s.acc = 0;
+    s.cur = 0x100;
+    s.cnt = 0;
+    s.lim = hold ? ~0u : 255u;
+    s.head_byte = 0;
+    s.head_len = 0;
+}
+
+__device__ __forceinline__ void rled_emit(RleD &s, uint32_t v) {
+    s.acc |= uint64_t(v & 0xffffu) << (16 * (s.np & 3));
+    if ((s.np & 3) == 3) {
+        *reinterpret_cast<uint64_t *>(s.out + (s.np & ~3u)) = s.acc;
+        s.acc = 0;
+    }
+    ++s.np;
+}
+
+__device__ __forceinline__ void rled_step(RleD &s, uint32_t x) {
+    const bool diff = x != s.cur;
+    if (diff && s.lim == ~0u && s.cnt) {
+        s.head_byte = s.cur;
+        s.head_len = s.cnt;
+        s.lim = 255u;
+        s.cnt = 0;
+    }
+    const uint32_t c1 = s.cnt + 1;
+    const bool emit = diff ? s.cnt != 0 : c1 == s.lim;
+    const uint32_t val = s.cur | ((diff ? s.cnt : 255u) << 8);
+    if (emit) rled_emit(s, val);
+    s.cnt = diff ? 1u : (emit ? 0u : c1);
+    s.cur = x;
+}
+
+__device__ __forceinline__ void rled_step_n(RleD &s, uint32_t x, uint32_t n) {
+    if (n == 0) return;
+    if (x != s.cur) {
+        rled_step(s, x);
+        --n;
+    }
+    if (s.lim == ~0u) {
+        s.cnt += n;
+        return;
+    }
+    uint32_t tot = s.cnt + n;
+    while (tot >= 255) {
+        rled_emit(s, x | (255u << 8));
+        tot -= 255;
+    }
+    s.cnt = tot;
+}
+
+__device__ __forceinline__ void rled_close(RleD &s, uint32_t h, EncHalf &m, int k) {
+    if (h == 0) {
+        m.edge_byte[k] = uint8_t(s.cur);
+        m.edge_len[k] = s.cnt;
+    } else {
+        if (s.lim == ~0u) {
+            s.head_byte = s.cur;
+            s.head_len = s.cnt;
+        } else if (s.cnt > 0) {
+            rled_emit(s, s.cur | (s.cnt << 8));
+        }
+        m.edge_byte[k] = uint8_t(s.head_byte);
+        m.edge_len[k] = s.head_len;
+    }
+    // the stored-so-far words end at np & ~3: the rest pair by pair
+    for (uint32_t i = s.np & ~3u; i < s.np; ++i) s.out[i] = uint16_t(s.acc >> (16 * (i & 3)));
+    m.npairs[k] = s.np;
+}
+
+// Lossy encode, direct-output variant (round 2): CTA = 32
+// chunks, 64 threads = (chunk, half); tiles staged by cp.async as in
+// k_enc_lossy, but every thread writes its two RLE streams itself (RleD,
+// 8-byte stores of four pairs) — no staging of pairs, no flush warps, a
+// third of the shared memory, so more chains per SM.  Same payload bytes.
+constexpr uint32_t kEncDThreads = 2 * kSlotsPerCta;
+constexpr size_t kEncDSmem = sizeof(double2) * kEncTileDoubles2 * kEncStages;
+
+template <bool FORCED>
+__global__ void __launch_bounds__(kEncDThreads) k_enc_lossy_direct(
+    const double2 *__restrict__ win, uint64_t nslots, CodecGeom g,
+    const uint64_t *__restrict__ forced, uint32_t nforced, uint8_t *__restrict__ scratch,
+    EncHalf *__restrict__ meta) {
+    extern __shared__ __align__(16) unsigned char enc_smem[];
+    double2 *tiles = reinterpret_cast<double2 *>(enc_smem);
+    const uint32_t r = threadIdx.x >> 1, h = threadIdx.x & 1;
+    const uint64_t slot0 = uint64_t(blockIdx.x) * kSlotsPerCta, s = slot0 + r;
+    const uint32_t rows = uint32_t(umin64(kSlotsPerCta, nslots - slot0));
+    const bool active = r < rows;
+    const uint64_t N = g.N;
+    const uint32_t te = tile_width(rows, N), lte = 31 - __clz(te);
+    const uint64_t ntiles = N / te;
+    uint8_t *base = scratch_half(scratch, g, active ? s : 0, h);
+    RleD lo, hi;
+    rled_start(lo, reinterpret_cast<uint16_t *>(base), h);
+    rled_start(hi, reinterpret_cast<uint16_t *>(base + g.scap), h);
+    double *raws = reinterpret_cast<double *>(base + 2 * g.scap);
+    uint32_t nraw = 0;
+    uint32_t fc = 0;
+    uint64_t next_forced = ~uint64_t(0);
+    if (FORCED) {
+        while (active && fc < nforced && forced[fc] < h * N) ++fc;
+        next_forced = fc < nforced ? forced[fc] : ~uint64_t(0);
+    }
+    const double eb = g.eb, twoeb = g.twoeb, inv = g.inv2eb;
+    const double kRne = 6755399441055744.0;   // 1.5 * 2^52
+    const double thr = __dmul_rn(0.99, eb);
+    double pred = 0.0;
+    auto tile = [&](uint64_t i) -> double2 * { return tiles + (i % kEncStages) * kEncTileDoubles2; };
+    auto issue = [&](uint64_t i) {
+        if (i < ntiles) {
+            double2 *dst = tile(i);
+            const uint64_t e0 = i * te;
+            for (uint32_t j = threadIdx.x; j < rows * te; j += blockDim.x) {
+                const uint32_t rr = j >> lte, e = j & (te - 1);
+                cp_async16(dst + rr * (te + 1) + e, win + (slot0 + rr) * N + e0 + e);
+            }
+        }
+        cp_async_commit();
+    };
+    issue(0);
+    for (uint64_t ti = 0; ti < ntiles; ++ti) {
+        issue(ti + 1);
+        cp_async_wait<1>();
+        __syncthreads();
+        if (active) {
+            const double *rowc = reinterpret_cast<const double *>(tile(ti) + r * (te + 1)) + h;
+            const uint64_t tile0 = h * N + ti * te;
+            bool ff = (!FORCED || next_forced >= tile0 + te) && fabs(__dsub_rn(rowc[0], pred)) < thr;
+            if (ff) {
+                bool all = true;
+#pragma unroll 8
+                for (uint32_t e = 1; e < te; ++e) all &= fabs(__dsub_rn(rowc[2 * e], pred)) < thr;
+                ff = all;
+                if (ff) {
+                    rled_step_n(lo, 0, te);
+                    rled_step_n(hi, 0, te);
+                    pred = __dadd_rn(pred, 0.0);
+                }
+            }
+            if (!ff) {
+                uint32_t fr = ~0u;
+                if (FORCED) fr = next_forced - tile0 < te ? uint32_t(next_forced - tile0) : ~0u;
+#pragma unroll 4
+                for (uint32_t e = 0; e < te; ++e) {
+                    const double v = rowc[2 * e];
+                    const double d = __dsub_rn(v, pred);
+                    const double t = __dmul_rn(d, inv);
+                    double q = __dsub_rn(__dadd_rn(t, kRne), kRne);
+                    const double f = __dsub_rn(t, q);
+                    bool raw = false;
+                    if (!(fabs(f) < 0.4999999 && fabs(t) < 32767.0) || (FORCED && e == fr)) {
+                        if (FORCED && e == fr) {
+                            raw = true;
+                            const uint64_t flat = tile0 + e;
+                            do { ++fc; } while (fc < nforced && forced[fc] == flat);
+                            next_forced = fc < nforced ? forced[fc] : ~uint64_t(0);
+                            fr = next_forced - tile0 < te ? uint32_t(next_forced - tile0) : ~0u;
+                        } else {
+                            q = round(__ddiv_rn(d, twoeb));
+                            if (!(fabs(q) < 32768.0)) raw = true;
+                            else q = __dadd_rn(q, 0.0);   // code 0 from -0
+                        }
+                    }
+                    const double rec = __dadd_rn(pred, __dmul_rn(q, twoeb));
+                    raw = raw || !(fabs(__dsub_rn(rec, v)) <= eb);
+                    pred = raw ? v : rec;
+                    const uint32_t z = raw ? 0xFFFFu : zigzag16(int32_t(q));
+                    if (raw) raws[nraw++] = v;
+                    rled_step(lo, z & 0xffu);
+                    rled_step(hi, z >> 8);
+                }
+            }
+        }
+        __syncthreads();   // the tile buffer is refilled next round
+    }
+    cp_async_wait<0>();
+    if (active) {
+        EncHalf &m = meta[2 * s + h];
+        rled_close(lo, h, m, 0);
+        rled_close(hi, h, m, 1);
+        m.nraw = nraw;
+    }
+}
+
 // Lossless encode (codec.cpp:169-181): thread = (slot, half, byte plane).
 constexpr int kLLSlots = 16;
 __global__ void __launch_bounds__(16 * kLLSlots) k_enc_lossless(
@@ -1633,16 +1832,36 @@ void launch_decode(const uint8_t *arena, const DecIdx *idx, const uint64_t *slot
 void launch_encode(const double2 *win, uint64_t nslots, const CodecGeom &g,
                    const uint64_t *forced, uint32_t nforced, uint8_t *scratch, EncHalf *meta,
                    cudaStream_t s) {
-    KProfScope prof(s, g.lossy ? "k_enc_lossy" : "k_enc_lossless", 0, 16.0 * double(g.N) * double(nslots));
+    static const int force_k = getenv("QZ_ENC_KERNEL") ? (std::string(getenv("QZ_ENC_KERNEL")) == "direct" ? 1 : 0) : -1;
+    const bool direct_k = g.lossy && (force_k >= 0 ? force_k == 1 : g.dense_hint == 0);
+    KProfScope prof(s, direct_k ? "k_enc_lossy_direct" : g.lossy ? "k_enc_lossy" : "k_enc_lossless", 0,
+                    16.0 * double(g.N) * double(nslots));
     static bool attr = false;
     if (!attr) {
         QZ_CUDA(cudaFuncSetAttribute(k_enc_lossy<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      int(kEncSmem)));
         QZ_CUDA(cudaFuncSetAttribute(k_enc_lossy<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      int(kEncSmem)));
+        QZ_CUDA(cudaFuncSetAttribute(k_enc_lossy_direct<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(kEncDSmem)));
+        QZ_CUDA(cudaFuncSetAttribute(k_enc_lossy_direct<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(kEncDSmem)));
         attr = true;
     }
-    if (g.lossy && nforced)
+    // QZ_ENC_KERNEL=staged|direct forces the choice (tests); default: the
+    // staged kernel after a dense stage (its coalesced pair flushes win when
+    // most elements emit pairs: supremacy-30 15.7 vs 23.6 ms), the direct one
+    // otherwise (less per-tile overhead on fast-forwarded tiles: QFT-30 3.7
+    // vs 4.3 ms)
+    static const int force = getenv("QZ_ENC_KERNEL") ? (std::string(getenv("QZ_ENC_KERNEL")) == "direct" ? 1 : 0) : -1;
+    const bool direct = g.lossy && (force >= 0 ? force == 1 : g.dense_hint == 0);
+    if (direct && nforced)
+        k_enc_lossy_direct<true><<<grid_for(nslots, kSlotsPerCta), kEncDThreads, kEncDSmem, s>>>(
+            win, nslots, g, forced, nforced, scratch, meta);
+    else if (direct)
+        k_enc_lossy_direct<false><<<grid_for(nslots, kSlotsPerCta), kEncDThreads, kEncDSmem, s>>>(
+            win, nslots, g, forced, nforced, scratch, meta);
+    else if (g.lossy && nforced)
         k_enc_lossy<true><<<grid_for(nslots, kSlotsPerCta), kEncThreads, kEncSmem, s>>>(
             win, nslots, g, forced, nforced, scratch, meta);
     else if (g.lossy)

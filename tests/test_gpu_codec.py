@@ -234,3 +234,48 @@ def test_dense_decoders_both_match_golden(golden, tmp_path, kernel):
     assert res.returncode == 0, res.stderr[-2000:]
     out = json.loads(res.stdout.strip().splitlines()[-1])
     assert out["bad"] == 0 and out["runs"] and all(out["runs"]), out
+
+
+@pytest.mark.parametrize("kernel", ["staged", "direct"])
+def test_encoders_both_match_golden(golden, kernel):
+    """Both lossy encoders (pairs staged in shared memory and flushed by
+    dedicated warps; each thread writing its own streams) reproduce the
+    reference's payload bytes on the golden codec corpus (forced raws
+    included) and the reference digests of lossy runs, single- and
+    multi-stage.  QZ_ENC_KERNEL is read once per process: fresh subprocess."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    script = (
+        "import hashlib, json, sys\n"
+        "sys.path.insert(0, 'tests')\n"
+        "from golden.inputs import CODEC_CASES, codec_input\n"
+        "from paper_2309_16979_b200 import engine as E, circuits as CI\n"
+        "from paper_2309_16979_b200.abi import to_array\n"
+        "golden = json.load(open('tests/golden/golden.json'))\n"
+        "eng = E.Engine()\n"
+        "bad = []\n"
+        "for case, rec in zip(CODEC_CASES, golden['codec']):\n"
+        "    amps, forced = codec_input(case)\n"
+        "    if case['eb'] <= 0: continue\n"
+        "    p, crc = eng.compress(amps, case['eb'], forced)\n"
+        "    if hashlib.sha256(bytes(p)).hexdigest() != rec['sha256'] or crc != rec['crc']: bad.append(case)\n"
+        "runs = [r for r in golden['runs'] if r['eb'] > 0][:6]\n"
+        "dig = []\n"
+        "for r in runs:\n"
+        "    k = r['circuit']\n"
+        "    g = CI.qft(int(k.split(':')[1])) if k.startswith('qft:') else CI.ghz(int(k.split(':')[1])) if k.startswith('ghz:') else to_array([(x[0], tuple(x[1]), tuple(x[2])) for x in golden['circuits'][k]])\n"
+        "    sim = eng.simulator(r['n'], r['c'], r['m'], r['eb'])\n"
+        "    sim.run(g)\n"
+        "    dig.append(f'{sim.digest():016x}' == r['digest'])\n"
+        "    sim.close()\n"
+        "print(json.dumps({'bad': len(bad), 'runs': dig}))\n")
+    env = dict(os.environ, QZ_ENC_KERNEL=kernel, PYTHONPATH=str(root))
+    res = subprocess.run([sys.executable, "-c", script], cwd=root, env=env, capture_output=True,
+                         text=True, timeout=900)
+    assert res.returncode == 0, res.stderr[-2000:]
+    out = json.loads(res.stdout.strip().splitlines()[-1])
+    assert out["bad"] == 0 and out["runs"] and all(out["runs"]), out
