@@ -256,7 +256,8 @@ void decode_into(qzc_context *ctx, DecIdx *idx, double2 *amps, const CodecGeom &
 // left in W.amps (the two buffers swap roles when needed).
 void run_window_passes(qzc_sim *sim, Window &W, const DevPlan &dp, const DevPlan &dsub, const DevPlan &dfull,
                        uint32_t wbits, cudaStream_t S,
-                       const std::function<void(double2 *, const uint32_t *)> &redecode);
+                       const std::function<void(double2 *, const uint32_t *)> &redecode,
+                       const std::function<bool(cudaStream_t)> &ensure_dfull);
 
 uint32_t log2u(uint64_t x) {
     uint32_t r = 0;
@@ -402,7 +403,8 @@ __global__ void k_fill_dead(double2 *win, uint64_t n, uint64_t mask, uint64_t va
 
 void run_window_passes(qzc_sim *sim, Window &W, const DevPlan &dp, const DevPlan &dsub, const DevPlan &dfull,
                        uint32_t wbits, cudaStream_t S,
-                       const std::function<void(double2 *, const uint32_t *)> &redecode) {
+                       const std::function<void(double2 *, const uint32_t *)> &redecode,
+                       const std::function<bool(cudaStream_t)> &ensure_dfull) {
     qzc_context *ctx = sim->ctx;
     const NzMap nz{W.nzslot.as<uint32_t>(), sim->c};
     if (!dp.relaxed) {
@@ -412,7 +414,8 @@ void run_window_passes(qzc_sim *sim, Window &W, const DevPlan &dp, const DevPlan
     uint32_t *pflag = W.replay.as<uint32_t>(), *wflag = pflag + 1;
     double2 *res = run_relaxed(dp, dsub, W.amps.as<double2>(), W.alt.p ? W.alt.as<double2>() : nullptr, wbits, S,
                                pflag, wflag, sim->replays.as<uint64_t>(), sim->force_replay, ctx->launches, nz);
-    if (!dfull.host_passes.empty()) {
+    // (the strict plan is built while the relaxed passes run on the device)
+    if (ensure_dfull(S)) {
         // a +0-safe relaxed pass flagged: decode the window again from its
         // untouched payloads and run the strict plan (no-ops unless flagged)
         redecode(res, wflag);
@@ -1314,12 +1317,26 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
         upload_plan(gp, dp, s, wbits, pass_fresh);
         dsub.host_passes.clear();
         dfull.host_passes.clear();
+        bool need_dfull = false;
         if (dp.relaxed) {
             upload_replay(dg, wbits, kTileBits, dp, dsub, s);
-            bool any_inplace = false;
-            for (const PassDesc &pd : dp.host_passes) any_inplace |= pd.relaxed == 1;
-            if (any_inplace) upload_plan(build_passes(dg, wbits, kTileBits, true, false), dfull, s);
+            for (const PassDesc &pd : dp.host_passes) need_dfull |= pd.relaxed == 1;
         }
+        // the whole-window strict plan (replayed device-side only when a +0-safe
+        // relaxed pass flags): built lazily, once the first window's relaxed
+        // passes are queued, so the host builds it while they run
+        bool dfull_built = false;
+        cudaEvent_t dfull_ready = ev(4 * nwin + 1);
+        auto ensure_dfull = [&](cudaStream_t S) -> bool {
+            if (!need_dfull) return false;
+            if (!dfull_built) {
+                upload_plan(build_passes(dg, wbits, kTileBits, true, false), dfull, S);
+                QZ_CUDA(cudaEventRecord(dfull_ready, S));
+                dfull_built = true;
+            }
+            QZ_CUDA(cudaStreamWaitEvent(S, dfull_ready, 0));
+            return true;
+        };
         const int a = sim->cur, b = 1 - sim->cur;
         // host-staged stores start with arenas sized for a typical ratio and
         // grow on demand: a stage whose output overflows its arena is re-run
@@ -1381,7 +1398,7 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
             run_window_passes(sim, W, dp, dsub, dfull, wbits, S, [&](double2 *dst, const uint32_t *cond) {
                 launch_decode(In.stage_in.as<uint8_t>(), In.idx.as<DecIdx>(), nullptr, nslots, sim->geom, dst,
                               ctx->status, S, cond, sim->sparse_store);
-            });
+            }, ensure_dfull);
             QZ_CUDA(cudaEventRecord(ev(4 * w + 2), S));
             // the output staging / table of window w-1 must be written back
             if (w) QZ_CUDA(cudaStreamWaitEvent(S, pev(3 * (w - 1) + 2), 0));
@@ -1439,7 +1456,7 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
                 else
                     launch_decode(sim->arena_ptr(a), W.idx.as<DecIdx>(), W.slot_chunk.as<uint64_t>(), nslots,
                                   sim->geom, dst, ctx->status, S, cond, sim->sparse_store);
-            });
+            }, ensure_dfull);
             QZ_CUDA(cudaEventRecord(ev(4 * w + 2), S));
             if (sim->host_res) {
                 QZ_CUDA(cudaMemsetAsync(W.lused.p, 0, 8, S));
