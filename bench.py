@@ -238,8 +238,15 @@ def run_reference_arm(args) -> int:
     ws = ReferenceSampler(warm)
     for i in range(args.warmup):
         ws.sample(ks[i % 2])
+    # each step is one full-size sample (~1 min at n=30 on 16 cores): the two
+    # the estimate needs, then more only while the run stays within a few
+    # minutes (QZ_REF_BUDGET_S, default 240 s); "steps" reports those done
+    budget = float(os.environ.get("QZ_REF_BUDGET_S", "240"))
     walls = []
+    t_start = time.perf_counter()
     for i in range(max(args.steps, 2)):
+        if i >= 2 and time.perf_counter() - t_start > budget:
+            break
         t0 = time.perf_counter()
         s.sample(ks[i % 2])
         walls.append(time.perf_counter() - t0)
@@ -247,7 +254,7 @@ def run_reference_arm(args) -> int:
     v = est["gates_per_s"]
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "gates/s",
-        "n_gpus": args.gpus, "steps": max(args.steps, 2), "warmup": args.warmup,
+        "n_gpus": args.gpus, "steps": len(walls), "warmup": args.warmup,
         "ms_per_step": 1e3 * statistics.mean(walls), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(args),
