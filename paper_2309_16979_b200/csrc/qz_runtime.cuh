@@ -218,6 +218,14 @@ struct qzc_sim {
     cudaEvent_t acct_ev[2] = {nullptr, nullptr};
     qzc_sim_stats stats{};
     bool initialized = false;
+    // the |0...0> store's two payloads (zero chunk, basis chunk) as the first
+    // init_basis produced them: later inits copy them back (no codec round trip)
+    struct InitCache {
+        bool valid = false;
+        std::vector<uint8_t> bytes;   // the arena's first `used` bytes
+        uint64_t used = 0, off[2] = {0, 0};
+        uint32_t len[2] = {0, 0}, crc[2] = {0, 0};
+    } init_cache;
     // qubits statically |0> (untouched by any non-diagonal gate since
     // init_basis, every gate keeping +0 zeros +0): Fresh for the stage plans
     uint64_t fresh_q = 0, fresh_v = 0;   // ... and their basis values
