@@ -383,7 +383,10 @@ class Simulator:
 
     def close(self) -> None:
         if getattr(self, "h", None):
-            self.lib.qzc_sim_destroy(self.h)
+            # (a simulator outliving its engine — interpreter teardown order —
+            # is leaked rather than destroyed against a freed context)
+            if getattr(self.eng, "h", None):
+                self.lib.qzc_sim_destroy(self.h)
             self.h = None
 
     def __del__(self):

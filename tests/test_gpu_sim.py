@@ -502,3 +502,22 @@ def test_skip_switches_off_same_digest(engine, golden, oracle, tmp_path, switch,
                          timeout=600)
     assert res.returncode == 0, res.stderr[-2000:]
     assert json.loads(res.stdout.strip().splitlines()[-1]) == [r["digest"] for r in recs]
+
+
+@pytest.mark.parametrize("eb", [1e-5, 0.0])
+def test_repeated_init_same_bytes(engine, oracle, eb):
+    """init_basis on a simulator that was already initialised copies the
+    first init's payloads back (no codec round trip): every later run from
+    it reproduces the oracle's store bytes, single- and multi-stage."""
+    from paper_2309_16979_b200 import circuits as CI
+    for n, c, m in ((14, 8, 14), (14, 8, 11)):
+        g = CI.qft(n)
+        want = oracle.run(n, g, c, m, eb)["digest"]
+        sim = engine.simulator(n, c, m, eb, init=False)
+        try:
+            for _ in range(3):
+                sim.init_basis()
+                sim.run(g)
+                assert sim.digest() == want, (n, c, m, eb)
+        finally:
+            sim.close()
