@@ -1257,13 +1257,52 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
         uint64_t bpw = std::max<uint64_t>(1, sim->win_amps >> mb);
         bpw = std::min(bpw, nbatches);
         const uint32_t wbits = mb + log2u(bpw);
+        // A stage that ends in a network of disjoint SWAPs (permutation pi of
+        // qubits) whose moved qubits are all fresh with pi-symmetric values:
+        // the live amplitudes are fixed by pi, so the decoded window is also
+        // the window laid out with qubit q on buffer bit pi(q).  Run the stage
+        // in that layout and the network is only a relabelling: at the stage's
+        // end the window holds the state in the natural layout (no permutation
+        // pass).  QFT from |0...0>: the bit reversal, and the qubits it opens
+        // last sit on the high buffer bits (contiguous live data throughout).
+        std::vector<uint32_t> relabel(n);
+        for (uint32_t q = 0; q < n; ++q) relabel[q] = q;
+        size_t ngates_run = st.ngates;
+        {
+            static const bool no_absorb = getenv("QZ_NO_ABSORB") != nullptr || getenv("QZ_NO_FRESH") != nullptr;
+            uint64_t used_q = 0;
+            size_t first = st.ngates;
+            while (first > 0) {
+                const qzc_gate &g = gates[st.first_gate + first - 1];
+                if (g.kind != QZC_SWAP || g.nqubits != 2) break;
+                const uint64_t m2 = (uint64_t(1) << g.qubits[0]) | (uint64_t(1) << g.qubits[1]);
+                if ((used_q & m2) || g.qubits[0] == g.qubits[1]) break;
+                used_q |= m2;
+                --first;
+            }
+            bool ok = !no_absorb && first < st.ngates;
+            for (size_t i = first; ok && i < st.ngates; ++i) {
+                const qzc_gate &g = gates[st.first_gate + i];
+                const uint32_t a = g.qubits[0], b = g.qubits[1];
+                ok = buffer_bit(st, a, c) >= 0 && buffer_bit(st, b, c) >= 0 && ((sim->fresh_q >> a) & 1) &&
+                     ((sim->fresh_q >> b) & 1) && (((sim->fresh_v >> a) ^ (sim->fresh_v >> b)) & 1) == 0;
+            }
+            if (ok) {
+                for (size_t i = first; i < st.ngates; ++i) {
+                    const qzc_gate &g = gates[st.first_gate + i];
+                    relabel[g.qubits[0]] = g.qubits[1];
+                    relabel[g.qubits[1]] = g.qubits[0];
+                }
+                ngates_run = first;
+            }
+        }
         // remap the stage's gates to buffer bits (remap_gate, planner.cpp:131-141)
         std::vector<DevGate> dg;
-        dg.reserve(st.ngates);
-        for (size_t i = 0; i < st.ngates; ++i) {
+        dg.reserve(ngates_run);
+        for (size_t i = 0; i < ngates_run; ++i) {
             qzc_gate g = gates[st.first_gate + i];
             for (uint32_t k = 0; k < g.nqubits; ++k) {
-                const int b = buffer_bit(st, g.qubits[k], c);
+                const int b = buffer_bit(st, relabel[g.qubits[k]], c);
                 if (b < 0) throw Failure(QZC_EPLAN, "qubit not mapped by the stage layout");
                 g.qubits[k] = uint32_t(b);
             }
@@ -1277,7 +1316,7 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
         static const bool no_fresh = getenv("QZ_NO_FRESH") != nullptr;   // control
         for (uint32_t q = 0; q < n && !no_fresh; ++q)
             if ((sim->fresh_q >> q) & 1) {
-                const int bq = buffer_bit(st, q, c);
+                const int bq = buffer_bit(st, relabel[q], c);
                 if (bq >= 0) {
                     stage_fresh.mask |= uint64_t(1) << bq;
                     stage_fresh.val |= ((sim->fresh_v >> q) & 1) << bq;
