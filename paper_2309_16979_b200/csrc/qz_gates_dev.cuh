@@ -1207,12 +1207,17 @@ __device__ __forceinline__ void tile_pass_body(const double2 *__restrict__ src, 
 #ifdef QZ_GROUP_CLOCKS
         const long long ck_t0 = clock64();
 #endif
+        uint32_t loaded = 0;   // elements this thread loads (the others are statically +0)
 #pragma unroll
         for (int i = 0; i < NB; ++i) {
             const uint32_t l = tid + i * nth;
             const uint64_t e = base + offhi[l >> L] + (l & lowmask);
-            if ((e & pd.fmask) != pd.fval) s[swz(l)] = make_double2(0.0, 0.0);   // statically +0
-            else cp_async16(s + swz(l), src + e);
+            if ((e & pd.fmask) != pd.fval) {
+                s[swz(l)] = make_double2(0.0, 0.0);
+            } else {
+                cp_async16(s + swz(l), src + e);
+                loaded |= 1u << i;
+            }
 #ifdef QZ_COUNT_FILL
             if (counters) atomicAdd(&counters[((e & pd.fmask) != pd.fval) ? 6 : 7], 1ull);
 #endif
@@ -1226,6 +1231,7 @@ __device__ __forceinline__ void tile_pass_body(const double2 *__restrict__ src, 
         uint32_t okv = 1;
 #pragma unroll
         for (int i = 0; i < NB; ++i) {
+            if (!((loaded >> i) & 1)) continue;   // a zero-filled +0: clean, zero
             const double2 x = s[swz(tid + i * nth)];
             any |= (unsigned long long)__double_as_longlong(x.x) |
                    (unsigned long long)__double_as_longlong(x.y);
