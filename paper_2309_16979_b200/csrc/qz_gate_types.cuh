@@ -135,6 +135,10 @@ struct PassDesc {
     // PASS_TILE: the swap network that followed is fused into the store —
     // out of place, element e written to perm(e) (perm[] as for PASS_SWAPS)
     uint32_t permute;
+    // one non-generic register group, no permuted store, >= 32 contiguous low
+    // tile bits: registers load / store global memory directly (lanes on the
+    // lowest bits: coalesced), no shared-memory tile, no barriers
+    uint32_t direct;
 };
 
 enum PassKind : uint32_t { PASS_TILE = 0, PASS_SWAPS = 1 };

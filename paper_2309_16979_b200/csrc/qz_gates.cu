@@ -862,8 +862,11 @@ std::vector<PassDesc> launch_passes(const GatePlan &plan) {
     // every group is in it (and no group needs the shared-memory generic path)
     static const bool narrow_off = getenv("QZ_NO_NARROW") != nullptr;
     static const bool wmap_off = getenv("QZ_NO_WMAP") != nullptr;
+    static const bool direct_off = getenv("QZ_NO_DIRECT") != nullptr;
     for (PassDesc &pd : out) {
         pd.wmap = wmap_off ? 0u : 1u;
+        pd.direct = !direct_off && pd.kind == PASS_TILE && pd.ngroups == 1 && !plan.groups[pd.first_group].generic &&
+                    !pd.permute && pd.lowbits >= 5 && pd.k >= (uint32_t)kRegBits + 1 ? 1u : 0u;
         pd.variant = kPassAll;
         for (int S : {kPassDiagH, kPassGen}) {
             bool narrow = !narrow_off && pd.kind != PASS_SWAPS;

@@ -1194,6 +1194,96 @@ __device__ __forceinline__ void tile_pass_body(const double2 *__restrict__ src, 
     // the window, so every visited tile is stored (no skip without a store)
     const bool opens = (pd.fmask & pd.tmask) != 0;
     const bool use_nz = nzslot && pd.pz_stable && src == dst && L <= cbits && !opens;
+    if (pd.direct) {
+        // register-direct pass (PassDesc::direct): the single group's block
+        // of 8 amplitudes per thread comes straight from global memory
+        const GroupDesc &G = groups[pd.first_group];
+        const TileGate *gp = gates + G.first_gate;
+        uint32_t mybase = tid;   // plain map: lanes on the lowest non-register tile bits
+#pragma unroll
+        for (int i = 0; i < kRegBits; ++i) {
+            const uint32_t b = G.gbits[i];
+            mybase = ((mybase >> b) << (b + 1)) | (mybase & ((1u << b) - 1));
+        }
+        uint32_t lidx[NB];
+#pragma unroll
+        for (int r = 0; r < NB; ++r) {
+            uint32_t a = mybase;
+#pragma unroll
+            for (int i = 0; i < kRegBits; ++i)
+                if ((r >> i) & 1) a |= 1u << G.gbits[i];
+            lidx[r] = a;
+        }
+        const uint32_t span = L > cbits ? 1u << (L - cbits) : 1u;
+        for (uint64_t t = blockIdx.x; t < ntiles;
+             t += gridDim.x, base = ((((base & ~zv) | ~ltmask) + dstep) & ltmask) | zv) {
+            uint64_t ea[NB];
+            double2 v[NB];
+#pragma unroll
+            for (int r = 0; r < NB; ++r) {
+                ea[r] = base + offhi[lidx[r] >> L] + (lidx[r] & lowmask);
+                v[r] = (ea[r] & pd.fmask) != pd.fval ? make_double2(0.0, 0.0) : src[ea[r]];
+            }
+            const uint64_t gidx = G.relaxed ? base + offhi[mybase >> L] + (mybase & lowmask) : 0;
+            unsigned long long nz = 0, raw = 0;
+#pragma unroll
+            for (int r = 0; r < NB; ++r) {
+                raw |= (unsigned long long)__double_as_longlong(v[r].x) |
+                       (unsigned long long)__double_as_longlong(v[r].y);
+                nz |= ((unsigned long long)__double_as_longlong(v[r].x) << 1) |
+                      ((unsigned long long)__double_as_longlong(v[r].y) << 1);
+            }
+            int path = 1;
+            if (raw == 0 && G.pz_stable) {
+            } else if (G.relaxed && nz == 0) {
+                *flag = 1u;
+            } else if (nz == 0) {
+                path = 2;
+                uint32_t SR = 0, SI = 0;
+#pragma unroll
+                for (int r = 0; r < NB; ++r) {
+                    SR |= sbit(v[r].x) << r;
+                    SI |= sbit(v[r].y) << r;
+                }
+                for (uint32_t q = 0; q < G.ngates; ++q) mask_apply(SR, SI, gp[q]);
+#pragma unroll
+                for (int r = 0; r < NB; ++r)
+                    v[r] = make_double2(signed_zero((SR >> r) & 1), signed_zero((SI >> r) & 1));
+            } else {
+                uint32_t okg = 1;
+#pragma unroll
+                for (int r = 0; r < NB; ++r) okg &= comp_ok(v[r].x) & comp_ok(v[r].y);
+                const bool okblk = okg != 0;
+                bool bad = !okblk;
+                path = okblk ? 3 : 4;
+                FP::run(0, gates + G.first_fast, G.nfast, v, gidx, bad);
+                if (bad && okblk) path = 5;
+                if (bad && G.relaxed) {
+                    *flag = 1u;
+                } else if (bad) {
+#pragma unroll
+                    for (int r = 0; r < NB; ++r)
+                        v[r] = (ea[r] & pd.fmask) != pd.fval ? make_double2(0.0, 0.0) : src[ea[r]];
+                    for (uint32_t q = 0; q < G.ngates; ++q) reg_apply(v, gp[q]);
+                }
+            }
+            if (!(raw == 0 && G.pz_stable) || opens || src != dst) {
+#pragma unroll
+                for (int r = 0; r < NB; ++r) __stcs(dst + ea[r], v[r]);
+            }
+#ifndef QZ_GROUP_CLOCKS
+            if (counters) atomicAdd(&counters[path], 1ull);
+#endif
+            if (nzslot) {
+                uint32_t *zcount = nzslot + (uint64_t(1) << (nbits - cbits));
+                for (uint32_t i = tid; i < nhi * span; i += nth) {
+                    uint32_t *w = nzslot + ((base + offhi[i / span]) >> cbits) + (i % span);
+                    if (*w == 0 && atomicExch(w, 1u) == 0) atomicSub(zcount, 1u);
+                }
+            }
+        }
+        return;
+    }
     for (uint64_t t = blockIdx.x; t < ntiles;
          t += gridDim.x, base = ((((base & ~zv) | ~ltmask) + dstep) & ltmask) | zv) {
         if (use_nz) {

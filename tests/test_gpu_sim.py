@@ -463,14 +463,16 @@ def test_full_case_set_same_digest(engine, golden, oracle, tmp_path):
                                     ("QZ_NO_FRESH", {}), ("QZ_NO_FRESH", {"fuse": "checked"}),
                                     ("QZ_NO_FRESH", {"residency": "host"}),
                                     ("QZ_NO_PERM_FUSE", {}), ("QZ_NO_PERM_FUSE", {"force_replay": True}),
-                                    ("QZ_NO_ABSORB", {}), ("QZ_NO_ABSORB", {"force_replay": True})])
+                                    ("QZ_NO_ABSORB", {}), ("QZ_NO_ABSORB", {"force_replay": True}),
+                                    ("QZ_NO_DIRECT", {}), ("QZ_NO_DIRECT", {"fuse": "checked"})])
 def test_skip_switches_off_same_digest(engine, golden, oracle, tmp_path, switch, kw):
     """Work-skipping devices only skip work: with QZ_NO_NZMAP=1 (no tile
     skipped on the zero-slot map's say-so), QZ_NO_WMAP=1 (register groups
     on the plain thread map, no warp-uniform block skips), QZ_NO_FRESH=1 (no
     fresh-qubit planning, dead-chunk skipping or static +0 registers),
     QZ_NO_PERM_FUSE=1 (swap networks as their own pass) or QZ_NO_ABSORB=1
-    (no trailing swap network absorbed into the stage layout) the reference
+    (no trailing swap network absorbed into the stage layout) or QZ_NO_DIRECT=1
+    (single-group passes through the shared-memory tile) the reference
     digests hold for the relaxed, checked, forced-replay and host-staged
     variants.  Fresh process: the switches are read once per process."""
     import json
