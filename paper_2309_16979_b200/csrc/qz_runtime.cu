@@ -257,7 +257,7 @@ void decode_into(qzc_context *ctx, DecIdx *idx, double2 *amps, const CodecGeom &
 void run_window_passes(qzc_sim *sim, Window &W, const DevPlan &dp, const DevPlan &dsub, const DevPlan &dfull,
                        uint32_t wbits, cudaStream_t S,
                        const std::function<void(double2 *, const uint32_t *)> &redecode,
-                       const std::function<bool(cudaStream_t)> &ensure_dfull);
+                       const std::function<bool(cudaStream_t)> &ensure_dfull, bool host_decides = false);
 
 uint32_t log2u(uint64_t x) {
     uint32_t r = 0;
@@ -404,7 +404,7 @@ __global__ void k_fill_dead(double2 *win, uint64_t n, uint64_t mask, uint64_t va
 void run_window_passes(qzc_sim *sim, Window &W, const DevPlan &dp, const DevPlan &dsub, const DevPlan &dfull,
                        uint32_t wbits, cudaStream_t S,
                        const std::function<void(double2 *, const uint32_t *)> &redecode,
-                       const std::function<bool(cudaStream_t)> &ensure_dfull) {
+                       const std::function<bool(cudaStream_t)> &ensure_dfull, bool host_decides) {
     qzc_context *ctx = sim->ctx;
     const NzMap nz{W.nzslot.as<uint32_t>(), sim->c};
     if (!dp.relaxed) {
@@ -414,8 +414,21 @@ void run_window_passes(qzc_sim *sim, Window &W, const DevPlan &dp, const DevPlan
     uint32_t *pflag = W.replay.as<uint32_t>(), *wflag = pflag + 1;
     double2 *res = run_relaxed(dp, dsub, W.amps.as<double2>(), W.alt.p ? W.alt.as<double2>() : nullptr, wbits, S,
                                pflag, wflag, sim->replays.as<uint64_t>(), sim->force_replay, ctx->launches, nz);
+    // host_decides (a stage's only window): wait for the relaxed passes and
+    // read the flag, so the strict replay is queued only when it is needed
+    // (instead of ~55 device-side no-op launches per stage)
+    if (host_decides) {
+        uint32_t raised = 0;
+        QZ_CUDA(cudaStreamSynchronize(S));
+        QZ_CUDA(cudaMemcpy(&raised, wflag, 4, cudaMemcpyDeviceToHost));
+        if (raised && ensure_dfull(S)) {
+            redecode(res, wflag);
+            ctx->launches += 1 + run_passes(dfull, res, wbits, S, wflag);
+            flag_done(wflag, sim->replays.as<uint64_t>(), S);
+            ++ctx->launches;
+        }
+    } else if (ensure_dfull(S)) {
     // (the strict plan is built while the relaxed passes run on the device)
-    if (ensure_dfull(S)) {
         // a +0-safe relaxed pass flagged: decode the window again from its
         // untouched payloads and run the strict plan (no-ops unless flagged)
         redecode(res, wflag);
@@ -1532,7 +1545,7 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
                 else
                     launch_decode(sim->arena_ptr(a), W.idx.as<DecIdx>(), W.slot_chunk.as<uint64_t>(), nslots,
                                   sim->geom, dst, ctx->status, S, cond, sim->sparse_store);
-            }, ensure_dfull);
+            }, ensure_dfull, nwin == 1 && !sim->two_windows);
             QZ_CUDA(cudaEventRecord(ev(4 * w + 2), S));
             if (sim->host_res) {
                 QZ_CUDA(cudaMemsetAsync(W.lused.p, 0, 8, S));
