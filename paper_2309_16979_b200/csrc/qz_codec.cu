@@ -1732,6 +1732,7 @@ CodecGeom make_geom(uint64_t N, double eb) {
         g.exact_inv = eb > 0.0 && mant == 0.5 && ex > -1020 && ex < 1020 ? 1u : 0u;
     }
     g.dense_hint = 0;
+    g.enc_dense = 0;
     g.scap = round_up(2 * N, 8);
     g.half_stride = round_up(g.lossy ? 2 * g.scap + 8 * N : 8 * g.scap, 16);
     g.dead_mask = g.dead_val = 0;
@@ -1833,7 +1834,7 @@ void launch_encode(const double2 *win, uint64_t nslots, const CodecGeom &g,
                    const uint64_t *forced, uint32_t nforced, uint8_t *scratch, EncHalf *meta,
                    cudaStream_t s) {
     static const int force_k = getenv("QZ_ENC_KERNEL") ? (std::string(getenv("QZ_ENC_KERNEL")) == "direct" ? 1 : 0) : -1;
-    const bool direct_k = g.lossy && (force_k >= 0 ? force_k == 1 : g.dense_hint == 0);
+    const bool direct_k = g.lossy && (force_k >= 0 ? force_k == 1 : g.enc_dense == 0);
     KProfScope prof(s, direct_k ? "k_enc_lossy_direct" : g.lossy ? "k_enc_lossy" : "k_enc_lossless", 0,
                     16.0 * double(g.N) * double(nslots));
     static bool attr = false;
@@ -1849,12 +1850,11 @@ void launch_encode(const double2 *win, uint64_t nslots, const CodecGeom &g,
         attr = true;
     }
     // QZ_ENC_KERNEL=staged|direct forces the choice (tests); default: the
-    // staged kernel after a dense stage (its coalesced pair flushes win when
-    // most elements emit pairs: supremacy-30 15.7 vs 23.6 ms), the direct one
-    // otherwise (less per-tile overhead on fast-forwarded tiles: QFT-30 3.7
-    // vs 4.3 ms)
-    static const int force = getenv("QZ_ENC_KERNEL") ? (std::string(getenv("QZ_ENC_KERNEL")) == "direct" ? 1 : 0) : -1;
-    const bool direct = g.lossy && (force >= 0 ? force == 1 : g.dense_hint == 0);
+    // staged kernel when the stage's output is expected dense (its coalesced
+    // pair flushes win when most elements emit pairs: supremacy-30 15.7 vs
+    // 23.6 ms), the direct one otherwise (less per-tile overhead on
+    // fast-forwarded tiles: QFT-30 3.7 vs 4.3 ms)
+    const bool direct = direct_k;
     if (direct && nforced)
         k_enc_lossy_direct<true><<<grid_for(nslots, kSlotsPerCta), kEncDThreads, kEncDSmem, s>>>(
             win, nslots, g, forced, nforced, scratch, meta);

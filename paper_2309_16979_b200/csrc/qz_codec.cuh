@@ -51,6 +51,8 @@ struct CodecGeom {
     uint32_t exact_inv;     // 2 eb is a power of two: the reciprocal is exact
     uint32_t dense_hint;    // the store compresses less than 16x: decode with the
                             // segmented kernel (set per stage by the runtime)
+    uint32_t enc_dense;     // the stage's output is expected dense (dense input or a
+                            // qubit mixed >= 4 times): staged encoder, else direct
     uint64_t scap;          // bytes per scratch stream (>= 2N, multiple of 8)
     uint64_t half_stride;   // scratch bytes per (slot, half)
     // decode only: chunks whose index differs from dead_val on dead_mask are

@@ -708,6 +708,7 @@ int qzc_decompress_host(qzc_context *ctx, const uint8_t *payloads, const uint64_
     uint64_t total = 0;
     for (uint64_t i = 0; i < count; ++i) total += sizes[i];
     g.dense_hint = total > count * elements ? 1u : 0u;   // compresses less than 16x
+    g.enc_dense = g.dense_hint;
     ctx->win.reserve(g, count);
     ctx->arena.ensure(span + 64);
     ctx->table_off.ensure(8 * count);
@@ -1320,6 +1321,25 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
                 g.qubits[k] = uint32_t(b);
             }
             dg.push_back(make_dev_gate(g));
+        }
+        {
+            // encoder choice for this stage's output: dense when the input
+            // is, or when some qubit sees >= 4 mixing gates (a row with two
+            // nonzero entries: H, sqrt-X, U3 ...; random-circuit layers)
+            uint32_t mix[64] = {}, most = 0;
+            for (const DevGate &d : dg) {
+                bool mixing = false;
+                for (uint32_t r = 0; r < d.dim && !mixing; ++r) {
+                    uint32_t nz = 0;
+                    for (uint32_t k = 0; k < d.dim; ++k)
+                        nz += ((d.kinds >> (4 * (r * d.dim + k))) & 15u) != CK_ZERO;
+                    mixing = nz > 1;
+                }
+                if (!mixing) continue;
+                most = std::max(most, ++mix[d.b0]);
+                if (d.nq == 2) most = std::max(most, ++mix[d.b1]);
+            }
+            sim->geom.enc_dense = sim->geom.dense_hint || most >= 4 ? 1u : 0u;
         }
         // relaxed plan (diagonal units need no tile bits) + the strict plan
         // it is replayed with, device-side, when a window raises the flag
