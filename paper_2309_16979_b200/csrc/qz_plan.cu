@@ -16,6 +16,9 @@ namespace qz {
 std::string validate_gates(uint32_t n, const qzc_gate *gates, uint64_t ngates) {
     for (uint64_t i = 0; i < ngates; ++i) {
         const qzc_gate &g = gates[i];
+        const bool ok = g.kind <= QZC_SWAP && g.nqubits == gate_arity(g.kind) && g.qubits[0] < n &&
+                        (g.nqubits == 1 || (g.qubits[1] < n && g.qubits[0] != g.qubits[1]));
+        if (ok) continue;   // message only on the failing gate (no per-gate strings)
         const std::string where = "gate " + std::to_string(i) + ": ";
         if (g.kind > QZC_SWAP) return where + "unknown gate kind";
         if (g.nqubits != gate_arity(g.kind))
@@ -44,6 +47,34 @@ std::vector<Stage> plan_stages(uint32_t n, const qzc_gate *gates, uint64_t ngate
     const uint32_t capacity = m - c, target = std::min(m - c, n - c);
     std::vector<Stage> out;
     Stage cur;
+    if (n <= 64) {
+        // the open stage's qubits >= c as a bit mask (one word: no per-gate set copies)
+        uint64_t high = 0;
+        auto close = [&]() {
+            if (cur.ngates == 0) return;
+            for (uint32_t q = c; uint32_t(__builtin_popcountll(high)) < target && q < n; ++q)
+                high |= uint64_t(1) << q;
+            for (uint64_t h = high; h; h &= h - 1) cur.high.push_back(uint32_t(__builtin_ctzll(h)));
+            out.push_back(cur);
+            cur = Stage{};
+            high = 0;
+        };
+        for (uint64_t i = 0; i < ngates; ++i) {
+            uint64_t gm = 0;
+            for (uint32_t k = 0; k < gates[i].nqubits; ++k)
+                if (gates[i].qubits[k] >= c) gm |= uint64_t(1) << gates[i].qubits[k];
+            if (uint32_t(__builtin_popcountll(high | gm)) > capacity) {
+                close();
+                high = gm;
+            } else {
+                high |= gm;
+            }
+            if (cur.ngates == 0) cur.first_gate = i;
+            ++cur.ngates;
+        }
+        close();
+        return out;
+    }
     std::set<uint32_t> high;
     auto close = [&]() {
         if (cur.ngates == 0) return;
