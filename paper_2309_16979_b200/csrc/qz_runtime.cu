@@ -1310,6 +1310,56 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
                 ngates_run = first;
             }
         }
+        // relaxed plan (diagonal units need no tile bits) + the strict plan
+        // it is replayed with, device-side, when a window raises the flag
+        const double tp0 = now_s();
+        // fresh buffer bits at the stage's start (qubits still |0>)
+        Fresh stage_fresh;
+        static const bool no_fresh = getenv("QZ_NO_FRESH") != nullptr;   // control
+        for (uint32_t q = 0; q < n && !no_fresh; ++q)
+            if ((sim->fresh_q >> q) & 1) {
+                const int bq = buffer_bit(st, relabel[q], c);
+                if (bq >= 0) {
+                    stage_fresh.mask |= uint64_t(1) << bq;
+                    stage_fresh.val |= ((sim->fresh_v >> q) & 1) << bq;
+                }
+            }
+        const uint64_t nwin = nbatches / bpw;
+        const uint64_t nslots = bpw << hs;
+        CodecGeom dgeom = sim->geom;
+        Fresh end_fresh;
+        bool dead_chunks = false;
+        {
+            // out-of-place checked passes exist only with relax level 2
+            const bool out_of_place = sim->relax == 2;
+            // chunk-index bits of the stage's fresh high qubits (only those:
+            // the passes know the stage's buffer bits alone)
+            uint64_t fq = 0, fv = 0;
+            for (uint32_t q : st.high)
+                if ((sim->fresh_q >> q) & 1) {
+                    fq |= uint64_t(1) << (q - c);
+                    fv |= ((sim->fresh_v >> q) & 1) << (q - c);
+                }
+            dead_chunks = !no_fresh && !sim->host_res && !out_of_place && fq && wbits >= 5;
+            if (dead_chunks) {
+                dgeom.dead_mask = fq;
+                dgeom.dead_val = fv;
+            }
+        }
+        // HBM store, one stream per window: the first window's decode does
+        // not depend on the plan, so it is issued before planning and runs
+        // while the host plans
+        const bool pre_decode = !sim->host_res && !sim->pipelined;
+        if (pre_decode) {
+            Window &W0 = sim->win;
+            cudaStream_t S0 = sim->streams[0];
+            QZ_CUDA(cudaEventRecord(ev(0), S0));
+            launch_slot_chunks(W0.slot_chunk.as<uint64_t>(), nslots, 0, hs, fmask, smask, S0);
+            decode_window(ctx, W0, dgeom, nslots, W0.slot_chunk.as<uint64_t>(), sim->arena_ptr(sim->cur),
+                          sim->table(sim->cur), ctx->launches, S0, sim->sparse_store);
+            QZ_CUDA(cudaEventRecord(ev(1), S0));
+        }
+        // (the gate list is built while the first window decodes)
         // remap the stage's gates to buffer bits (remap_gate, planner.cpp:131-141)
         std::vector<DevGate> dg;
         dg.reserve(ngates_run);
@@ -1341,58 +1391,11 @@ int qzc_sim_run(qzc_sim *sim, const qzc_gate *gates, uint64_t ngates) {
             }
             sim->geom.enc_dense = sim->geom.dense_hint || most >= 4 ? 1u : 0u;
         }
-        // relaxed plan (diagonal units need no tile bits) + the strict plan
-        // it is replayed with, device-side, when a window raises the flag
-        const double tp0 = now_s();
-        // fresh buffer bits at the stage's start (qubits still |0>)
-        Fresh stage_fresh;
-        static const bool no_fresh = getenv("QZ_NO_FRESH") != nullptr;   // control
-        for (uint32_t q = 0; q < n && !no_fresh; ++q)
-            if ((sim->fresh_q >> q) & 1) {
-                const int bq = buffer_bit(st, relabel[q], c);
-                if (bq >= 0) {
-                    stage_fresh.mask |= uint64_t(1) << bq;
-                    stage_fresh.val |= ((sim->fresh_v >> q) & 1) << bq;
-                }
-            }
-        const uint64_t nwin = nbatches / bpw;
-        const uint64_t nslots = bpw << hs;
-        CodecGeom dgeom = sim->geom;
-        Fresh end_fresh;
-        {
-            // out-of-place checked passes exist only with relax level 2
-            const bool out_of_place = sim->relax == 2;
-            // chunk-index bits of the stage's fresh high qubits (only those:
-            // the passes know the stage's buffer bits alone)
-            uint64_t fq = 0, fv = 0;
-            for (uint32_t q : st.high)
-                if ((sim->fresh_q >> q) & 1) {
-                    fq |= uint64_t(1) << (q - c);
-                    fv |= ((sim->fresh_v >> q) & 1) << (q - c);
-                }
-            if (!no_fresh && !sim->host_res && !out_of_place && fq && wbits >= 5) {
-                dgeom.dead_mask = fq;
-                dgeom.dead_val = fv;
-                end_fresh = fresh_after(dg, 0, dg.size(), stage_fresh);
-            }
-            if (trace)
-                fprintf(stderr, "qz trace: stage %zu dead-chunk mask %#llx val %#llx end-fresh %#llx pipelined %d\n",
-                        si, (unsigned long long)dgeom.dead_mask, (unsigned long long)dgeom.dead_val,
-                        (unsigned long long)end_fresh.mask, int(sim->pipelined));
-        }
-        // HBM store, one stream per window: the first window's decode does
-        // not depend on the plan, so it is issued before planning and runs
-        // while the host plans
-        const bool pre_decode = !sim->host_res && !sim->pipelined;
-        if (pre_decode) {
-            Window &W0 = sim->win;
-            cudaStream_t S0 = sim->streams[0];
-            QZ_CUDA(cudaEventRecord(ev(0), S0));
-            launch_slot_chunks(W0.slot_chunk.as<uint64_t>(), nslots, 0, hs, fmask, smask, S0);
-            decode_window(ctx, W0, dgeom, nslots, W0.slot_chunk.as<uint64_t>(), sim->arena_ptr(sim->cur),
-                          sim->table(sim->cur), ctx->launches, S0, sim->sparse_store);
-            QZ_CUDA(cudaEventRecord(ev(1), S0));
-        }
+        if (dead_chunks) end_fresh = fresh_after(dg, 0, dg.size(), stage_fresh);
+        if (trace)
+            fprintf(stderr, "qz trace: stage %zu dead-chunk mask %#llx val %#llx end-fresh %#llx pipelined %d\n", si,
+                    (unsigned long long)dgeom.dead_mask, (unsigned long long)dgeom.dead_val,
+                    (unsigned long long)end_fresh.mask, int(sim->pipelined));
         // a swap network after a tile pass is fused into its store (out of
         // place: needs the second window buffer; QZ_NO_PERM_FUSE=1 keeps the
         // separate swap pass)
